@@ -1,0 +1,180 @@
+#!/usr/bin/env python3
+"""Generate the committed golden fixtures from the REAL reference package.
+
+Run in the build container only (it imports ``blockeig`` from
+/root/reference/pkg/src, which does not exist on the GPU box):
+
+    python tests/golden/make_golden.py            # fast cases (~30 s)
+    python tests/golden/make_golden.py --heavy    # + reduced C3/C5 analogues, C1@1000
+
+Every fixture records the reference's own outputs for seeded inputs; the
+tests compare the oracle (CPU) and the CUDA path (GPU) against them.  The
+harness for the scaled BASELINE configs follows SURVEY 8c:
+A = MatrixFreeOperator(n, lambda v: s*L(v), spd=True, diag=6s), s=(N+1)^2.
+"""
+
+import argparse
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg")
+sys.path.insert(0, str(REF / "src"))
+
+import blockeig  # noqa: E402
+from blockeig import (  # noqa: E402
+    DiagonalOperator,
+    MatrixFreeOperator,
+    SolverConfig,
+    jacobi_preconditioner,
+    laplacian3d,
+    solve,
+)
+from blockeig import multivec as mv  # noqa: E402
+
+OUT = Path(__file__).parent
+
+
+def scaled_laplacian(N):
+    s = float((N + 1) ** 2)
+    L = laplacian3d((N, N, N))
+    return MatrixFreeOperator(N ** 3, lambda v: s * L(v), spd=True,
+                              diag=np.full(N ** 3, 6.0 * s))
+
+
+def record(report, m):
+    hist = report.history
+    ritz = np.array([h.ritz for h in hist]) if hist[0].ritz is not None else np.zeros((0, m))
+    resid = np.array([h.residual_norms for h in hist]) if hist[0].ritz is not None else np.zeros((0, m))
+    active = np.array([h.active for h in hist])
+    return dict(
+        eigenvalues=report.eigenvalues,
+        residual_norms=report.residual_norms,
+        iterations_used=np.int64(report.iterations_used),
+        converged=report.converged,
+        lock_iterations=report.lock_iterations,
+        status=np.array(report.status),
+        basis_fallbacks=np.int64(report.basis_fallbacks),
+        hist_ritz=ritz,
+        hist_resid=resid,
+        hist_active=active,
+    )
+
+
+def parse_csv():
+    """pkg/demos/convergence_history.csv: iter,j,ritz,resid,active with
+    np.float64(...) reprs (demos/convergence_history.py:29-46)."""
+    rows = []
+    for line in (REF / "demos" / "convergence_history.csv").read_text().splitlines()[1:]:
+        it, j, ritz, resid, act = line.split(",")
+        strip = lambda s: float(s.replace("np.float64(", "").rstrip(")"))  # noqa: E731
+        rows.append((int(it), int(j), strip(ritz), strip(resid), int(act)))
+    nit = max(r[0] for r in rows) + 1
+    m = max(r[1] for r in rows) + 1
+    ritz = np.zeros((nit, m))
+    resid = np.zeros((nit, m))
+    active = np.zeros((nit, m), dtype=bool)
+    for it, j, rz, rs, a in rows:
+        ritz[it, j], resid[it, j], active[it, j] = rz, rs, bool(a)
+    return ritz, resid, active
+
+
+def fast():
+    t0 = time.time()
+    # 1. golden trajectory, straight from the reference's CSV + a rerun.
+    ritz, resid, active = parse_csv()
+    a = laplacian3d((20, 20, 20))
+    rep = solve(a, t=jacobi_preconditioner(a),
+                config=SolverConfig(block_size=10, tol=1e-6, max_iter=200, seed=2))
+    r = record(rep, 10)
+    assert np.array_equal(r["hist_ritz"], ritz) and np.array_equal(r["hist_resid"], resid)
+    np.savez_compressed(OUT / "golden_20cubed_m10_jacobi_seed2.npz",
+                        csv_ritz=ritz, csv_resid=resid, csv_active=active, **r)
+
+    # 2. stencil known answers (operators.py:184-196), odd shapes, k=1..5.
+    st = {}
+    for case, (dims, k, seed) in enumerate([((5, 4, 3), 3, 11), ((7, 1, 2), 1, 12),
+                                            ((1, 1, 1), 2, 13), ((6, 5, 9), 5, 14),
+                                            ((3, 8, 4), 4, 15)]):
+        x = np.random.Generator(np.random.PCG64(seed)).standard_normal((int(np.prod(dims)), k))
+        y = laplacian3d(dims)(x)
+        st[f"dims{case}"] = np.array(dims)
+        st[f"x{case}"] = x
+        st[f"y{case}"] = np.ascontiguousarray(y)
+        s = float((dims[0] + 1) ** 2)
+        st[f"ys{case}"] = np.ascontiguousarray(s * y)
+    np.savez_compressed(OUT / "stencil_known_answers.npz", **st)
+
+    # 3. small Laplacian vs closed form (test_lobpcg.py:211-225)
+    a = laplacian3d((5, 5, 5))
+    rep = solve(a, t=jacobi_preconditioner(a),
+                config=SolverConfig(block_size=4, tol=1e-8, max_iter=300))
+    np.savez_compressed(OUT / "lap5_m4_jacobi.npz", **record(rep, 4))
+
+    # 4. generalized diagonal-B pencil (test_lobpcg.py:371-382)
+    n = 30
+    bd = np.random.Generator(np.random.PCG64(7)).uniform(0.5, 3.0, n)
+    rep = solve(DiagonalOperator(np.arange(1.0, n + 1.0)), b=DiagonalOperator(bd),
+                config=SolverConfig(block_size=4, tol=1e-10, max_iter=300))
+    vals, _ = mv.gen_sym_eig(np.diag(np.arange(1.0, n + 1.0)), np.diag(bd))
+    np.savez_compressed(OUT / "diag_pencil_n30_m4.npz", bdiag=bd, dense_vals=vals[:4],
+                        **record(rep, 4))
+
+    # 5. C1 (BASELINE configs[0]): 32^3 scaled, m=4, no T, tol 1e-6, 200 it, seed 0.
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    rep = solve(scaled_laplacian(32), config=SolverConfig(block_size=4, tol=1e-6, max_iter=200, seed=0))
+    np.savez_compressed(OUT / "c1_32cubed_m4_200it.npz", **record(rep, 4))
+
+    # 6. generalized Laplacian with diagonal B (C5 code path, small):
+    #    12^3 scaled, m=6, Jacobi, B=diag(U[1,2]) from PCG64(1000), tol 1e-6, 150 it.
+    N = 12
+    bd = np.random.Generator(np.random.PCG64(1000)).uniform(1.0, 2.0, N ** 3)
+    A = scaled_laplacian(N)
+    rep = solve(A, b=DiagonalOperator(bd), t=jacobi_preconditioner(A),
+                config=SolverConfig(block_size=6, tol=1e-6, max_iter=150, seed=0))
+    np.savez_compressed(OUT / "lap12_m6_diagB.npz", bdiag=bd, **record(rep, 6))
+
+    # 7. 10^3 m=5 tol 1e-8 Jacobi, unscaled (demos/staged_run1.json analogue)
+    a = laplacian3d((10, 10, 10))
+    rep = solve(a, t=jacobi_preconditioner(a),
+                config=SolverConfig(block_size=5, tol=1e-8, max_iter=300))
+    np.savez_compressed(OUT / "lap10_m5_jacobi.npz", **record(rep, 5))
+    print(f"fast fixtures written in {time.time() - t0:.1f} s")
+
+
+def heavy():
+    t0 = time.time()
+    # reduced C3 analogue: 48^3, m=16, Jacobi, tol 1e-6, 300 it.
+    A = scaled_laplacian(48)
+    rep = solve(A, t=jacobi_preconditioner(A),
+                config=SolverConfig(block_size=16, tol=1e-6, max_iter=300, seed=0, lock_history=True))
+    d = record(rep, 16)
+    np.savez_compressed(OUT / "c3r_48cubed_m16_300it.npz", **d)
+    print(f"C3r {rep.status} {time.time() - t0:.1f} s")
+    # C1 converging: max_iter 1000 (time-to-tol case)
+    rep = solve(scaled_laplacian(32), config=SolverConfig(block_size=4, tol=1e-6, max_iter=1000, seed=0))
+    np.savez_compressed(OUT / "c1_32cubed_m4_1000it.npz", **record(rep, 4))
+    print(f"C1@1000 {rep.status} {rep.iterations_used} {time.time() - t0:.1f} s")
+    # reduced C5 analogue: 32^3, m=64, B=diag(U[1,2]) PCG64(1000), Jacobi, 200 it.
+    N = 32
+    bd = np.random.Generator(np.random.PCG64(1000)).uniform(1.0, 2.0, N ** 3)
+    A = scaled_laplacian(N)
+    rep = solve(A, b=DiagonalOperator(bd), t=jacobi_preconditioner(A),
+                config=SolverConfig(block_size=64, tol=1e-6, max_iter=200, seed=0))
+    d = record(rep, 64)
+    np.savez_compressed(OUT / "c5r_32cubed_m64_diagB_200it.npz", **d)
+    print(f"C5r {rep.status} {time.time() - t0:.1f} s")
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--heavy", action="store_true")
+    args = ap.parse_args()
+    print("blockeig", blockeig.__version__)
+    if args.heavy:
+        heavy()
+    else:
+        fast()
