@@ -1,0 +1,119 @@
+/*
+ * libb200lobpcg -- C ABI of the B200 (sm_100a) LOBPCG hot path.
+ *
+ * Drop-in boundary for the reference package `blockeig`
+ * (/root/reference/pkg/src/blockeig).  The reference's Python entry point
+ * `solve(a, b=None, t=None, y=None, x0=None, config=None)`
+ * (lobpcg.py:343) stays in host Python; every operation it performs on the
+ * long dimension n is one of the calls below.  Each entry point names the
+ * reference interface it replaces.
+ *
+ * Conventions
+ *  - A "block" is a row-major (point-major) fp64 array of shape (n, ld): row r
+ *    holds the k <= ld columns of grid point r, exactly the reference's numpy
+ *    C-order (n, k) multivector (multivec.py:1-15, :220-229) padded to an even
+ *    leading dimension ld (16-byte rows, required by TMA).
+ *  - Grid point p = i + nx*(j + ny*k), x fastest (operators.py:63-67).
+ *  - All pointers are device pointers unless stated; all calls are
+ *    asynchronous on `stream` (a cudaStream_t / CUstream passed as void*).
+ *    The library never frees or retains caller memory.
+ *  - Every call returns 0 on success, a negative code on failure (-cudaError
+ *    for CUDA runtime errors, -1000.. for argument/driver errors); the message
+ *    is in b2l_last_error() (thread-local).
+ *  - Reductions are deterministic (fixed CTA row assignment, fixed-order
+ *    second stage): a given device, shape and input give identical bits.
+ *  - One host thread / one stream per device: the library keeps one growable
+ *    scratch buffer per device for CTA partials.
+ */
+#ifndef B200LOBPCG_H
+#define B200LOBPCG_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B2L_ABI_VERSION 1
+
+typedef struct {
+  const double* ptr; /* device pointer to an (n, ld) block */
+  int ld;            /* leading dimension (doubles per row), even */
+  int cols;          /* number of columns used, <= ld */
+} b2l_block;
+
+/* Last error message of this thread ("" if none). */
+const char* b2l_last_error(void);
+
+/* B2L_ABI_VERSION of the loaded library. */
+int b2l_abi_version(void);
+
+/* Fails unless the current device is sm_100 (B200). */
+int b2l_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/*
+ * K1 -- 7-point Dirichlet Laplacian, fused over all ld columns of a block.
+ * Replaces Laplacian3D._apply (operators.py:184-196) and the harness scaling
+ * MatrixFreeOperator(n, lambda v: s*L(v)) (operators.py:104-121):
+ *   out = scale * ((((((6x - x[i-1]) - x[i+1]) - x[j-1]) - x[j+1]) - x[k-1]) - x[k+1])
+ * bitwise equal to the reference (same operation order, no FMA contraction).
+ * `in` and `out` are (nx*ny*nz, ld) blocks of the nz locally owned z-planes.
+ * `halo` (nullable) holds two ghost planes [lo; hi] of shape (2*nx*ny, ld)
+ * for a z-slab partition; has_lo/has_hi select them, otherwise the missing
+ * neighbour plane is the Dirichlet zero.  in != out.
+ */
+int b2l_stencil7(const double* in, double* out, int nx, int ny, int nz, int ld,
+                 const double* halo, int has_lo, int has_hi, double scale,
+                 void* stream);
+
+/*
+ * K5 -- multi-block tall-skinny Gram  out = [L_0 .. L_{nl-1}]^T diag(w)^? [R_0 ..]
+ * Replaces multivec.gram (multivec.py:58-71) for all the Gram products of one
+ * LOBPCG step (lobpcg.py:419, :176, :318-338) in a single pass over the rows.
+ * Right block j is multiplied row-wise by `weight` (diag(B), DiagonalOperator
+ * operators.py:151-152) when bit j of right_weighted_mask is set.
+ * `out` is a dense row-major (sum L cols) x (sum R cols) device matrix.
+ * nleft <= 4, nright <= 8, at most 8 distinct blocks.
+ */
+int b2l_gram(int nrows, const b2l_block* left, int nleft, const b2l_block* right,
+             int nright, unsigned right_weighted_mask, const double* weight,
+             double* out, void* stream);
+
+/*
+ * K4+K2 -- residual, preconditioner, squared column norms.
+ * Replaces lobpcg.py:429-430 (W_full = AX - BX*lam; column_norms,
+ * multivec.py:214-217) and the preconditioner callback t(W) of lobpcg.py:467
+ * for the built-in Jacobi/identity preconditioners (operators.py:280-298):
+ *   wf[:, j] = AX[:, j] - (bdiag? bdiag*X[:, j] : X[:, j]) * lam[j]
+ *   sums_out[j]      = sum_r wf[r, j]^2                      (j < m)
+ *   sums_out[m + j]  = sum_r AX[r, j]^2  if want_ax_norms      (relative tol)
+ *   W[:, wpos[j]]    = T wf[:, j]  for every j with wpos[j] >= 0
+ * T: tmode 0 identity, 1 scalar tinv, 2 row vector tvec.  X and AX share ldx;
+ * lam, wpos and sums_out are device arrays of m (sums_out: 2m).
+ */
+int b2l_residual(int nrows, int m, const double* x, const double* ax, int ldx,
+                 const double* bdiag, const double* lam, int tmode, double tinv,
+                 const double* tvec, const int* wpos, int kw, double* w, int ldw,
+                 int want_ax_norms, double* sums_out, void* stream);
+
+/*
+ * K6 -- Ritz block update (lobpcg.py:520-540, multivec.multiply
+ * multivec.py:74-86), with the Cholesky-QR factors of W and P already folded
+ * into cw/cp (replaces tri_solve_right, multivec.py:125-146, at
+ * lobpcg.py:177-178 and :491):
+ *   P'  = W Cw + P[:, pcols] Cp        AP' = AW Cw + AP[:, pcols] Cp
+ *   X'  = X Cx (+ P' if x_plus_p)      AX' = AX Cx (+ AP')
+ * cx (m x m), cw (kw x m), cp (kp x m) row-major device matrices; pcols
+ * (kp ints) device.  ax/axo/aw/ap may be NULL (no A side); po/apo NULL skips
+ * writing P'.  Outputs must not alias inputs.
+ */
+int b2l_update(int nrows, int m, const double* x, const double* ax, int ldx,
+               const double* cx, const double* w, const double* aw, int ldw, int kw,
+               const double* cw, const double* p, const double* ap, int ldp,
+               const int* pcols, int kp, const double* cp, double* xo, double* axo,
+               int ldo, double* po, double* apo, int ldpo, int x_plus_p,
+               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* B200LOBPCG_H */

@@ -1,0 +1,94 @@
+"""ctypes binding of libb200lobpcg.so (include/b200lobpcg.h).
+
+This is the only place Python touches the native library.  There is no CPU
+fallback: if the library or a CUDA device is missing, every call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "lib" / "libb200lobpcg.so"
+
+_lock = threading.Lock()
+_lib = None
+
+c_dp = C.POINTER(C.c_double)
+c_ip = C.POINTER(C.c_int)
+
+
+class b2l_block(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("ld", C.c_int), ("cols", C.c_int)]
+
+
+# name -> (restype, argtypes); every exported symbol of include/b200lobpcg.h
+SIGNATURES = {
+    "b2l_last_error": (C.c_char_p, []),
+    "b2l_abi_version": (C.c_int, []),
+    "b2l_device_info": (C.c_int, [c_ip, c_ip, c_ip]),
+    "b2l_stencil7": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                               C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_void_p]),
+    "b2l_gram": (C.c_int, [C.c_int, C.POINTER(b2l_block), C.c_int, C.POINTER(b2l_block),
+                           C.c_int, C.c_uint, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "b2l_residual": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                               C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_void_p,
+                               C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int,
+                               C.c_void_p, C.c_void_p]),
+    "b2l_update": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                             C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                             C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                             C.c_void_p]),
+}
+
+ABI_VERSION = 1
+
+
+class NativeError(RuntimeError):
+    """A libb200lobpcg call failed (CUDA error or bad arguments)."""
+
+
+def load():
+    """Load (once) and return the native library; raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_0705_2626_b200.build` "
+                "(there is no CPU fallback)")
+        lib = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.b2l_abi_version() != ABI_VERSION:
+            raise ImportError("libb200lobpcg ABI version mismatch; rebuild")
+        _lib = lib
+        return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().b2l_last_error().decode(errors="replace")
+        raise NativeError(f"{what} failed ({rc}): {msg}")
+
+
+_device_checked = set()
+
+
+def ensure_device(dev_index: int) -> None:
+    """Fail loudly unless device dev_index is a B200 (sm_100)."""
+    if dev_index in _device_checked:
+        return
+    lib = load()
+    sm, ma, mi = C.c_int(), C.c_int(), C.c_int()
+    check(lib.b2l_device_info(C.byref(sm), C.byref(ma), C.byref(mi)), "b2l_device_info")
+    _device_checked.add(dev_index)

@@ -1,0 +1,171 @@
+// C ABI of libb200lobpcg.so -- see include/b200lobpcg.h for the contract and
+// the reference interface each entry point replaces.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <string>
+
+#include "../../include/b200lobpcg.h"
+#include "common.cuh"
+
+namespace b2l {
+
+int stencil7(const double* in, double* out, int nx, int ny, int nz, int ld,
+             const double* halo, int has_lo, int has_hi, double scale,
+             cudaStream_t st);
+struct HostBlock {
+  const double* p;
+  int ld, cols;
+};
+int gram(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr,
+         unsigned rw_mask, const double* d, double* out, cudaStream_t st);
+int residual(int nrows, int m, const double* x, const double* ax, int ldx,
+             const double* d, const double* lam, int tmode, double tinv,
+             const double* tvec, const int* pos, int kw, double* w, int ldw,
+             int want_ax, double* sums_out, cudaStream_t st);
+int update(int nrows, int m, const double* x, const double* ax, int ldx,
+           const double* cx, const double* w, const double* aw, int ldw, int kw,
+           const double* cw, const double* p, const double* ap, int ldp,
+           const int* pcols, int kp, const double* cp, double* xo, double* axo,
+           int ldo, double* po, double* apo, int ldpo, int x_plus_p,
+           cudaStream_t st);
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct DevWs {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+static DevWs g_ws[64];
+static int g_sms[64];
+
+void* workspace(size_t bytes, int* err) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevWs& w = g_ws[dev & 63];
+  if (w.bytes < bytes) {
+    // growth is rare (first call per shape); keep it stream-safe by syncing
+    if (w.ptr) {
+      cudaDeviceSynchronize();
+      cudaFree(w.ptr);
+    }
+    size_t nb = bytes < (1u << 20) ? (1u << 20) : bytes + bytes / 2;
+    if (cudaMalloc(&w.ptr, nb) != cudaSuccess) {
+      w.ptr = nullptr;
+      w.bytes = 0;
+      *err = fail(-B2L_ENOMEM, "workspace allocation failed");
+      return nullptr;
+    }
+    w.bytes = nb;
+  }
+  *err = 0;
+  return w.ptr;
+}
+
+int sm_count() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& c = g_sms[dev & 63];
+  if (c == 0) {
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    if (c <= 0) c = 148;
+  }
+  return c;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+
+int encode_tmap_4d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1,
+                   uint64_t d2, uint64_t d3, uint32_t b0, uint32_t b1,
+                   uint32_t b2, uint32_t b3) {
+  std::call_once(g_encode_once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  B2L_CHECK(g_encode != nullptr, -B2L_EDRIVER, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {d0, d1, d2, d3};
+  cuuint64_t strides[3] = {d0 * 8, d0 * d1 * 8, d0 * d1 * d2 * 8};
+  cuuint32_t box[4] = {b0, b1, b2, b3};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  B2L_CHECK(r == CUDA_SUCCESS, -B2L_EDRIVER,
+            "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
+  return 0;
+}
+
+}  // namespace b2l
+
+using namespace b2l;
+
+extern "C" {
+
+const char* b2l_last_error(void) { return g_err.c_str(); }
+
+int b2l_abi_version(void) { return B2L_ABI_VERSION; }
+
+int b2l_device_info(int* sm_count_out, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  B2L_CUDA(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  B2L_CUDA(cudaGetDeviceProperties(&prop, dev));
+  if (sm_count_out) *sm_count_out = prop.multiProcessorCount;
+  if (cc_major) *cc_major = prop.major;
+  if (cc_minor) *cc_minor = prop.minor;
+  B2L_CHECK(prop.major == 10 && prop.minor == 0, -B2L_EINVAL,
+            "libb200lobpcg is built for sm_100a (B200); found sm_" +
+                std::to_string(prop.major) + std::to_string(prop.minor));
+  return 0;
+}
+
+int b2l_stencil7(const double* in, double* out, int nx, int ny, int nz, int ld,
+                 const double* halo, int has_lo, int has_hi, double scale,
+                 void* stream) {
+  return stencil7(in, out, nx, ny, nz, ld, halo, has_lo, has_hi, scale,
+                  static_cast<cudaStream_t>(stream));
+}
+
+int b2l_gram(int nrows, const b2l_block* left, int nleft, const b2l_block* right,
+             int nright, unsigned right_weighted_mask, const double* weight,
+             double* out, void* stream) {
+  B2L_CHECK(left && right && out, -B2L_EINVAL, "gram: null argument");
+  HostBlock L[8], R[8];
+  B2L_CHECK(nleft <= 8 && nright <= 8, -B2L_EINVAL, "gram: too many blocks");
+  for (int i = 0; i < nleft; ++i) L[i] = HostBlock{left[i].ptr, left[i].ld, left[i].cols};
+  for (int i = 0; i < nright; ++i) R[i] = HostBlock{right[i].ptr, right[i].ld, right[i].cols};
+  return gram(nrows, L, nleft, R, nright, right_weighted_mask, weight, out,
+              static_cast<cudaStream_t>(stream));
+}
+
+int b2l_residual(int nrows, int m, const double* x, const double* ax, int ldx,
+                 const double* bdiag, const double* lam, int tmode, double tinv,
+                 const double* tvec, const int* wpos, int kw, double* w, int ldw,
+                 int want_ax_norms, double* sums_out, void* stream) {
+  return residual(nrows, m, x, ax, ldx, bdiag, lam, tmode, tinv, tvec, wpos, kw, w, ldw,
+                  want_ax_norms, sums_out, static_cast<cudaStream_t>(stream));
+}
+
+int b2l_update(int nrows, int m, const double* x, const double* ax, int ldx,
+               const double* cx, const double* w, const double* aw, int ldw, int kw,
+               const double* cw, const double* p, const double* ap, int ldp,
+               const int* pcols, int kp, const double* cp, double* xo, double* axo,
+               int ldo, double* po, double* apo, int ldpo, int x_plus_p,
+               void* stream) {
+  return update(nrows, m, x, ax, ldx, cx, w, aw, ldw, kw, cw, p, ap, ldp, pcols, kp, cp, xo,
+                axo, ldo, po, apo, ldpo, x_plus_p, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -169,12 +169,26 @@ def heavy():
     print(f"C5r {rep.status} {time.time() - t0:.1f} s")
 
 
+def c2():
+    """BASELINE configs[1] in full: 128^3, m=10, Jacobi, tol 1e-8, 300 it
+    (~16 min on 8 host threads)."""
+    t0 = time.time()
+    A = scaled_laplacian(128)
+    rep = solve(A, t=jacobi_preconditioner(A),
+                config=SolverConfig(block_size=10, tol=1e-8, max_iter=300, seed=0))
+    np.savez_compressed(OUT / "c2_128cubed_m10_300it.npz", **record(rep, 10))
+    print(f"C2 {rep.status} {time.time() - t0:.1f} s")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--heavy", action="store_true")
+    ap.add_argument("--c2", action="store_true")
     args = ap.parse_args()
     print("blockeig", blockeig.__version__)
-    if args.heavy:
+    if args.c2:
+        c2()
+    elif args.heavy:
         heavy()
     else:
         fast()

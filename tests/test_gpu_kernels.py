@@ -1,0 +1,189 @@
+"""GPU parity of each kernel against the CPU oracle, through the C ABI.
+
+Stencil (K1): bitwise equal to the reference Laplacian3D._apply (fixtures
+from the real reference + oracle at larger sizes).  Gram (K5), residual
+(K4+K2) and update (K6): fp64, compared to numpy on the same inputs at
+1e-13 relative (different summation order only).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import lobpcg_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_0705_2626_b200 import _lib
+
+    _lib.ensure_device(0)
+    return torch.device("cuda", 0)
+
+
+def rng(seed):
+    return np.random.Generator(np.random.PCG64(seed))
+
+
+def blk(a, dev, ld=None):
+    n, k = a.shape
+    ld = ld or (k + (k & 1) if k > 1 else 2)
+    t = torch.zeros((n, ld), dtype=torch.float64, device=dev)
+    t[:, :k] = torch.from_numpy(np.ascontiguousarray(a))
+    return t
+
+
+def run_stencil(x, dims, scale, dev):
+    from paper_0705_2626_b200 import device as dv
+
+    n, k = x.shape
+    xin = blk(x, dev)
+    out = torch.full_like(xin, np.nan)
+    dv.stencil7(xin, out, *dims, scale)
+    torch.cuda.synchronize()
+    return out[:, :k].cpu().numpy()
+
+
+def test_stencil_golden_bitwise(dev, golden):
+    g = golden("stencil_known_answers.npz")
+    for case in range(5):
+        dims = tuple(int(v) for v in g[f"dims{case}"])
+        x = g[f"x{case}"]
+        assert np.array_equal(run_stencil(x, dims, 1.0, dev), g[f"y{case}"]), case
+        s = float((dims[0] + 1) ** 2)
+        assert np.array_equal(run_stencil(x, dims, s, dev), g[f"ys{case}"]), case
+
+
+@pytest.mark.parametrize("dims,k", [((32, 32, 32), 4), ((40, 33, 17), 10), ((128, 128, 16), 10),
+                                    ((64, 64, 64), 16), ((20, 21, 22), 7), ((96, 8, 40), 1),
+                                    ((24, 24, 24), 64), ((5, 300, 3), 3)])
+def test_stencil_bitwise_vs_oracle(dev, dims, k):
+    x = rng(sum(dims) + k).uniform(-1, 1, (int(np.prod(dims)), k))
+    s = float((dims[0] + 1) ** 2)
+    ref = np.ascontiguousarray(orc.stencil7(x, *dims, s))
+    assert np.array_equal(run_stencil(x, dims, s, dev), ref)
+
+
+def test_stencil_ones_boundary_counts(dev):
+    dims = (3, 2, 4)
+    out = run_stencil(np.ones((24, 1)), dims, 1.0, dev)[:, 0]
+    ref = np.ascontiguousarray(orc.stencil7(np.ones((24, 1)), *dims))[:, 0]
+    assert np.array_equal(out, ref)
+    assert out.min() >= 3.0 and out.max() <= 4.0
+
+
+def test_stencil_halo_planes(dev):
+    """Slab with ghost planes equals the same rows of the global apply."""
+    from paper_0705_2626_b200 import device as dv
+
+    nx, ny, nz, k = 12, 10, 16, 6
+    x = rng(9).standard_normal((nx * ny * nz, k))
+    ref = np.ascontiguousarray(orc.stencil7(x, nx, ny, nz, 3.0))
+    plane = nx * ny
+    for z0, z1 in [(0, 5), (5, 11), (11, 16)]:
+        loc = blk(x[z0 * plane:z1 * plane], dev)
+        halo = torch.zeros((2 * plane, loc.shape[1]), dtype=torch.float64, device=dev)
+        if z0 > 0:
+            halo[:plane, :k] = torch.from_numpy(x[(z0 - 1) * plane:z0 * plane])
+        if z1 < nz:
+            halo[plane:, :k] = torch.from_numpy(x[z1 * plane:(z1 + 1) * plane])
+        out = torch.empty_like(loc)
+        dv.stencil7(loc, out, nx, ny, z1 - z0, 3.0, halo, z0 > 0, z1 < nz)
+        assert np.array_equal(out[:, :k].cpu().numpy(), ref[z0 * plane:z1 * plane])
+
+
+@pytest.mark.parametrize("n,cols", [(1000, (4, 4, 4)), (65537, (10, 9, 10)), (3, (2, 1, 2)),
+                                    (200000, (16, 16, 16)), (5000, (64, 13, 64))])
+def test_gram_multiblock(dev, n, cols):
+    from paper_0705_2626_b200 import device as dv
+
+    r = rng(n)
+    X, W, P = (r.standard_normal((n, c)) for c in cols)
+    AW, AP = r.standard_normal((n, cols[1])), r.standard_normal((n, cols[2]))
+    d = r.uniform(1, 2, n)
+    tX, tW, tP, tAW, tAP = (blk(a, dev) for a in (X, W, P, AW, AP))
+    td = torch.from_numpy(d).to(dev)
+    L = [(tX, cols[0]), (tW, cols[1]), (tP, cols[2])]
+    R = L + [(tAW, cols[1]), (tAP, cols[2])]
+    for mask, wt in ((0, None), (0b111, td)):
+        G = dv.gram(n, L, R, mask, wt).cpu().numpy()
+        Lh = np.hstack([X, W, P])
+        Rb = np.hstack([X, W, P]) * (d[:, None] if mask else 1.0)
+        Rh = np.hstack([Rb, AW, AP])
+        ref = Lh.T @ Rh
+        scale = np.abs(Lh).T @ np.abs(Rh)
+        assert np.all(np.abs(G - ref) <= 1e-13 * scale + 1e-300)
+
+
+def test_gram_is_deterministic(dev):
+    from paper_0705_2626_b200 import device as dv
+
+    x = blk(rng(1).standard_normal((300000, 10)), dev)
+    g1 = dv.gram(300000, [(x, 10)], [(x, 10)]).cpu().numpy()
+    g2 = dv.gram(300000, [(x, 10)], [(x, 10)]).cpu().numpy()
+    assert np.array_equal(g1, g2)
+
+
+@pytest.mark.parametrize("m,tmode,useb", [(10, 1, False), (4, 0, False), (7, 2, True), (64, 1, True)])
+def test_residual_kernel(dev, m, tmode, useb):
+    from paper_0705_2626_b200 import device as dv
+
+    n = 50000
+    r = rng(m)
+    X, AX = r.standard_normal((n, m)), r.standard_normal((n, m))
+    lam = r.uniform(1, 10, m)
+    d = r.uniform(1, 2, n) if useb else None
+    tvec = r.uniform(0.1, 1, n)
+    active = r.random(m) < 0.7
+    active[0] = True
+    jp = np.flatnonzero(active)
+    pos = np.full(m, -1, np.int32)
+    pos[jp] = np.arange(jp.size)
+    kw = jp.size
+    ldw = kw + (kw & 1)
+    W = torch.full((n, ldw), np.nan, dtype=torch.float64, device=dev)
+    sums = torch.zeros(2 * m, dtype=torch.float64, device=dev)
+    dv.residual(n, m, blk(X, dev), blk(AX, dev), torch.from_numpy(d).to(dev) if useb else None,
+                torch.from_numpy(lam).to(dev), tmode, 0.25, torch.from_numpy(tvec).to(dev),
+                torch.from_numpy(pos).to(dev), kw, W, True, sums)
+    bx = X * d[:, None] if useb else X
+    wf = AX - bx * lam
+    s = sums.cpu().numpy()
+    np.testing.assert_allclose(s[:m], (wf * wf).sum(0), rtol=1e-12)
+    np.testing.assert_allclose(s[m:], (AX * AX).sum(0), rtol=1e-12)
+    t = {0: 1.0, 1: 0.25}.get(tmode)
+    ref = (t * wf[:, jp]) if tmode != 2 else tvec[:, None] * wf[:, jp]
+    got = W.cpu().numpy()
+    assert np.array_equal(got[:, :kw], ref)  # elementwise ops are exact
+    if ldw > kw:
+        assert np.all(got[:, kw] == 0.0)
+
+
+@pytest.mark.parametrize("m,kw,kp", [(10, 10, 10), (10, 7, 7), (4, 3, 0), (16, 16, 9), (64, 40, 40)])
+def test_update_kernel(dev, m, kw, kp):
+    from paper_0705_2626_b200 import device as dv
+
+    n = 30000
+    r = rng(m * 100 + kw)
+    X, AX, P, AP = (r.standard_normal((n, m)) for _ in range(4))
+    W, AW = r.standard_normal((n, kw)), r.standard_normal((n, kw))
+    cx, cw, cp = r.standard_normal((m, m)), r.standard_normal((kw, m)), r.standard_normal((kp, m))
+    pcols = np.sort(r.choice(m, kp, replace=False)).astype(np.int32)
+    t = {k: blk(v, dev) for k, v in dict(X=X, AX=AX, P=P, AP=AP, W=W, AW=AW).items()}
+    out = {k: torch.full_like(t["X"], np.nan) for k in ("X", "AX", "P", "AP")}
+    c = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    dv.update(n, m, t["X"], t["AX"], c(cx), out["X"], out["AX"], w=t["W"], aw=t["AW"], kw=kw,
+              cw=c(cw), p=t["P"] if kp else None, ap=t["AP"] if kp else None,
+              pcols=c(pcols) if kp else c(np.zeros(1, np.int32)), kp=kp,
+              cp=c(cp) if kp else c(cx), po=out["P"], apo=out["AP"], x_plus_p=True)
+    pn = W @ cw + (P[:, pcols] @ cp if kp else 0)
+    apn = AW @ cw + (AP[:, pcols] @ cp if kp else 0)
+    refs = dict(P=pn, AP=apn, X=X @ cx + pn, AX=AX @ cx + apn)
+    for k, ref in refs.items():
+        got = out[k].cpu().numpy()
+        np.testing.assert_allclose(got[:, :m], ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+        if got.shape[1] > m:
+            assert np.all(got[:, m:] == 0.0)

@@ -1,0 +1,220 @@
+"""End-to-end parity of the GPU solve() against the reference's own outputs.
+
+Criteria (SURVEY 8c parity protocol, BASELINE.json north_star):
+  * eigenvalues within 1e-8 relative of the reference at matched iterations
+    and of the closed form on converging runs;
+  * iteration counts within +-1 of the reference on well-conditioned
+    converging cases;
+  * residual norms <= tol (or <= the reference's own final residual);
+  * status strings identical.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-8
+
+
+@pytest.fixture(scope="module")
+def pk():
+    assert torch.cuda.is_available()
+    import paper_0705_2626_b200 as pk
+
+    return pk
+
+
+def scaled(pk, N):
+    s = float((N + 1) ** 2)
+    return pk.Laplacian3D((N, N, N), scale=s), s
+
+
+def rel(a, b):
+    return np.abs(np.asarray(a) - np.asarray(b)) / np.abs(np.asarray(b))
+
+
+def test_golden_trajectory(pk, golden):
+    """20^3 unscaled, m=10, Jacobi, tol 1e-6, seed 2 -> Converged @180
+    (pkg/demos/convergence_history.csv)."""
+    g = golden("golden_20cubed_m10_jacobi_seed2.npz")
+    a = pk.laplacian3d((20, 20, 20))
+    rep = pk.solve(a, t=pk.jacobi_preconditioner(a),
+                   config=pk.SolverConfig(block_size=10, tol=1e-6, max_iter=200, seed=2))
+    assert rep.status == "Converged"
+    assert abs(rep.iterations_used - 180) <= 1
+    ref_locks = g["lock_iterations"]
+    assert np.all(np.abs(rep.lock_iterations - ref_locks) <= 1), rep.lock_iterations
+    ritz = np.array([h.ritz for h in rep.history])
+    nit = min(len(ritz), len(g["csv_ritz"]))
+    assert rel(ritz[:nit], g["csv_ritz"][:nit]).max() <= REL
+    exact = pk.exact_eigenvalues((20, 20, 20), 10)
+    assert rel(rep.eigenvalues, exact).max() < 1e-8
+    assert rel(rep.eigenvalues, g["eigenvalues"]).max() < 1e-10
+    assert np.all(rep.residual_norms <= np.maximum(1e-6, 10 * g["residual_norms"]))
+
+
+def test_c1_matched_iterations(pk, golden):
+    """BASELINE configs[0]: 32^3 scaled, m=4, no T, tol 1e-6, 200 it."""
+    g = golden("c1_32cubed_m4_200it.npz")
+    a, _ = scaled(pk, 32)
+    rep = pk.solve(a, config=pk.SolverConfig(block_size=4, tol=1e-6, max_iter=200, seed=0))
+    assert rep.status == str(g["status"]) == "MaxIterReached"
+    assert rep.iterations_used == 200
+    assert rel(rep.eigenvalues, g["eigenvalues"]).max() <= REL
+    ritz = np.array([h.ritz for h in rep.history])
+    assert rel(ritz, g["hist_ritz"]).max() <= 1e-6
+    assert rel(ritz[-1], g["hist_ritz"][-1]).max() <= REL
+    np.testing.assert_allclose(rep.residual_norms, g["residual_norms"], rtol=0.5)
+
+
+def test_c1_converging_time_to_tol(pk, golden):
+    """C1 with max_iter=1000 converges; the reference's own count moves
+    between 407 and 415 under 1-ulp perturbations."""
+    g = golden("c1_32cubed_m4_1000it.npz")
+    a, s = scaled(pk, 32)
+    rep = pk.solve(a, config=pk.SolverConfig(block_size=4, tol=1e-6, max_iter=1000, seed=0))
+    assert rep.status == "Converged"
+    assert 400 <= rep.iterations_used <= 425, rep.iterations_used
+    exact = pk.exact_eigenvalues((32, 32, 32), 4, scale=s)
+    assert rel(rep.eigenvalues, exact).max() <= REL
+    assert rel(rep.eigenvalues, g["eigenvalues"]).max() <= REL
+    assert np.all(rep.residual_norms <= np.maximum(1e-6, 10 * g["residual_norms"].max()))
+
+
+def test_small_laplacian_closed_form(pk, golden):
+    g = golden("lap5_m4_jacobi.npz")
+    a = pk.laplacian3d((5, 5, 5))
+    rep = pk.solve(a, t=pk.jacobi_preconditioner(a),
+                   config=pk.SolverConfig(block_size=4, tol=1e-8, max_iter=300))
+    assert rep.all_converged
+    assert abs(rep.iterations_used - int(g["iterations_used"])) <= 1
+    np.testing.assert_allclose(rep.eigenvalues, pk.exact_eigenvalues((5, 5, 5), 4), rtol=1e-8)
+    assert np.all(rep.residual_norms <= 1e-8 * 1.01)
+    x = rep.eigenvectors
+    assert np.abs(x.T @ x - np.eye(4)).max() <= 1e-8
+
+
+def test_lap10(pk, golden):
+    g = golden("lap10_m5_jacobi.npz")
+    a = pk.laplacian3d((10, 10, 10))
+    rep = pk.solve(a, t=pk.jacobi_preconditioner(a),
+                   config=pk.SolverConfig(block_size=5, tol=1e-8, max_iter=300))
+    assert rep.status == str(g["status"])
+    assert abs(rep.iterations_used - int(g["iterations_used"])) <= 1
+    assert rel(rep.eigenvalues, g["eigenvalues"]).max() <= 1e-10
+
+
+def test_generalized_diag_pencil(pk, golden):
+    """Generic A (DiagonalOperator callback) + diagonal B fused as weights
+    (test_lobpcg.py:371-382)."""
+    g = golden("diag_pencil_n30_m4.npz")
+    n = 30
+    a = pk.DiagonalOperator(np.arange(1.0, n + 1.0))
+    b = pk.DiagonalOperator(g["bdiag"])
+    rep = pk.solve(a, b=b, config=pk.SolverConfig(block_size=4, tol=1e-10, max_iter=300))
+    assert rep.all_converged
+    np.testing.assert_allclose(rep.eigenvalues, g["dense_vals"], rtol=1e-10)
+    x = rep.eigenvectors
+    assert np.abs(x.T @ (g["bdiag"][:, None] * x) - np.eye(4)).max() <= 1e-8
+    assert abs(rep.iterations_used - int(g["iterations_used"])) <= 2
+
+
+def test_laplacian_diag_b(pk, golden):
+    """12^3 scaled Laplacian, B = diag(U[1,2]), Jacobi (C5 code path)."""
+    g = golden("lap12_m6_diagB.npz")
+    a, _ = scaled(pk, 12)
+    rep = pk.solve(a, b=pk.DiagonalOperator(g["bdiag"]), t=pk.jacobi_preconditioner(a),
+                   config=pk.SolverConfig(block_size=6, tol=1e-6, max_iter=150, seed=0))
+    assert rep.status == str(g["status"])
+    assert abs(rep.iterations_used - int(g["iterations_used"])) <= 1
+    assert rel(rep.eigenvalues, g["eigenvalues"]).max() <= REL
+    assert np.all(np.abs(rep.lock_iterations - g["lock_iterations"]) <= 1)
+
+
+def test_c3_reduced(pk, golden):
+    """48^3, m=16, Jacobi, tol 1e-6, 300 it: partial soft locking (k < m)."""
+    g = golden("c3r_48cubed_m16_300it.npz")
+    a, _ = scaled(pk, 48)
+    rep = pk.solve(a, t=pk.jacobi_preconditioner(a),
+                   config=pk.SolverConfig(block_size=16, tol=1e-6, max_iter=300, seed=0))
+    assert rep.status == str(g["status"])
+    assert rep.iterations_used == int(g["iterations_used"])
+    assert rel(rep.eigenvalues, g["eigenvalues"]).max() <= REL
+    assert int(rep.converged.sum()) == int(g["converged"].sum())
+
+
+def test_c5_reduced(pk, golden):
+    """32^3, m=64, diagonal B, Jacobi, 200 it (large-block Gram path)."""
+    g = golden("c5r_32cubed_m64_diagB_200it.npz")
+    N = 32
+    bd = np.random.Generator(np.random.PCG64(1000)).uniform(1.0, 2.0, N ** 3)
+    a, _ = scaled(pk, N)
+    rep = pk.solve(a, b=pk.DiagonalOperator(bd), t=pk.jacobi_preconditioner(a),
+                   config=pk.SolverConfig(block_size=64, tol=1e-6, max_iter=200, seed=0))
+    assert rep.status == str(g["status"])
+    assert rel(rep.eigenvalues, g["eigenvalues"]).max() <= REL
+    assert abs(int(rep.converged.sum()) - int(g["converged"].sum())) <= 1
+
+
+def test_single_point_and_exact_guess(pk):
+    rep = pk.solve(pk.laplacian3d((1, 1, 1)), config=pk.SolverConfig(block_size=1))
+    assert rep.all_converged and rep.iterations_used == 0
+    np.testing.assert_allclose(rep.eigenvalues, [6.0], rtol=1e-14)
+    a = pk.DiagonalOperator(np.arange(1.0, 11.0))
+    rep = pk.solve(a, x0=np.eye(10)[:, :3], config=pk.SolverConfig(block_size=3, tol=1e-8))
+    assert rep.iterations_used == 0 and rep.all_converged
+    np.testing.assert_allclose(rep.eigenvalues, [1.0, 2.0, 3.0], atol=1e-12)
+
+
+def test_input_validation(pk):
+    a = pk.laplacian3d((4, 4, 4))
+    with pytest.raises(ValueError):
+        pk.solve(a, x0=np.ones((64, 2)), config=pk.SolverConfig(block_size=3))
+    x0 = np.random.default_rng(0).standard_normal((64, 2))
+    x0[3, 1] = np.nan
+    with pytest.raises(ValueError):
+        pk.solve(a, x0=x0, config=pk.SolverConfig(block_size=2))
+    with pytest.raises(ValueError):
+        pk.solve(a, config=pk.SolverConfig(block_size=65))
+    with pytest.raises(ValueError):
+        pk.SolverConfig(tol=0.0).validate()
+    with pytest.raises(ValueError, match="shape"):
+        pk.solve(a, t=lambda w: w[:, :1], config=pk.SolverConfig(block_size=3, max_iter=5))
+    with pytest.raises(ValueError, match="non-finite"):
+        pk.solve(a, t=lambda w: w * float("nan"), config=pk.SolverConfig(block_size=3, max_iter=5))
+    with pytest.raises(ValueError, match="degenerate"):
+        pk.solve(a, x0=np.ones((64, 2)), config=pk.SolverConfig(block_size=2))
+
+
+def test_generic_preconditioner_callback(pk):
+    """A user lambda preconditioner (CUDA tensor in, CUDA tensor out) gives
+    the same run as the built-in Jacobi it imitates."""
+    a = pk.laplacian3d((8, 8, 8))
+    cfg = pk.SolverConfig(block_size=4, tol=1e-8, max_iter=200)
+    r1 = pk.solve(a, t=pk.jacobi_preconditioner(a), config=cfg)
+    r2 = pk.solve(a, t=lambda w: (1.0 / 6.0) * w, config=cfg)
+    assert r1.iterations_used == r2.iterations_used
+    np.testing.assert_allclose(r1.eigenvalues, r2.eigenvalues, rtol=1e-12)
+
+
+def test_bitwise_reproducible(pk):
+    a, _ = scaled(pk, 24)
+    cfg = pk.SolverConfig(block_size=6, tol=1e-8, max_iter=60, seed=3)
+    t = pk.jacobi_preconditioner(a)
+    r1 = pk.solve(a, t=t, config=cfg)
+    r2 = pk.solve(a, t=t, config=cfg)
+    assert np.array_equal(r1.eigenvalues, r2.eigenvalues)
+    assert np.array_equal(r1.eigenvectors, r2.eigenvectors)
+
+
+def test_relative_tol_and_history_flags(pk):
+    a = pk.laplacian3d((6, 6, 6))
+    rep = pk.solve(a, t=pk.jacobi_preconditioner(a),
+                   config=pk.SolverConfig(block_size=3, tol=1e-8, max_iter=300,
+                                          relative_tol=True, lock_history=False,
+                                          check_invariants=True))
+    assert rep.all_converged
+    assert all(h.ritz is None for h in rep.history)
+    np.testing.assert_allclose(rep.eigenvalues, pk.exact_eigenvalues((6, 6, 6), 3), rtol=1e-8)
