@@ -219,6 +219,8 @@ int gram(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr,
   GramMap M{};
   A.nrows = nrows;
   A.nu = 0;
+  A.nl = nl;
+  A.nr = nr;
   auto uid = [&](const HostBlock& b) -> int {
     for (int u = 0; u < A.nu; ++u)
       if (A.up[u] == b.p && A.uld[u] == b.ld) return u;
