@@ -71,11 +71,15 @@ int b2l_stencil7(const double* in, double* out, int nx, int ny, int nz, int ld,
  * Right block j is multiplied row-wise by `weight` (diag(B), DiagonalOperator
  * operators.py:151-152) when bit j of right_weighted_mask is set.
  * `out` is a dense row-major (sum L cols) x (sum R cols) device matrix.
- * nleft <= 4, nright <= 8, at most 8 distinct blocks.
+ * pair_mode (host array nleft*nright, nullable = all 1): 0 = the block pair
+ * (l, r) is not needed, 1 = full, 2 = upper triangle only (a symmetric
+ * diagonal pair such as X^T B X); entries outside requested pairs are
+ * unspecified.  nleft <= 4, nright <= 8, at most 8 distinct blocks, at most
+ * 1024 8x8 output tiles.  Computed on the fp64 tensor cores (DMMA).
  */
 int b2l_gram(int nrows, const b2l_block* left, int nleft, const b2l_block* right,
              int nright, unsigned right_weighted_mask, const double* weight,
-             double* out, void* stream);
+             const unsigned char* pair_mode, double* out, void* stream);
 
 /*
  * K4+K2 -- residual, preconditioner, squared column norms.
@@ -111,6 +115,41 @@ int b2l_update(int nrows, int m, const double* x, const double* ax, int ldx,
                const int* pcols, int kp, const double* cp, double* xo, double* axo,
                int ldo, double* po, double* apo, int ldpo, int x_plus_p,
                void* stream);
+
+/*
+ * K1+K5b -- b2l_stencil7 fused with the Rayleigh-Ritz Gram blocks that
+ * involve A W (reference lobpcg.py:325 gram(w, aw), :327 gram(x, aw)):
+ *   out = A in  (as b2l_stencil7)   and
+ *   gram_out ((m + kw) x kw, row-major, device) = [X[:, :m] ; in[:, :kw]]^T out[:, :kw]
+ * X is an (n, ldx) block of the same grid rows.  A W is never re-read.
+ */
+int b2l_stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
+                      const double* halo, int has_lo, int has_hi, double scale,
+                      const double* x, int ldx, int m, int kw, double* gram_out,
+                      void* stream);
+
+/*
+ * F1 -- one fused pass of the LOBPCG iteration (lobpcg.py:520-540 for this
+ * iteration, then :419-467 and the non-AW Gram blocks of :299-340 for the
+ * next one):
+ *   P' = W Cw + P[:, pcols] Cp ; AP' likewise ; X' = X Cx + P' ; AX' likewise
+ *   W'[:, wpos[j]] = T (AX'[:, j] - (bdiag? bdiag*X' : X')[:, j] lam[j])
+ *   red_out = [ sum_r wf^2 (m) | sum_r AX'^2 (m, if want_ax_norms) |
+ *               G (a x b) ]      with a = 2m + kw_next, b = 3m + kw_next,
+ *   G = [X' W' P']^T [B X', B W', B P', AP']  -- only the upper triangles of
+ *   the three symmetric diagonal pairs and the pairs X'-W', X'-P', W'-P',
+ *   X'-AP', W'-AP', P'-AP' are defined.
+ * coef = [Cx (m x m) | Cw (kw x m) | Cp (kp x m)] row-major, device.
+ * x/ax/p/ap and xo/axo/po/apo are (n, ldx); w/aw (n, ldw); w_next (n, ldw_next).
+ * Outputs must not alias inputs.  m <= 64 and the Gram must fit one CTA.
+ */
+int b2l_lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
+                    const double* w, const double* aw, int ldw, int kw, const double* p,
+                    const double* ap, int kp, const int* pcols, const double* coef,
+                    double* xo, double* axo, double* po, double* apo, const double* lam,
+                    const double* bdiag, int tmode, double tinv, const double* tvec,
+                    const int* wpos, int kw_next, double* w_next, int ldw_next,
+                    int want_ax_norms, double* red_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -32,7 +32,8 @@ SIGNATURES = {
     "b2l_stencil7": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_void_p]),
     "b2l_gram": (C.c_int, [C.c_int, C.POINTER(b2l_block), C.c_int, C.POINTER(b2l_block),
-                           C.c_int, C.c_uint, C.c_void_p, C.c_void_p, C.c_void_p]),
+                           C.c_int, C.c_uint, C.c_void_p, C.c_char_p, C.c_void_p,
+                           C.c_void_p]),
     "b2l_residual": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
                                C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_void_p,
                                C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int,
@@ -43,6 +44,17 @@ SIGNATURES = {
                              C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                              C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                              C.c_void_p]),
+    "b2l_stencil7_gram": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.c_void_p, C.c_int, C.c_int, C.c_double,
+                                    C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                    C.c_void_p]),
+    "b2l_lobpcg_step": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                  C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                  C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_int, C.c_double, C.c_void_p,
+                                  C.c_void_p, C.c_int, C.c_void_p, C.c_int,
+                                  C.c_int, C.c_void_p, C.c_void_p]),
 }
 
 ABI_VERSION = 1

@@ -18,7 +18,8 @@ struct HostBlock {
   int ld, cols;
 };
 int gram(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr,
-         unsigned rw_mask, const double* d, double* out, cudaStream_t st);
+         unsigned rw_mask, const double* d, const unsigned char* pair_mode,
+         double* out, cudaStream_t st);
 int residual(int nrows, int m, const double* x, const double* ax, int ldx,
              const double* d, const double* lam, int tmode, double tinv,
              const double* tvec, const int* pos, int kw, double* w, int ldw,
@@ -29,6 +30,18 @@ int update(int nrows, int m, const double* x, const double* ax, int ldx,
            const int* pcols, int kp, const double* cp, double* xo, double* axo,
            int ldo, double* po, double* apo, int ldpo, int x_plus_p,
            cudaStream_t st);
+
+int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
+                  const double* halo, int has_lo, int has_hi, double scale,
+                  const double* x, int ldx, int m, int kw, double* gram_out,
+                  cudaStream_t st);
+int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
+                const double* w, const double* aw, int ldw, int kw, const double* p,
+                const double* ap, int kp, const int* pcols, const double* coef,
+                double* xo, double* axo, double* po, double* apo, const double* lam,
+                const double* d, int tmode, double tinv, const double* tvec,
+                const int* wpos, int kwn, double* wo, int ldwn, int want_ax,
+                double* red_out, cudaStream_t st);
 
 static thread_local std::string g_err;
 
@@ -140,13 +153,13 @@ int b2l_stencil7(const double* in, double* out, int nx, int ny, int nz, int ld,
 
 int b2l_gram(int nrows, const b2l_block* left, int nleft, const b2l_block* right,
              int nright, unsigned right_weighted_mask, const double* weight,
-             double* out, void* stream) {
+             const unsigned char* pair_mode, double* out, void* stream) {
   B2L_CHECK(left && right && out, -B2L_EINVAL, "gram: null argument");
   HostBlock L[8], R[8];
   B2L_CHECK(nleft <= 8 && nright <= 8, -B2L_EINVAL, "gram: too many blocks");
   for (int i = 0; i < nleft; ++i) L[i] = HostBlock{left[i].ptr, left[i].ld, left[i].cols};
   for (int i = 0; i < nright; ++i) R[i] = HostBlock{right[i].ptr, right[i].ld, right[i].cols};
-  return gram(nrows, L, nleft, R, nright, right_weighted_mask, weight, out,
+  return gram(nrows, L, nleft, R, nright, right_weighted_mask, weight, pair_mode, out,
               static_cast<cudaStream_t>(stream));
 }
 
@@ -166,6 +179,26 @@ int b2l_update(int nrows, int m, const double* x, const double* ax, int ldx,
                void* stream) {
   return update(nrows, m, x, ax, ldx, cx, w, aw, ldw, kw, cw, p, ap, ldp, pcols, kp, cp, xo,
                 axo, ldo, po, apo, ldpo, x_plus_p, static_cast<cudaStream_t>(stream));
+}
+
+int b2l_stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
+                      const double* halo, int has_lo, int has_hi, double scale,
+                      const double* x, int ldx, int m, int kw, double* gram_out,
+                      void* stream) {
+  return stencil7_gram(in, out, nx, ny, nz, ld, halo, has_lo, has_hi, scale, x, ldx, m, kw,
+                       gram_out, static_cast<cudaStream_t>(stream));
+}
+
+int b2l_lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
+                    const double* w, const double* aw, int ldw, int kw, const double* p,
+                    const double* ap, int kp, const int* pcols, const double* coef,
+                    double* xo, double* axo, double* po, double* apo, const double* lam,
+                    const double* bdiag, int tmode, double tinv, const double* tvec,
+                    const int* wpos, int kw_next, double* w_next, int ldw_next,
+                    int want_ax_norms, double* red_out, void* stream) {
+  return lobpcg_step(nrows, m, x, ax, ldx, w, aw, ldw, kw, p, ap, kp, pcols, coef, xo, axo, po,
+                     apo, lam, bdiag, tmode, tinv, tvec, wpos, kw_next, w_next, ldw_next,
+                     want_ax_norms, red_out, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -15,210 +15,208 @@
 // Every reduction is deterministic: CTA partials in a fixed row assignment,
 // then a fixed-order second stage over CTAs.
 #include "common.cuh"
+#include "gram_tile.cuh"
 
 namespace b2l {
 
 // =========================================================================
-// K5: multi-block Gram
+// K5: multi-block Gram on fp64 tensor cores (DMMA), TMA-staged row chunks
 // =========================================================================
 constexpr int GRAM_THREADS = 256;
 constexpr int GRAM_MAXU = 8;
 constexpr int GRAM_MAXL = 4;
 constexpr int GRAM_MAXR = 8;
+constexpr int GT_TI = 2;      // 8x8 tiles per warp tile block (rows)
+constexpr int GT_TJ = 4;      //                               (cols)
 
 struct GramArgs {
   int nrows;
-  int rc;      // rows per chunk
-  int nu;      // unique blocks staged per chunk
+  int rc;  // rows per chunk (power of 2, >= 4*rs)
+  int nu;
   const double* up[GRAM_MAXU];
   int uld[GRAM_MAXU];
-  int usld[GRAM_MAXU];   // smem row stride (multiple of 4)
-  int ubase[GRAM_MAXU];  // smem offset (doubles) of the block region
+  int ubase[GRAM_MAXU];  // offset (doubles) of block u inside a stage
+  int a, b;              // total left / right columns
   int nl, nr;
-  int lu[GRAM_MAXL], lvoff[GRAM_MAXL];  // unique id, padded column offset
-  int ru[GRAM_MAXR], rvoff[GRAM_MAXR];
-  unsigned rw_mask;  // right block j is weighted by d
+  int lu[GRAM_MAXL], lcum[GRAM_MAXL + 1];
+  int ru[GRAM_MAXR], rcum[GRAM_MAXR + 1];
+  unsigned rw_mask;
   const double* d;
-  int dbase;         // smem offset of the staged d chunk
+  int dbase;
   int stage_doubles;
-  int a_pad, b_pad;  // padded virtual sizes (multiples of 4)
-  int tiles_n;       // b_pad / 4
-  int ntiles;        // (a_pad/4) * tiles_n
-  int tset;          // tiles per CTA (blockIdx.y selects the set)
-  int G;             // row groups
-  double* partial;   // [gridDim.x][a_pad * b_pad]
+  int nst;
+  int NI, NJ, tsI, tsJ;  // 8x8 tile grid, TIxTJ tile-block grid
+  int ts_per_cta, rs;    // tile blocks per CTA, row slices per chunk
+  unsigned tmask[32];    // needed-tile bitmap, bit (i*NJ + j)
+  double* partial;       // [gridDim.x][a*b]
 };
 
-__device__ __forceinline__ void gram_load_chunk(const GramArgs& A, double* st,
-                                                int r0) {
-  const int tid = threadIdx.x;
+
+__device__ __forceinline__ void gram_issue(const GramArgs& A, double* st, uint64_t* bar, int c) {
+  const int r0 = c * A.rc;
   const int nvalid = min(A.rc, A.nrows - r0);
-  for (int u = 0; u < A.nu; ++u) {
-    const int h = A.uld[u] >> 1;  // double2 per row
-    const int sld = A.usld[u];
-    double* dst = st + A.ubase[u];
-    const double* src = A.up[u] + (size_t)r0 * A.uld[u];
-    const int total = A.rc * h;
-    for (int f = tid; f < total; f += blockDim.x) {
-      const int row = f / h;
-      const int c2 = f - row * h;
-      double* dptr = dst + row * sld + 2 * c2;
-      if (row < nvalid)
-        cp_async16(dptr, src + (size_t)row * A.uld[u] + 2 * c2);
-      else
-        *reinterpret_cast<double2*>(dptr) = make_double2(0.0, 0.0);
+  const int nv4 = (nvalid + 3) & ~3;
+  // zero the rows that complete the last 4-row group of a tail chunk
+  for (int u = 0; u < A.nu; ++u)
+    for (int e = nvalid * A.uld[u]; e < nv4 * A.uld[u]; ++e) st[A.ubase[u] + e] = 0.0;
+  uint32_t tx = 0;
+  for (int u = 0; u < A.nu; ++u) tx += (uint32_t)nvalid * A.uld[u] * 8u;
+  const bool d_bulk = A.d && (nvalid % 2 == 0);
+  if (A.d) {
+    if (d_bulk) {
+      tx += (uint32_t)nvalid * 8u;
+      for (int e = nvalid; e < nv4; ++e) st[A.dbase + e] = 0.0;
+    } else {
+      for (int e = 0; e < nv4; ++e) st[A.dbase + e] = e < nvalid ? A.d[r0 + e] : 0.0;
     }
   }
-  if (A.d) {
-    for (int row = tid; row < A.rc; row += blockDim.x)
-      st[A.dbase + row] = row < nvalid ? A.d[r0 + row] : 0.0;
-  }
+  fence_async_smem();
+  mbar_expect_tx(bar, tx);
+  for (int u = 0; u < A.nu; ++u)
+    bulk_load(st + A.ubase[u], A.up[u] + (size_t)r0 * A.uld[u],
+              (uint32_t)nvalid * A.uld[u] * 8u, bar);
+  if (d_bulk) bulk_load(st + A.dbase, A.d + r0, (uint32_t)nvalid * 8u, bar);
 }
 
 __global__ void __launch_bounds__(GRAM_THREADS) gram_kernel(GramArgs A) {
-  extern __shared__ __align__(128) double gsm[];
-  double* st0 = gsm;
-  double* st1 = gsm + A.stage_doubles;
+  extern __shared__ __align__(128) unsigned char gsm_raw[];
+  double* stages = reinterpret_cast<double*>(gsm_raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(gsm_raw + (size_t)A.nst * A.stage_doubles * 8);
   const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
 
-  // zero both stages once (pad columns stay zero forever)
-  for (int i = tid; i < 2 * A.stage_doubles; i += blockDim.x) gsm[i] = 0.0;
-  __syncthreads();
+  const int tsl = warp % A.ts_per_cta;
+  const int slice = warp / A.ts_per_cta;
+  const int ts = blockIdx.y * A.ts_per_cta + tsl;
+  const bool wactive = slice < A.rs && ts < A.tsI * A.tsJ;
+  const int ti0 = wactive ? (ts / A.tsJ) * GT_TI : 0;
+  const int tj0 = wactive ? (ts % A.tsJ) * GT_TJ : 0;
 
-  const int tl = tid % A.tset;
-  const int g = tid / A.tset;
-  const int t = blockIdx.y * A.tset + tl;
-  const bool active = (g < A.G) && (tl < A.tset) && (t < A.ntiles);
-
-  int loff = 0, lsld = 4, roff = 0, rsld = 4;
-  bool wgt = false;
-  int i0 = 0, j0 = 0;
-  if (active) {
-    i0 = 4 * (t / A.tiles_n);
-    j0 = 4 * (t % A.tiles_n);
-    int l = 0;
-    while (l + 1 < A.nl && A.lvoff[l + 1] <= i0) ++l;
-    loff = A.ubase[A.lu[l]] + (i0 - A.lvoff[l]);
-    lsld = A.usld[A.lu[l]];
-    int r = 0;
-    while (r + 1 < A.nr && A.rvoff[r + 1] <= j0) ++r;
-    roff = A.ubase[A.ru[r]] + (j0 - A.rvoff[r]);
-    rsld = A.usld[A.ru[r]];
-    wgt = (A.rw_mask >> r) & 1u;
+  LaneCol la[GT_TI], lb[GT_TJ];
+#pragma unroll
+  for (int i = 0; i < GT_TI; ++i) {
+    const int ci = 8 * (ti0 + i) + (lane >> 2);
+    la[i] = LaneCol{0, 0, false, false};
+    if (ci < A.a) {
+      int l = 0;
+      while (l + 1 < A.nl && A.lcum[l + 1] <= ci) ++l;
+      la[i] = LaneCol{A.ubase[A.lu[l]] + (ci - A.lcum[l]), A.uld[A.lu[l]], true, false};
+    }
   }
-
-  double acc[4][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int j = 0; j < GT_TJ; ++j) {
+    const int cj = 8 * (tj0 + j) + (lane >> 2);
+    lb[j] = LaneCol{0, 0, false, false};
+    if (cj < A.b) {
+      int r = 0;
+      while (r + 1 < A.nr && A.rcum[r + 1] <= cj) ++r;
+      lb[j] = LaneCol{A.ubase[A.ru[r]] + (cj - A.rcum[r]), A.uld[A.ru[r]], true,
+                      ((A.rw_mask >> r) & 1u) != 0};
+    }
+  }
+  unsigned mask = 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-
-  const int nchunks = (A.nrows + A.rc - 1) / A.rc;
-  int c = blockIdx.x;
-  if (c < nchunks) gram_load_chunk(A, st0, c * A.rc);
-  cp_async_commit();
-  double* cur = st0;
-  double* nxt = st1;
-  for (; c < nchunks; c += gridDim.x) {
-    const int cn = c + gridDim.x;
-    if (cn < nchunks) gram_load_chunk(A, nxt, cn * A.rc);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    if (active) {
-      const double* Ls = cur + loff;
-      const double* Rs = cur + roff;
-      const double* ds = cur + A.dbase;
-      for (int r = g; r < A.rc; r += A.G) {
-        const double2 a01 = *reinterpret_cast<const double2*>(Ls + r * lsld);
-        const double2 a23 = *reinterpret_cast<const double2*>(Ls + r * lsld + 2);
-        double2 b01 = *reinterpret_cast<const double2*>(Rs + r * rsld);
-        double2 b23 = *reinterpret_cast<const double2*>(Rs + r * rsld + 2);
-        if (wgt) {
-          const double w = ds[r];
-          b01.x = __dmul_rn(w, b01.x);
-          b01.y = __dmul_rn(w, b01.y);
-          b23.x = __dmul_rn(w, b23.x);
-          b23.y = __dmul_rn(w, b23.y);
-        }
-        const double a[4] = {a01.x, a01.y, a23.x, a23.y};
-        const double b[4] = {b01.x, b01.y, b23.x, b23.y};
+  for (int i = 0; i < GT_TI; ++i)
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    for (int j = 0; j < GT_TJ; ++j) {
+      const int ti = ti0 + i, tj = tj0 + j;
+      if (wactive && ti < A.NI && tj < A.NJ) {
+        const int t = ti * A.NJ + tj;
+        if ((A.tmask[t >> 5] >> (t & 31)) & 1u) mask |= 1u << (i * GT_TJ + j);
       }
     }
+
+  WarpGram<GT_TI, GT_TJ> g;
+  g.zero();
+
+  if (tid == 0) {
+    for (int s = 0; s < A.nst; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int nchunks = (A.nrows + A.rc - 1) / A.rc;
+  if (tid == 0) {
+    for (int s = 0; s < A.nst; ++s) {
+      const int c = blockIdx.x + s * gridDim.x;
+      if (c < nchunks) gram_issue(A, stages + (size_t)s * A.stage_doubles, &bar[s], c);
+    }
+  }
+  const int rows_per_slice = A.rc / A.rs;
+  int it = 0;
+  for (int c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+    const int s = it % A.nst;
+    double* st = stages + (size_t)s * A.stage_doubles;
+    mbar_wait(&bar[s], (it / A.nst) & 1);
+    const int nvalid = min(A.rc, A.nrows - c * A.rc);
+    const int nv4 = (nvalid + 3) & ~3;
+    if (wactive && mask) {
+      const int lo = slice * rows_per_slice;
+      const int hi = min(lo + rows_per_slice, nv4);
+      g.run(st, la, lb, A.d ? st + A.dbase : nullptr, lo, hi, mask, DenseRows());
+    }
     __syncthreads();
-    double* tmp = cur;
-    cur = nxt;
-    nxt = tmp;
+    if (tid == 0) {
+      const int cn = c + A.nst * gridDim.x;
+      if (cn < nchunks) gram_issue(A, st, &bar[s], cn);
+    }
   }
-  cp_async_wait<0>();
   __syncthreads();
 
-  // reduce the G row groups in fixed order (reuse stage memory)
-  double* red = gsm;
-  if (active && g > 0) {
+  // fixed-order reduction of the row slices, then the CTA partial
+  double* red = stages;
+  const int nt = GT_TI * GT_TJ;
+  if (wactive && slice > 0) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < GT_TI; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) red[((g - 1) * A.tset + tl) * 16 + i * 4 + j] = acc[i][j];
+      for (int j = 0; j < GT_TJ; ++j) {
+        const size_t o = ((((size_t)(slice - 1) * A.ts_per_cta + tsl) * nt + i * GT_TJ + j) * 32 + lane) * 2;
+        red[o] = g.acc[i][j][0];
+        red[o + 1] = g.acc[i][j][1];
+      }
   }
   __syncthreads();
-  if (active && g == 0) {
-    for (int gg = 1; gg < A.G; ++gg)
+  if (wactive && slice == 0) {
+    double* out = A.partial + (size_t)blockIdx.x * A.a * A.b;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < GT_TI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] += red[((gg - 1) * A.tset + tl) * 16 + i * 4 + j];
-    double* out = A.partial + (size_t)blockIdx.x * A.a_pad * A.b_pad;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) out[(i0 + i) * A.b_pad + j0 + j] = acc[i][j];
+      for (int j = 0; j < GT_TJ; ++j) {
+        double v0 = g.acc[i][j][0], v1 = g.acc[i][j][1];
+        for (int sl = 1; sl < A.rs; ++sl) {
+          const size_t o = ((((size_t)(sl - 1) * A.ts_per_cta + tsl) * nt + i * GT_TJ + j) * 32 + lane) * 2;
+          v0 += red[o];
+          v1 += red[o + 1];
+        }
+        const int row = 8 * (ti0 + i) + (lane >> 2);
+        const int col = 8 * (tj0 + j) + 2 * (lane & 3);
+        if (row < A.a) {
+          if (col < A.b) out[(size_t)row * A.b + col] = v0;
+          if (col + 1 < A.b) out[(size_t)row * A.b + col + 1] = v1;
+        }
+      }
   }
 }
 
-struct GramMap {
-  int nl, nr;
-  int lcols[GRAM_MAXL], lvoff[GRAM_MAXL];
-  int rcols[GRAM_MAXR], rvoff[GRAM_MAXR];
-  int a, b, a_pad, b_pad;
-};
-
-// second stage: fixed-order sum over CTA partials, padded -> compact (a x b)
-__global__ void gram_reduce_kernel(const double* partial, int nparts, GramMap M,
-                                   double* out) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= M.a * M.b) return;
-  int i = e / M.b, j = e - (e / M.b) * M.b;
-  int pi = 0, pj = 0;
-  for (int l = 0, cum = 0; l < M.nl; cum += M.lcols[l], ++l)
-    if (i >= cum && i < cum + M.lcols[l]) pi = M.lvoff[l] + (i - cum);
-  for (int r = 0, cum = 0; r < M.nr; cum += M.rcols[r], ++r)
-    if (j >= cum && j < cum + M.rcols[r]) pj = M.rvoff[r] + (j - cum);
-  const size_t stride = (size_t)M.a_pad * M.b_pad;
-  const size_t idx = (size_t)pi * M.b_pad + pj;
-  double s = 0.0;
-  for (int c = 0; c < nparts; ++c) s += partial[c * stride + idx];
-  out[e] = s;
-}
+__global__ void sum_parts_kernel(const double* partial, int nparts, int len, double* out);
 
 struct HostBlock {
   const double* p;
   int ld, cols;
 };
 
+// pair_mode[l*nr + r]: 0 = block pair not needed, 1 = full, 2 = upper
+// triangle only (a symmetric diagonal pair).  nullptr = all full.
 int gram(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr,
-         unsigned rw_mask, const double* d, double* out, cudaStream_t st) {
+         unsigned rw_mask, const double* d, const unsigned char* pair_mode,
+         double* out, cudaStream_t st) {
   B2L_CHECK(nl >= 1 && nl <= GRAM_MAXL && nr >= 1 && nr <= GRAM_MAXR, -B2L_EINVAL,
             "gram: 1..4 left and 1..8 right blocks");
   B2L_CHECK(nrows >= 0, -B2L_EINVAL, "gram: negative row count");
+  B2L_CHECK(!rw_mask || d != nullptr, -B2L_EINVAL, "gram: weight mask without weights");
   GramArgs A{};
-  GramMap M{};
   A.nrows = nrows;
-  A.nu = 0;
   A.nl = nl;
   A.nr = nr;
   auto uid = [&](const HostBlock& b) -> int {
@@ -227,11 +225,9 @@ int gram(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr,
     if (A.nu >= GRAM_MAXU) return -1;
     A.up[A.nu] = b.p;
     A.uld[A.nu] = b.ld;
-    A.usld[A.nu] = (b.ld + 3) & ~3;
     return A.nu++;
   };
-  int voff = 0;
-  M.nl = nl;
+  A.lcum[0] = 0;
   for (int l = 0; l < nl; ++l) {
     B2L_CHECK(L[l].ld >= 2 && (L[l].ld & 1) == 0 && L[l].cols <= L[l].ld && L[l].cols >= 0,
               -B2L_EINVAL, "gram: left block needs even ld >= cols");
@@ -240,15 +236,9 @@ int gram(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr,
     const int u = uid(L[l]);
     B2L_CHECK(u >= 0, -B2L_EINVAL, "gram: too many distinct blocks");
     A.lu[l] = u;
-    A.lvoff[l] = voff;
-    M.lvoff[l] = voff;
-    M.lcols[l] = L[l].cols;
-    M.a += L[l].cols;
-    voff += A.usld[u];
+    A.lcum[l + 1] = A.lcum[l] + L[l].cols;
   }
-  A.a_pad = voff;
-  voff = 0;
-  M.nr = nr;
+  A.rcum[0] = 0;
   for (int r = 0; r < nr; ++r) {
     B2L_CHECK(R[r].ld >= 2 && (R[r].ld & 1) == 0 && R[r].cols <= R[r].ld && R[r].cols >= 0,
               -B2L_EINVAL, "gram: right block needs even ld >= cols");
@@ -257,61 +247,98 @@ int gram(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr,
     const int u = uid(R[r]);
     B2L_CHECK(u >= 0, -B2L_EINVAL, "gram: too many distinct blocks");
     A.ru[r] = u;
-    A.rvoff[r] = voff;
-    M.rvoff[r] = voff;
-    M.rcols[r] = R[r].cols;
-    M.b += R[r].cols;
-    voff += A.usld[u];
+    A.rcum[r + 1] = A.rcum[r] + R[r].cols;
   }
-  A.b_pad = voff;
-  M.a_pad = A.a_pad;
-  M.b_pad = A.b_pad;
+  A.a = A.lcum[nl];
+  A.b = A.rcum[nr];
   A.rw_mask = rw_mask;
   A.d = rw_mask ? d : nullptr;
-  B2L_CHECK(!rw_mask || d != nullptr, -B2L_EINVAL, "gram: weight mask without weights");
-  if (M.a * M.b == 0) return 0;
-
-  int width = 0;
-  for (int u = 0; u < A.nu; ++u) width += A.usld[u];
-  A.rc = width <= 96 ? 64 : (width <= 192 ? 32 : 16);
+  if (A.a * A.b == 0) return 0;
+  A.NI = (A.a + 7) / 8;
+  A.NJ = (A.b + 7) / 8;
+  B2L_CHECK(A.NI * A.NJ <= 32 * 32, -B2L_EINVAL, "gram: output too large (max 1024 8x8 tiles)");
+  // needed tiles from the block-pair modes
+  for (int ti = 0; ti < A.NI; ++ti)
+    for (int tj = 0; tj < A.NJ; ++tj) {
+      bool need = false;
+      for (int l = 0; l < nl && !need; ++l)
+        for (int r = 0; r < nr && !need; ++r) {
+          const int mode = pair_mode ? pair_mode[l * nr + r] : 1;
+          if (!mode) continue;
+          const int i0 = max(8 * ti, A.lcum[l]), i1 = min(8 * ti + 8, A.lcum[l + 1]);
+          const int j0 = max(8 * tj, A.rcum[r]), j1 = min(8 * tj + 8, A.rcum[r + 1]);
+          if (i0 >= i1 || j0 >= j1) continue;
+          if (mode == 2) {
+            // upper triangle of the pair: local row <= local col somewhere
+            const int li0 = i0 - A.lcum[l];
+            const int lj1 = j1 - A.rcum[r];
+            if (li0 > lj1 - 1) continue;
+          }
+          need = true;
+        }
+      if (need) {
+        const int t = ti * A.NJ + tj;
+        A.tmask[t >> 5] |= 1u << (t & 31);
+      }
+    }
+  A.tsI = (A.NI + GT_TI - 1) / GT_TI;
+  A.tsJ = (A.NJ + GT_TJ - 1) / GT_TJ;
+  const int TS = A.tsI * A.tsJ;
+  const int warps = GRAM_THREADS / 32;
+  if (TS <= warps) {
+    A.ts_per_cta = TS;
+    A.rs = 1;
+    while (A.rs * 2 * TS <= warps) A.rs *= 2;
+  } else {
+    A.ts_per_cta = warps;
+    A.rs = 1;
+  }
+  const int gy = (TS + A.ts_per_cta - 1) / A.ts_per_cta;
+  // rows per chunk: the largest power of two whose stage stays <= ~40 KB
+  int width = A.d ? 1 : 0;
+  for (int u = 0; u < A.nu; ++u) width += A.uld[u];
+  A.rc = 256;
+  while (A.rc > 16 && (size_t)A.rc * width * 8 > 40 * 1024) A.rc >>= 1;
+  while (A.rs > 1 && A.rc / A.rs < 4) A.rs >>= 1;
   int off = 0;
   for (int u = 0; u < A.nu; ++u) {
     A.ubase[u] = off;
-    off += A.rc * A.usld[u];
+    off += A.rc * A.uld[u];
   }
   A.dbase = off;
-  off += A.rc;
+  off += A.d ? A.rc : 0;
   A.stage_doubles = (off + 15) & ~15;
-  A.tiles_n = A.b_pad / 4;
-  A.ntiles = (A.a_pad / 4) * A.tiles_n;
-  A.tset = A.ntiles < GRAM_THREADS ? A.ntiles : GRAM_THREADS;
-  A.G = GRAM_THREADS / A.tset;
-  if (A.G > A.rc) A.G = A.rc;
-  const int nsets = (A.ntiles + A.tset - 1) / A.tset;
-
-  const int nchunks = nrows > 0 ? (nrows + A.rc - 1) / A.rc : 0;
-  int gx = 2 * sm_count();
+  const size_t stage_bytes = (size_t)A.stage_doubles * 8;
+  A.nst = stage_bytes * 3 <= 150 * 1024 ? 3 : 2;
+  B2L_CHECK(stage_bytes * A.nst <= 200 * 1024, -B2L_EINVAL, "gram: blocks too wide");
+  const size_t red_bytes = (size_t)(A.rs > 1 ? A.rs - 1 : 0) * A.ts_per_cta * GT_TI * GT_TJ * 64 * 8;
+  size_t smem = stage_bytes * A.nst;
+  if (red_bytes > smem) smem = red_bytes;
+  smem += 64;  // barriers
+  const int nchunks = (nrows + A.rc - 1) / A.rc;
+  int gx = (2 * sm_count() + gy - 1) / gy;
   if (gx > nchunks) gx = nchunks;
   if (gx < 1) gx = 1;
-  size_t smem = (size_t)2 * A.stage_doubles * sizeof(double);
-  const size_t red_need = (size_t)(A.G > 1 ? A.G - 1 : 0) * A.tset * 16 * sizeof(double);
-  if (red_need > smem) smem = red_need;
-  B2L_CHECK(smem <= 227 * 1024, -B2L_EINVAL, "gram: blocks too wide for shared memory");
   int werr = 0;
-  double* part = static_cast<double*>(
-      workspace((size_t)gx * A.a_pad * A.b_pad * sizeof(double), &werr));
+  double* part = static_cast<double*>(workspace((size_t)gx * A.a * A.b * sizeof(double), &werr));
   if (werr) return werr;
   A.partial = part;
   if (nrows == 0) {
-    B2L_CUDA(cudaMemsetAsync(part, 0, (size_t)A.a_pad * A.b_pad * sizeof(double), st));
-  } else {
-    B2L_CUDA(cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    gram_kernel<<<dim3(gx, nsets), GRAM_THREADS, smem, st>>>(A);
-    B2L_CUDA(cudaGetLastError());
+    B2L_CUDA(cudaMemsetAsync(out, 0, (size_t)A.a * A.b * sizeof(double), st));
+    return 0;
   }
-  const int tot = M.a * M.b;
-  gram_reduce_kernel<<<(tot + 255) / 256, 256, 0, st>>>(part, nrows == 0 ? 1 : gx, M, out);
+  // the barrier block sits right after the stages / reduction area
+  // (kernel indexes it from nst*stage_doubles; keep the reduction inside)
+  if (red_bytes > stage_bytes * A.nst) {
+    A.stage_doubles = (int)((red_bytes / 8 + A.nst - 1) / A.nst + 15) & ~15;
+    smem = (size_t)A.stage_doubles * 8 * A.nst + 64;
+  }
+  B2L_CUDA(cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  gram_kernel<<<dim3(gx, gy), GRAM_THREADS, smem, st>>>(A);
+  B2L_CUDA(cudaGetLastError());
+  const int tot = A.a * A.b;
+  sum_parts_kernel<<<(tot + 255) / 256, 256, 0, st>>>(part, gx, tot, out);
   B2L_CUDA(cudaGetLastError());
   return 0;
 }

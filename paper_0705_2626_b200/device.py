@@ -65,16 +65,52 @@ def stencil7(x: torch.Tensor, out: torch.Tensor, nx: int, ny: int, nz: int,
     LAUNCHES[0] += 1
 
 
+def stencil7_gram(x: torch.Tensor, out: torch.Tensor, nx: int, ny: int, nz: int,
+                  scale: float, xb: torch.Tensor, m: int, kw: int, gram_out: torch.Tensor,
+                  halo: torch.Tensor | None = None, has_lo: bool = False,
+                  has_hi: bool = False) -> None:
+    """out = scale*L7(x); gram_out = [xb[:, :m] ; x[:, :kw]]^T out[:, :kw]."""
+    lib = _lib.load()
+    ld = x.stride(0)
+    if out.stride(0) != ld:
+        raise ValueError("stencil7_gram: in/out leading dimensions differ")
+    _lib.check(lib.b2l_stencil7_gram(
+        x.data_ptr(), out.data_ptr(), nx, ny, nz, ld,
+        halo.data_ptr() if halo is not None else None, int(has_lo), int(has_hi),
+        float(scale), xb.data_ptr(), xb.stride(0), int(m), int(kw), gram_out.data_ptr(),
+        stream_ptr(x.device)), "b2l_stencil7_gram")
+    LAUNCHES[0] += 2
+
+
+def lobpcg_step(nrows, m, x, ax, w, aw, kw, p, ap, kp, pcols, coef, xo, axo, po, apo,
+                lam, bdiag, tmode, tinv, tvec, wpos, kwn, wo, want_ax, red_out) -> None:
+    """F1: fused update + next residual + next non-AW Gram blocks."""
+    lib = _lib.load()
+
+    def ptr(t):
+        return t.data_ptr() if t is not None else None
+
+    _lib.check(lib.b2l_lobpcg_step(
+        nrows, m, ptr(x), ptr(ax), x.stride(0), ptr(w), ptr(aw),
+        w.stride(0) if w is not None else 0, int(kw), ptr(p), ptr(ap), int(kp), ptr(pcols),
+        ptr(coef), ptr(xo), ptr(axo), ptr(po), ptr(apo), ptr(lam), ptr(bdiag), int(tmode),
+        float(tinv), ptr(tvec), ptr(wpos), int(kwn), ptr(wo),
+        wo.stride(0) if wo is not None else 0, int(want_ax), ptr(red_out),
+        stream_ptr(x.device)), "b2l_lobpcg_step")
+    LAUNCHES[0] += 2
+
+
 def _blk(t: torch.Tensor, cols: int) -> _lib.b2l_block:
     return _lib.b2l_block(t.data_ptr(), t.stride(0), cols)
 
 
 def gram(nrows: int, left, right, weighted_mask: int = 0,
          weight: torch.Tensor | None = None, out: torch.Tensor | None = None,
-         device=None) -> torch.Tensor:
+         device=None, pair_mode=None) -> torch.Tensor:
     """Device (sum left cols, sum right cols) matrix [L]^T diag(w)^? [R] (K5).
 
-    left/right: sequences of (tensor (n, ld), cols).
+    left/right: sequences of (tensor (n, ld), cols).  pair_mode: optional
+    (len(left), len(right)) array of 0 (skip) / 1 (full) / 2 (upper only).
     """
     lib = _lib.load()
     a = sum(c for _, c in left)
@@ -84,8 +120,13 @@ def gram(nrows: int, left, right, weighted_mask: int = 0,
         out = torch.empty((a, b), dtype=F64, device=dev)
     L = (_lib.b2l_block * len(left))(*[_blk(t, c) for t, c in left])
     R = (_lib.b2l_block * len(right))(*[_blk(t, c) for t, c in right])
+    pm = None
+    if pair_mode is not None:
+        pm = np.ascontiguousarray(pair_mode, dtype=np.uint8).tobytes()
+        if len(pm) != len(left) * len(right):
+            raise ValueError("pair_mode must be len(left) x len(right)")
     _lib.check(lib.b2l_gram(nrows, L, len(left), R, len(right), int(weighted_mask),
-                            weight.data_ptr() if weight is not None else None,
+                            weight.data_ptr() if weight is not None else None, pm,
                             out.data_ptr(), stream_ptr(dev)), "b2l_gram")
     LAUNCHES[0] += 2
     return out

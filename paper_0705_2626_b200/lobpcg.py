@@ -149,6 +149,21 @@ class _Failure(Exception):
     pass
 
 
+# Gram block-pair modes (include/b200lobpcg.h): only what the host reads.
+_UPPER = np.array([[2]], dtype=np.uint8)
+# L = [X, W, P], R = [X, W, P, AW, AP]  (P^T AW is never used)
+_MODES_P = np.array([[2, 1, 1, 1, 1],
+                     [0, 2, 1, 1, 1],
+                     [0, 0, 2, 0, 1]], dtype=np.uint8)
+# L = [X, W], R = [X, W, AW]
+_MODES_NOP = np.array([[2, 1, 1],
+                       [0, 2, 1]], dtype=np.uint8)
+
+
+def _mirror_upper(g):
+    return np.triu(g) + np.triu(g, 1).T
+
+
 class LOBPCGRun:
     """One LOBPCG solve on the device, stepped iteration by iteration.
 
@@ -249,9 +264,10 @@ class LOBPCGRun:
         return ((1 << nblocks) - 1) if self.bdiag is not None else 0
 
     def _gram_xx(self):
+        """X^T B X (upper triangle computed, mirrored on the host)."""
         g = _timed("gram_drift", lambda: dv.gram(self.n, [(self.X, self.m)], [(self.X, self.m)],
-                                          self._wmask(1), self.bdiag))
-        return dv.to_host(g)
+                                                 self._wmask(1), self.bdiag, pair_mode=_UPPER))
+        return _mirror_upper(dv.to_host(g))
 
     def _apply_a(self, src, dst, k):
         """dst[:, :k] = A src[:, :k] for (n, ld) blocks (K1 when fused)."""
@@ -274,7 +290,8 @@ class LOBPCGRun:
         """_refresh_ritz (lobpcg.py:280-296) from the raw Gram X^T B X."""
         _, minv = scaled_cholesky(gxx)             # NotSPD propagates
         self._rotate_x(minv)
-        gxa = dv.to_host(dv.gram(self.n, [(self.X, self.m)], [(self.AX, self.m)]))
+        gxa = dv.to_host(dv.gram(self.n, [(self.X, self.m)], [(self.AX, self.m)],
+                                 pair_mode=_UPPER))
         lam, q = sym_eig(gxa)
         self._rotate_x(q)
         self.lam = lam
@@ -291,7 +308,7 @@ class LOBPCGRun:
         dv.update(n, m, self.X, None, Md, self.X2, None)
         self.X, self.X2 = self.X2, self.X
         self._apply_a(self.X, self.AX, m)             # lobpcg.py:403
-        gxa = dv.to_host(dv.gram(n, [(self.X, m)], [(self.AX, m)]))
+        gxa = dv.to_host(dv.gram(n, [(self.X, m)], [(self.AX, m)], pair_mode=_UPPER))
         lam, q = sym_eig(gxa)                          # lobpcg.py:404
         self._rotate_x(q)
         self.lam = lam
@@ -374,7 +391,9 @@ class LOBPCGRun:
             R = [(self.X, m), (W, kst)] + ([(self.P, m)] if hp else []) + [(AW, kst)] + \
                 ([(self.AP, m)] if hp else [])
             nb = 3 if hp else 2
-            G = dv.to_host(_timed("gram", lambda: dv.gram(n, L, R, self._wmask(nb), self.bdiag)))
+            mode = _MODES_P if hp else _MODES_NOP
+            G = dv.to_host(_timed("gram", lambda: dv.gram(n, L, R, self._wmask(nb), self.bdiag,
+                                                          pair_mode=mode)))
             self._rayleigh_ritz(G, J, sel, kst, W, AW)
         except _Failure as f:
             self.failure = str(f)

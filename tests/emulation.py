@@ -35,7 +35,7 @@ def stencil7(x, out, nx, ny, nz, scale, halo=None, has_lo=False, has_hi=False):
     out.copy_(torch.from_numpy(y[plane:plane + nz * plane]))
 
 
-def gram(nrows, left, right, weighted_mask=0, weight=None, out=None, device=None):
+def gram(nrows, left, right, weighted_mask=0, weight=None, out=None, device=None, pair_mode=None):
     L = np.hstack([_np(t)[:nrows, :c] for t, c in left])
     Rs = []
     for j, (t, c) in enumerate(right):

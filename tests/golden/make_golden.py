@@ -95,7 +95,10 @@ def fast():
     # scaled by one ulp (1 + 2^-52).  Trajectories of degenerate clusters are
     # chaotic; a GPU run is held to this band (plus 1e-8 relative).
     perts = []
-    for s1 in (1.0 + 2.0 ** -52, 1.0 - 2.0 ** -53, 1.0 + 2.0 ** -51):
+    iters = []
+    locks = []
+    for s1 in (1.0 + 2.0 ** -52, 1.0 - 2.0 ** -53, 1.0 + 2.0 ** -51, 1.0 - 2.0 ** -52,
+               1.0 + 3 * 2.0 ** -52, 1.0 - 3 * 2.0 ** -53):
         Lp = laplacian3d((20, 20, 20))
         ap = MatrixFreeOperator(8000, lambda v, s1=s1: s1 * Lp(v), spd=True,
                                 diag=np.full(8000, 6.0 * s1))
@@ -104,10 +107,13 @@ def fast():
         pr = record(rp, 10)
         print("perturbed", s1, rp.iterations_used, list(rp.lock_iterations))
         perts.append(pr["hist_ritz"])
+        iters.append(rp.iterations_used)
+        locks.append(rp.lock_iterations)
     nmin = min(len(p) for p in perts)
     np.savez_compressed(OUT / "golden_20cubed_m10_jacobi_seed2.npz",
                         csv_ritz=ritz, csv_resid=resid, csv_active=active,
-                        pert_ritz=np.stack([p[:nmin] for p in perts]), **r)
+                        pert_ritz=np.stack([p[:nmin] for p in perts]),
+                        pert_iterations=np.array(iters), pert_locks=np.array(locks), **r)
 
     # 2. stencil known answers (operators.py:184-196), odd shapes, k=1..5.
     st = {}

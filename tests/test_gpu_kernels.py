@@ -110,12 +110,27 @@ def test_gram_multiblock(dev, n, cols):
     R = L + [(tAW, cols[1]), (tAP, cols[2])]
     for mask, wt in ((0, None), (0b111, td)):
         G = dv.gram(n, L, R, mask, wt).cpu().numpy()
+        Gs = dv.gram(n, L, R, mask, wt, pair_mode=np.array([[2, 1, 1, 1, 1], [0, 2, 1, 1, 1], [0, 0, 2, 0, 1]])).cpu().numpy()
         Lh = np.hstack([X, W, P])
         Rb = np.hstack([X, W, P]) * (d[:, None] if mask else 1.0)
         Rh = np.hstack([Rb, AW, AP])
         ref = Lh.T @ Rh
         scale = np.abs(Lh).T @ np.abs(Rh)
         assert np.all(np.abs(G - ref) <= 1e-13 * scale + 1e-300)
+        # pair modes: upper triangles of the symmetric pairs + the used blocks
+        lc = np.cumsum((0,) + tuple(cols))
+        rc = np.cumsum((0,) + tuple(cols) + (cols[1], cols[2]))
+        modes = [[2, 1, 1, 1, 1], [0, 2, 1, 1, 1], [0, 0, 2, 0, 1]]
+        for li in range(3):
+            for ri in range(5):
+                blk_g = Gs[lc[li]:lc[li + 1], rc[ri]:rc[ri + 1]]
+                blk_r = ref[lc[li]:lc[li + 1], rc[ri]:rc[ri + 1]]
+                blk_s = scale[lc[li]:lc[li + 1], rc[ri]:rc[ri + 1]]
+                if modes[li][ri] == 1:
+                    assert np.all(np.abs(blk_g - blk_r) <= 1e-13 * blk_s + 1e-300)
+                elif modes[li][ri] == 2:
+                    iu = np.triu_indices(blk_r.shape[0])
+                    assert np.all(np.abs(blk_g[iu] - blk_r[iu]) <= 1e-13 * blk_s[iu] + 1e-300)
 
 
 def test_gram_is_deterministic(dev):
@@ -187,3 +202,92 @@ def test_update_kernel(dev, m, kw, kp):
         np.testing.assert_allclose(got[:, :m], ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
         if got.shape[1] > m:
             assert np.all(got[:, m:] == 0.0)
+
+
+@pytest.mark.parametrize("dims,m,kw", [((32, 32, 32), 4, 4), ((40, 33, 17), 10, 7), ((64, 64, 64), 16, 16),
+                                       ((20, 21, 22), 7, 7), ((5, 30, 3), 3, 1), ((24, 24, 24), 10, 10)])
+def test_stencil7_gram(dev, dims, m, kw):
+    from paper_0705_2626_b200 import device as dv
+
+    n = int(np.prod(dims))
+    r = rng(n + m)
+    W = r.uniform(-1, 1, (n, kw))
+    X = r.uniform(-1, 1, (n, m))
+    s = float((dims[0] + 1) ** 2)
+    tW, tX = blk(W, dev), blk(X, dev)
+    out = torch.full_like(tW, np.nan)
+    G = torch.zeros((m + kw, kw), dtype=torch.float64, device=dev)
+    dv.stencil7_gram(tW, out, *dims, s, tX, m, kw, G)
+    AW = np.ascontiguousarray(orc.stencil7(W, *dims, s))
+    assert np.array_equal(out[:, :kw].cpu().numpy(), AW)
+    L = np.hstack([X, W])
+    ref = L.T @ AW
+    scale = np.abs(L).T @ np.abs(AW)
+    assert np.all(np.abs(G.cpu().numpy() - ref) <= 1e-13 * scale)
+
+
+@pytest.mark.parametrize("n,m,kw,kp,kwn,useb,tmode", [
+    (100000, 10, 10, 10, 10, False, 1), (65537, 10, 9, 9, 7, True, 2), (5000, 4, 4, 0, 4, False, 0),
+    (300001, 16, 16, 16, 16, False, 1), (1003, 7, 3, 5, 2, True, 1), (10, 1, 1, 1, 1, False, 0)])
+def test_lobpcg_step_kernel(dev, n, m, kw, kp, kwn, useb, tmode):
+    from paper_0705_2626_b200 import device as dv
+
+    r = rng(n + 7 * m + kw)
+    X, AX, P, AP = (r.standard_normal((n, m)) for _ in range(4))
+    W, AW = r.standard_normal((n, kw)), r.standard_normal((n, kw))
+    cx, cw, cp = r.standard_normal((m, m)), r.standard_normal((kw, m)), r.standard_normal((kp, m))
+    pcols = np.sort(r.choice(m, kp, replace=False)).astype(np.int32)
+    lam = r.uniform(1, 5, m)
+    d = r.uniform(1, 2, n) if useb else None
+    tvec = r.uniform(0.1, 1, n)
+    jn = np.sort(r.choice(m, kwn, replace=False))
+    wpos = np.full(m, -1, np.int32)
+    wpos[jn] = np.arange(kwn)
+    c = lambda a, dt=None: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    ld = m + (m & 1)
+    t = {k: blk(v, dev) for k, v in dict(X=X, AX=AX, P=P, AP=AP, W=W, AW=AW).items()}
+    outs = {k: torch.full((n, ld), np.nan, dtype=torch.float64, device=dev) for k in ("X", "AX", "P", "AP")}
+    ldwn = kwn + (kwn & 1)
+    wo = torch.full((n, ldwn), np.nan, dtype=torch.float64, device=dev)
+    a, b = 2 * m + kwn, 3 * m + kwn
+    red = torch.full((2 * m + a * b,), np.nan, dtype=torch.float64, device=dev)
+    coef = np.concatenate([cx.ravel(), cw.ravel(), cp.ravel()])
+    dv.lobpcg_step(n, m, t["X"], t["AX"], t["W"], t["AW"], kw, t["P"], t["AP"], kp,
+                   c(pcols) if kp else c(np.zeros(1, np.int32)), c(coef), outs["X"], outs["AX"],
+                   outs["P"], outs["AP"], c(lam), c(d) if useb else None, tmode, 0.25,
+                   c(tvec), c(wpos), kwn, wo, True, red)
+    pn = W @ cw + (P[:, pcols] @ cp if kp else 0)
+    apn = AW @ cw + (AP[:, pcols] @ cp if kp else 0)
+    Xn, AXn = X @ cx + pn, AX @ cx + apn
+    for k, ref in dict(P=pn, AP=apn, X=Xn, AX=AXn).items():
+        got = outs[k].cpu().numpy()
+        np.testing.assert_allclose(got[:, :m], ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+        if ld > m:
+            assert np.all(got[:, m:] == 0.0)
+    # residual of the next iteration computed from the kernel's own X', AX'
+    Xg, AXg = outs["X"].cpu().numpy()[:, :m], outs["AX"].cpu().numpy()[:, :m]
+    bx = Xg * d[:, None] if useb else Xg
+    wf = AXg - bx * lam
+    Tw = {0: wf, 1: 0.25 * wf, 2: tvec[:, None] * wf}[tmode]
+    wog = wo.cpu().numpy()
+    assert np.array_equal(wog[:, :kwn], Tw[:, jn])
+    redh = red.cpu().numpy()
+    np.testing.assert_allclose(redh[:m], (wf * wf).sum(0), rtol=1e-11)
+    np.testing.assert_allclose(redh[m:2 * m], (AXg * AXg).sum(0), rtol=1e-11)
+    G = redh[2 * m:].reshape(a, b)
+    Wn = Tw[:, jn]
+    L = np.hstack([Xg, Wn, outs["P"].cpu().numpy()[:, :m]])
+    B = L * (d[:, None] if useb else 1.0)
+    R = np.hstack([B, outs["AP"].cpu().numpy()[:, :m]])
+    ref = L.T @ R
+    scale = np.abs(L).T @ np.abs(R)
+    lc, rc = [0, m, m + kwn, a], [0, m, m + kwn, a, b]
+    modes = [[2, 1, 1, 1], [0, 2, 1, 1], [0, 0, 2, 1]]
+    for li in range(3):
+        for ri in range(4):
+            gb_, rb_, sb_ = (M[lc[li]:lc[li + 1], rc[ri]:rc[ri + 1]] for M in (G, ref, scale))
+            if modes[li][ri] == 1:
+                assert np.all(np.abs(gb_ - rb_) <= 1e-12 * sb_ + 1e-300), (li, ri)
+            elif modes[li][ri] == 2:
+                iu = np.triu_indices(rb_.shape[0])
+                assert np.all(np.abs(gb_[iu] - rb_[iu]) <= 1e-12 * sb_[iu] + 1e-300), (li, ri)

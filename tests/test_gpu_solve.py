@@ -45,9 +45,14 @@ def test_golden_trajectory(pk, golden):
     rep = pk.solve(a, t=pk.jacobi_preconditioner(a),
                    config=pk.SolverConfig(block_size=10, tol=1e-6, max_iter=200, seed=2))
     assert rep.status == "Converged"
-    assert abs(rep.iterations_used - 180) <= 1
-    ref_locks = g["lock_iterations"]
-    assert np.all(np.abs(rep.lock_iterations - ref_locks) <= 1), rep.lock_iterations
+    # The reference itself moves between 180 and 187 iterations when its
+    # operator is perturbed by 1-3 ulp (golden pert_iterations); hold the GPU
+    # run to that band +-1, and each column's lock iteration likewise.
+    its = np.concatenate([[180], g["pert_iterations"]])
+    assert its.min() - 1 <= rep.iterations_used <= its.max() + 1, rep.iterations_used
+    locks = np.vstack([g["lock_iterations"], g["pert_locks"]])
+    assert np.all(rep.lock_iterations >= locks.min(0) - 1), rep.lock_iterations
+    assert np.all(rep.lock_iterations <= locks.max(0) + 1), rep.lock_iterations
     ritz = np.array([h.ritz for h in rep.history])
     ok, worst = trajectory_band_ok(ritz, g)
     assert ok, worst
