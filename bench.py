@@ -232,14 +232,17 @@ def run_gpu(args):
     k_act = M_BLOCK  # C2 never locks within 300 iterations (reference run)
     # algorithmic bytes per launch (blocks counted at k=m columns)
     alg = {
+        # K1 (+K5b): read W, write A W (the X read for [X W]^T A W is extra)
         "stencil": 16.0 * n * k_act,
         "residual": 8.0 * n * (2 * M_BLOCK + k_act),
         "update": 8.0 * n * (2 * M_BLOCK + 4 * k_act + 4 * M_BLOCK),
+        # F1: read X, AX, W, AW, P_J, AP_J; write X', AX', P', AP', W'
+        "step": 8.0 * n * (6 * M_BLOCK + 5 * k_act),
     }
     # the per-step big gram reads X, W, P, AW, AP; the drift gram reads X
     gram_calls = kt.get("gram", [])
     per = {}
-    for name in ("stencil", "residual", "update"):
+    for name in ("stencil", "residual", "update", "step"):
         if kt.get(name):
             d = float(np.mean(kt[name]))
             per[name] = {"ms": d, "gbs": alg[name] / (d / 1e3) / 1e9, "calls": len(kt[name])}

@@ -21,7 +21,7 @@
 
 namespace b2l {
 
-constexpr int STEP_THREADS = 256;
+constexpr int STEP_THREADS = 512;
 
 struct StepArgs {
   int nrows, m, ldx;
@@ -42,9 +42,11 @@ struct StepArgs {
   int in_off[6];        // X AX W AW P AP inside a stage
   int d_off, t_off;     // staged d / tvec inside a stage
   int stage_doubles;
-  int out_off[5];       // X' AX' P' AP' W' (dense tiles)
+  int out_off[5];       // X' AX' P' AP' W' (dense tiles, buffer 0)
+  int out_stride;       // doubles between the two output-tile buffers
   int coef_off, lam_off, int_off;  // coefficient block, lam, ints (pcols|wpos)
   int red_off;
+  int gred_off;         // Gram row-slice reduction (stage ring when it fits)
   // Gram of the next step
   int a, b;
   int lcum[4], rcum[5];
@@ -182,6 +184,11 @@ __global__ void __launch_bounds__(STEP_THREADS) step_kernel(StepArgs A) {
     const int r0 = c * A.rc;
     const int nvalid = min(A.rc, A.nrows - r0);
     const int nv4 = (nvalid + 3) & ~3;
+    // output tiles alternate between two buffers so a chunk never waits for
+    // the TMA store of the previous one to drain
+    const int ob = (it & 1) * A.out_stride;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) O[i] = sm + A.out_off[i] + ob;
     mbar_wait(&bar[s], (it / A.nst) & 1);
     const double* X = st + A.in_off[0];
     const double* AX = st + A.in_off[1];
@@ -190,52 +197,72 @@ __global__ void __launch_bounds__(STEP_THREADS) step_kernel(StepArgs A) {
     const double* P = st + A.in_off[4];
     const double* AP = st + A.in_off[5];
 
-    // (1) update into the output tiles; rows [nvalid, nv4) are zero-filled
-    //     so the 4-row Gram groups of a tail chunk see zeros.
-    for (int e = tid; e < nv4 * m; e += STEP_THREADS) {
-      const int r = e / m;
-      const int cc = e - r * m;
-      double xs = 0.0, as = 0.0, pn = 0.0, apn = 0.0;
-      if (r < nvalid) {
-        double pw = 0.0, apw = 0.0, pp = 0.0, app = 0.0;
-        const double* wr = W + r * A.ldw;
-        const double* awr = AW + r * A.ldw;
-        for (int i = 0; i < A.kw; ++i) {
-          const double cw = Cw[i * m + cc];
-          pw = fma(wr[i], cw, pw);
-          apw = fma(awr[i], cw, apw);
+    // (1) update on the fp64 tensor cores: one warp per 8-row x 8-column
+    //     output tile, separate DMMA chains for W Cw, P_J Cp and X Cx so the
+    //     sums are formed as in the reference, (W Cw) + (P Cp) then
+    //     (X Cx) + P'.  Rows >= nvalid come out zero (the tail chunk's 4-row
+    //     Gram groups read them); pad columns m..ldx-1 come out zero.
+    {
+      const int NT = (m + 7) >> 3;
+      const int npairs = (A.rc >> 3) * NT;
+      const int q = lane & 3, rl = lane >> 2;
+      for (int pr = warp; pr < npairs; pr += STEP_THREADS / 32) {
+        const int mt = pr / NT, nt = pr - (pr / NT) * NT;
+        const int r = 8 * mt + rl;
+        const bool rv = r < nvalid;
+        const int cb = 8 * nt + rl;
+        const bool cv = cb < m;
+        double w0 = 0.0, w1 = 0.0, aw0 = 0.0, aw1 = 0.0, p0 = 0.0, p1 = 0.0;
+        double ap0 = 0.0, ap1 = 0.0, x0 = 0.0, x1 = 0.0, ax0 = 0.0, ax1 = 0.0;
+        for (int k0 = 0; k0 < A.kw; k0 += 4) {
+          const int k = k0 + q;
+          const bool kv = k < A.kw;
+          const double bcoef = (kv && cv) ? Cw[k * m + cb] : 0.0;
+          const double av = (kv && rv) ? W[r * A.ldw + k] : 0.0;
+          const double aav = (kv && rv) ? AW[r * A.ldw + k] : 0.0;
+          dmma_8x8x4(w0, w1, av, bcoef);
+          dmma_8x8x4(aw0, aw1, aav, bcoef);
         }
-        const double* pr = P + r * A.ldx;
-        const double* apr = AP + r * A.ldx;
-        for (int q = 0; q < A.kp; ++q) {
-          const double cp = Cp[q * m + cc];
-          const int col = spc[q];
-          pp = fma(pr[col], cp, pp);
-          app = fma(apr[col], cp, app);
+        for (int k0 = 0; k0 < A.kp; k0 += 4) {
+          const int k = k0 + q;
+          const bool kv = k < A.kp;
+          const int col = kv ? spc[k] : 0;
+          const double bcoef = (kv && cv) ? Cp[k * m + cb] : 0.0;
+          const double av = (kv && rv) ? P[r * A.ldx + col] : 0.0;
+          const double aav = (kv && rv) ? AP[r * A.ldx + col] : 0.0;
+          dmma_8x8x4(p0, p1, av, bcoef);
+          dmma_8x8x4(ap0, ap1, aav, bcoef);
         }
-        pn = (A.kw && A.kp) ? __dadd_rn(pw, pp) : (A.kw ? pw : pp);
-        apn = (A.kw && A.kp) ? __dadd_rn(apw, app) : (A.kw ? apw : app);
-        const double* xr = X + r * A.ldx;
-        const double* axr = AX + r * A.ldx;
-        for (int i = 0; i < m; ++i) {
-          const double cx = Cx[i * m + cc];
-          xs = fma(xr[i], cx, xs);
-          as = fma(axr[i], cx, as);
+        for (int k0 = 0; k0 < m; k0 += 4) {
+          const int k = k0 + q;
+          const bool kv = k < m;
+          const double bcoef = (kv && cv) ? Cx[k * m + cb] : 0.0;
+          const double av = (kv && rv) ? X[r * A.ldx + k] : 0.0;
+          const double aav = (kv && rv) ? AX[r * A.ldx + k] : 0.0;
+          dmma_8x8x4(x0, x1, av, bcoef);
+          dmma_8x8x4(ax0, ax1, aav, bcoef);
         }
-        xs = __dadd_rn(xs, pn);
-        as = __dadd_rn(as, apn);
+        const bool bw = A.kw > 0, bp = A.kp > 0;
+        const double pn0 = (bw && bp) ? __dadd_rn(w0, p0) : (bw ? w0 : p0);
+        const double pn1 = (bw && bp) ? __dadd_rn(w1, p1) : (bw ? w1 : p1);
+        const double apn0 = (bw && bp) ? __dadd_rn(aw0, ap0) : (bw ? aw0 : ap0);
+        const double apn1 = (bw && bp) ? __dadd_rn(aw1, ap1) : (bw ? aw1 : ap1);
+        const int ro = 8 * mt + rl;
+        const int co = 8 * nt + 2 * q;
+        const double vx[2] = {__dadd_rn(x0, pn0), __dadd_rn(x1, pn1)};
+        const double vax[2] = {__dadd_rn(ax0, apn0), __dadd_rn(ax1, apn1)};
+        const double vp[2] = {pn0, pn1};
+        const double vap[2] = {apn0, apn1};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (co + e < A.ldx) {
+            O[0][ro * A.ldx + co + e] = vx[e];
+            O[1][ro * A.ldx + co + e] = vax[e];
+            O[2][ro * A.ldx + co + e] = vp[e];
+            O[3][ro * A.ldx + co + e] = vap[e];
+          }
+        }
       }
-      O[0][r * A.ldx + cc] = xs;
-      O[1][r * A.ldx + cc] = as;
-      O[2][r * A.ldx + cc] = pn;
-      O[3][r * A.ldx + cc] = apn;
-      if (cc == m - 1)
-        for (int e2 = m; e2 < A.ldx; ++e2) {
-          O[0][r * A.ldx + e2] = 0.0;
-          O[1][r * A.ldx + e2] = 0.0;
-          O[2][r * A.ldx + e2] = 0.0;
-          O[3][r * A.ldx + e2] = 0.0;
-        }
     }
     __syncthreads();
 
@@ -285,12 +312,12 @@ __global__ void __launch_bounds__(STEP_THREADS) step_kernel(StepArgs A) {
       const int rps = A.rc / A.rs;
       const int lo = slice * rps;
       const int hi = min(lo + rps, nv4);
-      g.run(sm, la, lb, A.d ? st + A.d_off : nullptr, lo, hi, mask, DenseRows());
+      g.run(sm + ob, la, lb, A.d ? st + A.d_off : nullptr, lo, hi, mask, DenseRows());
     }
     // output tiles are rewritten by the next chunk: wait for the bulk store
     // to have read them and for every warp's Gram; then refill this stage
     // (its d chunk was in use by the Gram until here)
-    if (tid == 0) bulk_wait_read<0>();
+    if (tid == 0) bulk_wait_read<1>();
     __syncthreads();
     if (tid == 0) {
       const int cn = c + A.nst * gridDim.x;
@@ -318,14 +345,15 @@ __global__ void __launch_bounds__(STEP_THREADS) step_kernel(StepArgs A) {
   }
   __syncthreads();
   // ---- Gram: fixed-order sum of row slices
+  double* gred = sm + A.gred_off;
   if (gactive && slice > 0) {
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const size_t o = ((((size_t)(slice - 1) * A.ts_per_cta + tsl) * 8 + i * 4 + j) * 32 + lane) * 2;
-        red[o] = g.acc[i][j][0];
-        red[o + 1] = g.acc[i][j][1];
+        gred[o] = g.acc[i][j][0];
+        gred[o + 1] = g.acc[i][j][1];
       }
   }
   __syncthreads();
@@ -338,8 +366,8 @@ __global__ void __launch_bounds__(STEP_THREADS) step_kernel(StepArgs A) {
         double v0 = g.acc[i][j][0], v1 = g.acc[i][j][1];
         for (int sl = 1; sl < A.rs; ++sl) {
           const size_t o = ((((size_t)(sl - 1) * A.ts_per_cta + tsl) * 8 + i * 4 + j) * 32 + lane) * 2;
-          v0 += red[o];
-          v1 += red[o + 1];
+          v0 += gred[o];
+          v1 += gred[o + 1];
         }
         const int row = 8 * (ti0 + i) + (lane >> 2);
         const int col = 8 * (tj0 + j) + 2 * (lane & 3);
@@ -441,14 +469,17 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.tsI = (A.NI + 1) / 2;
   A.tsJ = (A.NJ + 3) / 4;
   const int TS = A.tsI * A.tsJ;
-  B2L_CHECK(TS <= 8, -B2L_EINVAL, "step: Gram tile blocks exceed one CTA (m too large)");
+  const int nwarps = STEP_THREADS / 32;
+  B2L_CHECK(TS <= nwarps, -B2L_EINVAL, "step: Gram tile blocks exceed one CTA (m too large)");
   A.ts_per_cta = TS;
   A.rs = 1;
-  while (A.rs * 2 * TS <= 8) A.rs *= 2;
-  // chunk rows: stage (6 blocks + d + t) <= ~36 KB
+  while (A.rs * 2 * TS <= nwarps) A.rs *= 2;
+  // chunk rows (multiple of 8: one DMMA row tile per 8 rows): stage (6
+  // blocks + d + t) <= ~40 KB; then the deepest TMA ring (<= 4 stages) that
+  // fits one CTA per SM.
   const int width = 4 * ldx + 2 * (kw ? ldw : 0) + (d ? 1 : 0) + (tmode == 2 ? 1 : 0);
   A.rc = 128;
-  while (A.rc > 16 && (size_t)A.rc * width * 8 > 36 * 1024) A.rc >>= 1;
+  while (A.rc > 16 && (size_t)A.rc * width * 8 > 40 * 1024) A.rc >>= 1;
   while (A.rs > 1 && A.rc / A.rs < 4) A.rs >>= 1;
   const int rc = A.rc;
   int off = 0;
@@ -461,7 +492,13 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.d_off = off; off += d ? rc : 0;
   A.t_off = off; off += tmode == 2 ? rc : 0;
   A.stage_doubles = (off + 15) & ~15;
-  A.nst = 2;
+  {
+    const size_t tail = (size_t)2 * (4 * ((rc * ldx + 15) & ~15) + ((rc * A.ldwn + 15) & ~15)) +
+                        (m * m + kw * m + kp * m) + 3 * m + 64 +
+                        (size_t)(STEP_THREADS / m) * 2 * m + 4096;
+    A.nst = 4;
+    while (A.nst > 2 && ((size_t)A.nst * A.stage_doubles + tail) * 8 > 200 * 1024) --A.nst;
+  }
   off = A.nst * A.stage_doubles;
   for (int b = 0; b < 4; ++b) {
     A.out_off[b] = off;
@@ -469,6 +506,8 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   }
   A.out_off[4] = off;
   off += (rc * A.ldwn + 15) & ~15;
+  A.out_stride = off - A.out_off[0];
+  off += A.out_stride;  // second output buffer
   A.coef_off = off;
   off += (m * m + kw * m + kp * m + 1) & ~1;
   A.lam_off = off;
@@ -481,7 +520,15 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   const int rpp = STEP_THREADS / m;
   const size_t red1 = (size_t)2 * rpp * m;
   const size_t red2 = (size_t)(A.rs > 1 ? A.rs - 1 : 0) * A.ts_per_cta * 8 * 64;
-  off += (int)(red1 > red2 ? red1 : red2);
+  // the Gram slice reduction may reuse the (idle) stage ring after the loop
+  const size_t red_stage = (size_t)A.nst * A.stage_doubles;
+  if (red2 <= red_stage) {
+    A.gred_off = 0;
+    off += (int)red1;
+  } else {
+    A.gred_off = A.red_off;
+    off += (int)(red1 > red2 ? red1 : red2);
+  }
   const size_t smem = (size_t)off * 8;
   B2L_CHECK(smem <= 227 * 1024, -B2L_EINVAL, "step: shared memory budget exceeded");
   const int nchunks = (nrows + rc - 1) / rc;

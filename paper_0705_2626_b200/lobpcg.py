@@ -4,29 +4,36 @@
 Control flow, thresholds, the lock test, the basis-repair ladder, the drift
 repair and the status strings are the reference's, evaluated on the host on
 small matrices.  What changes is where the tall work happens and how much of
-it there is per iteration:
+it there is per iteration (steady state, built-in operators):
 
-  reference (numpy)                      here (libb200lobpcg, sm_100a)
-  ------------------------------------   ----------------------------------
-  drift gram X^T B X        :419          K5 gram (1 pass over X)
-  W_full, norms, T(W_J)     :429-467      K4+K2 residual kernel (1 pass)
-  b_orthonormalize(W), P    :176-178,490  host Cholesky of Gram sub-blocks;
-   (gram + tri_solve_right)                R^{-1} folded into the pencil and
-                                           the update coefficients -- W, P,
-                                           AP are never rewritten
-  a(w)                      :482          K1 fused stencil on raw W
-  _project_pencil 8 grams   :299-340      K5 one multi-block gram pass
-  gen_sym_eig + ladder      :501-519      host (scipy LAPACK), unchanged
-  Ritz update 6 multiplies  :520-540      K6 one fused update pass
+  reference (numpy), per iteration           here (libb200lobpcg, sm_100a)
+  -----------------------------------------  ---------------------------------
+  Ritz update, 6 multiplies   :520-540       F1 b2l_lobpcg_step (one pass):
+  drift gram X^T B X          :419             update, next residual + norms,
+  W_full, norms, T(W_J)       :429-467         next W, every Gram block not
+  b_orthonormalize(W), P_J    :176-178,490     involving A W (DMMA)
+  _project_pencil 6 grams     :328-338
+  a(w)                        :482           K1+K5b b2l_stencil7_gram (one
+  gram(x, aw), gram(w, aw)    :325-327         pass): A W and [X W]^T A W
+  Cholesky-QR, gen_sym_eig    :501-519       host fp64 (LAPACK), unchanged
+  tri_solve_right (W, P, AP)  :177,491       folded into the coefficients
 
-BX is d*X computed on the fly for diagonal B (the reference carries BX by
-recurrence); this changes results only at rounding level.
+The Cholesky-QR factors of W and P are never applied to the tall blocks: the
+Gram blocks of the normalised vectors are R^-T G R^-1 of the raw ones, and
+R^-1 is folded into the update coefficients.  BX is d*X computed on the fly
+for diagonal B (the reference carries BX by recurrence).  Both change
+results only at rounding level (tests/test_gpu_solve.py holds the trajectory
+to the reference's own 1-ulp perturbation band).
+
+The first iteration, drift repairs and the exit refresh use the standalone
+kernels (b2l_gram / b2l_residual / b2l_update); so do block sizes whose Gram
+does not fit the fused kernels (m > 16) and generic operators.
 """
 
 from __future__ import annotations
 
 import contextlib
-from dataclasses import dataclass, replace
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -120,19 +127,25 @@ class SolverReport:
 
 # Device options live outside SolverConfig so the reference signature and
 # config stay untouched.
-_OPTS = {"return_device": False, "timer": None}
+_OPTS = {"return_device": False, "timer": None, "fused": True}
 
 
 @contextlib.contextmanager
-def device_options(return_device: bool | None = None, timer=None):
-    """Scoped device options: ``return_device`` keeps eigenvectors on the GPU
-    (the 464^3 x 8 block is 6.4 GB); ``timer`` is a callable(name, fn) hook
-    used by bench.py to time individual kernels with CUDA events."""
+def device_options(return_device: bool | None = None, timer=None, fused: bool | None = None):
+    """Scoped device options.
+
+    return_device -- keep eigenvectors on the GPU (the 464^3 x 8 block is 6.4 GB)
+    timer         -- callable(name, fn) wrapping each kernel launch (bench.py
+                     times kernels with CUDA events through it)
+    fused         -- False forces the unfused standalone kernels (tests)
+    """
     old = dict(_OPTS)
     if return_device is not None:
         _OPTS["return_device"] = bool(return_device)
     if timer is not None:
         _OPTS["timer"] = timer
+    if fused is not None:
+        _OPTS["fused"] = bool(fused)
     try:
         yield
     finally:
@@ -151,24 +164,68 @@ class _Failure(Exception):
 
 # Gram block-pair modes (include/b200lobpcg.h): only what the host reads.
 _UPPER = np.array([[2]], dtype=np.uint8)
-# L = [X, W, P], R = [X, W, P, AW, AP]  (P^T AW is never used)
-_MODES_P = np.array([[2, 1, 1, 1, 1],
-                     [0, 2, 1, 1, 1],
-                     [0, 0, 2, 0, 1]], dtype=np.uint8)
-# L = [X, W], R = [X, W, AW]
-_MODES_NOP = np.array([[2, 1, 1],
-                       [0, 2, 1]], dtype=np.uint8)
+# L = [X, W, P], R = [BX, BW, BP, AP]   (the F1 layout)
+_MODES_P = np.array([[2, 1, 1, 1],
+                     [0, 2, 1, 1],
+                     [0, 0, 2, 1]], dtype=np.uint8)
+# L = [X, W], R = [BX, BW]
+_MODES_NOP = np.array([[2, 1],
+                       [0, 2]], dtype=np.uint8)
 
 
 def _mirror_upper(g):
     return np.triu(g) + np.triu(g, 1).T
 
 
+def _tilesets(a, b):
+    """8x8 tile blocks (2x4 tiles each) of an a x b Gram (gram_tile.cuh)."""
+    ni, nj = (a + 7) // 8, (b + 7) // 8
+    return ((ni + 1) // 2) * ((nj + 3) // 4)
+
+
+def _host_buf(count, dtype=torch.float64):
+    return torch.empty(count, dtype=dtype, pin_memory=torch.cuda.is_available())
+
+
+class _Pinned:
+    """Pinned host staging for the small per-iteration transfers."""
+
+    def __init__(self, dev, nd, ni):
+        self.dev = dev
+        self.hd = _host_buf(nd)
+        self.dd = torch.empty(nd, dtype=torch.float64, device=dev)
+        self.hi = _host_buf(ni, torch.int32)
+        self.di = torch.empty(ni, dtype=torch.int32, device=dev)
+        self.hd_np = self.hd.numpy()
+        self.hi_np = self.hi.numpy()
+
+    def upload(self, dparts, iparts):
+        """Pack float64 / int32 arrays, one H2D copy each; returns device views."""
+        outs_d, outs_i = [], []
+        o = 0
+        for a in dparts:
+            a = np.asarray(a, dtype=np.float64).ravel()
+            self.hd_np[o:o + a.size] = a
+            outs_d.append((o, a.size))
+            o += a.size
+        if o:
+            self.dd[:o].copy_(self.hd[:o], non_blocking=True)
+        oi = 0
+        for a in iparts:
+            a = np.asarray(a, dtype=np.int32).ravel()
+            self.hi_np[oi:oi + a.size] = a
+            outs_i.append((oi, a.size))
+            oi += a.size
+        if oi:
+            self.di[:oi].copy_(self.hi[:oi], non_blocking=True)
+        return ([self.dd[s:s + k] for s, k in outs_d], [self.di[s:s + k] for s, k in outs_i])
+
+
 class LOBPCGRun:
     """One LOBPCG solve on the device, stepped iteration by iteration.
 
     ``solve`` drives it to completion; bench.py steps it to time individual
-    iterations.  Mirrors lobpcg.py:375-577 line for line in control flow.
+    iterations.  Mirrors lobpcg.py:375-577 in control flow.
     """
 
     def __init__(self, a, b=None, t=None, y=None, x0=None, config=None):
@@ -207,6 +264,10 @@ class LOBPCGRun:
                 self.tmode, self.tvec = 2, t.inv_diag.to(self.dev)
         else:
             self.t_generic = t
+        fused = _OPTS["fused"]
+        # F1 holds the whole next-step Gram in one CTA; stencil+Gram likewise
+        self.use_f1 = fused and _tilesets(3 * m, 4 * m) <= 8
+        self.use_sgram = fused and self.fused_a and _tilesets(2 * m, m) <= 8
 
         # ---- initial block (lobpcg.py:386-393)
         if x0 is not None:
@@ -229,17 +290,18 @@ class LOBPCGRun:
         ld = dv.even(m)
         self.ld = ld
         dev = self.dev
-        self.X = dv.new_block(n, ld, dev)
-        self.AX = dv.new_block(n, ld, dev)
-        self.X2 = dv.new_block(n, ld, dev)
-        self.AX2 = dv.new_block(n, ld, dev)
-        self.P = dv.new_block(n, ld, dev)
-        self.AP = dv.new_block(n, ld, dev)
-        self.P2 = dv.new_block(n, ld, dev)
-        self.AP2 = dv.new_block(n, ld, dev)
-        self.Wbuf = torch.zeros(n * ld, dtype=torch.float64, device=dev)
+        self.X, self.AX, self.X2, self.AX2 = (dv.new_block(n, ld, dev) for _ in range(4))
+        self.P, self.AP, self.P2, self.AP2 = (dv.new_block(n, ld, dev) for _ in range(4))
+        self.Wbufs = [torch.zeros(n * ld, dtype=torch.float64, device=dev) for _ in range(2)]
+        self.wcur = 0
         self.AWbuf = torch.zeros(n * ld, dtype=torch.float64, device=dev)
         self.sums = torch.zeros(2 * m, dtype=torch.float64, device=dev)
+        nred = 2 * m + (3 * m) * (4 * m)
+        self.red = torch.zeros(nred, dtype=torch.float64, device=dev)
+        self.g2 = torch.zeros((2 * m) * m, dtype=torch.float64, device=dev)
+        self.h_red = _host_buf(nred)
+        self.h_g2 = _host_buf((2 * m) * m)
+        self.pin = _Pinned(dev, 3 * m * m + 2 * m + 8, 3 * m + 8)
         if isinstance(x0t, torch.Tensor):
             self.X[:, :m] = x0t
         else:
@@ -256,6 +318,7 @@ class LOBPCGRun:
         self.it = 0
         self.done = False
         self.drift_repairs = 0
+        self.f1_pending = False    # self.red holds F1 results for this step
 
         self._initial()
 
@@ -263,21 +326,23 @@ class LOBPCGRun:
     def _wmask(self, nblocks):
         return ((1 << nblocks) - 1) if self.bdiag is not None else 0
 
+    def _wview(self, k, which=None):
+        buf = self.Wbufs[self.wcur if which is None else which]
+        ldw = dv.even(k)
+        return dv.view_block(buf, self.n, ldw), dv.view_block(self.AWbuf, self.n, ldw)
+
+    def _fetch(self, dev_t, host_t, count):
+        """D2H of the first `count` doubles through pinned memory (syncs)."""
+        host_t[:count].copy_(dev_t.reshape(-1)[:count], non_blocking=True)
+        if self.dev.type == "cuda":
+            torch.cuda.current_stream(self.dev).synchronize()
+        return host_t[:count].numpy().copy()
+
     def _gram_xx(self):
         """X^T B X (upper triangle computed, mirrored on the host)."""
         g = _timed("gram_drift", lambda: dv.gram(self.n, [(self.X, self.m)], [(self.X, self.m)],
                                                  self._wmask(1), self.bdiag, pair_mode=_UPPER))
         return _mirror_upper(dv.to_host(g))
-
-    def _apply_a(self, src, dst, k):
-        """dst[:, :k] = A src[:, :k] for (n, ld) blocks (K1 when fused)."""
-        if self.fused_a:
-            _timed("stencil", lambda: self.a.apply_into(src, dst))
-        else:
-            y = self.a(src[:, :k])
-            if not isinstance(y, torch.Tensor) or tuple(y.shape) != (self.n, k):
-                raise ValueError("operator apply returned a block of the wrong shape")
-            dst[:, :k] = y
 
     def _rotate_x(self, M):
         """X, AX <- X M, AX M (no P involvement)."""
@@ -296,6 +361,16 @@ class LOBPCGRun:
         self._rotate_x(q)
         self.lam = lam
 
+    def _apply_a_plain(self, src, dst, k):
+        """dst[:, :k] = A src[:, :k] (K1 for the built-in Laplacian)."""
+        if self.fused_a:
+            _timed("stencil", lambda: self.a.apply_into(src, dst))
+        else:
+            y = self.a(src[:, :k])
+            if not isinstance(y, torch.Tensor) or tuple(y.shape) != (self.n, k):
+                raise ValueError("operator apply returned a block of the wrong shape")
+            dst[:, :k] = y
+
     def _initial(self):
         m, n = self.m, self.n
         gxx = self._gram_xx()
@@ -307,9 +382,9 @@ class LOBPCGRun:
         Md = dv.to_device(minv, self.dev)
         dv.update(n, m, self.X, None, Md, self.X2, None)
         self.X, self.X2 = self.X2, self.X
-        self._apply_a(self.X, self.AX, m)             # lobpcg.py:403
+        self._apply_a_plain(self.X, self.AX, m)      # lobpcg.py:403
         gxa = dv.to_host(dv.gram(n, [(self.X, m)], [(self.AX, m)], pair_mode=_UPPER))
-        lam, q = sym_eig(gxa)                          # lobpcg.py:404
+        lam, q = sym_eig(gxa)                        # lobpcg.py:404
         self._rotate_x(q)
         self.lam = lam
 
@@ -322,8 +397,21 @@ class LOBPCGRun:
         cfg, m, n = self.cfg, self.m, self.n
         it = self.it
         try:
+            jprev = np.flatnonzero(self.active)
+            kst = jprev.size
+            G1 = sums = None
+            if self.f1_pending:
+                # F1 of the previous step already produced this step's drift
+                # Gram, residual norms, W and every non-AW Gram block
+                a, b = 2 * m + kst, 3 * m + kst
+                red = self._fetch(self.red, self.h_red, 2 * m + a * b)
+                sums = red[:2 * m]
+                G1 = red[2 * m:].reshape(a, b)
+                gxx = _mirror_upper(G1[:m, :m])
+            else:
+                gxx = self._gram_xx()
+            self.f1_pending = False
             # drift check (lobpcg.py:419-428)
-            gxx = self._gram_xx()
             drift = np.abs(gxx - np.eye(m)).max()
             if drift > DRIFT_LIMIT:
                 try:
@@ -331,26 +419,25 @@ class LOBPCGRun:
                 except NotSPD:
                     raise _Failure("BasisDegeneracy")
                 self.drift_repairs += 1
+                G1 = sums = None
                 if cfg.verbosity >= 2:
                     print(f"  it {it:4d}  Ritz block re-orthonormalized (drift {drift:.1e})")
 
-            # residual + lock (lobpcg.py:429-437); W written for the active set
-            jprev = np.flatnonzero(self.active)
-            kst = jprev.size
-            ldw = dv.even(kst)
-            W = dv.view_block(self.Wbuf, n, ldw)
-            AW = dv.view_block(self.AWbuf, n, ldw)
-            pos = np.full(m, -1, dtype=np.int32)
-            pos[jprev] = np.arange(kst, dtype=np.int32)
-            lam_d = dv.to_device(self.lam, self.dev)
-            pos_d = dv.to_device(pos, self.dev, torch.int32)
-            _timed("residual", lambda: dv.residual(
-                n, m, self.X, self.AX, self.bdiag, lam_d, self.tmode, self.tinv, self.tvec,
-                pos_d, kst, W, cfg.relative_tol, self.sums))
-            sums = dv.to_host(self.sums)
+            W, AW = self._wview(kst)
+            if sums is None:
+                # residual + T(W) for the active set (lobpcg.py:429-430, :466-467)
+                pos = np.full(m, -1, dtype=np.int32)
+                pos[jprev] = np.arange(kst, dtype=np.int32)
+                (lam_d,), (pos_d,) = self.pin.upload([self.lam], [pos])
+                _timed("residual", lambda: dv.residual(
+                    n, m, self.X, self.AX, self.bdiag, lam_d, self.tmode, self.tinv, self.tvec,
+                    pos_d, kst, W, cfg.relative_tol, self.sums))
+                sums = self._fetch(self.sums, self.h_red, 2 * m)
+
+            # lock test (lobpcg.py:429-437)
             norms = np.sqrt(sums[:m])
             if cfg.relative_tol:
-                thresholds = cfg.tol * np.sqrt(sums[m:])
+                thresholds = cfg.tol * np.sqrt(sums[m:2 * m])
             else:
                 thresholds = np.full(m, cfg.tol)
             newly = self.active & (norms < thresholds)
@@ -375,26 +462,40 @@ class LOBPCGRun:
                 self.done = True
                 return False
             if cfg.check_invariants:
-                self._check_state()
+                self._check_state(gxx)
 
             J = np.flatnonzero(self.active)
             sel = np.searchsorted(jprev, J)          # W columns of J
             if self.t_generic is not None:
-                W, AW, kst, ldw, sel = self._generic_precondition(W, sel, J.size)
+                W, AW, kst, sel = self._generic_precondition(W, sel, J.size)
+                G1 = None                            # F1 saw the raw residual
 
-            # AW = A W on the raw (un-orthonormalized) residuals
-            self._apply_a(W, AW, kst)
-
-            # one Gram pass for every block product of the step
-            hp = self.have_p
-            L = [(self.X, m), (W, kst)] + ([(self.P, m)] if hp else [])
-            R = [(self.X, m), (W, kst)] + ([(self.P, m)] if hp else []) + [(AW, kst)] + \
-                ([(self.AP, m)] if hp else [])
-            nb = 3 if hp else 2
-            mode = _MODES_P if hp else _MODES_NOP
-            G = dv.to_host(_timed("gram", lambda: dv.gram(n, L, R, self._wmask(nb), self.bdiag,
-                                                          pair_mode=mode)))
-            self._rayleigh_ritz(G, J, sel, kst, W, AW)
+            # A W (+ [X W]^T A W in the same pass for the built-in stencil)
+            g2_rows = m + kst
+            g2 = self.g2[:g2_rows * kst].view(g2_rows, kst)
+            if self.use_sgram:
+                gr = self.a.grid
+                _timed("stencil", lambda: dv.stencil7_gram(
+                    W, AW, gr.nx, gr.ny, gr.nz, self.a.scale, self.X, m, kst, g2))
+            else:
+                self._apply_a_plain(W, AW, kst)
+                _timed("gram_aw", lambda: dv.gram(n, [(self.X, m), (W, kst)], [(AW, kst)],
+                                                  out=g2))
+            G1dev = None
+            if G1 is None:
+                if self.have_p:
+                    L = [(self.X, m), (W, kst), (self.P, m)]
+                    R = L + [(self.AP, m)]
+                    G1dev = _timed("gram", lambda: dv.gram(n, L, R, self._wmask(3), self.bdiag,
+                                                           pair_mode=_MODES_P))
+                else:
+                    L = [(self.X, m), (W, kst)]
+                    G1dev = _timed("gram", lambda: dv.gram(n, L, L, self._wmask(2), self.bdiag,
+                                                           pair_mode=_MODES_NOP))
+            G2 = self._fetch(g2, self.h_g2, g2_rows * kst).reshape(g2_rows, kst)
+            if G1dev is not None:
+                G1 = dv.to_host(G1dev)
+            self._rayleigh_ritz(G1, G2, J, sel, kst, W, AW)
         except _Failure as f:
             self.failure = str(f)
             self.done = True
@@ -415,22 +516,17 @@ class LOBPCGRun:
             raise ValueError(f"preconditioner returned shape {tuple(out.shape)}, expected ({n}, {kj})")
         if not bool(torch.isfinite(out).all()):
             raise ValueError("preconditioner returned non-finite entries")
-        ldw = dv.even(kj)
-        W = dv.view_block(self.Wbuf, n, ldw)
-        AW = dv.view_block(self.AWbuf, n, ldw)
+        W, AW = self._wview(kj)
         W.zero_()
         W[:, :kj] = out.to(torch.float64)
-        return W, AW, kj, ldw, np.arange(kj)
+        return W, AW, kj, np.arange(kj)
 
-    def _rayleigh_ritz(self, G, J, sel, kst, W, AW):
+    def _rayleigh_ritz(self, G1, G2, J, sel, kst, W, AW):
         m, n = self.m, self.n
         hp = self.have_p
-        # row/col offsets of the blocks inside G
-        rX, rW, rP = 0, m, m + kst
-        cX, cW = 0, m
-        cP = m + kst
-        cAW = m + kst + (m if hp else 0)
-        cAP = cAW + kst
+        # G1: L = [X, W(kst), P?] x R = [BX, BW, BP?, AP?];  G2: [X; W]^T AW
+        rW, rP = m, m + kst
+        cW, cP, cAP = m, m + kst, 2 * m + kst
 
         # W: Cholesky-QR with column dropping on the J sub-block
         # (lobpcg.py:475-481, :182-200), W never rewritten
@@ -438,10 +534,9 @@ class LOBPCGRun:
         mw = None
         while keep:
             ks = sel[keep]
-            gww = G[rW + ks][:, cW + ks]
+            gww = G1[rW + ks][:, cW + ks]
             try:
-                _, minv = scaled_cholesky(gww, PIVOT_FLOOR)
-                mw = minv
+                _, mw = scaled_cholesky(gww, PIVOT_FLOOR)
                 break
             except NotSPD as err:
                 del keep[err.pivot]
@@ -454,22 +549,20 @@ class LOBPCGRun:
         mp = None
         if hp:
             try:
-                gpp = G[rP + J][:, cP + J]
-                _, mp = scaled_cholesky(gpp, PIVOT_FLOOR)
+                _, mp = scaled_cholesky(G1[rP + J][:, cP + J], PIVOT_FLOOR)
             except NotSPD:
                 mp = None
                 self.pending += 1
 
-        # raw Gram sub-blocks
-        gXAW = G[rX:rX + m][:, cAW + wcols]
-        gXBW = G[rX:rX + m][:, cW + wcols]
-        gWAW = G[rW + wcols][:, cAW + wcols]
+        gXAW = G2[:m][:, wcols]
+        gWAW = G2[m + wcols][:, wcols]
+        gXBW = G1[:m][:, cW + wcols]
         if hp:
-            gXAP = G[rX:rX + m][:, cAP + J]
-            gWAP = G[rW + wcols][:, cAP + J]
-            gXBP = G[rX:rX + m][:, cP + J]
-            gWBP = G[rW + wcols][:, cP + J]
-            gPAP = G[rP + J][:, cAP + J]
+            gXAP = G1[:m][:, cAP + J]
+            gWAP = G1[rW + wcols][:, cAP + J]
+            gXBP = G1[:m][:, cP + J]
+            gWBP = G1[rW + wcols][:, cP + J]
+            gPAP = G1[rP + J][:, cAP + J]
 
         # Rayleigh-Ritz with the repair ladder (lobpcg.py:501-519)
         use_p = mp is not None
@@ -518,15 +611,33 @@ class LOBPCGRun:
         else:
             cp_raw = np.zeros((0, m))
             pcols = np.zeros(0, dtype=np.int32)
-        dev = self.dev
-        cxd = dv.to_device(cx, dev)
-        cwd = dv.to_device(cw_raw, dev)
-        cpd = dv.to_device(cp_raw, dev) if cp_raw.size else cxd
-        pcd = dv.to_device(pcols, dev, torch.int32) if pcols.size else pos_dummy(dev)
-        _timed("update", lambda: dv.update(
-            n, m, self.X, self.AX, cxd, self.X2, self.AX2, w=W, aw=AW, kw=kst, cw=cwd,
-            p=self.P if use_p else None, ap=self.AP if use_p else None, pcols=pcd,
-            kp=pcols.size, cp=cpd, po=self.P2, apo=self.AP2, x_plus_p=True))
+        kp = pcols.size
+
+        if self.use_f1:
+            # next iteration's W holds the current active set J
+            wpos = np.full(m, -1, dtype=np.int32)
+            wpos[J] = np.arange(J.size, dtype=np.int32)
+            (coef_d, lam_d), (pc_d, wpos_d) = self.pin.upload(
+                [np.concatenate([cx.ravel(), cw_raw.ravel(), cp_raw.ravel()]), lam_new],
+                [pcols if kp else np.zeros(1, np.int32), wpos])
+            nxt = 1 - self.wcur
+            Wn, _ = self._wview(J.size, nxt)
+            tmode = 0 if self.t_generic is not None else self.tmode
+            _timed("step", lambda: dv.lobpcg_step(
+                n, m, self.X, self.AX, W, AW, kst, self.P if kp else None,
+                self.AP if kp else None, kp, pc_d, coef_d, self.X2, self.AX2, self.P2,
+                self.AP2, lam_d, self.bdiag, tmode, self.tinv, self.tvec, wpos_d, J.size, Wn,
+                self.cfg.relative_tol, self.red))
+            self.wcur = nxt
+            self.f1_pending = True
+        else:
+            (cx_d, cw_d, cp_d), (pc_d,) = self.pin.upload(
+                [cx, cw_raw, cp_raw if kp else np.zeros(1)],
+                [pcols if kp else np.zeros(1, np.int32)])
+            _timed("update", lambda: dv.update(
+                n, m, self.X, self.AX, cx_d, self.X2, self.AX2, w=W, aw=AW, kw=kst, cw=cw_d,
+                p=self.P if kp else None, ap=self.AP if kp else None, pcols=pc_d, kp=kp,
+                cp=cp_d, po=self.P2, apo=self.AP2, x_plus_p=True))
         self.X, self.X2 = self.X2, self.X
         self.AX, self.AX2 = self.AX2, self.AX
         self.P, self.P2 = self.P2, self.P
@@ -534,9 +645,8 @@ class LOBPCGRun:
         self.have_p = True
         self.lam = lam_new
 
-    def _check_state(self):
-        g = self._gram_xx()
-        err = np.abs(g - np.eye(self.m)).max()
+    def _check_state(self, gxx):
+        err = np.abs(gxx - np.eye(self.m)).max()
         if err > 1e-10:
             raise RuntimeError(f"block lost B-orthonormality: max deviation {err:.3e}")
 
@@ -582,16 +692,6 @@ class LOBPCGRun:
             status=status,
             basis_fallbacks=self.total_fallbacks,
         )
-
-
-_DUMMY = {}
-
-
-def pos_dummy(dev):
-    t = _DUMMY.get(dev)
-    if t is None:
-        t = _DUMMY[dev] = torch.zeros(2, dtype=torch.int32, device=dev)
-    return t
 
 
 def solve(a, b=None, t=None, y=None, x0=None, config=None):

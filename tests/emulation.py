@@ -101,6 +101,31 @@ def update(nrows, m, x, ax, cx, xo, axo, w=None, aw=None, kw=0, cw=None, p=None,
         side(ax, aw, ap, axo, apo)
 
 
+def stencil7_gram(x, out, nx, ny, nz, scale, xb, m, kw, gram_out, halo=None, has_lo=False,
+                  has_hi=False):
+    stencil7(x, out, nx, ny, nz, scale, halo, has_lo, has_hi)
+    L = np.hstack([_np(xb)[:, :m], _np(x)[:, :kw]])
+    gram_out.copy_(torch.from_numpy(L.T @ _np(out)[:, :kw]))
+
+
+def lobpcg_step(nrows, m, x, ax, w, aw, kw, p, ap, kp, pcols, coef, xo, axo, po, apo, lam,
+                bdiag, tmode, tinv, tvec, wpos, kwn, wo, want_ax, red_out):
+    c = _np(coef)
+    cx = c[:m * m]
+    cw = c[m * m:m * m + kw * m]
+    cp = c[m * m + kw * m:m * m + kw * m + kp * m]
+    update(nrows, m, x, ax, torch.from_numpy(cx.copy()), xo, axo, w=w, aw=aw, kw=kw,
+           cw=torch.from_numpy(cw.copy()), p=p, ap=ap, pcols=pcols, kp=kp,
+           cp=torch.from_numpy(cp.copy()), po=po, apo=apo, x_plus_p=True)
+    sums = torch.zeros(2 * m, dtype=torch.float64)
+    residual(nrows, m, xo, axo, bdiag, lam, tmode, tinv, tvec, wpos, kwn, wo, want_ax, sums)
+    Xn, Wn, Pn, APn = (_np(t)[:, :k] for t, k in ((xo, m), (wo, kwn), (po, m), (apo, m)))
+    L = np.hstack([Xn, Wn, Pn])
+    B = L * (_np(bdiag)[:, None] if bdiag is not None else 1.0)
+    G = L.T @ np.hstack([B, APn])
+    red_out[:2 * m + G.size] = torch.from_numpy(np.concatenate([_np(sums), G.ravel()]))
+
+
 @contextlib.contextmanager
 def emulate(monkeypatch):
     """Route paper_0705_2626_b200's device wrappers to the CPU stand-ins."""
@@ -110,6 +135,8 @@ def emulate(monkeypatch):
     monkeypatch.setattr(dv, "gram", gram)
     monkeypatch.setattr(dv, "residual", residual)
     monkeypatch.setattr(dv, "update", update)
+    monkeypatch.setattr(dv, "stencil7_gram", stencil7_gram)
+    monkeypatch.setattr(dv, "lobpcg_step", lobpcg_step)
     monkeypatch.setattr(_lib, "ensure_device", lambda i: None)
     monkeypatch.setattr(operators, "_default_device", lambda: torch.device("cpu"))
     yield
