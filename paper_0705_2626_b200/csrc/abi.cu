@@ -95,9 +95,7 @@ int sm_count() {
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static std::once_flag g_encode_once;
 
-int encode_tmap_4d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1,
-                   uint64_t d2, uint64_t d3, uint32_t b0, uint32_t b1,
-                   uint32_t b2, uint32_t b3) {
+static int ensure_encode() {
   std::call_once(g_encode_once, [] {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
@@ -107,6 +105,13 @@ int encode_tmap_4d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1,
       g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   });
   B2L_CHECK(g_encode != nullptr, -B2L_EDRIVER, "cuTensorMapEncodeTiled unavailable");
+  return 0;
+}
+
+int encode_tmap_4d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1,
+                   uint64_t d2, uint64_t d3, uint32_t b0, uint32_t b1,
+                   uint32_t b2, uint32_t b3) {
+  if (int rc = ensure_encode()) return rc;
   cuuint64_t dims[4] = {d0, d1, d2, d3};
   cuuint64_t strides[3] = {d0 * 8, d0 * d1 * 8, d0 * d1 * d2 * 8};
   cuuint32_t box[4] = {b0, b1, b2, b3};
@@ -117,6 +122,25 @@ int encode_tmap_4d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   B2L_CHECK(r == CUDA_SUCCESS, -B2L_EDRIVER,
             "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
+  return 0;
+}
+
+// 2-D map over a row-major (rows x cols) fp64 block with row stride cols;
+// the box may be wider than cols (out-of-bounds columns: zero on load,
+// clipped on store).
+int encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
+                   uint32_t box_cols, uint32_t box_rows) {
+  if (int rc = ensure_encode()) return rc;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 8};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  B2L_CHECK(r == CUDA_SUCCESS, -B2L_EDRIVER,
+            "cuTensorMapEncodeTiled(2d) failed (code " + std::to_string((int)r) + ")");
   return 0;
 }
 

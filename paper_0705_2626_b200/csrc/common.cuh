@@ -92,6 +92,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Waiting variant for warps that idle a long time (warp-specialised kernels):
+// the thread is suspended in hardware until the phase completes (or the time
+// hint, in ns, expires) instead of re-polling, so it does not steal issue
+// slots from the warps doing the work.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+  } while (!ok);
+}
+
 // TMA tiled 4-D load global -> shared, completion on an mbarrier.
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map,
                                             uint64_t* bar, int c0, int c1,
@@ -114,6 +131,38 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map,
       "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+
+// TMA tiled 2-D load / store (a box of rows of a row-major block).
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_"
+      "tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// Shared-memory row stride (doubles) for a block of `ld` doubles per row:
+// >= ld and == 4 or 12 (mod 16), so the DMMA fragment patterns (4 rows x 4
+// doubles per half-warp) hit 16 distinct bank pairs.  The TMA box is this
+// wide; the columns past `ld` are out of bounds, zero-filled on load and
+// clipped on store.
+__host__ __device__ inline int smem_stride(int ld) {
+  int s = ld < 4 ? 4 : ld;
+  while ((s & 15) != 4 && (s & 15) != 12) ++s;
+  return s;
+}
+
+int encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
+                   uint32_t box_cols, uint32_t box_rows);
 
 // 1-D bulk copy global -> shared (16-B aligned, size multiple of 16).
 __device__ __forceinline__ void bulk_load(void* dst, const void* src,

@@ -57,6 +57,7 @@ struct WarpGram {
                                       const LaneCol (&b)[TJ], const double* d, int r0,
                                       int r1, unsigned mask, RowMap rowmap) {
     const int q = threadIdx.x & 3;
+#pragma unroll 2
     for (int r = r0; r < r1; r += 4) {
       const int rr = rowmap(r + q);
       double av[TI], bv[TJ];

@@ -1,15 +1,28 @@
 """Host fp64 algebra on the small projected matrices (<= 3m x 3m).
 
-The reference does this on the host too (multivec.py:89-211, scipy LAPACK):
-the k x k Cholesky is written out so a failure names its pivot (the first
-numerically dependent column), which drives the basis-repair ladder of
-lobpcg.py:182-200 and :501-519.  Sizes here are at most 192 x 192.
+The reference does this on the host too (multivec.py:89-211, scipy LAPACK).
+Here the LAPACK routines are called directly (scipy.linalg.lapack: dpotrf,
+dtrtrs, dtrtri, dsyevr) to keep the per-iteration host latency -- which sits
+on the critical path between the two device passes -- small.
+
+The reference writes its Cholesky out row by row so that a failure names its
+pivot (the first numerically dependent column), which drives the basis-repair
+ladder of lobpcg.py:182-200 and :501-519.  dpotrf computes the same factor;
+the first pivot that is non-positive, non-finite or below the relative floor
+is recovered from its diagonal (pivot_j = R_jj^2 vs floor * G_jj), so the
+NotSPD(pivot) contract is unchanged.  The symmetric eigensolver is dsyevr,
+the driver scipy.linalg.eigh (the reference's call) uses.
 """
 
 from __future__ import annotations
 
 import numpy as np
-from scipy.linalg import eigh, solve_triangular
+from scipy.linalg import lapack
+
+_potrf = lapack.dpotrf
+_trtrs = lapack.dtrtrs
+_trtri = lapack.dtrtri
+_syevr = lapack.dsyevr
 
 
 class NotSPD(Exception):
@@ -28,22 +41,38 @@ def cholesky(g: np.ndarray, pivot_floor: float = 0.0) -> np.ndarray:
     k = g.shape[0]
     if g.ndim != 2 or g.shape[1] != k:
         raise ValueError(f"matrix must be square, got shape {g.shape}")
-    r = np.zeros((k, k))
-    for j in range(k):
-        col = r[:j, j]
-        piv = g[j, j] - col @ col
-        if not (piv > pivot_floor * g[j, j]) or not np.isfinite(piv):
-            raise NotSPD(j)
-        rjj = np.sqrt(piv)
-        r[j, j] = rjj
-        if j + 1 < k:
-            r[j, j + 1:] = (g[j, j + 1:] - col @ r[:j, j + 1:]) / rjj
+    if k == 0:
+        return np.zeros((0, 0))
+    r, info = _potrf(g, lower=0, clean=1, overwrite_a=0)
+    if info < 0:
+        raise ValueError(f"dpotrf: illegal argument {-info}")
+    ok = k if info == 0 else info - 1          # leading pivots dpotrf accepted
+    piv = np.diag(r)[:ok] ** 2
+    gd = np.diag(g)[:ok]
+    bad = ~(piv > pivot_floor * gd) | ~np.isfinite(piv)
+    if bad.any():
+        raise NotSPD(int(np.flatnonzero(bad)[0]))
+    if info > 0:
+        raise NotSPD(info - 1)
     return r
 
 
 def sym_eig(g: np.ndarray):
-    """Ascending eigenpairs of a symmetric matrix, upper triangle read."""
-    return eigh(np.asarray(g, dtype=np.float64), lower=False)
+    """Ascending eigenpairs of a symmetric matrix, upper triangle read
+    (scipy.linalg.eigh(g, lower=False), multivec.py:161-171)."""
+    g = np.asarray(g, dtype=np.float64)
+    w, v, _, _, info = _syevr(g, compute_v=1, range="A", lower=0)
+    if info != 0:
+        raise np.linalg.LinAlgError(f"dsyevr failed ({info})")
+    return w, v
+
+
+def _lsolve_t(r, b):
+    """R^{-T} b for upper R (dtrtrs, trans='T')."""
+    x, info = _trtrs(r, b, lower=0, trans=1)
+    if info != 0:
+        raise np.linalg.LinAlgError(f"dtrtrs failed ({info})")
+    return x
 
 
 def gen_sym_eig(ga: np.ndarray, gb: np.ndarray, want: int, pivot_floor: float = 0.0):
@@ -51,11 +80,13 @@ def gen_sym_eig(ga: np.ndarray, gb: np.ndarray, want: int, pivot_floor: float = 
     (multivec.py:174-211); only upper triangles are read."""
     ga = np.triu(ga) + np.triu(ga, 1).T
     r = cholesky(gb, pivot_floor)
-    t = solve_triangular(r, ga, trans="T", lower=False)
-    t = solve_triangular(r, t.T, trans="T", lower=False)
+    t = _lsolve_t(r, ga)
+    t = _lsolve_t(r, np.ascontiguousarray(t.T))
     t = 0.5 * (t + t.T)
-    vals, vecs = eigh(t, lower=False)
-    c = solve_triangular(r, vecs[:, :want], trans="N", lower=False)
+    vals, vecs = sym_eig(t)
+    c, info = _trtrs(r, vecs[:, :want], lower=0, trans=0)
+    if info != 0:
+        raise np.linalg.LinAlgError(f"dtrtrs failed ({info})")
     return vals[:want], c
 
 
@@ -66,7 +97,10 @@ def upper_inverse(r: np.ndarray) -> np.ndarray:
     k = r.shape[0]
     if k == 0:
         return np.zeros((0, 0))
-    return solve_triangular(r, np.eye(k), lower=False)
+    inv, info = _trtri(r, lower=0, unitdiag=0)
+    if info != 0:
+        raise np.linalg.LinAlgError(f"dtrtri failed ({info})")
+    return np.triu(inv)
 
 
 def scaled_cholesky(g: np.ndarray, pivot_floor: float = 0.0):
