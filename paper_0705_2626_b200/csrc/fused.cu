@@ -19,14 +19,16 @@
 // (stencil.cu), which also produces [X' W']^T A W'.
 //
 // Warp-specialised pipeline (no CTA-wide barrier inside the chunk loop):
-//   warp 0 lane 0  TMA producer + storer: refills the NST-deep input ring and
-//                  stores each finished output buffer;
+//   warp 0         TMA producer + storer (lane 0 issues): refills the NST-deep
+//                  input ring and stores each finished output buffer;
 //   warps 1..8     update + residual, one 8-row tile (all columns) per warp,
-//                  so the residual of a row needs no other warp;
-//   warps 9..16    Gram of the previous chunk's output buffer (double
-//                  buffered), overlapping the update of the next chunk.
-// mbarriers: full[s] (TMA -> update), empty[s] (update+Gram -> producer),
-// ofull[b] (update -> Gram, storer), oempty[b] (Gram + store -> update).
+//                  so the residual of a row needs no other warp; the update
+//                  coefficients live in registers for the whole kernel;
+//   warps 9..12    Gram of the finished output buffer (double buffered),
+//                  overlapping the update of the next chunk; each warp owns
+//                  up to two (tile block, row slice) items.
+// Handoffs: mbarriers for TMA (full[s]) and stage reuse (empty[s]); hardware
+// named barriers (sleeping, not polling) for output buffer full / empty.
 //
 // Shared-memory rows are padded to smem_stride(ld) doubles (4 or 12 mod 16):
 // the TMA box is wider than the block's row, the extra columns are zero-filled
@@ -35,14 +37,14 @@
 #include "common.cuh"
 #include "gram_tile.cuh"
 
-#include <cstdio>
-#include <cstdlib>
-
 namespace b2l {
 
-constexpr int STEP_NU = 8;                               // update warps
-constexpr int STEP_NG = 8;                               // Gram warps
-constexpr int STEP_THREADS = 32 * (1 + STEP_NU + STEP_NG);  // 544
+constexpr int STEP_NU = 8;                                  // update warps
+constexpr int STEP_NG = 3;                                  // Gram warps
+constexpr int STEP_GI = 2;                                  // Gram items per Gram warp
+constexpr int STEP_THREADS = 32 * (1 + STEP_NU + STEP_NG);  // 416
+constexpr int NB_OFULL = 1;                                 // named barriers 1,2
+constexpr int NB_OEMPTY = 3;                                // named barriers 3,4
 
 struct StepMaps {
   CUtensorMap in[6];   // X AX W AW P AP          box (stride, rc)
@@ -62,7 +64,6 @@ struct StepArgs {
   int tmode;
   double tinv;
   int want_ax;
-  int debug;           // B2L_STEP_DEBUG bits: 1 no update, 2 no residual, 4 no Gram
   int rc, nst;
   uint32_t stage_tx;    // TMA bytes per stage (full boxes)
   // shared-memory layout, in doubles
@@ -71,39 +72,29 @@ struct StepArgs {
   int stage_doubles;
   int out_off[5];       // buffer 0
   int out_stride;       // doubles between the two output buffers
-  int coef_off, lam_off, int_off;
+  int coef_off, lam_off, int_off, zero_off;
   int bar_off, red_off, gred_off;
   // Gram of the next step
   int a, b;
   int lcum[4], rcum[5];
-  int NI, NJ, tsI, tsJ, ts_per_cta, rs;
+  int NI, NJ, tsI, tsJ, TS, rs;
   unsigned tmask[32];
   double* partial;      // [gridDim.x][2m + a*b]
-  unsigned long long* dbg;
 };
 
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define TSTAMP(slot) \
-  do { if ((A.debug & 8) && blockIdx.x == 0 && (threadIdx.x & 31) == 0 && it < 64) A.dbg[it * 16 + (slot)] = gtime(); } while (0)
-
-// Hardware named barriers for the output-buffer handoff: waiting warps sleep
-// in the barrier unit instead of polling an mbarrier (polling cost a third of
-// all issue slots).  Ids: 1,2 = buffer full; 3,4 = buffer empty.
-constexpr int NB_OFULL = 1;
-constexpr int NB_OEMPTY = 3;
 __device__ __forceinline__ void nbar_sync(int id, int count) {
   asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 __device__ __forceinline__ void nbar_arrive(int id, int count) {
   asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
-
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ double lds64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
 }
 
 __device__ __forceinline__ void step_issue(const StepMaps& M, const StepArgs& A, double* st,
@@ -133,16 +124,20 @@ __device__ __forceinline__ void step_issue(const StepMaps& M, const StepArgs& A,
   if (A.tmode == 2 && even) bulk_load(st + A.t_off, A.tvec + r0, (uint32_t)nvalid * 8u, bar);
 }
 
+// NT = ceil(m/8) output column tiles, KS = ceil(m/4) k-steps (kw, kp <= m),
+// WGT: B = diag(d) weights the B-Gram blocks.
+template <int NT, int KS, bool WGT>
 __global__ void __launch_bounds__(STEP_THREADS, 1)
     step_kernel(const __grid_constant__ StepMaps M, const __grid_constant__ StepArgs Ain) {
   extern __shared__ __align__(128) unsigned char sm_raw[];
-  // Kernel parameters (1.7 KB with the tensor maps) overflow the constant
-  // cache when the hot loops keep re-reading fields; keep a shared copy.
+  // The parameters (1.7 KB with the tensor maps) overflow the constant cache
+  // when the hot loops re-read fields: keep a shared copy.
   __shared__ StepArgs sA;
   if (threadIdx.x == 0) sA = Ain;
   __syncthreads();
   const StepArgs& A = sA;
   double* sm = reinterpret_cast<double*>(sm_raw);
+  const uint32_t sm_base = smem_u32(sm_raw);
   double* stages = sm;
   double* coef = sm + A.coef_off;
   double* slam = sm + A.lam_off;
@@ -150,8 +145,6 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
   int* swp = spc + A.kp;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + A.bar_off);
   uint64_t* empty = full + 4;
-  uint64_t* ofull = full + 8;
-  uint64_t* oempty = full + 10;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -164,48 +157,38 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
     swp[i] = A.wpos[i];
   }
   for (int i = tid; i < A.kp; i += blockDim.x) spc[i] = A.pcols[i];
+  for (int i = tid; i < 16; i += blockDim.x) sm[A.zero_off + i] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < A.nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], STEP_NU + STEP_NG);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&ofull[b], STEP_NU);
-      mbar_init(&oempty[b], STEP_NG + 1);
-    }
     fence_mbar_init();
   }
   __syncthreads();
-  const double* Cx = coef;
-  const double* Cw = coef + m * m;
-  const double* Cp = Cw + A.kw * m;
 
   const int nchunks = (A.nrows + A.rc - 1) / A.rc;
   const int nloc = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   auto chunk_of = [&](int it) { return blockIdx.x + it * gridDim.x; };
 
-  // per-thread state carried to the final reduction
-  double s_w0 = 0.0, s_w1 = 0.0, s_a0 = 0.0, s_a1 = 0.0;  // update warps: cols lane, lane+32
-  WarpGram<2, 4> g;
-  g.zero();
-  const int gw = warp - 1 - STEP_NU;                        // Gram warp index
-  const int tsl = gw >= 0 ? gw % A.ts_per_cta : 0;
-  const int slice = gw >= 0 ? gw / A.ts_per_cta : 0;
-  const bool gactive = gw >= 0 && slice < A.rs && tsl < A.tsI * A.tsJ;
-  const int ti0 = gactive ? (tsl / A.tsJ) * 2 : 0;
-  const int tj0 = gactive ? (tsl % A.tsJ) * 4 : 0;
+  double s_w0 = 0.0, s_w1 = 0.0, s_a0 = 0.0, s_a1 = 0.0;  // update warps: norm partials
+  double gacc[STEP_GI][2][4][2];                           // Gram warps
+#pragma unroll
+  for (int u = 0; u < STEP_GI; ++u)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) gacc[u][i][j][0] = gacc[u][i][j][1] = 0.0;
+  const int gw = warp - 1 - STEP_NU;
 
   if (warp == 0) {
     // ================= producer / storer =================
-    // whole warp runs the loop (named-barrier counts are per thread); lane 0
-    // issues the TMA operations
     if (lane == 0)
       for (int j = 0; j < A.nst && j < nloc; ++j)
         step_issue(M, A, stages + (size_t)j * A.stage_doubles, &full[j], chunk_of(j));
     for (int it = 0; it < nloc; ++it) {
       const int b = it & 1;
       nbar_sync(NB_OFULL + b, STEP_THREADS);
-      TSTAMP(0);
       if (lane == 0) {
         const int r0 = chunk_of(it) * A.rc;
         const int ob = b * A.out_stride;
@@ -214,10 +197,7 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
           tma_store_2d(&M.out[k], sm + A.out_off[k] + ob, 0, r0);
         }
         bulk_commit();
-        TSTAMP(1);
-        // release this buffer as soon as its store has read it
-        bulk_wait_read<0>();
-        TSTAMP(2);
+        bulk_wait_read<0>();           // release the buffer once read
       }
       __syncwarp();
       nbar_arrive(NB_OEMPTY + b, STEP_THREADS);
@@ -225,9 +205,7 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
       if (lane == 0 && jn < nloc) {
         const int s = it % A.nst;
         mbar_wait(&empty[s], (it / A.nst) & 1);
-        TSTAMP(3);
         step_issue(M, A, stages + (size_t)s * A.stage_doubles, &full[s], chunk_of(jn));
-        TSTAMP(4);
       }
       __syncwarp();
     }
@@ -235,16 +213,38 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
   } else if (warp <= STEP_NU) {
     // ================= update + residual =================
     const int wu = warp - 1;
-    const int NT = (m + 7) >> 3;
     const int q = lane & 3, rl = lane >> 2;
+    // coefficient B-fragments for the whole kernel: C[k][cb], k = 4 ks + q
+    double cW[NT][KS], cP[NT][KS], cX[NT][KS];
+    int pcol[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = 4 * ks + q;
+      pcol[ks] = k < A.kp ? spc[k] : 0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int cb = 8 * nt + rl;
+        const bool cv = cb < m;
+        cW[nt][ks] = (cv && k < A.kw) ? coef[m * m + k * m + cb] : 0.0;
+        cP[nt][ks] = (cv && k < A.kp) ? coef[m * m + A.kw * m + k * m + cb] : 0.0;
+        cX[nt][ks] = (cv && k < m) ? coef[k * m + cb] : 0.0;
+      }
+    }
+    const int RP = m <= 32 ? 32 / m : 1;
+    const int rsub = m <= 32 ? lane / m : 0;
+    const int j0 = m <= 32 ? lane % m : lane;
+    const bool on0 = rsub < RP && j0 < m;
+    const bool on1 = m > 32 && lane + 32 < m;
+    const double lam0 = on0 ? slam[j0] : 0.0;
+    const double lam1 = on1 ? slam[lane + 32] : 0.0;
+    const int jpos0 = on0 ? swp[j0] : -1;
+    const int jpos1 = on1 ? swp[lane + 32] : -1;
     for (int it = 0; it < nloc; ++it) {
       const int s = it % A.nst, b = it & 1;
       const int r0 = chunk_of(it) * A.rc;
       const int nvalid = min(A.rc, A.nrows - r0);
       if (it >= 2) nbar_sync(NB_OEMPTY + b, STEP_THREADS);
-      if (warp == 1) TSTAMP(5);
-      mbar_wait_sleep(&full[s], (it / A.nst) & 1);
-      if (warp == 1) TSTAMP(6);
+      mbar_wait(&full[s], (it / A.nst) & 1);
       const double* st = stages + (size_t)s * A.stage_doubles;
       const double* X = st + A.in_off[0];
       const double* AX = st + A.in_off[1];
@@ -259,110 +259,94 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
       double* O4 = sm + A.out_off[4] + b * A.out_stride;
       for (int mt = wu; mt < (A.rc >> 3); mt += STEP_NU) {
         const int r = 8 * mt + rl;
-        for (int nt = 0; nt < ((A.debug & 1) ? 0 : NT); ++nt) {
-          const int cb = 8 * nt + rl;
-          const bool cv = cb < m;
-          double w0 = 0.0, w1 = 0.0, aw0 = 0.0, aw1 = 0.0, p0 = 0.0, p1 = 0.0;
-          double ap0 = 0.0, ap1 = 0.0, x0 = 0.0, x1 = 0.0, ax0 = 0.0, ax1 = 0.0;
-          // six independent DMMA chains per k-step; (W Cw) + (P Cp) and
-          // (X Cx) + P' are added as the reference does
-          // Branch-free: every chain runs kmax (all three K padded with zero
-          // operands), so the DMMAs are unconditional (no per-DMMA warpsync)
-          // and all nine operands of a k-step are loaded before its DMMAs.
-          const int kmax = max(max(A.kw, A.kp), m);
-#pragma unroll 2
-          for (int k0 = 0; k0 < kmax; k0 += 4) {
-            const int k = k0 + q;
-            const bool kw_ok = k < A.kw, kp_ok = k < A.kp, km_ok = k < m;
-            const int col = kp_ok ? spc[k] : 0;
-            const double bw_ = (kw_ok && cv) ? Cw[k * m + cb] : 0.0;
-            const double bp_ = (kp_ok && cv) ? Cp[k * m + cb] : 0.0;
-            const double bx_ = (km_ok && cv) ? Cx[k * m + cb] : 0.0;
-            const double wv = kw_ok ? W[r * sw + k] : 0.0;
-            const double awv = kw_ok ? AW[r * sw + k] : 0.0;
-            const double pv = kp_ok ? P[r * sx + col] : 0.0;
-            const double apv = kp_ok ? AP[r * sx + col] : 0.0;
-            const double xv = km_ok ? X[r * sx + k] : 0.0;
-            const double axv = km_ok ? AX[r * sx + k] : 0.0;
-            dmma_8x8x4(w0, w1, wv, bw_);
-            dmma_8x8x4(aw0, aw1, awv, bw_);
-            dmma_8x8x4(p0, p1, pv, bp_);
-            dmma_8x8x4(ap0, ap1, apv, bp_);
-            dmma_8x8x4(x0, x1, xv, bx_);
-            dmma_8x8x4(ax0, ax1, axv, bx_);
+        // six chains x NT column tiles; the A operands of a k-step are
+        // loaded once and shared by the column tiles
+        double acc[NT][6][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int c = 0; c < 6; ++c) acc[nt][c][0] = acc[nt][c][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int k = 4 * ks + q;
+          const bool kw_ok = k < A.kw, kp_ok = k < A.kp, km_ok = k < m;
+          const double wv = kw_ok ? W[r * sw + k] : 0.0;
+          const double awv = kw_ok ? AW[r * sw + k] : 0.0;
+          const double pv = kp_ok ? P[r * sx + pcol[ks]] : 0.0;
+          const double apv = kp_ok ? AP[r * sx + pcol[ks]] : 0.0;
+          const double xv = km_ok ? X[r * sx + k] : 0.0;
+          const double axv = km_ok ? AX[r * sx + k] : 0.0;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            dmma_8x8x4(acc[nt][0][0], acc[nt][0][1], wv, cW[nt][ks]);
+            dmma_8x8x4(acc[nt][1][0], acc[nt][1][1], awv, cW[nt][ks]);
+            dmma_8x8x4(acc[nt][2][0], acc[nt][2][1], pv, cP[nt][ks]);
+            dmma_8x8x4(acc[nt][3][0], acc[nt][3][1], apv, cP[nt][ks]);
+            dmma_8x8x4(acc[nt][4][0], acc[nt][4][1], xv, cX[nt][ks]);
+            dmma_8x8x4(acc[nt][5][0], acc[nt][5][1], axv, cX[nt][ks]);
           }
-          const bool bw = A.kw > 0, bp = A.kp > 0;
-          const double pn0 = (bw && bp) ? __dadd_rn(w0, p0) : (bw ? w0 : p0);
-          const double pn1 = (bw && bp) ? __dadd_rn(w1, p1) : (bw ? w1 : p1);
-          const double apn0 = (bw && bp) ? __dadd_rn(aw0, ap0) : (bw ? aw0 : ap0);
-          const double apn1 = (bw && bp) ? __dadd_rn(aw1, ap1) : (bw ? aw1 : ap1);
+        }
+        const bool bw = A.kw > 0, bp = A.kp > 0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
           const int co = 8 * nt + 2 * q;
-          const double vx[2] = {__dadd_rn(x0, pn0), __dadd_rn(x1, pn1)};
-          const double vax[2] = {__dadd_rn(ax0, apn0), __dadd_rn(ax1, apn1)};
-          const double vp[2] = {pn0, pn1};
-          const double vap[2] = {apn0, apn1};
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
+            // (W Cw) + (P Cp), then (X Cx) + P', as the reference sums them
+            const double pn = (bw && bp) ? __dadd_rn(acc[nt][0][e], acc[nt][2][e])
+                                         : (bw ? acc[nt][0][e] : acc[nt][2][e]);
+            const double apn = (bw && bp) ? __dadd_rn(acc[nt][1][e], acc[nt][3][e])
+                                          : (bw ? acc[nt][1][e] : acc[nt][3][e]);
             if (co + e < A.ldx) {
-              O0[r * sx + co + e] = vx[e];
-              O1[r * sx + co + e] = vax[e];
-              O2[r * sx + co + e] = vp[e];
-              O3[r * sx + co + e] = vap[e];
+              O0[r * sx + co + e] = __dadd_rn(acc[nt][4][e], pn);
+              O1[r * sx + co + e] = __dadd_rn(acc[nt][5][e], apn);
+              O2[r * sx + co + e] = pn;
+              O3[r * sx + co + e] = apn;
             }
           }
         }
         __syncwarp();
-        if (warp == 1) TSTAMP(7);
-        // residual of the 8 rows of this tile.  m <= 32: lane = (rsub, j),
-        // RP = 32/m rows in flight per instruction; m > 32: lane owns
-        // columns j and j+32.  Each lane's columns are fixed for the whole
-        // kernel, so its norm partials accumulate in registers.
-        if (!(A.debug & 2)) {
-          const int RP = m <= 32 ? 32 / m : 1;
-          const int rsub = m <= 32 ? lane / m : 0;
-          const int j0 = m <= 32 ? lane % m : lane;
-          const double lam0 = (rsub < RP && j0 < m) ? slam[j0] : 0.0;
-          const double lam1 = (m > 32 && lane + 32 < m) ? slam[lane + 32] : 0.0;
+        // residual of the 8 rows: m <= 32 -> lane = (rsub, j), RP rows per
+        // instruction; m > 32 -> lane owns columns j, j+32.  A lane's columns
+        // are fixed for the whole kernel: its norm partials stay in registers.
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int j = j0 + 32 * h;
-            const bool on = h == 0 ? (rsub < RP && j0 < m) : (m > 32 && j < m);
-            if (!on) continue;
-            const double lam = h == 0 ? lam0 : lam1;
-            const int jpos = swp[j];
-            double sw_ = 0.0, sa_ = 0.0;
-            for (int rr = rsub; rr < 8; rr += RP) {
-              const int row = 8 * mt + rr;
-              double wv = 0.0;
-              if (row < nvalid) {
-                const double xv = O0[row * sx + j];
-                const double av = O1[row * sx + j];
-                const double bx = A.d ? __dmul_rn(st[A.d_off + row], xv) : xv;
-                const double wf = __dsub_rn(av, __dmul_rn(bx, lam));
-                sw_ = fma(wf, wf, sw_);
-                if (A.want_ax) sa_ = fma(av, av, sa_);
-                wv = wf;
-                if (A.tmode == 1) wv = __dmul_rn(A.tinv, wf);
-                else if (A.tmode == 2) wv = __dmul_rn(st[A.t_off + row], wf);
-              }
-              if (jpos >= 0) O4[row * swn + jpos] = wv;
+        for (int h = 0; h < 2; ++h) {
+          const bool on = h == 0 ? on0 : on1;
+          if (!on) continue;
+          const int j = h == 0 ? j0 : lane + 32;
+          const double lam = h == 0 ? lam0 : lam1;
+          const int jpos = h == 0 ? jpos0 : jpos1;
+          double sw_ = 0.0, sa_ = 0.0;
+          for (int rr = rsub; rr < 8; rr += RP) {
+            const int row = 8 * mt + rr;
+            double wv = 0.0;
+            if (row < nvalid) {
+              const double xv = O0[row * sx + j];
+              const double av = O1[row * sx + j];
+              const double bx = A.d ? __dmul_rn(st[A.d_off + row], xv) : xv;
+              const double wf = __dsub_rn(av, __dmul_rn(bx, lam));
+              sw_ = fma(wf, wf, sw_);
+              if (A.want_ax) sa_ = fma(av, av, sa_);
+              wv = wf;
+              if (A.tmode == 1) wv = __dmul_rn(A.tinv, wf);
+              else if (A.tmode == 2) wv = __dmul_rn(st[A.t_off + row], wf);
             }
-            if (h == 0) {
-              s_w0 += sw_;
-              s_a0 += sa_;
-            } else {
-              s_w1 += sw_;
-              s_a1 += sa_;
-            }
+            if (jpos >= 0) O4[row * swn + jpos] = wv;
           }
-          // zero W' pad columns kwn..swn-1 of the 8 rows
-          const int npad = swn - A.kwn;
-          for (int e = lane; e < 8 * npad; e += 32)
-            O4[(8 * mt + e / npad) * swn + A.kwn + e % npad] = 0.0;
+          if (h == 0) {
+            s_w0 += sw_;
+            s_a0 += sa_;
+          } else {
+            s_w1 += sw_;
+            s_a1 += sa_;
+          }
         }
+        // zero W' pad columns kwn..swn-1 of the 8 rows
+        const int npad = swn - A.kwn;
+        for (int e = lane; e < 8 * npad; e += 32)
+          O4[(8 * mt + e / npad) * swn + A.kwn + e % npad] = 0.0;
       }
       fence_async_smem();   // generic writes -> the TMA store (async proxy)
-      if (warp == 1) TSTAMP(8);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       nbar_arrive(NB_OFULL + b, STEP_THREADS);
@@ -372,66 +356,106 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
       nbar_sync(NB_OEMPTY + (it & 1), STEP_THREADS);
   } else {
     // ================= Gram of the finished output buffers =================
+    // item = (tile block ts, row slice sl); warp gw owns items gw, gw + NG.
     const int Lblk[3] = {0, 4, 2};        // X', W', P' (indices into out_off)
     const int Rblk[4] = {0, 4, 2, 3};     // X', W', P', AP'
-    LaneCol la[2], lb[4];
+    uint32_t aadr[STEP_GI][2], bsadr[STEP_GI][4];  // lane column byte addresses (buffer 0)
+    uint32_t astr[STEP_GI][2], bstr[STEP_GI][4];   // byte stride per row
+    bool bwt[STEP_GI][4];
+    unsigned mask[STEP_GI];
+    int lo[STEP_GI], hi_[STEP_GI];
+    const int rps = A.rc / A.rs;
+    const uint32_t zero_adr = sm_base + (uint32_t)A.zero_off * 8u;
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int ci = 8 * (ti0 + i) + (lane >> 2);
-      la[i] = LaneCol{0, 0, false, false};
-      if (gactive && ci < A.a) {
-        int l = 0;
-        while (l + 1 < 3 && A.lcum[l + 1] <= ci) ++l;
-        la[i] = LaneCol{A.out_off[Lblk[l]] + (ci - A.lcum[l]), l == 1 ? swn : sx, true, false};
-      }
-    }
+    for (int u = 0; u < STEP_GI; ++u) {
+      const int item = gw + u * STEP_NG;
+      const int ts = item % A.TS, sl = item / A.TS;
+      const bool act = sl < A.rs;
+      const int ti0 = (ts / A.tsJ) * 2, tj0 = (ts % A.tsJ) * 4;
+      lo[u] = sl * rps;
+      hi_[u] = lo[u] + rps;
+      mask[u] = 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int cj = 8 * (tj0 + j) + (lane >> 2);
-      lb[j] = LaneCol{0, 0, false, false};
-      if (gactive && cj < A.b) {
-        int r = 0;
-        while (r + 1 < 4 && A.rcum[r + 1] <= cj) ++r;
-        lb[j] = LaneCol{A.out_off[Rblk[r]] + (cj - A.rcum[r]), r == 1 ? swn : sx, true,
-                        A.d != nullptr && r < 3};
-      }
-    }
-    unsigned mask = 0;
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int ti = ti0 + i, tj = tj0 + j;
-        if (gactive && ti < A.NI && tj < A.NJ) {
-          const int t = ti * A.NJ + tj;
-          if ((A.tmask[t >> 5] >> (t & 31)) & 1u) mask |= 1u << (i * 4 + j);
+      for (int i = 0; i < 2; ++i) {
+        const int ci = 8 * (ti0 + i) + (lane >> 2);
+        aadr[u][i] = zero_adr;
+        astr[u][i] = 0;
+        if (act && ci < A.a) {
+          int l = 0;
+          while (l + 1 < 3 && A.lcum[l + 1] <= ci) ++l;
+          aadr[u][i] = sm_base + 8u * (A.out_off[Lblk[l]] + (ci - A.lcum[l]));
+          astr[u][i] = 8u * (l == 1 ? swn : sx);
         }
       }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int cj = 8 * (tj0 + j) + (lane >> 2);
+        bsadr[u][j] = zero_adr;
+        bstr[u][j] = 0;
+        bwt[u][j] = false;
+        if (act && cj < A.b) {
+          int r = 0;
+          while (r + 1 < 4 && A.rcum[r + 1] <= cj) ++r;
+          bsadr[u][j] = sm_base + 8u * (A.out_off[Rblk[r]] + (cj - A.rcum[r]));
+          bstr[u][j] = 8u * (r == 1 ? swn : sx);
+          bwt[u][j] = r < 3;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int ti = ti0 + i, tj = tj0 + j;
+          if (act && ti < A.NI && tj < A.NJ) {
+            const int t = ti * A.NJ + tj;
+            if ((A.tmask[t >> 5] >> (t & 31)) & 1u) mask[u] |= 1u << (i * 4 + j);
+          }
+        }
+    }
+    const int q = lane & 3;
     for (int it = 0; it < nloc; ++it) {
       const int s = it % A.nst, b = it & 1;
       const int r0 = chunk_of(it) * A.rc;
       const int nvalid = min(A.rc, A.nrows - r0);
       const int nv4 = (nvalid + 3) & ~3;
       nbar_sync(NB_OFULL + b, STEP_THREADS);
-      if (warp == 1 + STEP_NU) TSTAMP(10);
-      if (gactive && mask && !(A.debug & 4)) {
-        const double* st = stages + (size_t)s * A.stage_doubles;
-        const int rps = A.rc / A.rs;
-        const int lo = slice * rps;
-        const int hi = min(lo + rps, nv4);
-        g.run(sm + b * A.out_stride, la, lb, A.d ? st + A.d_off : nullptr, lo, hi, mask,
-              DenseRows());
+      const uint32_t boff = 8u * (uint32_t)(b * A.out_stride);
+      const double* dst_ = stages + (size_t)s * A.stage_doubles + A.d_off;
+#pragma unroll
+      for (int u = 0; u < STEP_GI; ++u) {
+        if (!mask[u]) continue;
+        const int h = min(hi_[u], nv4);
+        for (int r = lo[u]; r < h; r += 4) {
+          const uint32_t row = (uint32_t)(r + q);
+          double av[2], bv[4];
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+            av[i] = lds64(aadr[u][i] + (astr[u][i] ? boff : 0u) + row * astr[u][i]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            bv[j] = lds64(bsadr[u][j] + (bstr[u][j] ? boff : 0u) + row * bstr[u][j]);
+          if (WGT) {
+            const double w = dst_[r + q];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (bwt[u][j]) bv[j] = __dmul_rn(w, bv[j]);
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (mask[u] & (1u << (i * 4 + j)))
+                dmma_8x8x4(gacc[u][i][j][0], gacc[u][i][j][1], av[i], bv[j]);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       nbar_arrive(NB_OEMPTY + b, STEP_THREADS);
-      if (warp == 1 + STEP_NU) TSTAMP(11);
     }
   }
   __syncthreads();
 
-  // ---- CTA reduction: residual sums (fixed order over update warps)
-  // red layout: [4][STEP_NU][32] = s_w0, s_a0, s_w1, s_a1 per (warp, lane)
+  // ---- CTA reduction: residual sums, fixed order over (update warp, lane)
   double* red = sm + A.red_off;
   const int NL = STEP_NU * 32;
   if (warp >= 1 && warp <= STEP_NU) {
@@ -444,56 +468,56 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
   __syncthreads();
   double* out = A.partial + (size_t)blockIdx.x * (2 * m + A.a * A.b);
   if (tid < m) {
-    double a = 0.0, b = 0.0;
+    double a = 0.0, bb = 0.0;
     const int RP = m <= 32 ? 32 / m : 1;
-    for (int q = 0; q < STEP_NU; ++q) {
+    for (int qq = 0; qq < STEP_NU; ++qq) {
       if (m <= 32) {
-        for (int rs_ = 0; rs_ < RP; ++rs_) {
-          a += red[q * 32 + rs_ * m + tid];
-          b += red[NL + q * 32 + rs_ * m + tid];
+        for (int r_ = 0; r_ < RP; ++r_) {
+          a += red[qq * 32 + r_ * m + tid];
+          bb += red[NL + qq * 32 + r_ * m + tid];
         }
       } else {
         const int h = tid >= 32;
-        a += red[2 * h * NL + q * 32 + (tid & 31)];
-        b += red[(2 * h + 1) * NL + q * 32 + (tid & 31)];
+        a += red[2 * h * NL + qq * 32 + (tid & 31)];
+        bb += red[(2 * h + 1) * NL + qq * 32 + (tid & 31)];
       }
     }
     out[tid] = a;
-    out[m + tid] = b;
+    out[m + tid] = bb;
   }
   __syncthreads();
-  // ---- Gram: fixed-order sum of row slices
-  double* gred = sm + A.gred_off;
-  if (gactive && slice > 0) {
+  // ---- Gram: per item, fixed-order sum over row slices
+  double* gred = sm + A.gred_off;  // [item][8 tiles][32 lanes][2]
+  if (gw >= 0) {
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int u = 0; u < STEP_GI; ++u) {
+      const int item = gw + u * STEP_NG;
+      if (item >= A.TS * A.rs) continue;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const size_t o = ((((size_t)(slice - 1) * A.ts_per_cta + tsl) * 8 + i * 4 + j) * 32 + lane) * 2;
-        gred[o] = g.acc[i][j][0];
-        gred[o + 1] = g.acc[i][j][1];
+      for (int t = 0; t < 8; ++t) {
+        gred[((size_t)item * 8 + t) * 64 + lane * 2] = gacc[u][t >> 2][t & 3][0];
+        gred[((size_t)item * 8 + t) * 64 + lane * 2 + 1] = gacc[u][t >> 2][t & 3][1];
       }
+    }
   }
   __syncthreads();
-  if (gactive && slice == 0) {
-    double* go = out + 2 * m;
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        double v0 = g.acc[i][j][0], v1 = g.acc[i][j][1];
-        for (int sl = 1; sl < A.rs; ++sl) {
-          const size_t o = ((((size_t)(sl - 1) * A.ts_per_cta + tsl) * 8 + i * 4 + j) * 32 + lane) * 2;
-          v0 += gred[o];
-          v1 += gred[o + 1];
-        }
-        const int row = 8 * (ti0 + i) + (lane >> 2);
-        const int col = 8 * (tj0 + j) + 2 * (lane & 3);
-        if (row < A.a) {
-          if (col < A.b) go[(size_t)row * A.b + col] = v0;
-          if (col + 1 < A.b) go[(size_t)row * A.b + col + 1] = v1;
-        }
-      }
+  // thread per (tile block, tile, lane): sum the row slices in order
+  double* go = out + 2 * m;
+  for (int e = tid; e < A.TS * 8 * 32; e += blockDim.x) {
+    const int ts = e / 256, t = (e / 32) & 7, ln = e & 31;
+    double v0 = 0.0, v1 = 0.0;
+    for (int sl = 0; sl < A.rs; ++sl) {
+      const int item = sl * A.TS + ts;
+      v0 += gred[((size_t)item * 8 + t) * 64 + ln * 2];
+      v1 += gred[((size_t)item * 8 + t) * 64 + ln * 2 + 1];
+    }
+    const int ti0 = (ts / A.tsJ) * 2, tj0 = (ts % A.tsJ) * 4;
+    const int row = 8 * (ti0 + (t >> 2)) + (ln >> 2);
+    const int col = 8 * (tj0 + (t & 3)) + 2 * (ln & 3);
+    if (row < A.a && ti0 + (t >> 2) < A.NI && tj0 + (t & 3) < A.NJ) {
+      if (col < A.b) go[(size_t)row * A.b + col] = v0;
+      if (col + 1 < A.b) go[(size_t)row * A.b + col + 1] = v1;
+    }
   }
 }
 
@@ -524,6 +548,365 @@ void tile_mask(int NI, int NJ, const int* lcum, int nl, const int* rcum, int nr,
     }
 }
 
+// ---------------------------------------------------------------------------
+// F1, warp-local variant (m <= 10): every compute warp owns 8 rows of a chunk
+// and does everything for them -- update, residual, and the Gram over those 8
+// rows for all needed tiles, with the whole Gram accumulator (NI x NJ 8x8
+// tiles) in its registers.  No hand-off between compute warps at all: the only
+// synchronisation is TMA -> warp (full), warp -> producer (empty / buffer
+// full) and producer -> warp (buffer empty).  8 warps keep the fp64 tensor
+// pipe busy without the load imbalance of a separate Gram warp group.
+constexpr int LOC_NW = 8;                        // compute warps (8 x 8 = 64 rows)
+constexpr int LOC_THREADS = 32 * (1 + LOC_NW);   // 288
+
+template <int NT, int KS, int NI, int NJ, bool WGT>
+__global__ void __launch_bounds__(LOC_THREADS, 1)
+    step_local_kernel(const __grid_constant__ StepMaps M, const __grid_constant__ StepArgs Ain) {
+  extern __shared__ __align__(128) unsigned char sm_raw[];
+  __shared__ StepArgs sA;
+  if (threadIdx.x == 0) sA = Ain;
+  __syncthreads();
+  const StepArgs& A = sA;
+  double* sm = reinterpret_cast<double*>(sm_raw);
+  const uint32_t sm_base = smem_u32(sm_raw);
+  double* stages = sm;
+  double* coef = sm + A.coef_off;
+  double* slam = sm + A.lam_off;
+  int* spc = reinterpret_cast<int*>(sm + A.int_off);
+  int* swp = spc + A.kp;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + A.bar_off);
+  uint64_t* empty = full + 4;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int m = A.m;
+  const int sx = A.sx, sw = A.sw, swn = A.swn;
+  const int ncoef = m * m + A.kw * m + A.kp * m;
+  for (int i = tid; i < ncoef; i += blockDim.x) coef[i] = A.coef[i];
+  for (int i = tid; i < m; i += blockDim.x) {
+    slam[i] = A.lam[i];
+    swp[i] = A.wpos[i];
+  }
+  for (int i = tid; i < A.kp; i += blockDim.x) spc[i] = A.pcols[i];
+  for (int i = tid; i < 16; i += blockDim.x) sm[A.zero_off + i] = 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < A.nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], LOC_NW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int nchunks = (A.nrows + A.rc - 1) / A.rc;
+  const int nloc = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto chunk_of = [&](int it) { return blockIdx.x + it * gridDim.x; };
+
+  double s_w0 = 0.0, s_a0 = 0.0;
+  double gacc[NI][NJ][2];
+#pragma unroll
+  for (int i = 0; i < NI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) gacc[i][j][0] = gacc[i][j][1] = 0.0;
+
+  if (warp == 0) {
+    // ================= producer / storer =================
+    if (lane == 0)
+      for (int j = 0; j < A.nst && j < nloc; ++j)
+        step_issue(M, A, stages + (size_t)j * A.stage_doubles, &full[j], chunk_of(j));
+    for (int it = 0; it < nloc; ++it) {
+      const int b = it & 1;
+      nbar_sync(NB_OFULL + b, LOC_THREADS);
+      if (lane == 0) {
+        const int r0 = chunk_of(it) * A.rc;
+        const int ob = b * A.out_stride;
+        for (int k = 0; k < 5; ++k) {
+          if (k == 4 && A.kwn == 0) continue;
+          tma_store_2d(&M.out[k], sm + A.out_off[k] + ob, 0, r0);
+        }
+        bulk_commit();
+        bulk_wait_read<0>();
+      }
+      __syncwarp();
+      nbar_arrive(NB_OEMPTY + b, LOC_THREADS);
+      const int jn = it + A.nst;
+      if (lane == 0 && jn < nloc) {
+        const int s = it % A.nst;
+        mbar_wait(&empty[s], (it / A.nst) & 1);
+        step_issue(M, A, stages + (size_t)s * A.stage_doubles, &full[s], chunk_of(jn));
+      }
+      __syncwarp();
+    }
+    if (lane == 0) bulk_wait<0>();
+  } else {
+    const int mt = warp - 1;                   // this warp's 8-row tile
+    const int q = lane & 3, rl = lane >> 2;
+    // update coefficients (B fragments) for the whole kernel
+    double cW[NT][KS], cP[NT][KS], cX[NT][KS];
+    int pcol[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = 4 * ks + q;
+      pcol[ks] = k < A.kp ? spc[k] : 0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int cb = 8 * nt + rl;
+        const bool cv = cb < m;
+        cW[nt][ks] = (cv && k < A.kw) ? coef[m * m + k * m + cb] : 0.0;
+        cP[nt][ks] = (cv && k < A.kp) ? coef[m * m + A.kw * m + k * m + cb] : 0.0;
+        cX[nt][ks] = (cv && k < m) ? coef[k * m + cb] : 0.0;
+      }
+    }
+    // residual lanes (m <= 10 < 32): lane = (rsub, j)
+    const int RP = 32 / m;
+    const int rsub = lane / m, j0 = lane % m;
+    const bool on0 = rsub < RP;
+    const double lam0 = on0 ? slam[j0] : 0.0;
+    const int jpos0 = on0 ? swp[j0] : -1;
+    // Gram lane columns: L = [X' W' P'] (a cols), R = [X' W' P' AP'] (b cols)
+    const uint32_t zero_adr = sm_base + (uint32_t)A.zero_off * 8u;
+    uint32_t la_[NI], ls_[NI], rb_[NJ], rs_[NJ];
+    bool rw_[NJ];
+    const int Lblk[3] = {0, 4, 2};
+    const int Rblk[4] = {0, 4, 2, 3};
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const int ci = 8 * i + (lane >> 2);
+      la_[i] = zero_adr;
+      ls_[i] = 0;
+      if (ci < A.a) {
+        int l = 0;
+        while (l + 1 < 3 && A.lcum[l + 1] <= ci) ++l;
+        la_[i] = sm_base + 8u * (A.out_off[Lblk[l]] + (ci - A.lcum[l]));
+        ls_[i] = 8u * (l == 1 ? swn : sx);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int cj = 8 * j + (lane >> 2);
+      rb_[j] = zero_adr;
+      rs_[j] = 0;
+      rw_[j] = false;
+      if (cj < A.b) {
+        int r = 0;
+        while (r + 1 < 4 && A.rcum[r + 1] <= cj) ++r;
+        rb_[j] = sm_base + 8u * (A.out_off[Rblk[r]] + (cj - A.rcum[r]));
+        rs_[j] = 8u * (r == 1 ? swn : sx);
+        rw_[j] = r < 3;
+      }
+    }
+    unsigned tm[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      tm[i] = 0;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int t = i * A.NJ + j;
+        if (i < A.NI && j < A.NJ && ((A.tmask[t >> 5] >> (t & 31)) & 1u)) tm[i] |= 1u << j;
+      }
+    }
+
+    for (int it = 0; it < nloc; ++it) {
+      const int s = it % A.nst, b = it & 1;
+      const int r0 = chunk_of(it) * A.rc;
+      const int nvalid = min(A.rc, A.nrows - r0);
+      if (it >= 2) nbar_sync(NB_OEMPTY + b, LOC_THREADS);
+      mbar_wait(&full[s], (it / A.nst) & 1);
+      const double* st = stages + (size_t)s * A.stage_doubles;
+      const double* X = st + A.in_off[0];
+      const double* AX = st + A.in_off[1];
+      const double* W = st + A.in_off[2];
+      const double* AW = st + A.in_off[3];
+      const double* P = st + A.in_off[4];
+      const double* AP = st + A.in_off[5];
+      const int ob = b * A.out_stride;
+      double* O0 = sm + A.out_off[0] + ob;
+      double* O1 = sm + A.out_off[1] + ob;
+      double* O2 = sm + A.out_off[2] + ob;
+      double* O3 = sm + A.out_off[3] + ob;
+      double* O4 = sm + A.out_off[4] + ob;
+      const int r = 8 * mt + rl;
+      {
+        // ---- (1) update of the 8 rows, all column tiles
+        double acc[NT][6][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int c = 0; c < 6; ++c) acc[nt][c][0] = acc[nt][c][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int k = 4 * ks + q;
+          const bool kw_ok = k < A.kw, kp_ok = k < A.kp, km_ok = k < m;
+          const double wv = kw_ok ? W[r * sw + k] : 0.0;
+          const double awv = kw_ok ? AW[r * sw + k] : 0.0;
+          const double pv = kp_ok ? P[r * sx + pcol[ks]] : 0.0;
+          const double apv = kp_ok ? AP[r * sx + pcol[ks]] : 0.0;
+          const double xv = km_ok ? X[r * sx + k] : 0.0;
+          const double axv = km_ok ? AX[r * sx + k] : 0.0;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            dmma_8x8x4(acc[nt][0][0], acc[nt][0][1], wv, cW[nt][ks]);
+            dmma_8x8x4(acc[nt][1][0], acc[nt][1][1], awv, cW[nt][ks]);
+            dmma_8x8x4(acc[nt][2][0], acc[nt][2][1], pv, cP[nt][ks]);
+            dmma_8x8x4(acc[nt][3][0], acc[nt][3][1], apv, cP[nt][ks]);
+            dmma_8x8x4(acc[nt][4][0], acc[nt][4][1], xv, cX[nt][ks]);
+            dmma_8x8x4(acc[nt][5][0], acc[nt][5][1], axv, cX[nt][ks]);
+          }
+        }
+        const bool bw = A.kw > 0, bp = A.kp > 0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int co = 8 * nt + 2 * q;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double pn = (bw && bp) ? __dadd_rn(acc[nt][0][e], acc[nt][2][e])
+                                         : (bw ? acc[nt][0][e] : acc[nt][2][e]);
+            const double apn = (bw && bp) ? __dadd_rn(acc[nt][1][e], acc[nt][3][e])
+                                          : (bw ? acc[nt][1][e] : acc[nt][3][e]);
+            if (co + e < A.ldx) {
+              O0[r * sx + co + e] = __dadd_rn(acc[nt][4][e], pn);
+              O1[r * sx + co + e] = __dadd_rn(acc[nt][5][e], apn);
+              O2[r * sx + co + e] = pn;
+              O3[r * sx + co + e] = apn;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      // ---- (2) residual of the 8 rows
+      if (on0) {
+        double sw_ = 0.0, sa_ = 0.0;
+        for (int rr = rsub; rr < 8; rr += RP) {
+          const int row = 8 * mt + rr;
+          double wv = 0.0;
+          if (row < nvalid) {
+            const double xv = O0[row * sx + j0];
+            const double av = O1[row * sx + j0];
+            const double bx = A.d ? __dmul_rn(st[A.d_off + row], xv) : xv;
+            const double wf = __dsub_rn(av, __dmul_rn(bx, lam0));
+            sw_ = fma(wf, wf, sw_);
+            if (A.want_ax) sa_ = fma(av, av, sa_);
+            wv = wf;
+            if (A.tmode == 1) wv = __dmul_rn(A.tinv, wf);
+            else if (A.tmode == 2) wv = __dmul_rn(st[A.t_off + row], wf);
+          }
+          if (jpos0 >= 0) O4[row * swn + jpos0] = wv;
+        }
+        s_w0 += sw_;
+        s_a0 += sa_;
+      }
+      {
+        const int npad = swn - A.kwn;
+        for (int e = lane; e < 8 * npad; e += 32)
+          O4[(8 * mt + e / npad) * swn + A.kwn + e % npad] = 0.0;
+      }
+      __syncwarp();
+      // ---- (3) Gram over the 8 rows, every needed tile
+      const uint32_t boff = 8u * (uint32_t)ob;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const uint32_t row = (uint32_t)(8 * mt + 4 * ks + q);
+        double av[NI], bv[NJ];
+#pragma unroll
+        for (int i = 0; i < NI; ++i) av[i] = lds64(la_[i] + (ls_[i] ? boff : 0u) + row * ls_[i]);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) bv[j] = lds64(rb_[j] + (rs_[j] ? boff : 0u) + row * rs_[j]);
+        if (WGT) {
+          const double w = st[A.d_off + row];
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+            if (rw_[j]) bv[j] = __dmul_rn(w, bv[j]);
+        }
+        // unconditional: a warp-divergence-safe predicate costs a WARPSYNC
+        // per DMMA; the unneeded tiles are simply never read back
+#pragma unroll
+        for (int i = 0; i < NI; ++i)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) dmma_8x8x4(gacc[i][j][0], gacc[i][j][1], av[i], bv[j]);
+      }
+      fence_async_smem();   // generic writes -> the TMA store (async proxy)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      nbar_arrive(NB_OFULL + b, LOC_THREADS);
+    }
+    for (int it = (nloc > 2 ? nloc : 2); it < nloc + 2; ++it)
+      nbar_sync(NB_OEMPTY + (it & 1), LOC_THREADS);
+  }
+  __syncthreads();
+
+  // ---- CTA reductions (fixed order over compute warps / lanes)
+  double* red = sm + A.red_off;
+  const int NL = LOC_NW * 32;
+  if (warp >= 1) {
+    const int o = (warp - 1) * 32 + lane;
+    red[o] = s_w0;
+    red[NL + o] = s_a0;
+  }
+  __syncthreads();
+  double* out = A.partial + (size_t)blockIdx.x * (2 * m + A.a * A.b);
+  if (tid < m) {
+    double a = 0.0, bb = 0.0;
+    const int RP = 32 / m;
+    for (int w = 0; w < LOC_NW; ++w)
+      for (int r_ = 0; r_ < RP; ++r_) {
+        a += red[w * 32 + r_ * m + tid];
+        bb += red[NL + w * 32 + r_ * m + tid];
+      }
+    out[tid] = a;
+    out[m + tid] = bb;
+  }
+  double* gred = sm + A.gred_off;   // [warp][NI*NJ tiles][32][2]
+  if (warp >= 1) {
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const size_t o = (((size_t)(warp - 1) * NI * NJ + i * NJ + j) * 32 + lane) * 2;
+        gred[o] = gacc[i][j][0];
+        gred[o + 1] = gacc[i][j][1];
+      }
+  }
+  __syncthreads();
+  double* go = out + 2 * m;
+  for (int e = tid; e < NI * NJ * 32; e += blockDim.x) {
+    const int t = e / 32, ln = e & 31;
+    const int i = t / NJ, j = t % NJ;
+    double v0 = 0.0, v1 = 0.0;
+    for (int w = 0; w < LOC_NW; ++w) {
+      const size_t o = (((size_t)w * NI * NJ + t) * 32 + ln) * 2;
+      v0 += gred[o];
+      v1 += gred[o + 1];
+    }
+    const int row = 8 * i + (ln >> 2);
+    const int col = 8 * j + 2 * (ln & 3);
+    if (row < A.a) {
+      if (col < A.b) go[(size_t)row * A.b + col] = v0;
+      if (col + 1 < A.b) go[(size_t)row * A.b + col + 1] = v1;
+    }
+  }
+}
+
+template <int NT, int KS, int NI, int NJ>
+static int launch_local(bool wgt, size_t smem, int gx, const StepMaps& M, const StepArgs& A,
+                        cudaStream_t st) {
+  auto kern = wgt ? step_local_kernel<NT, KS, NI, NJ, true>
+                  : step_local_kernel<NT, KS, NI, NJ, false>;
+  B2L_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<gx, LOC_THREADS, smem, st>>>(M, A);
+  B2L_CUDA(cudaGetLastError());
+  return 0;
+}
+
+template <int NT, int KS>
+static int launch_step(bool wgt, size_t smem, int gx, const StepMaps& M, const StepArgs& A,
+                       cudaStream_t st) {
+  auto kern = wgt ? step_kernel<NT, KS, true> : step_kernel<NT, KS, false>;
+  B2L_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<gx, STEP_THREADS, smem, st>>>(M, A);
+  B2L_CUDA(cudaGetLastError());
+  return 0;
+}
+
 int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
                 const double* w, const double* aw, int ldw, int kw, const double* p,
                 const double* ap, int kp, const int* pcols, const double* coef,
@@ -531,10 +914,11 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
                 const double* d, int tmode, double tinv, const double* tvec,
                 const int* wpos, int kwn, double* wo, int ldwn, int want_ax,
                 double* red_out, cudaStream_t st) {
-  B2L_CHECK(m >= 1 && m <= 64, -B2L_EINVAL, "step: 1 <= m <= 64");
+  B2L_CHECK(m >= 1 && m <= 16, -B2L_EINVAL, "step: 1 <= m <= 16 (larger blocks: b2l_update)");
   B2L_CHECK(nrows >= 1, -B2L_EINVAL, "step: empty block");
   B2L_CHECK(ldx >= m && (ldx & 1) == 0, -B2L_EINVAL, "step: ldx must be even and >= m");
-  B2L_CHECK(kw >= 0 && kw <= ldw && (kw == 0 || (ldw & 1) == 0), -B2L_EINVAL, "step: bad W");
+  B2L_CHECK(kw >= 0 && kw <= m && kw <= ldw && (kw == 0 || (ldw & 1) == 0), -B2L_EINVAL,
+            "step: bad W");
   B2L_CHECK(kp >= 0 && kp <= m, -B2L_EINVAL, "step: bad kp");
   B2L_CHECK(kw + kp > 0, -B2L_EINVAL, "step: nothing to update (kw + kp == 0)");
   B2L_CHECK(kwn >= 0 && kwn <= m && (kwn == 0 || (ldwn >= kwn && (ldwn & 1) == 0)),
@@ -547,7 +931,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.kp = kp;
   A.kwn = kwn;
   A.sx = smem_stride(ldx);
-  A.sw = kw ? smem_stride(ldw) : 0;
+  A.sw = kw ? smem_stride(ldw) : 4;
   A.swn = smem_stride(kwn ? ldwn : 2);
   A.d = d;
   A.tvec = tvec;
@@ -558,7 +942,6 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.tmode = tmode;
   A.tinv = tinv;
   A.want_ax = want_ax;
-  A.debug = getenv("B2L_STEP_DEBUG") ? atoi(getenv("B2L_STEP_DEBUG")) : 0;
   // Gram of the next step: L = [X' W' P'], R = [X' W' P' AP']
   A.lcum[0] = 0;
   A.lcum[1] = m;
@@ -573,21 +956,23 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.b = 3 * m + kwn;
   A.NI = (A.a + 7) / 8;
   A.NJ = (A.b + 7) / 8;
-  B2L_CHECK(A.NI * A.NJ <= 1024, -B2L_EINVAL, "step: Gram too large");
   static const unsigned char modes[12] = {2, 1, 1, 1, 0, 2, 1, 1, 0, 0, 2, 1};
   tile_mask(A.NI, A.NJ, A.lcum, 3, A.rcum, 4, modes, A.tmask);
   A.tsI = (A.NI + 1) / 2;
   A.tsJ = (A.NJ + 3) / 4;
-  const int TS = A.tsI * A.tsJ;
-  B2L_CHECK(TS <= STEP_NG, -B2L_EINVAL, "step: Gram tile blocks exceed one CTA (m too large)");
-  A.ts_per_cta = TS;
+  A.TS = A.tsI * A.tsJ;
+  const int items = STEP_NG * STEP_GI;
+  const bool local = m <= 10;       // warp-local variant
+  const int lNI = m <= 4 ? 2 : (m <= 8 ? 3 : 4);
+  const int lNJ = m <= 4 ? 2 : (m <= 8 ? 4 : 5);
+  B2L_CHECK(local || A.TS <= items, -B2L_EINVAL, "step: Gram tile blocks exceed one CTA");
   A.rs = 1;
-  while (A.rs * 2 * TS <= STEP_NG) A.rs *= 2;
-  // chunk rows (multiple of 16): 8 update warps x 8-row tiles = 64 rows, or
-  // fewer when a stage (6 blocks + d + t) would exceed ~48 KB; then the
-  // deepest TMA ring (<= 4 stages) that fits one CTA per SM.
-  const int width = 4 * A.sx + 2 * A.sw + (d ? 1 : 0) + (tmode == 2 ? 1 : 0);
-  A.rc = getenv("B2L_RC") ? atoi(getenv("B2L_RC")) : 64;
+  while (A.rs * 2 * A.TS <= items) A.rs *= 2;
+  // chunk rows: 8 update warps x 8-row tiles = 64 rows, fewer when a stage
+  // (6 blocks + d + t) would exceed ~48 KB; then the deepest TMA ring (<= 4)
+  // that fits one CTA per SM.
+  const int width = 4 * A.sx + 2 * (kw ? A.sw : 0) + (d ? 1 : 0) + (tmode == 2 ? 1 : 0);
+  A.rc = 64;
   while (A.rc > 16 && (size_t)A.rc * width * 8 > 48 * 1024) A.rc >>= 1;
   while (A.rs > 1 && A.rc / A.rs < 4) A.rs >>= 1;
   const int rc = A.rc;
@@ -609,9 +994,9 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   const int tile_w = (rc * A.swn + 15) & ~15;
   {
     const size_t tail = (size_t)2 * (4 * tile_x + tile_w) + (m * m + kw * m + kp * m) + 3 * m +
-                        64 + (size_t)2 * STEP_NU * m + 64;
-    A.nst = getenv("B2L_NST") ? atoi(getenv("B2L_NST")) : 4;
-    while (A.nst > 2 && ((size_t)A.nst * A.stage_doubles + tail) * 8 > 210 * 1024) --A.nst;
+                        64 + (size_t)4 * STEP_NU * 32 + 64;
+    A.nst = 4;
+    while (A.nst > 2 && ((size_t)A.nst * A.stage_doubles + tail) * 8 > 200 * 1024) --A.nst;
   }
   off = A.nst * A.stage_doubles;
   for (int b = 0; b < 4; ++b) {
@@ -629,12 +1014,14 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.int_off = off;
   off += (kp + m + 1) / 2 + 1;
   off = (off + 15) & ~15;
+  A.zero_off = off;
+  off += 16;
   A.bar_off = off;
-  off += 16;  // 12 mbarriers
+  off += 16;  // mbarriers
   A.red_off = off;
   const size_t red1 = (size_t)4 * STEP_NU * 32;
-  const size_t red2 = (size_t)(A.rs > 1 ? A.rs - 1 : 0) * A.ts_per_cta * 8 * 64;
-  // the Gram slice reduction reuses the (idle) stage ring after the loop
+  const size_t red2 = local ? (size_t)LOC_NW * lNI * lNJ * 64 : (size_t)A.TS * A.rs * 8 * 64;
+  // the Gram item reduction reuses the (idle) stage ring after the loop
   if (red2 <= (size_t)A.nst * A.stage_doubles) {
     A.gred_off = 0;
     off += (int)red1;
@@ -677,28 +1064,18 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   double* part = static_cast<double*>(workspace((size_t)gx * len * sizeof(double), &werr));
   if (werr) return werr;
   A.partial = part;
-  static unsigned long long* dbgbuf = nullptr;
-  if (A.debug & 8) {
-    if (!dbgbuf) cudaMalloc(&dbgbuf, 64 * 16 * 8);
-    cudaMemsetAsync(dbgbuf, 0, 64 * 16 * 8, st);
-    A.dbg = dbgbuf;
-  }
-  B2L_CUDA(cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
-  step_kernel<<<gx, STEP_THREADS, smem, st>>>(M, A);
-  B2L_CUDA(cudaGetLastError());
-  if (A.debug & 8) {
-    unsigned long long h[64 * 16];
-    cudaStreamSynchronize(st);
-    cudaMemcpy(h, dbgbuf, sizeof(h), cudaMemcpyDeviceToHost);
-    unsigned long long t0 = h[6];
-    for (int i = 0; i < 24; ++i) {
-      fprintf(stderr, "it %2d:", i);
-      for (int k = 0; k < 12; ++k)
-        fprintf(stderr, " %7lld", h[i * 16 + k] ? (long long)(h[i * 16 + k] - t0) : -1LL);
-      fprintf(stderr, "\n");
-    }
-  }
+  const bool wgt = d != nullptr;
+  int rcode;
+  if (local) {
+    B2L_CHECK(rc == 8 * LOC_NW, -B2L_EINVAL, "step: warp-local variant needs 64-row chunks");
+    if (m <= 4) rcode = launch_local<1, 1, 2, 2>(wgt, smem, gx, M, A, st);
+    else if (m <= 8) rcode = launch_local<1, 2, 3, 4>(wgt, smem, gx, M, A, st);
+    else rcode = launch_local<2, 3, 4, 5>(wgt, smem, gx, M, A, st);
+  } else if (m <= 4) rcode = launch_step<1, 1>(wgt, smem, gx, M, A, st);
+  else if (m <= 8) rcode = launch_step<1, 2>(wgt, smem, gx, M, A, st);
+  else if (m <= 12) rcode = launch_step<2, 3>(wgt, smem, gx, M, A, st);
+  else rcode = launch_step<2, 4>(wgt, smem, gx, M, A, st);
+  if (rcode) return rcode;
   sum_parts_kernel<<<(len + 255) / 256, 256, 0, st>>>(part, gx, len, red_out);
   B2L_CUDA(cudaGetLastError());
   return 0;
