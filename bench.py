@@ -17,8 +17,10 @@ iteration of the hot loop (lobpcg.py:418-540) on that state.
 
 --impl reference runs the CPU oracle alone (the reference is a Python
 package; its restatement oracle/lobpcg_oracle.py is pinned bit-exact to it).
-Multi-GPU (torchrun, N>1): one independent C2 solve per rank ("replicas";
-the z-slab partition is not yet in this build), max-over-ranks time.
+Multi-GPU (torchrun, N>1): weak scaling, one distributed solve on a
+128 x 128 x 128N grid split in z-slabs (one C2-sized slab per GPU; halo
+send/recv and Gram all-reduce over NCCL); value = N x global it/s
+(C2-slab-iterations/s), max-over-ranks time.
 """
 
 from __future__ import annotations
@@ -60,7 +62,8 @@ def config_dict(n_gpus):
         "max_iter": MAX_ITER,
         "seed": SEED,
         "l2": "inputs larger than L2 (10 live 168 MB blocks per iteration >> 126 MB L2)",
-        "parallelism": f"replicas x{n_gpus}" if n_gpus > 1 else "single GPU",
+        "parallelism": (f"z-slab x{n_gpus} (grid 128x128x{128 * n_gpus}, one C2-size slab per "
+                        "GPU, NCCL halo + Gram all-reduce)") if n_gpus > 1 else "single GPU",
     }
 
 
@@ -171,11 +174,20 @@ def run_gpu(args):
         if world > 1:
             dist.barrier()
 
-    n = N_GRID ** 3
     s = float((N_GRID + 1) ** 2)
-    A = pk.Laplacian3D((N_GRID,) * 3, scale=s)
+    if world > 1:
+        # weak scaling: a 128 x 128 x (128 P) grid, one C2-sized z-slab per
+        # GPU, one-plane halos + Gram all-reduces over NCCL
+        from paper_0705_2626_b200.distributed import SlabLaplacian3D, slab_initial_block
+
+        A = SlabLaplacian3D((N_GRID, N_GRID, N_GRID * world), scale=s)
+        x0 = slab_initial_block(A.grid, A.part, M_BLOCK, SEED)
+        n = A.local_rows
+    else:
+        n = N_GRID ** 3
+        A = pk.Laplacian3D((N_GRID,) * 3, scale=s)
+        x0 = np.random.Generator(np.random.PCG64(SEED)).uniform(-1.0, 1.0, size=(n, M_BLOCK))
     T = pk.jacobi_preconditioner(A)
-    x0 = np.random.Generator(np.random.PCG64(SEED)).uniform(-1.0, 1.0, size=(n, M_BLOCK))
     cfg = pk.SolverConfig(block_size=M_BLOCK, tol=TOL, max_iter=MAX_ITER, seed=SEED)
 
     def new_run():
@@ -282,7 +294,7 @@ def run_gpu(args):
         e2e_s = float(t.item())
     it_used = rep.iterations_used
     e2e_val = world * it_used / e2e_s
-    exact = pk.exact_eigenvalues((N_GRID,) * 3, M_BLOCK, scale=s)
+    exact = pk.exact_eigenvalues(A.grid, M_BLOCK, scale=s)
 
     line = {
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,

@@ -240,7 +240,13 @@ class LOBPCGRun:
         if m > n:
             raise ValueError(f"block size {m} exceeds the constrained problem dimension {n} - 0")
         self.a, self.b, self.t = a, b, t
-        self.m, self.n = m, n
+        # z-slab runs (distributed.SlabLaplacian3D): blocks hold this rank's
+        # rows; every small reduction is summed over ranks before the host
+        # reads it, so all ranks take identical decisions
+        self.n_global = n
+        rows = int(getattr(a, "local_rows", n))
+        self._allreduce = getattr(a, "allreduce_", None)
+        self.m, self.n = m, rows
         self.dev = getattr(a, "device", None) or torch.device("cuda", torch.cuda.current_device())
         _lib.load()
         _lib.ensure_device(self.dev.index if self.dev.index is not None else 0)
@@ -273,19 +279,31 @@ class LOBPCGRun:
         if x0 is not None:
             if isinstance(x0, torch.Tensor):
                 x0t = x0.detach().to(self.dev, torch.float64)
-                if tuple(x0t.shape) != (n, m):
+                if tuple(x0t.shape) not in ((n, m), (rows, m)):
                     raise ValueError(f"x0 has shape {tuple(x0t.shape)}, expected ({n}, {m})")
                 if not bool(torch.isfinite(x0t).all()):
                     raise ValueError("x0 contains non-finite entries")
             else:
                 xh = np.array(x0, dtype=np.float64, copy=True)
-                if xh.shape != (n, m):
+                # a z-slab run also accepts this rank's rows only
+                if xh.shape not in ((n, m), (rows, m)):
                     raise ValueError(f"x0 has shape {xh.shape}, expected ({n}, {m})")
                 if not np.all(np.isfinite(xh)):
                     raise ValueError("x0 contains non-finite entries")
                 x0t = xh
+        elif rows != n:
+            from .distributed import slab_initial_block
+
+            x0t = slab_initial_block(a.grid, a.part, m, cfg.seed)
         else:
             x0t = np.random.Generator(np.random.PCG64(cfg.seed)).uniform(-1.0, 1.0, size=(n, m))
+        if rows != n and x0t.shape[0] == n:
+            r0 = a.part.z0 * a.plane
+            x0t = x0t[r0:r0 + rows]
+        if b is not None and self.bdiag is not None and self.bdiag.numel() == n and rows != n:
+            r0 = a.part.z0 * a.plane
+            self.bdiag = self.bdiag[r0:r0 + rows].contiguous()
+        n = rows
 
         ld = dv.even(m)
         self.ld = ld
@@ -319,10 +337,24 @@ class LOBPCGRun:
         self.done = False
         self.drift_repairs = 0
         self.f1_pending = False    # self.red holds F1 results for this step
+        self.sg_pending = False    # self.g2 / AW hold the stencil pass for this step
 
         self._initial()
 
     # ------------------------------------------------------------ helpers
+    def _reduce(self, t):
+        """Sum a device reduction over the z-slab ranks (identity on one)."""
+        if self._allreduce is not None:
+            self._allreduce(t)
+        return t
+
+    def _gram(self, *args, **kw):
+        return self._reduce(dv.gram(*args, **kw))
+
+    def _residual(self, *args):
+        dv.residual(*args)
+        self._reduce(args[-1])
+
     def _wmask(self, nblocks):
         return ((1 << nblocks) - 1) if self.bdiag is not None else 0
 
@@ -340,7 +372,7 @@ class LOBPCGRun:
 
     def _gram_xx(self):
         """X^T B X (upper triangle computed, mirrored on the host)."""
-        g = _timed("gram_drift", lambda: dv.gram(self.n, [(self.X, self.m)], [(self.X, self.m)],
+        g = _timed("gram_drift", lambda: self._gram(self.n, [(self.X, self.m)], [(self.X, self.m)],
                                                  self._wmask(1), self.bdiag, pair_mode=_UPPER))
         return _mirror_upper(dv.to_host(g))
 
@@ -355,7 +387,7 @@ class LOBPCGRun:
         """_refresh_ritz (lobpcg.py:280-296) from the raw Gram X^T B X."""
         _, minv = scaled_cholesky(gxx)             # NotSPD propagates
         self._rotate_x(minv)
-        gxa = dv.to_host(dv.gram(self.n, [(self.X, self.m)], [(self.AX, self.m)],
+        gxa = dv.to_host(self._gram(self.n, [(self.X, self.m)], [(self.AX, self.m)],
                                  pair_mode=_UPPER))
         lam, q = sym_eig(gxa)
         self._rotate_x(q)
@@ -383,7 +415,7 @@ class LOBPCGRun:
         dv.update(n, m, self.X, None, Md, self.X2, None)
         self.X, self.X2 = self.X2, self.X
         self._apply_a_plain(self.X, self.AX, m)      # lobpcg.py:403
-        gxa = dv.to_host(dv.gram(n, [(self.X, m)], [(self.AX, m)], pair_mode=_UPPER))
+        gxa = dv.to_host(self._gram(n, [(self.X, m)], [(self.AX, m)], pair_mode=_UPPER))
         lam, q = sym_eig(gxa)                        # lobpcg.py:404
         self._rotate_x(q)
         self.lam = lam
@@ -399,18 +431,32 @@ class LOBPCGRun:
         try:
             jprev = np.flatnonzero(self.active)
             kst = jprev.size
-            G1 = sums = None
+            G1 = sums = G2 = None
+            g2_rows = m + kst
             if self.f1_pending:
                 # F1 of the previous step already produced this step's drift
-                # Gram, residual norms, W and every non-AW Gram block
+                # Gram, residual norms, W and every non-AW Gram block; the
+                # stencil pass queued right behind it produced A W and
+                # [X W]^T A W.  One host synchronisation for both.
                 a, b = 2 * m + kst, 3 * m + kst
-                red = self._fetch(self.red, self.h_red, 2 * m + a * b)
+                nred = 2 * m + a * b
+                self._reduce(self.red[:nred])
+                self.h_red[:nred].copy_(self.red[:nred], non_blocking=True)
+                if self.sg_pending:
+                    self._reduce(self.g2[:g2_rows * kst])
+                    self.h_g2[:g2_rows * kst].copy_(self.g2[:g2_rows * kst], non_blocking=True)
+                if self.dev.type == "cuda":
+                    torch.cuda.current_stream(self.dev).synchronize()
+                red = self.h_red[:nred].numpy().copy()
                 sums = red[:2 * m]
                 G1 = red[2 * m:].reshape(a, b)
                 gxx = _mirror_upper(G1[:m, :m])
+                if self.sg_pending:
+                    G2 = self.h_g2[:g2_rows * kst].numpy().copy().reshape(g2_rows, kst)
             else:
                 gxx = self._gram_xx()
             self.f1_pending = False
+            self.sg_pending = False
             # drift check (lobpcg.py:419-428)
             drift = np.abs(gxx - np.eye(m)).max()
             if drift > DRIFT_LIMIT:
@@ -419,7 +465,7 @@ class LOBPCGRun:
                 except NotSPD:
                     raise _Failure("BasisDegeneracy")
                 self.drift_repairs += 1
-                G1 = sums = None
+                G1 = sums = G2 = None
                 if cfg.verbosity >= 2:
                     print(f"  it {it:4d}  Ritz block re-orthonormalized (drift {drift:.1e})")
 
@@ -429,7 +475,7 @@ class LOBPCGRun:
                 pos = np.full(m, -1, dtype=np.int32)
                 pos[jprev] = np.arange(kst, dtype=np.int32)
                 (lam_d,), (pos_d,) = self.pin.upload([self.lam], [pos])
-                _timed("residual", lambda: dv.residual(
+                _timed("residual", lambda: self._residual(
                     n, m, self.X, self.AX, self.bdiag, lam_d, self.tmode, self.tinv, self.tvec,
                     pos_d, kst, W, cfg.relative_tol, self.sums))
                 sums = self._fetch(self.sums, self.h_red, 2 * m)
@@ -468,31 +514,28 @@ class LOBPCGRun:
             sel = np.searchsorted(jprev, J)          # W columns of J
             if self.t_generic is not None:
                 W, AW, kst, sel = self._generic_precondition(W, sel, J.size)
-                G1 = None                            # F1 saw the raw residual
+                G1 = G2 = None                       # F1 saw the raw residual
+                g2_rows = m + kst
 
             # A W (+ [X W]^T A W in the same pass for the built-in stencil)
-            g2_rows = m + kst
             g2 = self.g2[:g2_rows * kst].view(g2_rows, kst)
-            if self.use_sgram:
-                gr = self.a.grid
-                _timed("stencil", lambda: dv.stencil7_gram(
-                    W, AW, gr.nx, gr.ny, gr.nz, self.a.scale, self.X, m, kst, g2))
-            else:
-                self._apply_a_plain(W, AW, kst)
-                _timed("gram_aw", lambda: dv.gram(n, [(self.X, m), (W, kst)], [(AW, kst)],
-                                                  out=g2))
+            if G2 is None:
+                self._launch_aw(W, AW, kst, g2)
             G1dev = None
             if G1 is None:
                 if self.have_p:
                     L = [(self.X, m), (W, kst), (self.P, m)]
                     R = L + [(self.AP, m)]
-                    G1dev = _timed("gram", lambda: dv.gram(n, L, R, self._wmask(3), self.bdiag,
+                    G1dev = _timed("gram", lambda: self._gram(n, L, R, self._wmask(3), self.bdiag,
                                                            pair_mode=_MODES_P))
                 else:
                     L = [(self.X, m), (W, kst)]
-                    G1dev = _timed("gram", lambda: dv.gram(n, L, L, self._wmask(2), self.bdiag,
+                    G1dev = _timed("gram", lambda: self._gram(n, L, L, self._wmask(2), self.bdiag,
                                                            pair_mode=_MODES_NOP))
-            G2 = self._fetch(g2, self.h_g2, g2_rows * kst).reshape(g2_rows, kst)
+            if G2 is None:
+                if self.use_sgram:
+                    self._reduce(g2)   # the callback path reduced inside self._gram
+                G2 = self._fetch(g2, self.h_g2, g2_rows * kst).reshape(g2_rows, kst)
             if G1dev is not None:
                 G1 = dv.to_host(G1dev)
             self._rayleigh_ritz(G1, G2, J, sel, kst, W, AW)
@@ -502,6 +545,17 @@ class LOBPCGRun:
             return False
         self.it += 1
         return True
+
+    def _launch_aw(self, W, AW, kst, g2):
+        """A W on the stored columns of W and G2 = [X W]^T A W (K1+K5b for
+        the built-in stencil; callback + K5 otherwise)."""
+        m, n = self.m, self.n
+        if self.use_sgram:
+            _timed("stencil", lambda: self.a.stencil_gram_into(W, AW, self.X, m, kst, g2))
+        else:
+            self._apply_a_plain(W, AW, kst)
+            _timed("gram_aw", lambda: self._gram(n, [(self.X, m), (W, kst)], [(AW, kst)],
+                                              out=g2))
 
     def _generic_precondition(self, W, sel, kj):
         """User preconditioner callback on the active residual block
@@ -643,6 +697,15 @@ class LOBPCGRun:
         self.P, self.P2 = self.P2, self.P
         self.AP, self.AP2 = self.AP2, self.AP
         self.have_p = True
+        if self.use_f1 and self.use_sgram and self.t_generic is None:
+            # queue the next step's stencil pass right behind F1: it needs
+            # only W' and X', and its columns are a superset of the next
+            # active set, so the lock test can run after it
+            k_next = J.size
+            Wn, AWn = self._wview(k_next)
+            g2n = self.g2[:(m + k_next) * k_next].view(m + k_next, k_next)
+            self._launch_aw(Wn, AWn, k_next, g2n)
+            self.sg_pending = True
         self.lam = lam_new
 
     def _check_state(self, gxx):
@@ -662,7 +725,7 @@ class LOBPCGRun:
             try:
                 self._refresh_ritz(self._gram_xx())
                 lam_d = dv.to_device(self.lam, self.dev)
-                dv.residual(n, m, self.X, self.AX, self.bdiag, lam_d, 0, 1.0, None, None, 0,
+                self._residual(n, m, self.X, self.AX, self.bdiag, lam_d, 0, 1.0, None, None, 0,
                             None, False, self.sums)
                 norms = np.sqrt(dv.to_host(self.sums)[:m])
             except NotSPD:

@@ -215,6 +215,12 @@ class Laplacian3D(LinearOperator):
         g = self.grid
         dv.stencil7(x, out, g.nx, g.ny, g.nz, self.scale)
 
+    def stencil_gram_into(self, x, out, xb, m, kw, gram_out) -> None:
+        """out = A x and gram_out = [xb[:, :m] ; x[:, :kw]]^T out[:, :kw] in
+        one pass (K1+K5b)."""
+        g = self.grid
+        dv.stencil7_gram(x, out, g.nx, g.ny, g.nz, self.scale, xb, m, kw, gram_out)
+
     def _apply(self, x):
         n, k = x.shape
         ld = dv.even(k)
