@@ -20,8 +20,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "lib"
 LIBNAME = "libb200lobpcg.so"
-SOURCES = ["abi.cu", "stencil.cu", "blockops.cu", "fused.cu"]
-HEADERS = ["common.cuh", "gram_tile.cuh"]
+SOURCES = ["abi.cu", "stencil.cu", "stencil_gram.cu", "blockops.cu", "fused.cu"]
+HEADERS = ["common.cuh", "gram_tile.cuh", "stencil.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

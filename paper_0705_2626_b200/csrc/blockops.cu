@@ -199,7 +199,6 @@ __global__ void __launch_bounds__(GRAM_THREADS) gram_kernel(GramArgs A) {
   }
 }
 
-__global__ void sum_parts_kernel(const double* partial, int nparts, int len, double* out);
 
 struct HostBlock {
   const double* p;
@@ -338,9 +337,7 @@ int gram(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr,
   gram_kernel<<<dim3(gx, gy), GRAM_THREADS, smem, st>>>(A);
   B2L_CUDA(cudaGetLastError());
   const int tot = A.a * A.b;
-  sum_parts_kernel<<<(tot + 255) / 256, 256, 0, st>>>(part, gx, tot, out);
-  B2L_CUDA(cudaGetLastError());
-  return 0;
+  return sum_parts(part, gx, tot, out, st);
 }
 
 // =========================================================================
@@ -408,13 +405,41 @@ __global__ void __launch_bounds__(256) resid_kernel(ResidArgs A) {
   }
 }
 
-__global__ void sum_parts_kernel(const double* partial, int nparts, int len,
-                                 double* out) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= len) return;
-  double s = 0.0;
-  for (int c = 0; c < nparts; ++c) s += partial[(size_t)c * len + e];
-  out[e] = s;
+// out[e] = sum_c partial[c][e].  A 32 x 32 block per 32 outputs: column
+// lane x, part slice y (parts y, y+32, ...; four independent chains), then a
+// fixed-order sum of the 32 slices -- deterministic, and latency bound on
+// nparts/128 dependent loads instead of nparts.
+__global__ void __launch_bounds__(1024) sum_parts_kernel(const double* partial, int nparts,
+                                                         int len, double* out) {
+  __shared__ double red[32][33];
+  const int e = blockIdx.x * 32 + threadIdx.x;
+  const int y = threadIdx.y;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (e < len) {
+    int c = y;
+    for (; c + 96 < nparts; c += 128) {
+      s0 += partial[(size_t)c * len + e];
+      s1 += partial[(size_t)(c + 32) * len + e];
+      s2 += partial[(size_t)(c + 64) * len + e];
+      s3 += partial[(size_t)(c + 96) * len + e];
+    }
+    for (; c < nparts; c += 32) s0 += partial[(size_t)c * len + e];
+  }
+  red[y][threadIdx.x] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (y == 0 && e < len) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) s += red[k][threadIdx.x];
+    out[e] = s;
+  }
+}
+
+int sum_parts(const double* partial, int nparts, int len, double* out, cudaStream_t st) {
+  if (len <= 0) return 0;
+  sum_parts_kernel<<<(len + 31) / 32, dim3(32, 32), 0, st>>>(partial, nparts, len, out);
+  B2L_CUDA(cudaGetLastError());
+  return 0;
 }
 
 int residual(int nrows, int m, const double* x, const double* ax, int ldx,
@@ -452,9 +477,7 @@ int residual(int nrows, int m, const double* x, const double* ax, int ldx,
   const size_t smem = (size_t)2 * A.rp * m * sizeof(double);
   resid_kernel<<<blocks, 256, smem, st>>>(A);
   B2L_CUDA(cudaGetLastError());
-  sum_parts_kernel<<<(2 * m + 127) / 128, 128, 0, st>>>(part, blocks, 2 * m, sums_out);
-  B2L_CUDA(cudaGetLastError());
-  return 0;
+  return sum_parts(part, blocks, 2 * m, sums_out, st);
 }
 
 // =========================================================================

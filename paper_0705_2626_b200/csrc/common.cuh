@@ -46,6 +46,8 @@ enum : int {
 // driven by one host thread / one stream per device.
 void* workspace(size_t bytes, int* err);
 int sm_count();
+// out[e] = sum over parts c of partial[c * len + e] (fixed order, deterministic)
+int sum_parts(const double* partial, int nparts, int len, double* out, cudaStream_t st);
 
 // ------------------------------------------------------------ tensor maps
 int encode_tmap_4d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1,

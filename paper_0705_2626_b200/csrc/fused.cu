@@ -521,7 +521,6 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
   }
 }
 
-__global__ void sum_parts_kernel(const double* partial, int nparts, int len, double* out);
 
 // Needed 8x8 tiles of a Gram with column segments lcum/rcum and block-pair
 // modes (0 skip, 1 full, 2 upper triangle).
@@ -1076,9 +1075,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   else if (m <= 12) rcode = launch_step<2, 3>(wgt, smem, gx, M, A, st);
   else rcode = launch_step<2, 4>(wgt, smem, gx, M, A, st);
   if (rcode) return rcode;
-  sum_parts_kernel<<<(len + 255) / 256, 256, 0, st>>>(part, gx, len, red_out);
-  B2L_CUDA(cudaGetLastError());
-  return 0;
+  return sum_parts(part, gx, len, red_out, st);
 }
 
 }  // namespace b2l

@@ -16,24 +16,10 @@
 // Arithmetic order is exactly the reference's: ((((((6c - x-) - x+) - y-) -
 // y+) - z-) - z+) then * scale, with explicit _rn intrinsics (no FMA
 // contraction), so the result is bitwise equal to the numpy reference.
-#include "common.cuh"
-#include "gram_tile.cuh"
+#include "stencil.cuh"
 
 namespace b2l {
 
-struct StencilGeom {
-  int nx, ny, nz;  // local grid (nz = owned planes)
-  int ld;          // doubles per point (row stride), even
-  int TX, TY;      // interior tile
-  int tiles_x;
-  int zchunk;
-  int nelem;       // TX*TY*ld
-  int has_lo, has_hi;
-  double scale;
-  uint32_t stage_bytes;  // (TX+2)(TY+2) ld 8
-  uint32_t stage_stride; // stage_bytes rounded to 128
-  uint32_t out_stride;   // TX TY ld 8 rounded to 128
-};
 
 template <int EPT, int NST>
 __global__ void __launch_bounds__(256)
@@ -145,256 +131,9 @@ __global__ void __launch_bounds__(256)
   if (tid == 0) bulk_wait<0>();
 }
 
-// ------------------------------------------------------ stencil + Gram
-// Same z-streaming stencil, plus the Gram blocks of the Rayleigh-Ritz step
-// that involve A W (reference lobpcg.py:327 gram(x, aw) and :325 gram(w, aw)):
-//   G = [X ; W]^T (A W)   ((m + kw) x kw)
-// accumulated on the fp64 tensor cores from the shared-memory tiles the
-// stencil already holds (W centre plane, A W output plane) plus one TMA box of
-// X per plane, so A W is never re-read from HBM.
-struct SGramGeom {
-  int m, ldx, kw;   // X columns / leading dim, W columns used
-  int a, b;         // m + kw, kw
-  int NI, NJ, tsI, tsJ, ts_per_cta, rs;
-  unsigned tmask[8];
-  uint32_t x_bytes, x_stride;
-  double* partial;  // [grid][a*b]
-};
-
-template <int EPT, int NST>
-__global__ void __launch_bounds__(256)
-    stencil7_gram_kernel(const __grid_constant__ CUtensorMap tin,
-                         const __grid_constant__ CUtensorMap thalo,
-                         const __grid_constant__ CUtensorMap tout,
-                         const __grid_constant__ CUtensorMap tx_map, StencilGeom g,
-                         SGramGeom G) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  unsigned char* base = smem_raw;
-  auto stage = [&](int s) -> double* {
-    return reinterpret_cast<double*>(base + s * g.stage_stride);
-  };
-  double* outbuf0 = reinterpret_cast<double*>(base + NST * g.stage_stride);
-  double* outbuf1 = reinterpret_cast<double*>(base + NST * g.stage_stride + g.out_stride);
-  double* xbuf0 = reinterpret_cast<double*>(base + NST * g.stage_stride + 2 * g.out_stride);
-  double* xbuf1 = reinterpret_cast<double*>(base + NST * g.stage_stride + 2 * g.out_stride +
-                                            G.x_stride);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(base + NST * g.stage_stride + 2 * g.out_stride +
-                                              2 * G.x_stride);
-  uint64_t* xbar = bar + NST;
-
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int tx0 = (blockIdx.x % g.tiles_x) * g.TX;
-  const int ty0 = (blockIdx.x / g.tiles_x) * g.TY;
-  const int z0 = blockIdx.y * g.zchunk;
-  const int z1 = min(g.nz, z0 + g.zchunk);
-
-  // Gram job of this warp
-  const int tsl = warp % G.ts_per_cta;
-  const int slice = warp / G.ts_per_cta;
-  const bool gactive = slice < G.rs && tsl < G.tsI * G.tsJ && z0 < z1;
-  const int ti0 = gactive ? (tsl / G.tsJ) * 2 : 0;
-  const int tj0 = gactive ? (tsl % G.tsJ) * 4 : 0;
-  int acol[2], bcol[4];
-  bool aok[2], aisx[2], bok[4];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int ci = 8 * (ti0 + i) + (lane >> 2);
-    aok[i] = ci < G.a;
-    aisx[i] = ci < G.m;
-    acol[i] = aisx[i] ? ci : ci - G.m;
-  }
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int cj = 8 * (tj0 + j) + (lane >> 2);
-    bok[j] = cj < G.b;
-    bcol[j] = cj;
-  }
-  unsigned mask = 0;
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int ti = ti0 + i, tj = tj0 + j;
-      if (gactive && ti < G.NI && tj < G.NJ) {
-        const int t = ti * G.NJ + tj;
-        if ((G.tmask[t >> 5] >> (t & 31)) & 1u) mask |= 1u << (i * 4 + j);
-      }
-    }
-  WarpGram<2, 4> acc;
-  acc.zero();
-  const int npts = g.TX * g.TY;
-  const int rps = ((npts + 3) / 4 + G.rs - 1) / G.rs * 4;  // rows per slice
-  const int glo = slice * rps;
-  const int ghi = min(glo + rps, (npts + 3) & ~3);
-
-  if (z0 < z1) {
-    const int nplanes = (z1 - z0) + 2;
-    if (tid == 0) {
-#pragma unroll
-      for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
-      mbar_init(&xbar[0], 1);
-      mbar_init(&xbar[1], 1);
-      fence_mbar_init();
-    }
-    __syncthreads();
-    auto issue = [&](int q) {
-      const int z = z0 - 1 + q;
-      const int s = q % NST;
-      mbar_expect_tx(&bar[s], g.stage_bytes);
-      if (z < 0 && g.has_lo)
-        tma_load_4d(stage(s), &thalo, &bar[s], 0, tx0 - 1, ty0 - 1, 0);
-      else if (z >= g.nz && g.has_hi)
-        tma_load_4d(stage(s), &thalo, &bar[s], 0, tx0 - 1, ty0 - 1, 1);
-      else
-        tma_load_4d(stage(s), &tin, &bar[s], 0, tx0 - 1, ty0 - 1, z);
-    };
-    auto issue_x = [&](int z) {
-      const int sl = (z - z0) & 1;
-      mbar_expect_tx(&xbar[sl], G.x_bytes);
-      tma_load_4d(sl ? xbuf1 : xbuf0, &tx_map, &xbar[sl], 0, tx0, ty0, z);
-    };
-    if (tid == 0) {
-      for (int q = 0; q < NST && q < nplanes; ++q) issue(q);
-      issue_x(z0);
-      if (z0 + 1 < z1) issue_x(z0 + 1);
-    }
-    const int rowlen = g.TX * g.ld;
-    const int ystride = (g.TX + 2) * g.ld;
-    int off[EPT];
-    bool valid[EPT];
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int e = tid + 256 * i;
-      valid[i] = e < g.nelem;
-      const int ty = valid[i] ? e / rowlen : 0;
-      const int rem = valid[i] ? e - ty * rowlen : 0;
-      off[i] = (ty + 1) * ystride + g.ld + rem;
-    }
-    double prev[EPT], cur[EPT];
-    mbar_wait(&bar[0], 0);
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) prev[i] = valid[i] ? stage(0)[off[i]] : 0.0;
-    mbar_wait(&bar[1 % NST], (1 / NST) & 1);
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) cur[i] = valid[i] ? stage(1 % NST)[off[i]] : 0.0;
-    __syncthreads();
-    if (tid == 0 && NST < nplanes) issue(NST);
-
-    const double six = 6.0;
-    const double sc = g.scale;
-    const int q4 = lane & 3;
-    for (int z = z0; z < z1; ++z) {
-      const int q = z - z0 + 1;
-      const int sn = (q + 1) % NST;
-      mbar_wait(&bar[sn], ((q + 1) / NST) & 1);
-      const double* P = stage(q % NST);
-      const double* N = stage(sn);
-      double* O = (z & 1) ? outbuf1 : outbuf0;
-#pragma unroll
-      for (int i = 0; i < EPT; ++i) {
-        if (valid[i]) {
-          const int o = off[i];
-          const double nx_ = N[o];
-          double r = __dmul_rn(six, cur[i]);
-          r = __dsub_rn(r, P[o - g.ld]);
-          r = __dsub_rn(r, P[o + g.ld]);
-          r = __dsub_rn(r, P[o - ystride]);
-          r = __dsub_rn(r, P[o + ystride]);
-          r = __dsub_rn(r, prev[i]);
-          r = __dsub_rn(r, nx_);
-          O[tid + 256 * i] = __dmul_rn(sc, r);
-          prev[i] = cur[i];
-          cur[i] = nx_;
-        }
-      }
-      __syncthreads();
-      // Gram over the tile's points: rows = points, [X ; W]^T (A W)
-      if (gactive && mask) {
-        const int xs = (z - z0) & 1;
-        mbar_wait(&xbar[xs], ((z - z0) >> 1) & 1);
-        const double* Xb = xs ? xbuf1 : xbuf0;
-        for (int r = glo; r < ghi; r += 4) {
-          const int rr = r + q4;
-          const bool rok = rr < npts;
-          const int rh = (rr / g.TX + 1) * (g.TX + 2) + (rr % g.TX) + 1;
-          double av[2], bv[4];
-#pragma unroll
-          for (int i = 0; i < 2; ++i)
-            av[i] = (aok[i] && rok) ? (aisx[i] ? Xb[rr * G.ldx + acol[i]] : P[rh * g.ld + acol[i]])
-                                    : 0.0;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) bv[j] = (bok[j] && rok) ? O[rr * g.ld + bcol[j]] : 0.0;
-#pragma unroll
-          for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (mask & (1u << (i * 4 + j)))
-                dmma_8x8x4(acc.acc[i][j][0], acc.acc[i][j][1], av[i], bv[j]);
-        }
-      }
-      __syncthreads();
-      if (tid == 0) {
-        fence_async_smem();
-        tma_store_4d(&tout, O, 0, tx0, ty0, z);
-        bulk_commit();
-        bulk_wait_read<1>();
-        if (q + NST < nplanes) issue(q + NST);
-        if (z + 2 < z1) issue_x(z + 2);
-      }
-      __syncthreads();
-    }
-    if (tid == 0) bulk_wait<0>();
-  }
-
-  // CTA partial: fixed-order sum over row slices (reuse stage memory)
-  __syncthreads();
-  double* red = reinterpret_cast<double*>(base);
-  if (gactive && slice > 0) {
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const size_t o = ((((size_t)(slice - 1) * G.ts_per_cta + tsl) * 8 + i * 4 + j) * 32 + lane) * 2;
-        red[o] = acc.acc[i][j][0];
-        red[o + 1] = acc.acc[i][j][1];
-      }
-  }
-  __syncthreads();
-  const size_t cta = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
-  double* outp = G.partial + cta * G.a * G.b;
-  if (slice == 0 && tsl < G.tsI * G.tsJ) {
-    const int ti0w = (tsl / G.tsJ) * 2, tj0w = (tsl % G.tsJ) * 4;
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        double v0 = gactive ? acc.acc[i][j][0] : 0.0, v1 = gactive ? acc.acc[i][j][1] : 0.0;
-        if (gactive)
-          for (int sl = 1; sl < G.rs; ++sl) {
-            const size_t o = ((((size_t)(sl - 1) * G.ts_per_cta + tsl) * 8 + i * 4 + j) * 32 + lane) * 2;
-            v0 += red[o];
-            v1 += red[o + 1];
-          }
-        const int row = 8 * (ti0w + i) + (lane >> 2);
-        const int col = 8 * (tj0w + j) + 2 * (lane & 3);
-        if (row < G.a) {
-          if (col < G.b) outp[(size_t)row * G.b + col] = v0;
-          if (col + 1 < G.b) outp[(size_t)row * G.b + col + 1] = v1;
-        }
-      }
-  }
-}
-
 // ------------------------------------------------------------------ host
-struct StencilPlan {
-  StencilGeom g;
-  int ept, nst;
-  size_t smem;
-  dim3 grid;
-};
 
-static int plan_stencil(int nx, int ny, int nz, int ld, StencilPlan* p) {
+int plan_stencil(int nx, int ny, int nz, int ld, StencilPlan* p) {
   StencilGeom& g = p->g;
   g.nx = nx;
   g.ny = ny;
@@ -485,126 +224,6 @@ int stencil7(const double* in, double* out, int nx, int ny, int nz, int ld,
   if (p.ept == 8 && p.nst == 3) return launch_stencil_t<8, 3>(p, tin, thalo, tout, st);
   if (p.ept == 16 && p.nst == 4) return launch_stencil_t<16, 4>(p, tin, thalo, tout, st);
   return launch_stencil_t<16, 3>(p, tin, thalo, tout, st);
-}
-
-__global__ void sum_parts_kernel(const double* partial, int nparts, int len, double* out);
-void tile_mask(int NI, int NJ, const int* lcum, int nl, const int* rcum, int nr,
-               const unsigned char* modes, unsigned* tmask);
-
-template <int EPT, int NST>
-static int launch_sgram_t(const StencilPlan& p, size_t smem, const CUtensorMap& tin,
-                          const CUtensorMap& thalo, const CUtensorMap& tout,
-                          const CUtensorMap& txm, const SGramGeom& G, cudaStream_t st) {
-  auto kern = stencil7_gram_kernel<EPT, NST>;
-  B2L_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<p.grid, 256, smem, st>>>(tin, thalo, tout, txm, p.g, G);
-  B2L_CUDA(cudaGetLastError());
-  return 0;
-}
-
-int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
-                  const double* halo, int has_lo, int has_hi, double scale,
-                  const double* x, int ldx, int m, int kw, double* gram_out,
-                  cudaStream_t st) {
-  B2L_CHECK(nx > 0 && ny > 0 && nz > 0, -B2L_EINVAL, "stencil: empty grid");
-  B2L_CHECK(ld >= 2 && (ld % 2) == 0 && ldx >= 2 && (ldx % 2) == 0, -B2L_EINVAL,
-            "stencil: ld and ldx must be even (16-B rows for TMA)");
-  B2L_CHECK(kw >= 1 && kw <= ld && m >= 1 && m <= ldx, -B2L_EINVAL, "stencil: bad m / kw");
-  B2L_CHECK(in != out, -B2L_EINVAL, "stencil: in-place apply not supported");
-  B2L_CHECK(!(has_lo || has_hi) || halo != nullptr, -B2L_EINVAL,
-            "stencil: halo flags set without a halo buffer");
-  SGramGeom G{};
-  G.m = m;
-  G.ldx = ldx;
-  G.kw = kw;
-  G.a = m + kw;
-  G.b = kw;
-  G.NI = (G.a + 7) / 8;
-  G.NJ = (G.b + 7) / 8;
-  G.tsI = (G.NI + 1) / 2;
-  G.tsJ = (G.NJ + 3) / 4;
-  const int TS = G.tsI * G.tsJ;
-  B2L_CHECK(TS <= 8, -B2L_EINVAL, "stencil_gram: Gram too large for one CTA (use b2l_gram)");
-  G.ts_per_cta = TS;
-  G.rs = 1;
-  while (G.rs * 2 * TS <= 8) G.rs *= 2;
-  const int lcum[3] = {0, m, m + kw};
-  const int rcum[2] = {0, kw};
-  const unsigned char modes[2] = {1, 1};
-  unsigned tm[32];
-  tile_mask(G.NI, G.NJ, lcum, 2, rcum, 1, modes, tm);
-  for (int i = 0; i < 8; ++i) G.tmask[i] = tm[i];
-  B2L_CHECK(G.NI * G.NJ <= 256, -B2L_EINVAL, "stencil_gram: too many tiles");
-
-  StencilPlan p;
-  // smaller tiles than the plain stencil: room for the X planes, 2 CTAs/SM
-  int rc = plan_stencil(nx, ny, nz, ld, &p);
-  if (rc) return rc;
-  StencilGeom& g = p.g;
-  int TY = g.TY;
-  auto need = [&](int ty, int nst) {
-    const size_t stg = (((size_t)(g.TX + 2) * (ty + 2) * ld * 8) + 127) & ~(size_t)127;
-    const size_t ob = (((size_t)g.TX * ty * ld * 8) + 127) & ~(size_t)127;
-    const size_t xb = (((size_t)g.TX * ty * ldx * 8) + 127) & ~(size_t)127;
-    return nst * stg + 2 * ob + 2 * xb + 128;
-  };
-  int nst = 3;
-  while (TY > 1 && need(TY, nst) > 110 * 1024) --TY;
-  if (need(TY, nst) > 110 * 1024) nst = 2;
-  g.TY = TY;
-  g.nelem = g.TX * TY * ld;
-  const int tiles_y = (ny + TY - 1) / TY;
-  const int tiles = g.tiles_x * tiles_y;
-  g.stage_bytes = (uint32_t)((g.TX + 2) * (TY + 2) * ld * 8);
-  g.stage_stride = (g.stage_bytes + 127u) & ~127u;
-  g.out_stride = ((uint32_t)(g.TX * TY * ld * 8) + 127u) & ~127u;
-  G.x_bytes = (uint32_t)(g.TX * TY * ldx * 8);
-  G.x_stride = (G.x_bytes + 127u) & ~127u;
-  size_t smem = need(TY, nst);
-  const size_t red = (size_t)(G.rs > 1 ? G.rs - 1 : 0) * G.ts_per_cta * 8 * 64 * 8;
-  if (red > smem) smem = red + 128;
-  B2L_CHECK(smem <= 227 * 1024, -B2L_EINVAL, "stencil_gram: tile does not fit");
-  const int target = 4 * sm_count();
-  int zsplit = (target + tiles - 1) / tiles;
-  int maxsplit = nz / 8;
-  if (maxsplit < 1) maxsplit = 1;
-  if (zsplit > maxsplit) zsplit = maxsplit;
-  if (zsplit < 1) zsplit = 1;
-  g.zchunk = (nz + zsplit - 1) / zsplit;
-  zsplit = (nz + g.zchunk - 1) / g.zchunk;
-  p.grid = dim3(tiles, zsplit, 1);
-  g.has_lo = has_lo;
-  g.has_hi = has_hi;
-  g.scale = scale;
-  const int nparts = tiles * zsplit;
-  int werr = 0;
-  double* part = static_cast<double*>(
-      workspace((size_t)nparts * G.a * G.b * sizeof(double), &werr));
-  if (werr) return werr;
-  G.partial = part;
-  CUtensorMap tin, thalo, tout, txm;
-  const uint32_t TX = g.TX;
-  rc = encode_tmap_4d(&tin, in, ld, nx, ny, nz, ld, TX + 2, TY + 2, 1);
-  if (rc) return rc;
-  rc = encode_tmap_4d(&tout, out, ld, nx, ny, nz, ld, TX, TY, 1);
-  if (rc) return rc;
-  rc = encode_tmap_4d(&txm, x, ldx, nx, ny, nz, ldx, TX, TY, 1);
-  if (rc) return rc;
-  if (halo) {
-    rc = encode_tmap_4d(&thalo, halo, ld, nx, ny, 2, ld, TX + 2, TY + 2, 1);
-    if (rc) return rc;
-  } else {
-    thalo = tin;
-  }
-  if (p.ept == 8 && nst == 3) rc = launch_sgram_t<8, 3>(p, smem, tin, thalo, tout, txm, G, st);
-  else if (p.ept == 8) rc = launch_sgram_t<8, 2>(p, smem, tin, thalo, tout, txm, G, st);
-  else if (nst == 3) rc = launch_sgram_t<16, 3>(p, smem, tin, thalo, tout, txm, G, st);
-  else rc = launch_sgram_t<16, 2>(p, smem, tin, thalo, tout, txm, G, st);
-  if (rc) return rc;
-  const int len = G.a * G.b;
-  sum_parts_kernel<<<(len + 255) / 256, 256, 0, st>>>(part, nparts, len, gram_out);
-  B2L_CUDA(cudaGetLastError());
-  return 0;
 }
 
 }  // namespace b2l

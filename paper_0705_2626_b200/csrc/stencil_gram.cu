@@ -1,0 +1,424 @@
+// K1+K5b: the z-streaming 7-point stencil fused with the Rayleigh-Ritz Gram
+// blocks that involve A W (reference lobpcg.py:325 gram(w, aw) and :327
+// gram(x, aw)):   AW = s L7 W   and   G = [X ; W]^T AW   ((m + kw) x kw).
+//
+// Same TMA plane ring as stencil.cu (4-D tile loads with a one-point xy halo,
+// OOB zero fill = Dirichlet), plus one TMA box of X per plane.  Work is
+// warp-local: a warp owns fixed groups of 8 points of the tile; for each
+// plane it computes the stencil for all columns of its points (bitwise the
+// reference's operation order) and immediately folds those 8-point rows into
+// its own Gram accumulators on the fp64 tensor cores (DMMA) -- no hand-off
+// between warps, one CTA barrier per plane (output tiles triple buffered, X
+// boxes double buffered).  A W is never re-read from HBM.
+#include "gram_tile.cuh"
+#include "stencil.cuh"
+
+namespace b2l {
+
+struct SGramGeom {
+  int m, ldx, kw;   // X columns / leading dim, W columns used
+  int a, b;         // m + kw, kw
+  int npts;         // points per tile (TX*TY)
+  int ngroups;      // ceil(npts / 8)
+  uint32_t x_bytes, x_stride;
+  double* partial;  // [grid][a*b]
+};
+
+// LD = doubles per point of W / AW (template: it fixes the per-lane element
+// count EPT = GPW*LD/4 and the Gram tile counts); GPW = 8-point groups per
+// warp.  Every per-lane offset is precomputed once, so the plane loop is
+// branch free: the stencil chains of a lane's EPT elements interleave and the
+// Gram loads of all its rows issue ahead of the DMMAs.
+template <int LD, int GPW, int NST>
+__global__ void __launch_bounds__(256, 2)
+    stencil7_gram_kernel(const __grid_constant__ CUtensorMap tin,
+                         const __grid_constant__ CUtensorMap thalo,
+                         const __grid_constant__ CUtensorMap tout,
+                         const __grid_constant__ CUtensorMap tx_map, StencilGeom g,
+                         SGramGeom G) {
+  constexpr int EPT = (GPW * LD + 3) / 4;
+  constexpr int NI = (2 * LD + 7) / 8, NJ = (LD + 7) / 8;
+  constexpr int NA = (NI * NJ >= 4) ? 1 : (NI * NJ >= 2 ? 2 : 4);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* base = smem_raw;
+  auto stage = [&](int s) -> double* {
+    return reinterpret_cast<double*>(base + s * g.stage_stride);
+  };
+  auto outbuf = [&](int i) -> double* {
+    return reinterpret_cast<double*>(base + NST * g.stage_stride + i * g.out_stride);
+  };
+  auto xbuf = [&](int i) -> double* {
+    return reinterpret_cast<double*>(base + NST * g.stage_stride + 3 * g.out_stride +
+                                     i * G.x_stride);
+  };
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + NST * g.stage_stride + 3 * g.out_stride +
+                                              2 * G.x_stride);
+  uint64_t* xbar = bar + NST;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int tx0 = (blockIdx.x % g.tiles_x) * g.TX;
+  const int ty0 = (blockIdx.x / g.tiles_x) * g.TY;
+  const int z0 = blockIdx.y * g.zchunk;
+  const int z1 = min(g.nz, z0 + g.zchunk);
+  const int ystride = (g.TX + 2) * LD;
+  auto staged_row = [&](int pt) { return (pt / g.TX + 1) * (g.TX + 2) + (pt % g.TX) + 1; };
+
+  // stencil elements: the warp's groups (grp = warp + 8 gi) enumerated flat,
+  // lane-contiguous (conflict-free smem).  Invalid slots read point 0.
+  int off[EPT], oel[EPT];
+  unsigned vmask = 0;
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const int idx = lane + 32 * i;
+    const int gi = idx / (8 * LD), r = idx % (8 * LD);
+    const int grp = warp + 8 * gi;
+    const int e = grp * 8 * LD + r;
+    const bool v = gi < GPW && grp < G.ngroups && e < g.nelem;
+    const int p = v ? e / LD : 0;
+    const int c = v ? e - p * LD : 0;
+    off[i] = staged_row(p) * LD + c;
+    oel[i] = v ? e : 0;
+    vmask |= (v ? 1u : 0u) << i;
+  }
+  // Gram rows: lane (q4 = lane & 3) holds point 8 grp + 4 ks + q4
+  const int q4 = lane & 3;
+  int xo[GPW][2], po[GPW][2], oo[GPW][2];
+  unsigned rmask = 0;
+#pragma unroll
+  for (int gi = 0; gi < GPW; ++gi)
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int pt0 = 8 * (warp + 8 * gi) + 4 * ks + q4;
+      const bool ok = pt0 < G.npts;
+      const int pt = ok ? pt0 : 0;
+      xo[gi][ks] = pt * G.ldx;
+      po[gi][ks] = staged_row(pt) * LD;
+      oo[gi][ks] = pt * LD;
+      rmask |= (ok ? 1u : 0u) << (2 * gi + ks);
+    }
+  // lane columns: L = [X (m) ; W (kw)], R = AW (kw)
+  int acol[NI], bcol[NJ];
+  bool aisx[NI], aok[NI], bok[NJ];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int ci = 8 * i + (lane >> 2);
+    aok[i] = ci < G.a;
+    aisx[i] = ci < G.m;
+    acol[i] = !aok[i] ? 0 : (aisx[i] ? ci : ci - G.m);
+  }
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int cj = 8 * j + (lane >> 2);
+    bok[j] = cj < G.b;
+    bcol[j] = bok[j] ? cj : 0;
+  }
+  const int ni = (G.a + 7) / 8, nj = (G.b + 7) / 8;
+
+  double gacc[NA][NI][NJ][2];
+#pragma unroll
+  for (int sa = 0; sa < NA; ++sa)
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) gacc[sa][i][j][0] = gacc[sa][i][j][1] = 0.0;
+
+  if (z0 < z1) {
+    const int nplanes = (z1 - z0) + 2;
+    if (tid == 0) {
+#pragma unroll
+      for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
+      mbar_init(&xbar[0], 1);
+      mbar_init(&xbar[1], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int q) {
+      const int z = z0 - 1 + q;
+      const int s = q % NST;
+      mbar_expect_tx(&bar[s], g.stage_bytes);
+      if (z < 0 && g.has_lo)
+        tma_load_4d(stage(s), &thalo, &bar[s], 0, tx0 - 1, ty0 - 1, 0);
+      else if (z >= g.nz && g.has_hi)
+        tma_load_4d(stage(s), &thalo, &bar[s], 0, tx0 - 1, ty0 - 1, 1);
+      else
+        tma_load_4d(stage(s), &tin, &bar[s], 0, tx0 - 1, ty0 - 1, z);
+    };
+    auto issue_x = [&](int z) {
+      const int sl = (z - z0) & 1;
+      mbar_expect_tx(&xbar[sl], G.x_bytes);
+      tma_load_4d(xbuf(sl), &tx_map, &xbar[sl], 0, tx0, ty0, z);
+    };
+    if (tid == 0) {
+      for (int q = 0; q < NST && q < nplanes; ++q) issue(q);
+      issue_x(z0);
+      if (z0 + 1 < z1) issue_x(z0 + 1);
+    }
+    double prev[EPT], cur[EPT];
+    mbar_wait(&bar[0], 0);
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) prev[i] = stage(0)[off[i]];
+    mbar_wait(&bar[1 % NST], (1 / NST) & 1);
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) cur[i] = stage(1 % NST)[off[i]];
+    __syncthreads();
+    if (tid == 0 && NST < nplanes) issue(NST);
+
+    const double six = 6.0;
+    const double sc = g.scale;
+    for (int z = z0; z < z1; ++z) {
+      const int q = z - z0 + 1;
+      const int sn = (q + 1) % NST;
+      mbar_wait(&bar[sn], ((q + 1) / NST) & 1);
+      const double* P = stage(q % NST);
+      const double* N = stage(sn);
+      double* O = outbuf((z - z0) % 3);
+      // ---- stencil, reference operation order, no FMA contraction
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        const int o = off[i];
+        const double nx_ = N[o];
+        double r = __dmul_rn(six, cur[i]);
+        r = __dsub_rn(r, P[o - LD]);
+        r = __dsub_rn(r, P[o + LD]);
+        r = __dsub_rn(r, P[o - ystride]);
+        r = __dsub_rn(r, P[o + ystride]);
+        r = __dsub_rn(r, prev[i]);
+        r = __dsub_rn(r, nx_);
+        if (vmask & (1u << i)) O[oel[i]] = __dmul_rn(sc, r);
+        prev[i] = cur[i];
+        cur[i] = nx_;
+      }
+      __syncwarp();
+      // ---- Gram over this warp's rows (points); the lane reads only rows
+      // its own warp wrote, so no CTA barrier is needed before it
+      const int xs = (z - z0) & 1;
+      mbar_wait(&xbar[xs], ((z - z0) >> 1) & 1);
+      const double* Xb = xbuf(xs);
+#pragma unroll
+      for (int gi = 0; gi < GPW; ++gi)
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const bool rok = rmask & (1u << (2 * gi + ks));
+          double av[NI], bv[NJ];
+#pragma unroll
+          for (int i = 0; i < NI; ++i) {
+            const double v = aisx[i] ? Xb[xo[gi][ks] + acol[i]] : P[po[gi][ks] + acol[i]];
+            av[i] = (aok[i] && rok) ? v : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) {
+            const double v = O[oo[gi][ks] + bcol[j]];
+            bv[j] = (bok[j] && rok) ? v : 0.0;
+          }
+          const int sa = (2 * gi + ks) % NA;
+#pragma unroll
+          for (int i = 0; i < NI; ++i)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+              if (i < ni && j < nj) {
+#pragma unroll
+                for (int t = 0; t < NA; ++t)
+                  if (t == sa) dmma_8x8x4(gacc[t][i][j][0], gacc[t][i][j][1], av[i], bv[j]);
+              }
+        }
+      __syncthreads();
+      if (tid == 0) {
+        fence_async_smem();
+        tma_store_4d(&tout, O, 0, tx0, ty0, z);
+        bulk_commit();
+        bulk_wait_read<2>();   // output slots are triple buffered
+        if (q + NST < nplanes) issue(q + NST);
+        if (z + 2 < z1) issue_x(z + 2);
+      }
+    }
+    if (tid == 0) bulk_wait<0>();
+  }
+
+  // ---- CTA partial: fixed-order sum over the 8 warps (reuse stage memory)
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(base);
+#pragma unroll
+  for (int i = 0; i < NI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const size_t o = (((size_t)warp * NI * NJ + i * NJ + j) * 32 + lane) * 2;
+      double v0 = gacc[0][i][j][0], v1 = gacc[0][i][j][1];
+#pragma unroll
+      for (int sa = 1; sa < NA; ++sa) {
+        v0 += gacc[sa][i][j][0];
+        v1 += gacc[sa][i][j][1];
+      }
+      red[o] = v0;
+      red[o + 1] = v1;
+    }
+  __syncthreads();
+  const size_t cta = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+  double* outp = G.partial + cta * G.a * G.b;
+  for (int e = tid; e < NI * NJ * 32; e += blockDim.x) {
+    const int t = e / 32, ln = e & 31;
+    double v0 = 0.0, v1 = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      const size_t o = (((size_t)w * NI * NJ + t) * 32 + ln) * 2;
+      v0 += red[o];
+      v1 += red[o + 1];
+    }
+    const int row = 8 * (t / NJ) + (ln >> 2);
+    const int col = 8 * (t % NJ) + 2 * (ln & 3);
+    if (row < G.a) {
+      if (col < G.b) outp[(size_t)row * G.b + col] = v0;
+      if (col + 1 < G.b) outp[(size_t)row * G.b + col + 1] = v1;
+    }
+  }
+}
+
+int stencil7(const double* in, double* out, int nx, int ny, int nz, int ld, const double* halo,
+             int has_lo, int has_hi, double scale, cudaStream_t st);
+struct HostBlock {
+  const double* p;
+  int ld, cols;
+};
+int gram(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr, unsigned rw_mask,
+         const double* d, const unsigned char* pair_mode, double* out, cudaStream_t st);
+
+template <int LD, int GPW>
+static int launch_sgram_t(const StencilPlan& p, size_t smem, const CUtensorMap& tin,
+                          const CUtensorMap& thalo, const CUtensorMap& tout,
+                          const CUtensorMap& txm, const SGramGeom& G, cudaStream_t st) {
+  auto kern = stencil7_gram_kernel<LD, GPW, 3>;
+  B2L_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<p.grid, 256, smem, st>>>(tin, thalo, tout, txm, p.g, G);
+  B2L_CUDA(cudaGetLastError());
+  return 0;
+}
+
+template <int LD>
+static int launch_sgram_ld(int gpw, const StencilPlan& p, size_t smem, const CUtensorMap& tin,
+                           const CUtensorMap& thalo, const CUtensorMap& tout,
+                           const CUtensorMap& txm, const SGramGeom& G, cudaStream_t st) {
+  switch (gpw) {
+    case 1: return launch_sgram_t<LD, 1>(p, smem, tin, thalo, tout, txm, G, st);
+    case 2: return launch_sgram_t<LD, 2>(p, smem, tin, thalo, tout, txm, G, st);
+    case 3: return launch_sgram_t<LD, 3>(p, smem, tin, thalo, tout, txm, G, st);
+    default: return launch_sgram_t<LD, 4>(p, smem, tin, thalo, tout, txm, G, st);
+  }
+}
+
+int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
+                  const double* halo, int has_lo, int has_hi, double scale,
+                  const double* x, int ldx, int m, int kw, double* gram_out,
+                  cudaStream_t st) {
+  B2L_CHECK(nx > 0 && ny > 0 && nz > 0, -B2L_EINVAL, "stencil: empty grid");
+  B2L_CHECK(ld >= 2 && (ld % 2) == 0 && ldx >= 2 && (ldx % 2) == 0, -B2L_EINVAL,
+            "stencil: ld and ldx must be even (16-B rows for TMA)");
+  B2L_CHECK(kw >= 1 && kw <= ld && m >= 1 && m <= ldx, -B2L_EINVAL, "stencil: bad m / kw");
+  B2L_CHECK(in != out, -B2L_EINVAL, "stencil: in-place apply not supported");
+  B2L_CHECK(!(has_lo || has_hi) || halo != nullptr, -B2L_EINVAL,
+            "stencil: halo flags set without a halo buffer");
+  if (ld > 16 || m > ld) {
+    // outside the fused kernel's templates: the two-pass form (K1, then K5)
+    int rc = stencil7(in, out, nx, ny, nz, ld, halo, has_lo, has_hi, scale, st);
+    if (rc) return rc;
+    const HostBlock L[2] = {{x, ldx, m}, {in, ld, kw}};
+    const HostBlock R[1] = {{out, ld, kw}};
+    return gram(nx * ny * nz, L, 2, R, 1, 0u, nullptr, nullptr, gram_out, st);
+  }
+  SGramGeom G{};
+  G.m = m;
+  G.ldx = ldx;
+  G.kw = kw;
+  G.a = m + kw;
+  G.b = kw;
+
+  StencilPlan p;
+  int rc = plan_stencil(nx, ny, nz, ld, &p);
+  if (rc) return rc;
+  StencilGeom& g = p.g;
+  const int TX = g.TX;
+  auto need = [&](int ty) {
+    const size_t stg = (((size_t)(TX + 2) * (ty + 2) * ld * 8) + 127) & ~(size_t)127;
+    const size_t ob = (((size_t)TX * ty * ld * 8) + 127) & ~(size_t)127;
+    const size_t xb = (((size_t)TX * ty * ldx * 8) + 127) & ~(size_t)127;
+    return 3 * stg + 3 * ob + 2 * xb + 128;
+  };
+  // 8 warps x GPW groups of 8 points per tile; the largest tile that keeps
+  // two CTAs resident per SM (<= ~110 KB shared memory) wins
+  int gpw = 0, TY = 1;
+  for (int cand = 4; cand >= 1; --cand) {
+    if ((cand * ld + 3) / 4 > 16) continue;
+    int ty = (64 * cand) / TX;
+    if (ty < 1) ty = 1;
+    if (ty > ny) ty = ny;
+    if (ty > 254) ty = 254;
+    if (TX * ty > 64 * cand) continue;
+    if (need(ty) > 110 * 1024) continue;
+    gpw = cand;
+    TY = ty;
+    break;
+  }
+  B2L_CHECK(gpw > 0, -B2L_EINVAL, "stencil_gram: no tile fits shared memory");
+  // shrink the group count to what the tile actually holds
+  while (gpw > 1 && 64 * (gpw - 1) >= TX * TY) --gpw;
+  g.TY = TY;
+  g.nelem = TX * TY * ld;
+  G.npts = TX * TY;
+  G.ngroups = (G.npts + 7) / 8;
+  const int tiles_y = (ny + TY - 1) / TY;
+  const int tiles = g.tiles_x * tiles_y;
+  g.stage_bytes = (uint32_t)((TX + 2) * (TY + 2) * ld * 8);
+  g.stage_stride = (g.stage_bytes + 127u) & ~127u;
+  g.out_stride = ((uint32_t)(TX * TY * ld * 8) + 127u) & ~127u;
+  G.x_bytes = (uint32_t)(TX * TY * ldx * 8);
+  G.x_stride = (G.x_bytes + 127u) & ~127u;
+  size_t smem = need(TY);
+  const int NI = (2 * ld + 7) / 8, NJ = (ld + 7) / 8;
+  const size_t red = (size_t)8 * NI * NJ * 64 * 8;
+  if (red > smem) smem = red + 128;
+  B2L_CHECK(smem <= 227 * 1024, -B2L_EINVAL, "stencil_gram: tile does not fit");
+  const int target = 4 * sm_count();
+  int zsplit = (target + tiles - 1) / tiles;
+  int maxsplit = nz / 8;
+  if (maxsplit < 1) maxsplit = 1;
+  if (zsplit > maxsplit) zsplit = maxsplit;
+  if (zsplit < 1) zsplit = 1;
+  g.zchunk = (nz + zsplit - 1) / zsplit;
+  zsplit = (nz + g.zchunk - 1) / g.zchunk;
+  p.grid = dim3(tiles, zsplit, 1);
+  g.has_lo = has_lo;
+  g.has_hi = has_hi;
+  g.scale = scale;
+  const int nparts = tiles * zsplit;
+  int werr = 0;
+  double* part = static_cast<double*>(
+      workspace((size_t)nparts * G.a * G.b * sizeof(double), &werr));
+  if (werr) return werr;
+  G.partial = part;
+  CUtensorMap tin, thalo, tout, txm;
+  rc = encode_tmap_4d(&tin, in, ld, nx, ny, nz, ld, TX + 2, TY + 2, 1);
+  if (rc) return rc;
+  rc = encode_tmap_4d(&tout, out, ld, nx, ny, nz, ld, TX, TY, 1);
+  if (rc) return rc;
+  rc = encode_tmap_4d(&txm, x, ldx, nx, ny, nz, ldx, TX, TY, 1);
+  if (rc) return rc;
+  if (halo) {
+    rc = encode_tmap_4d(&thalo, halo, ld, nx, ny, 2, ld, TX + 2, TY + 2, 1);
+    if (rc) return rc;
+  } else {
+    thalo = tin;
+  }
+  switch (ld) {
+    case 2: rc = launch_sgram_ld<2>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
+    case 4: rc = launch_sgram_ld<4>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
+    case 6: rc = launch_sgram_ld<6>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
+    case 8: rc = launch_sgram_ld<8>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
+    case 10: rc = launch_sgram_ld<10>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
+    case 12: rc = launch_sgram_ld<12>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
+    case 14: rc = launch_sgram_ld<14>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
+    default: rc = launch_sgram_ld<16>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
+  }
+  if (rc) return rc;
+  const int len = G.a * G.b;
+  return sum_parts(part, nparts, len, gram_out, st);
+}
+
+}  // namespace b2l
