@@ -141,7 +141,7 @@ int b2l_stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int
  *   X'-AP', W'-AP', P'-AP' are defined.
  * coef = [Cx (m x m) | Cw (kw x m) | Cp (kp x m)] row-major, device.
  * x/ax/p/ap and xo/axo/po/apo are (n, ldx); w/aw (n, ldw); w_next (n, ldw_next).
- * Outputs must not alias inputs.  m <= 64 and the Gram must fit one CTA.
+ * Outputs must not alias inputs.  m <= 16.
  */
 int b2l_lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
                     const double* w, const double* aw, int ldw, int kw, const double* p,
@@ -150,6 +150,35 @@ int b2l_lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx
                     const double* bdiag, int tmode, double tinv, const double* tvec,
                     const int* wpos, int kw_next, double* w_next, int ldw_next,
                     int want_ax_norms, double* red_out, void* stream);
+
+/*
+ * Host, small dense: register the LAPACK routines the Rayleigh-Ritz step uses
+ * (dpotrf, dtrtrs, dtrtri, dsyevr with the Fortran-style signatures of
+ * scipy.linalg.cython_lapack, i.e. the routines scipy.linalg.cholesky /
+ * solve_triangular / eigh run for the reference, multivec.py:89-211).
+ */
+int b2l_set_lapack(void* dpotrf, void* dtrtrs, void* dtrtri, void* dsyevr);
+
+/*
+ * Host, small dense -- the Rayleigh-Ritz step of one iteration with the
+ * reference's repair ladders (lobpcg.py:475-519; b_orthonormalize :147-200;
+ * rayleigh_ritz :299-340 on the projected blocks), given the device Grams:
+ *   g1 (a x ldg1, row-major): rows [X (m) | W (kst) | P (m, if have_p)],
+ *       cols [BX (m) | BW (kst) | BP (m) | AP (m)]  (b2l_lobpcg_step / b2l_gram)
+ *   g2 ((m + kst) x kst, row-major): [X ; W]^T A W  (b2l_stencil7_gram)
+ *   lam (m) current Ritz values; jact (kj) active columns; sel (kj) their
+ *   positions among the kst stored W columns.
+ * Outputs: lam_out (m) next Ritz values; coef_out = [Cx (m x m) | Cw (kst x m)
+ * | Cp (kp x m)] row-major with the W / P Cholesky-QR factors folded in (the
+ * b2l_lobpcg_step / b2l_update layout); pcols_out (kp = *kp_out, 0 when P was
+ * dropped); *fallbacks_out = basis repairs taken (dropped W columns, dropped
+ * P, eigensolve retries).  Returns -B2L_EDEGENERATE (-1003) when the ladder
+ * is exhausted (the reference's BasisDegeneracy status).
+ */
+int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, int ldg1,
+                      const double* g2, const double* lam, const int* jact, int kj,
+                      const int* sel, double pivot_floor, double* lam_out, double* coef_out,
+                      int* pcols_out, int* kp_out, int* fallbacks_out);
 
 #ifdef __cplusplus
 }

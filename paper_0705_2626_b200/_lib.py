@@ -55,7 +55,13 @@ SIGNATURES = {
                                   C.c_void_p, C.c_int, C.c_double, C.c_void_p,
                                   C.c_void_p, C.c_int, C.c_void_p, C.c_int,
                                   C.c_int, C.c_void_p, C.c_void_p]),
+    "b2l_set_lapack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "b2l_rayleigh_ritz": (C.c_int, [C.c_int, C.c_int, C.c_int, c_dp, C.c_int, c_dp, c_dp,
+                                    c_ip, C.c_int, c_ip, C.c_double, c_dp, c_dp, c_ip, c_ip,
+                                    c_ip]),
 }
+
+EDEGENERATE = -1003
 
 ABI_VERSION = 1
 
@@ -83,8 +89,31 @@ def load():
             fn.argtypes = args
         if lib.b2l_abi_version() != ABI_VERSION:
             raise ImportError("libb200lobpcg ABI version mismatch; rebuild")
+        _register_lapack(lib)
         _lib = lib
         return lib
+
+
+def _register_lapack(lib) -> None:
+    """Hand the host Rayleigh-Ritz (b2l_rayleigh_ritz) scipy's LAPACK -- the
+    routines scipy.linalg.cholesky / solve_triangular / eigh run for the
+    reference -- as plain function pointers from scipy.linalg.cython_lapack."""
+    from scipy.linalg import cython_lapack
+
+    get = C.pythonapi.PyCapsule_GetPointer
+    get.restype = C.c_void_p
+    get.argtypes = [C.py_object, C.c_char_p]
+    getname = C.pythonapi.PyCapsule_GetName
+    getname.restype = C.c_char_p
+    getname.argtypes = [C.py_object]
+    caps = cython_lapack.__pyx_capi__
+    ptrs = []
+    for name in ("dpotrf", "dtrtrs", "dtrtri", "dsyevr"):
+        cap = caps[name]
+        ptrs.append(get(cap, getname(cap)))
+    rc = lib.b2l_set_lapack(*ptrs)
+    if rc != 0:
+        raise ImportError("b2l_set_lapack failed: " + lib.b2l_last_error().decode())
 
 
 def check(rc: int, what: str) -> None:

@@ -38,6 +38,8 @@ enum : int {
   B2L_EINVAL = 1000,   // returned negated
   B2L_ENOMEM = 1001,
   B2L_EDRIVER = 1002,
+  B2L_EDEGENERATE = 1003,   // Rayleigh-Ritz basis repair exhausted
+  B2L_ELAPACK = 1004,
 };
 
 // ------------------------------------------------------------- workspace

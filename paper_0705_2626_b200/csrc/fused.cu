@@ -34,6 +34,9 @@
 // the TMA box is wider than the block's row, the extra columns are zero-filled
 // on load and clipped on store, and the DMMA fragment loads are free of bank
 // conflicts.  Out-of-range rows of the last chunk are zero-filled by the TMA.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "gram_tile.cuh"
 
@@ -885,6 +888,342 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// F1, warp-pair variant (m <= 10): 16 compute warps, two per 8-row tile.  Of a
+// pair, warp h = 0 forms P' and X', warp h = 1 forms AP' and AX' (the same
+// coefficients on the A-side blocks); after a pair barrier the 64 threads
+// form the residual of the 8 rows, and after a second one each warp folds
+// the 8 rows into its half of the Gram tiles.  Halving every warp's
+// accumulators keeps 4 compute warps per SM sub-partition resident (vs 2 in
+// the one-warp-per-tile layout), which is what keeps the DMMA pipe fed.
+constexpr int PAIR_NW = 14;                        // compute warps (7 pairs, 56-row chunks)
+constexpr int PAIR_THREADS = 32 * (1 + PAIR_NW);   // 480: <= 4 warps per SMSP
+constexpr int NB_PAIR = 5;                         // named barriers 5..12
+
+template <int NT, int KS, int NI, int NJ, bool SPLIT_I, bool WGT>
+__global__ void __launch_bounds__(PAIR_THREADS, 1)
+    step_pair_kernel(const __grid_constant__ StepMaps M, const __grid_constant__ StepArgs Ain) {
+  constexpr int GI = SPLIT_I ? NI / 2 : NI;          // this warp's Gram tile block
+  constexpr int GJ = SPLIT_I ? NJ : (NJ + 1) / 2;
+  extern __shared__ __align__(128) unsigned char sm_raw[];
+  __shared__ StepArgs sA;
+  if (threadIdx.x == 0) sA = Ain;
+  __syncthreads();
+  const StepArgs& A = sA;
+  double* sm = reinterpret_cast<double*>(sm_raw);
+  const uint32_t sm_base = smem_u32(sm_raw);
+  double* stages = sm;
+  double* coef = sm + A.coef_off;
+  double* slam = sm + A.lam_off;
+  int* spc = reinterpret_cast<int*>(sm + A.int_off);
+  int* swp = spc + A.kp;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + A.bar_off);
+  uint64_t* empty = full + 4;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int m = A.m;
+  const int sx = A.sx, sw = A.sw, swn = A.swn;
+  const int ncoef = m * m + A.kw * m + A.kp * m;
+  for (int i = tid; i < ncoef; i += blockDim.x) coef[i] = A.coef[i];
+  for (int i = tid; i < m; i += blockDim.x) {
+    slam[i] = A.lam[i];
+    swp[i] = A.wpos[i];
+  }
+  for (int i = tid; i < A.kp; i += blockDim.x) spc[i] = A.pcols[i];
+  for (int i = tid; i < 16; i += blockDim.x) sm[A.zero_off + i] = 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < A.nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], PAIR_NW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int nchunks = (A.nrows + A.rc - 1) / A.rc;
+  const int nloc = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto chunk_of = [&](int it) { return blockIdx.x + it * gridDim.x; };
+
+  double s_w0 = 0.0, s_a0 = 0.0;
+  double gacc[GI][GJ][2];
+#pragma unroll
+  for (int i = 0; i < GI; ++i)
+#pragma unroll
+    for (int j = 0; j < GJ; ++j) gacc[i][j][0] = gacc[i][j][1] = 0.0;
+
+  if (warp == 0) {
+    // ================= producer / storer =================
+    if (lane == 0)
+      for (int j = 0; j < A.nst && j < nloc; ++j)
+        step_issue(M, A, stages + (size_t)j * A.stage_doubles, &full[j], chunk_of(j));
+    for (int it = 0; it < nloc; ++it) {
+      const int b = it & 1;
+      nbar_sync(NB_OFULL + b, PAIR_THREADS);
+      if (lane == 0) {
+        const int r0 = chunk_of(it) * A.rc;
+        const int ob = b * A.out_stride;
+        for (int k = 0; k < 5; ++k) {
+          if (k == 4 && A.kwn == 0) continue;
+          tma_store_2d(&M.out[k], sm + A.out_off[k] + ob, 0, r0);
+        }
+        bulk_commit();
+        bulk_wait_read<0>();
+      }
+      __syncwarp();
+      nbar_arrive(NB_OEMPTY + b, PAIR_THREADS);
+      const int jn = it + A.nst;
+      if (lane == 0 && jn < nloc) {
+        const int s = it % A.nst;
+        mbar_wait(&empty[s], (it / A.nst) & 1);
+        step_issue(M, A, stages + (size_t)s * A.stage_doubles, &full[s], chunk_of(jn));
+      }
+      __syncwarp();
+    }
+    if (lane == 0) bulk_wait<0>();
+  } else {
+    const int cw = warp - 1;
+    const int mt = cw >> 1, h = cw & 1;        // 8-row tile, half
+    const int pbar = NB_PAIR + mt;
+    const int q = lane & 3, rl = lane >> 2;
+    // update coefficients (B fragments), shared by both halves
+    double cW[NT][KS], cP[NT][KS], cX[NT][KS];
+    int pcol[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = 4 * ks + q;
+      pcol[ks] = k < A.kp ? spc[k] : 0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int cb = 8 * nt + rl;
+        const bool cv = cb < m;
+        cW[nt][ks] = (cv && k < A.kw) ? coef[m * m + k * m + cb] : 0.0;
+        cP[nt][ks] = (cv && k < A.kp) ? coef[m * m + A.kw * m + k * m + cb] : 0.0;
+        cX[nt][ks] = (cv && k < m) ? coef[k * m + cb] : 0.0;
+      }
+    }
+    // residual: the pair's 64 threads as (rsub, j), RP2 rows per pass
+    const int pt = h * 32 + lane;
+    const int RP2 = 64 / m;
+    const int rsub = pt / m, j0 = pt % m;
+    const bool on0 = rsub < RP2;
+    const double lam0 = on0 ? slam[j0] : 0.0;
+    const int jpos0 = on0 ? swp[j0] : -1;
+    // Gram lane columns of this warp's tile block
+    const int i0 = SPLIT_I ? h * GI : 0;
+    const int jb0 = SPLIT_I ? 0 : h * GJ;
+    const uint32_t zero_adr = sm_base + (uint32_t)A.zero_off * 8u;
+    uint32_t la_[GI], ls_[GI], rb_[GJ], rs_[GJ];
+    bool rw_[GJ];
+    const int Lblk[3] = {0, 4, 2};
+    const int Rblk[4] = {0, 4, 2, 3};
+#pragma unroll
+    for (int i = 0; i < GI; ++i) {
+      const int ci = 8 * (i0 + i) + (lane >> 2);
+      la_[i] = zero_adr;
+      ls_[i] = 0;
+      if (ci < A.a) {
+        int l = 0;
+        while (l + 1 < 3 && A.lcum[l + 1] <= ci) ++l;
+        la_[i] = sm_base + 8u * (A.out_off[Lblk[l]] + (ci - A.lcum[l]));
+        ls_[i] = 8u * (l == 1 ? swn : sx);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < GJ; ++j) {
+      const int cj = 8 * (jb0 + j) + (lane >> 2);
+      rb_[j] = zero_adr;
+      rs_[j] = 0;
+      rw_[j] = false;
+      if (jb0 + j < NJ && cj < A.b) {
+        int r = 0;
+        while (r + 1 < 4 && A.rcum[r + 1] <= cj) ++r;
+        rb_[j] = sm_base + 8u * (A.out_off[Rblk[r]] + (cj - A.rcum[r]));
+        rs_[j] = 8u * (r == 1 ? swn : sx);
+        rw_[j] = r < 3;
+      }
+    }
+
+    for (int it = 0; it < nloc; ++it) {
+      const int s = it % A.nst, b = it & 1;
+      const int r0 = chunk_of(it) * A.rc;
+      const int nvalid = min(A.rc, A.nrows - r0);
+      if (it >= 2) nbar_sync(NB_OEMPTY + b, PAIR_THREADS);
+      mbar_wait(&full[s], (it / A.nst) & 1);
+      const double* st = stages + (size_t)s * A.stage_doubles;
+      const int ob = b * A.out_stride;
+      const int r = 8 * mt + rl;
+      {
+        // ---- (1) update, this warp's side (h = 0: P', X'; h = 1: AP', AX')
+        const double* Wb = st + A.in_off[2 + h];
+        const double* Pb = st + A.in_off[4 + h];
+        const double* Xb = st + A.in_off[0 + h];
+        double* Ox = sm + A.out_off[0 + h] + ob;
+        double* Op = sm + A.out_off[2 + h] + ob;
+        double acc[NT][3][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) acc[nt][c][0] = acc[nt][c][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int k = 4 * ks + q;
+          const double wv = k < A.kw ? Wb[r * sw + k] : 0.0;
+          const double pv = k < A.kp ? Pb[r * sx + pcol[ks]] : 0.0;
+          const double xv = k < m ? Xb[r * sx + k] : 0.0;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            dmma_8x8x4(acc[nt][0][0], acc[nt][0][1], wv, cW[nt][ks]);
+            dmma_8x8x4(acc[nt][1][0], acc[nt][1][1], pv, cP[nt][ks]);
+            dmma_8x8x4(acc[nt][2][0], acc[nt][2][1], xv, cX[nt][ks]);
+          }
+        }
+        const bool bw = A.kw > 0, bp = A.kp > 0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int co = 8 * nt + 2 * q;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double pn = (bw && bp) ? __dadd_rn(acc[nt][0][e], acc[nt][1][e])
+                                         : (bw ? acc[nt][0][e] : acc[nt][1][e]);
+            if (co + e < A.ldx) {
+              Ox[r * sx + co + e] = __dadd_rn(acc[nt][2][e], pn);
+              Op[r * sx + co + e] = pn;
+            }
+          }
+        }
+      }
+      nbar_sync(pbar, 64);
+      // ---- (2) residual of the 8 rows (both warps of the pair)
+      {
+        const double* O0 = sm + A.out_off[0] + ob;
+        const double* O1 = sm + A.out_off[1] + ob;
+        double* O4 = sm + A.out_off[4] + ob;
+        if (on0) {
+          double sw_ = 0.0, sa_ = 0.0;
+          for (int rr = rsub; rr < 8; rr += RP2) {
+            const int row = 8 * mt + rr;
+            double wv = 0.0;
+            if (row < nvalid) {
+              const double xv = O0[row * sx + j0];
+              const double av = O1[row * sx + j0];
+              const double bx = A.d ? __dmul_rn(st[A.d_off + row], xv) : xv;
+              const double wf = __dsub_rn(av, __dmul_rn(bx, lam0));
+              sw_ = fma(wf, wf, sw_);
+              if (A.want_ax) sa_ = fma(av, av, sa_);
+              wv = wf;
+              if (A.tmode == 1) wv = __dmul_rn(A.tinv, wf);
+              else if (A.tmode == 2) wv = __dmul_rn(st[A.t_off + row], wf);
+            }
+            if (jpos0 >= 0) O4[row * swn + jpos0] = wv;
+          }
+          s_w0 += sw_;
+          s_a0 += sa_;
+        }
+        const int npad = swn - A.kwn;
+        for (int e = pt; e < 8 * npad; e += 64)
+          O4[(8 * mt + e / npad) * swn + A.kwn + e % npad] = 0.0;
+      }
+      nbar_sync(pbar, 64);
+      // ---- (3) Gram over the 8 rows, this warp's tile block
+      const uint32_t boff = 8u * (uint32_t)ob;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const uint32_t row = (uint32_t)(8 * mt + 4 * ks + q);
+        double av[GI], bv[GJ];
+#pragma unroll
+        for (int i = 0; i < GI; ++i) av[i] = lds64(la_[i] + (ls_[i] ? boff : 0u) + row * ls_[i]);
+#pragma unroll
+        for (int j = 0; j < GJ; ++j) bv[j] = lds64(rb_[j] + (rs_[j] ? boff : 0u) + row * rs_[j]);
+        if (WGT) {
+          const double w = st[A.d_off + row];
+#pragma unroll
+          for (int j = 0; j < GJ; ++j)
+            if (rw_[j]) bv[j] = __dmul_rn(w, bv[j]);
+        }
+#pragma unroll
+        for (int i = 0; i < GI; ++i)
+#pragma unroll
+          for (int j = 0; j < GJ; ++j) dmma_8x8x4(gacc[i][j][0], gacc[i][j][1], av[i], bv[j]);
+      }
+      fence_async_smem();   // generic writes -> the TMA store (async proxy)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      nbar_arrive(NB_OFULL + b, PAIR_THREADS);
+    }
+    for (int it = (nloc > 2 ? nloc : 2); it < nloc + 2; ++it)
+      nbar_sync(NB_OEMPTY + (it & 1), PAIR_THREADS);
+  }
+  __syncthreads();
+
+  // ---- CTA reductions (fixed order over pairs / threads)
+  double* red = sm + A.red_off;
+  const int NL = PAIR_NW * 32;
+  if (warp >= 1) {
+    const int o = (warp - 1) * 32 + lane;
+    red[o] = s_w0;
+    red[NL + o] = s_a0;
+  }
+  __syncthreads();
+  double* out = A.partial + (size_t)blockIdx.x * (2 * m + A.a * A.b);
+  if (tid < m) {
+    double a = 0.0, bb = 0.0;
+    const int RP2 = 64 / m;
+    for (int p = 0; p < PAIR_NW / 2; ++p)
+      for (int r_ = 0; r_ < RP2; ++r_) {
+        a += red[p * 64 + r_ * m + tid];
+        bb += red[NL + p * 64 + r_ * m + tid];
+      }
+    out[tid] = a;
+    out[m + tid] = bb;
+  }
+  double* gred = sm + A.gred_off;   // [pair][NI*NJ tiles][32][2]
+  if (warp >= 1) {
+    const int cw = warp - 1, pr = cw >> 1, h = cw & 1;
+    const int i0 = SPLIT_I ? h * GI : 0;
+    const int jb0 = SPLIT_I ? 0 : h * GJ;
+#pragma unroll
+    for (int i = 0; i < GI; ++i)
+#pragma unroll
+      for (int j = 0; j < GJ; ++j) {
+        if (jb0 + j >= NJ) continue;
+        const int t = (i0 + i) * NJ + jb0 + j;
+        const size_t o = (((size_t)pr * NI * NJ + t) * 32 + lane) * 2;
+        gred[o] = gacc[i][j][0];
+        gred[o + 1] = gacc[i][j][1];
+      }
+  }
+  __syncthreads();
+  double* go = out + 2 * m;
+  for (int e = tid; e < NI * NJ * 32; e += blockDim.x) {
+    const int t = e / 32, ln = e & 31;
+    const int i = t / NJ, j = t % NJ;
+    double v0 = 0.0, v1 = 0.0;
+    for (int p = 0; p < PAIR_NW / 2; ++p) {
+      const size_t o = (((size_t)p * NI * NJ + t) * 32 + ln) * 2;
+      v0 += gred[o];
+      v1 += gred[o + 1];
+    }
+    const int row = 8 * i + (ln >> 2);
+    const int col = 8 * j + 2 * (ln & 3);
+    if (row < A.a) {
+      if (col < A.b) go[(size_t)row * A.b + col] = v0;
+      if (col + 1 < A.b) go[(size_t)row * A.b + col + 1] = v1;
+    }
+  }
+}
+
+template <int NT, int KS, int NI, int NJ, bool SPLIT_I>
+static int launch_pair(bool wgt, size_t smem, int gx, const StepMaps& M, const StepArgs& A,
+                       cudaStream_t st) {
+  auto kern = wgt ? step_pair_kernel<NT, KS, NI, NJ, SPLIT_I, true>
+                  : step_pair_kernel<NT, KS, NI, NJ, SPLIT_I, false>;
+  B2L_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<gx, PAIR_THREADS, smem, st>>>(M, A);
+  B2L_CUDA(cudaGetLastError());
+  return 0;
+}
+
 template <int NT, int KS, int NI, int NJ>
 static int launch_local(bool wgt, size_t smem, int gx, const StepMaps& M, const StepArgs& A,
                         cudaStream_t st) {
@@ -971,7 +1310,11 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   // (6 blocks + d + t) would exceed ~48 KB; then the deepest TMA ring (<= 4)
   // that fits one CTA per SM.
   const int width = 4 * A.sx + 2 * (kw ? A.sw : 0) + (d ? 1 : 0) + (tmode == 2 ? 1 : 0);
-  A.rc = 64;
+  static const bool one_warp = [] {
+    const char* v = getenv("B2L_STEP_VARIANT");
+    return v && strcmp(v, "local") == 0;
+  }();
+  A.rc = (local && !one_warp) ? 4 * PAIR_NW : 64;
   while (A.rc > 16 && (size_t)A.rc * width * 8 > 48 * 1024) A.rc >>= 1;
   while (A.rs > 1 && A.rc / A.rs < 4) A.rs >>= 1;
   const int rc = A.rc;
@@ -1066,10 +1409,17 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   const bool wgt = d != nullptr;
   int rcode;
   if (local) {
-    B2L_CHECK(rc == 8 * LOC_NW, -B2L_EINVAL, "step: warp-local variant needs 64-row chunks");
-    if (m <= 4) rcode = launch_local<1, 1, 2, 2>(wgt, smem, gx, M, A, st);
-    else if (m <= 8) rcode = launch_local<1, 2, 3, 4>(wgt, smem, gx, M, A, st);
-    else rcode = launch_local<2, 3, 4, 5>(wgt, smem, gx, M, A, st);
+    B2L_CHECK(rc == (one_warp ? 8 * LOC_NW : 4 * PAIR_NW), -B2L_EINVAL,
+              "step: warp-local variants need 64- / 56-row chunks");
+    if (one_warp) {
+      if (m <= 4) rcode = launch_local<1, 1, 2, 2>(wgt, smem, gx, M, A, st);
+      else if (m <= 8) rcode = launch_local<1, 2, 3, 4>(wgt, smem, gx, M, A, st);
+      else rcode = launch_local<2, 3, 4, 5>(wgt, smem, gx, M, A, st);
+    } else {
+      if (m <= 4) rcode = launch_pair<1, 1, 2, 2, true>(wgt, smem, gx, M, A, st);
+      else if (m <= 8) rcode = launch_pair<1, 2, 3, 4, false>(wgt, smem, gx, M, A, st);
+      else rcode = launch_pair<2, 3, 4, 5, true>(wgt, smem, gx, M, A, st);
+    }
   } else if (m <= 4) rcode = launch_step<1, 1>(wgt, smem, gx, M, A, st);
   else if (m <= 8) rcode = launch_step<1, 2>(wgt, smem, gx, M, A, st);
   else if (m <= 12) rcode = launch_step<2, 3>(wgt, smem, gx, M, A, st);

@@ -1,0 +1,356 @@
+// Host side of one LOBPCG iteration: the Rayleigh-Ritz step on the projected
+// pencil, with the reference's basis-repair ladders (reference lobpcg.py:475-519
+// and the small dense algebra of multivec.py:89-211).
+//
+// Input is the Gram data the device passes produced (F1 / K5: G1; K1+K5b: G2);
+// output is the next Ritz values and the update coefficients with the
+// Cholesky-QR factors of W and P folded in (so the tall blocks are never
+// rewritten).  Everything here is O(m^3) on <= 3m x 3m matrices; it sits on
+// the critical path between two device passes, which is why it is native.
+//
+// LAPACK: the caller registers dpotrf / dtrtrs / dtrtri / dsyevr with the
+// Fortran-style C signatures of scipy.linalg.cython_lapack (the routines
+// scipy.linalg.cholesky / solve_triangular / eigh -- the reference's calls --
+// run), see b2l_set_lapack.  The small matrix products are plain loops.
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+
+namespace b2l {
+namespace {
+
+using potrf_t = void(char*, int*, double*, int*, int*);
+using trtrs_t = void(char*, char*, char*, int*, int*, double*, int*, double*, int*, int*);
+using trtri_t = void(char*, char*, int*, double*, int*, int*);
+using syevr_t = void(char*, char*, char*, int*, double*, int*, double*, double*, int*, int*,
+                     double*, int*, double*, double*, int*, int*, double*, int*, int*, int*,
+                     int*);
+
+potrf_t* g_potrf = nullptr;
+trtrs_t* g_trtrs = nullptr;
+trtri_t* g_trtri = nullptr;
+syevr_t* g_syevr = nullptr;
+
+// column-major dense matrix
+struct Mat {
+  int r = 0, c = 0;
+  std::vector<double> a;
+  Mat() = default;
+  Mat(int r_, int c_) : r(r_), c(c_), a((size_t)r_ * c_, 0.0) {}
+  double& operator()(int i, int j) { return a[(size_t)i + (size_t)j * r]; }
+  double operator()(int i, int j) const { return a[(size_t)i + (size_t)j * r]; }
+  double* p() { return a.data(); }
+};
+
+struct NotSPD {
+  int pivot;
+};
+struct LapackError {
+  const char* what;
+  int info;
+};
+
+Mat matmul(const Mat& x, const Mat& y) {
+  Mat z(x.r, y.c);
+  for (int j = 0; j < y.c; ++j)
+    for (int i = 0; i < x.r; ++i) {
+      double s = 0.0;
+      for (int k = 0; k < x.c; ++k) s += x(i, k) * y(k, j);
+      z(i, j) = s;
+    }
+  return z;
+}
+
+Mat transpose(const Mat& x) {
+  Mat z(x.c, x.r);
+  for (int j = 0; j < x.c; ++j)
+    for (int i = 0; i < x.r; ++i) z(j, i) = x(i, j);
+  return z;
+}
+
+// Upper R with g = R^T R from g's upper triangle; a pivot <= floor * g_jj (or
+// non-finite) throws NotSPD(j)  (small.cholesky; multivec.py:89-122).
+Mat cholesky(const Mat& g, double floor_) {
+  const int k = g.r;
+  Mat r = g;
+  if (k == 0) return r;
+  char uplo = 'U';
+  int n = k, lda = k, info = 0;
+  g_potrf(&uplo, &n, r.p(), &lda, &info);
+  if (info < 0) throw LapackError{"dpotrf", info};
+  for (int j = 0; j < k; ++j)
+    for (int i = j + 1; i < k; ++i) r(i, j) = 0.0;   // clean
+  const int ok = info == 0 ? k : info - 1;
+  for (int j = 0; j < ok; ++j) {
+    const double piv = r(j, j) * r(j, j);
+    if (!(piv > floor_ * g(j, j)) || !std::isfinite(piv)) throw NotSPD{j};
+  }
+  if (info > 0) throw NotSPD{info - 1};
+  return r;
+}
+
+// R^{-T} b (trans) or R^{-1} b for upper R
+Mat trsolve(const Mat& r, const Mat& b, bool trans) {
+  Mat x = b;
+  if (r.r == 0 || b.c == 0) return x;
+  char uplo = 'U', tr = trans ? 'T' : 'N', diag = 'N';
+  int n = r.r, nrhs = b.c, lda = r.r, ldb = b.r, info = 0;
+  Mat rc = r;
+  g_trtrs(&uplo, &tr, &diag, &n, &nrhs, rc.p(), &lda, x.p(), &ldb, &info);
+  if (info != 0) throw LapackError{"dtrtrs", info};
+  return x;
+}
+
+Mat upper_inverse(const Mat& r) {
+  Mat inv = r;
+  if (r.r == 0) return inv;
+  char uplo = 'U', diag = 'N';
+  int n = r.r, lda = r.r, info = 0;
+  g_trtri(&uplo, &diag, &n, inv.p(), &lda, &info);
+  if (info != 0) throw LapackError{"dtrtri", info};
+  for (int j = 0; j < n; ++j)
+    for (int i = j + 1; i < n; ++i) inv(i, j) = 0.0;
+  return inv;
+}
+
+// Cholesky-QR factor of a block from its raw Gram (small.scaled_cholesky,
+// b_orthonormalize lobpcg.py:147-179): returns inv(R D).
+Mat scaled_cholesky_inv(const Mat& g, double floor_) {
+  const int k = g.r;
+  std::vector<double> s(k);
+  for (int j = 0; j < k; ++j) {
+    const double sq = g(j, j);
+    if (!(sq > 0.0) || !std::isfinite(sq)) throw NotSPD{j};
+    s[j] = std::sqrt(sq);
+  }
+  Mat gs(k, k);
+  for (int j = 0; j < k; ++j)
+    for (int i = 0; i < k; ++i) gs(i, j) = g(i, j) / s[i] / s[j];
+  Mat r = cholesky(gs, floor_);
+  for (int j = 0; j < k; ++j)
+    for (int i = 0; i < k; ++i) r(i, j) *= s[j];
+  return upper_inverse(r);
+}
+
+// Smallest `want` pairs of ga c = lam gb c via gb = R^T R (small.gen_sym_eig,
+// multivec.py:174-211); only upper triangles are read.
+void gen_sym_eig(const Mat& ga_in, const Mat& gb, int want, double floor_, double* vals_out,
+                 Mat* c_out) {
+  const int d = ga_in.r;
+  Mat ga(d, d);
+  for (int j = 0; j < d; ++j)
+    for (int i = 0; i <= j; ++i) ga(i, j) = ga(j, i) = ga_in(i, j);
+  Mat r = cholesky(gb, floor_);
+  Mat t = trsolve(r, ga, true);
+  t = trsolve(r, transpose(t), true);
+  Mat ts(d, d);
+  for (int j = 0; j < d; ++j)
+    for (int i = 0; i < d; ++i) ts(i, j) = 0.5 * (t(i, j) + t(j, i));
+  // dsyevr, range 'A', upper, abstol 0 (scipy.linalg.eigh defaults)
+  char jobz = 'V', range = 'A', uplo = 'U';
+  int n = d, lda = d, il = 1, iu = d, mfound = 0, ldz = d, info = 0;
+  double vl = 0.0, vu = 0.0, abstol = 0.0;
+  std::vector<double> w(d), z((size_t)d * d), work((size_t)26 * d + 64);
+  std::vector<int> isuppz(2 * d + 2), iwork((size_t)10 * d + 16);
+  int lwork = (int)work.size(), liwork = (int)iwork.size();
+  g_syevr(&jobz, &range, &uplo, &n, ts.p(), &lda, &vl, &vu, &il, &iu, &abstol, &mfound, w.data(),
+          z.data(), &ldz, isuppz.data(), work.data(), &lwork, iwork.data(), &liwork, &info);
+  if (info != 0) throw LapackError{"dsyevr", info};
+  Mat v(d, want);
+  for (int j = 0; j < want; ++j)
+    for (int i = 0; i < d; ++i) v(i, j) = z[(size_t)i + (size_t)j * d];
+  *c_out = trsolve(r, v, false);
+  for (int j = 0; j < want; ++j) vals_out[j] = w[j];
+}
+
+}  // namespace
+}  // namespace b2l
+
+using namespace b2l;
+
+extern "C" int b2l_set_lapack(void* dpotrf, void* dtrtrs, void* dtrtri, void* dsyevr) {
+  if (!dpotrf || !dtrtrs || !dtrtri || !dsyevr)
+    return fail(-B2L_EINVAL, "set_lapack: null routine");
+  g_potrf = reinterpret_cast<potrf_t*>(dpotrf);
+  g_trtrs = reinterpret_cast<trtrs_t*>(dtrtrs);
+  g_trtri = reinterpret_cast<trtri_t*>(dtrtri);
+  g_syevr = reinterpret_cast<syevr_t*>(dsyevr);
+  return 0;
+}
+
+extern "C" int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, int ldg1,
+                                 const double* g2, const double* lam, const int* jact, int kj,
+                                 const int* sel, double pivot_floor, double* lam_out,
+                                 double* coef_out, int* pcols_out, int* kp_out,
+                                 int* fallbacks_out) {
+  if (!g_potrf) return fail(-B2L_EINVAL, "rayleigh_ritz: LAPACK not registered (b2l_set_lapack)");
+  if (m < 1 || kst < 0 || kj < 1 || kj > kst || kj > m || !g1 || !g2 || !lam || !jact || !sel)
+    return fail(-B2L_EINVAL, "rayleigh_ritz: bad arguments");
+  const int rW = m, rP = m + kst;
+  const int cW = m, cP = m + kst, cAP = 2 * m + kst;
+  auto G1 = [&](int i, int j) { return g1[(size_t)i * ldg1 + j]; };
+  auto G2 = [&](int i, int j) { return g2[(size_t)i * kst + j]; };
+  int pending = 0;
+  *fallbacks_out = 0;
+  *kp_out = 0;
+  try {
+    // W: Cholesky-QR with column dropping on the J sub-block (lobpcg.py:475-481)
+    std::vector<int> keep(kj);
+    for (int i = 0; i < kj; ++i) keep[i] = i;
+    Mat mw;
+    while (!keep.empty()) {
+      const int k = (int)keep.size();
+      Mat gww(k, k);
+      for (int b = 0; b < k; ++b)
+        for (int a = 0; a < k; ++a) gww(a, b) = G1(rW + sel[keep[a]], cW + sel[keep[b]]);
+      try {
+        mw = scaled_cholesky_inv(gww, pivot_floor);
+        break;
+      } catch (const NotSPD& e) {
+        keep.erase(keep.begin() + e.pivot);
+      }
+    }
+    pending += kj - (int)keep.size();
+    if (keep.empty()) {
+      *fallbacks_out = pending;
+      return fail(-B2L_EDEGENERATE, "BasisDegeneracy");
+    }
+    const int nw = (int)keep.size();
+    std::vector<int> wcols(nw);
+    for (int i = 0; i < nw; ++i) wcols[i] = sel[keep[i]];
+
+    // P_J: Cholesky-QR with floor; NotSPD drops P (lobpcg.py:484-494)
+    Mat mp;
+    bool use_p = false;
+    if (have_p) {
+      Mat gpp(kj, kj);
+      for (int b = 0; b < kj; ++b)
+        for (int a = 0; a < kj; ++a) gpp(a, b) = G1(rP + jact[a], cP + jact[b]);
+      try {
+        mp = scaled_cholesky_inv(gpp, pivot_floor);
+        use_p = true;
+      } catch (const NotSPD&) {
+        pending += 1;
+      }
+    }
+    auto block1 = [&](int r0, const int* ri, int nr, int c0, const int* ci, int nc) {
+      Mat z(nr, nc);
+      for (int b = 0; b < nc; ++b)
+        for (int a = 0; a < nr; ++a) z(a, b) = G1(r0 + (ri ? ri[a] : a), c0 + ci[b]);
+      return z;
+    };
+    Mat gXAW(m, nw), gWAW(nw, nw);
+    for (int b = 0; b < nw; ++b) {
+      for (int a = 0; a < m; ++a) gXAW(a, b) = G2(a, wcols[b]);
+      for (int a = 0; a < nw; ++a) gWAW(a, b) = G2(m + wcols[a], wcols[b]);
+    }
+    Mat gXBW = block1(0, nullptr, m, cW, wcols.data(), nw);
+    Mat gXAP, gWAP, gXBP, gWBP, gPAP;
+    if (have_p) {
+      gXAP = block1(0, nullptr, m, cAP, jact, kj);
+      gWAP = block1(rW, wcols.data(), nw, cAP, jact, kj);
+      gXBP = block1(0, nullptr, m, cP, jact, kj);
+      gWBP = block1(rW, wcols.data(), nw, cP, jact, kj);
+      gPAP = block1(rP, jact, kj, cAP, jact, kj);
+    }
+
+    // Rayleigh-Ritz with the repair ladder (lobpcg.py:501-519)
+    Mat c;
+    std::vector<double> vals(m);
+    while (true) {
+      const int kw = mw.c;
+      const int kp = use_p ? kj : 0;
+      const int d = m + kw + kp;
+      Mat ga(d, d), gb(d, d);
+      for (int i = 0; i < m; ++i) {
+        ga(i, i) = lam[i];
+        gb(i, i) = 1.0;
+      }
+      const Mat mwT = transpose(mw);
+      const Mat aww = matmul(matmul(mwT, gWAW), mw);
+      const Mat axw = matmul(gXAW, mw), bxw = matmul(gXBW, mw);
+      for (int j = 0; j < kw; ++j) {
+        gb(m + j, m + j) = 1.0;
+        for (int i = 0; i < kw; ++i) ga(m + i, m + j) = aww(i, j);
+        for (int i = 0; i < m; ++i) {
+          ga(i, m + j) = axw(i, j);
+          gb(i, m + j) = bxw(i, j);
+        }
+      }
+      if (kp) {
+        const Mat mpT = transpose(mp);
+        const Mat axp = matmul(gXAP, mp), bxp = matmul(gXBP, mp);
+        const Mat awp = matmul(matmul(mwT, gWAP), mp), bwp = matmul(matmul(mwT, gWBP), mp);
+        const Mat app = matmul(matmul(mpT, gPAP), mp);
+        const int o = m + kw;
+        for (int j = 0; j < kp; ++j) {
+          gb(o + j, o + j) = 1.0;
+          for (int i = 0; i < m; ++i) {
+            ga(i, o + j) = axp(i, j);
+            gb(i, o + j) = bxp(i, j);
+          }
+          for (int i = 0; i < kw; ++i) {
+            ga(m + i, o + j) = awp(i, j);
+            gb(m + i, o + j) = bwp(i, j);
+          }
+          for (int i = 0; i < kp; ++i) ga(o + i, o + j) = app(i, j);
+        }
+      }
+      try {
+        gen_sym_eig(ga, gb, m, pivot_floor, vals.data(), &c);
+        break;
+      } catch (const NotSPD& e) {
+        pending += 1;
+        if (use_p) {
+          use_p = false;
+        } else if (m <= e.pivot && e.pivot < m + kw && kw > 1) {
+          Mat mw2(mw.r, kw - 1);
+          int jj = 0;
+          for (int j = 0; j < kw; ++j) {
+            if (j == e.pivot - m) continue;
+            for (int i = 0; i < mw.r; ++i) mw2(i, jj) = mw(i, j);
+            ++jj;
+          }
+          mw = mw2;
+        } else {
+          *fallbacks_out = pending;
+          return fail(-B2L_EDEGENERATE, "BasisDegeneracy");
+        }
+      }
+    }
+    // fold the orthonormalization into raw-block coefficients
+    const int kw = mw.c;
+    const int kp = use_p ? kj : 0;
+    Mat cw(kw, m), cp(kp, m);
+    for (int j = 0; j < m; ++j) {
+      for (int i = 0; i < kw; ++i) cw(i, j) = c(m + i, j);
+      for (int i = 0; i < kp; ++i) cp(i, j) = c(m + kw + i, j);
+    }
+    const Mat cwr = matmul(mw, cw);   // nw x m -> rows wcols of the kst x m block
+    double* cx_o = coef_out;
+    double* cw_o = coef_out + (size_t)m * m;
+    double* cp_o = cw_o + (size_t)kst * m;
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) cx_o[(size_t)i * m + j] = c(i, j);
+    for (size_t e = 0; e < (size_t)kst * m; ++e) cw_o[e] = 0.0;
+    for (int i = 0; i < nw; ++i)
+      for (int j = 0; j < m; ++j) cw_o[(size_t)wcols[i] * m + j] = cwr(i, j);
+    if (kp) {
+      const Mat cpr = matmul(mp, cp);
+      for (int i = 0; i < kp; ++i) {
+        pcols_out[i] = jact[i];
+        for (int j = 0; j < m; ++j) cp_o[(size_t)i * m + j] = cpr(i, j);
+      }
+    }
+    for (int j = 0; j < m; ++j) lam_out[j] = vals[j];
+    *kp_out = kp;
+    *fallbacks_out = pending;
+    return 0;
+  } catch (const LapackError& e) {
+    return fail(-B2L_ELAPACK, std::string("rayleigh_ritz: ") + e.what + " info " +
+                                   std::to_string(e.info));
+  } catch (const std::bad_alloc&) {
+    return fail(-B2L_ENOMEM, "rayleigh_ritz: out of host memory");
+  }
+}

@@ -47,7 +47,7 @@ from .operators import (
     JacobiPreconditioner,
     Laplacian3D,
 )
-from .small import NotSPD, gen_sym_eig, scaled_cholesky, sym_eig
+from .small import NativeRitz, NotSPD, RitzFailure, gen_sym_eig, scaled_cholesky, sym_eig
 
 __all__ = [
     "SolverConfig",
@@ -330,6 +330,7 @@ class LOBPCGRun:
         self.have_p = False
         self.history = []
         self.pending = 0
+        self._ritz = NativeRitz(self.m)
         self.total_fallbacks = 0
         self.failure = None
         self.norms = np.zeros(m)
@@ -576,103 +577,27 @@ class LOBPCGRun:
         return W, AW, kj, np.arange(kj)
 
     def _rayleigh_ritz(self, G1, G2, J, sel, kst, W, AW):
+        """Rayleigh-Ritz on the projected blocks (lobpcg.py:475-519) in the
+        native host routine b2l_rayleigh_ritz, then the device update."""
         m, n = self.m, self.n
-        hp = self.have_p
-        # G1: L = [X, W(kst), P?] x R = [BX, BW, BP?, AP?];  G2: [X; W]^T AW
-        rW, rP = m, m + kst
-        cW, cP, cAP = m, m + kst, 2 * m + kst
-
-        # W: Cholesky-QR with column dropping on the J sub-block
-        # (lobpcg.py:475-481, :182-200), W never rewritten
-        keep = list(range(J.size))
-        mw = None
-        while keep:
-            ks = sel[keep]
-            gww = G1[rW + ks][:, cW + ks]
-            try:
-                _, mw = scaled_cholesky(gww, PIVOT_FLOOR)
-                break
-            except NotSPD as err:
-                del keep[err.pivot]
-        self.pending += J.size - len(keep)
-        if not keep:
+        try:
+            lam_new, coef, pcols, fb = self._ritz(m, kst, self.have_p, G1, G2, self.lam, J, sel,
+                                                  PIVOT_FLOOR)
+        except RitzFailure as f:
+            self.pending += f.fallbacks
             raise _Failure("BasisDegeneracy")
-        wcols = sel[keep]                 # stored W columns in the basis
-
-        # P_J: Cholesky-QR with floor; NotSPD drops P (lobpcg.py:484-494)
-        mp = None
-        if hp:
-            try:
-                _, mp = scaled_cholesky(G1[rP + J][:, cP + J], PIVOT_FLOOR)
-            except NotSPD:
-                mp = None
-                self.pending += 1
-
-        gXAW = G2[:m][:, wcols]
-        gWAW = G2[m + wcols][:, wcols]
-        gXBW = G1[:m][:, cW + wcols]
-        if hp:
-            gXAP = G1[:m][:, cAP + J]
-            gWAP = G1[rW + wcols][:, cAP + J]
-            gXBP = G1[:m][:, cP + J]
-            gWBP = G1[rW + wcols][:, cP + J]
-            gPAP = G1[rP + J][:, cAP + J]
-
-        # Rayleigh-Ritz with the repair ladder (lobpcg.py:501-519)
-        use_p = mp is not None
-        while True:
-            kw = mw.shape[1]
-            kp = J.size if use_p else 0
-            d = m + kw + kp
-            ga = np.zeros((d, d))
-            gb = np.zeros((d, d))
-            sx, sw, sp = slice(0, m), slice(m, m + kw), slice(m + kw, d)
-            ga[sx, sx] = np.diag(self.lam)
-            gb[sx, sx] = np.eye(m)
-            ga[sw, sw] = mw.T @ gWAW @ mw
-            gb[sw, sw] = np.eye(kw)
-            ga[sx, sw] = gXAW @ mw
-            gb[sx, sw] = gXBW @ mw
-            if kp:
-                ga[sx, sp] = gXAP @ mp
-                ga[sw, sp] = mw.T @ gWAP @ mp
-                gb[sx, sp] = gXBP @ mp
-                gb[sw, sp] = mw.T @ gWBP @ mp
-                ga[sp, sp] = mp.T @ gPAP @ mp
-                gb[sp, sp] = np.eye(kp)
-            try:
-                lam_new, c = gen_sym_eig(ga, gb, m, PIVOT_FLOOR)
-                break
-            except NotSPD as err:
-                self.pending += 1
-                if use_p:
-                    use_p = False
-                elif m <= err.pivot < m + kw and kw > 1:
-                    keepc = np.arange(kw) != err.pivot - m
-                    mw = mw[:, keepc]
-                else:
-                    raise _Failure("BasisDegeneracy")
-        kw = mw.shape[1]
-        cx = c[:m]
-        cw = c[m:m + kw]
-        cp = c[m + kw:]
-        # fold the orthonormalization into raw-block coefficients
-        cw_raw = np.zeros((kst, m))
-        cw_raw[wcols] = mw @ cw
-        if use_p:
-            cp_raw = mp @ cp
-            pcols = J.astype(np.int32)
-        else:
-            cp_raw = np.zeros((0, m))
-            pcols = np.zeros(0, dtype=np.int32)
+        self.pending += fb
         kp = pcols.size
+        cx = coef[:m * m].reshape(m, m)
+        cw_raw = coef[m * m:m * m + kst * m].reshape(kst, m)
+        cp_raw = coef[m * m + kst * m:].reshape(kp, m)
 
         if self.use_f1:
             # next iteration's W holds the current active set J
             wpos = np.full(m, -1, dtype=np.int32)
             wpos[J] = np.arange(J.size, dtype=np.int32)
             (coef_d, lam_d), (pc_d, wpos_d) = self.pin.upload(
-                [np.concatenate([cx.ravel(), cw_raw.ravel(), cp_raw.ravel()]), lam_new],
+                [coef, lam_new],
                 [pcols if kp else np.zeros(1, np.int32), wpos])
             nxt = 1 - self.wcur
             Wn, _ = self._wview(J.size, nxt)

@@ -121,3 +121,55 @@ def scaled_cholesky(g: np.ndarray, pivot_floor: float = 0.0):
     r = cholesky(gs, pivot_floor)
     reff = r * s[None, :]
     return reff, upper_inverse(reff)
+
+
+class RitzFailure(Exception):
+    """b2l_rayleigh_ritz exhausted the repair ladder (BasisDegeneracy)."""
+
+    def __init__(self, fallbacks):
+        super().__init__("BasisDegeneracy")
+        self.fallbacks = int(fallbacks)
+
+
+class NativeRitz:
+    """Host Rayleigh-Ritz step in the native library (b2l_rayleigh_ritz):
+    W / P Cholesky-QR with the column-drop and P-drop ladders, the projected
+    pencil, the generalised eigensolve with its retry ladder and the
+    coefficient folding of lobpcg.py:475-540, in one call.  Output buffers are
+    reused across iterations."""
+
+    def __init__(self, m):
+        import ctypes as C
+
+        from . import _lib
+
+        self._C = C
+        self._lib = _lib
+        self.m = m
+        self.lam = np.zeros(m)
+        self.coef = np.zeros(3 * m * m)
+        self.pcols = np.zeros(m, dtype=np.int32)
+        self._kp = C.c_int()
+        self._fb = C.c_int()
+
+    def __call__(self, m, kst, have_p, g1, g2, lam, jact, sel, pivot_floor):
+        C, L = self._C, self._lib
+        lib = L.load()
+        g1 = np.ascontiguousarray(g1, dtype=np.float64)
+        g2 = np.ascontiguousarray(g2, dtype=np.float64)
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        jact = np.ascontiguousarray(jact, dtype=np.int32)
+        sel = np.ascontiguousarray(sel, dtype=np.int32)
+        dp, ip = L.c_dp, L.c_ip
+        rc = lib.b2l_rayleigh_ritz(
+            m, kst, int(have_p), g1.ctypes.data_as(dp), g1.shape[1], g2.ctypes.data_as(dp),
+            lam.ctypes.data_as(dp), jact.ctypes.data_as(ip), jact.size, sel.ctypes.data_as(ip),
+            float(pivot_floor), self.lam.ctypes.data_as(dp), self.coef.ctypes.data_as(dp),
+            self.pcols.ctypes.data_as(ip), C.byref(self._kp), C.byref(self._fb))
+        if rc == L.EDEGENERATE:
+            raise RitzFailure(self._fb.value)
+        L.check(rc, "b2l_rayleigh_ritz")
+        kp = self._kp.value
+        ncoef = m * m + kst * m + kp * m
+        return (self.lam.copy(), self.coef[:ncoef].copy(), self.pcols[:kp].copy(),
+                self._fb.value)

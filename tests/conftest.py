@@ -45,3 +45,33 @@ def trajectory_band_ok(ritz, g, floor=1e-8, factor=10.0, window=5):
     env = np.array([band[max(0, i - window):i + window + 1].max() for i in range(nit)])
     allowed = np.maximum(floor, factor * env)[:, None]
     return bool(np.all(dev <= allowed)), float((dev / allowed).max())
+
+
+def golden20_band(golden):
+    """The 20^3 golden case with its full reference band: the CSV run, the
+    coherent-scaling runs (golden_20cubed_m10_jacobi_seed2.npz) and the
+    rounding-noise runs (golden_20cubed_band.npz: operator outputs and Ritz
+    coefficients perturbed by +-1 ulp; make_golden.py --band20)."""
+    import numpy as np
+
+    g = golden("golden_20cubed_m10_jacobi_seed2.npz")
+    b = golden("golden_20cubed_band.npz")
+    n = min(g["pert_ritz"].shape[1], b["pert_ritz"].shape[1])
+    out = dict(g)
+    out["pert_ritz"] = np.concatenate([g["pert_ritz"][:, :n], b["pert_ritz"][:, :n]])
+    out["all_iterations"] = np.concatenate([[int(g["iterations_used"])], g["pert_iterations"],
+                                            b["pert_iterations"]])
+    out["all_locks"] = np.vstack([g["lock_iterations"], g["pert_locks"], b["pert_locks"]])
+    return out
+
+
+def locks_in_band(locks, all_locks, slack=0.1):
+    """Lock iterations of degenerate clusters are not a stable observable
+    (two basins, long tails under rounding noise): each column's lock
+    iteration must lie within the reference band widened by `slack`
+    (relative) + 1."""
+    import numpy as np
+
+    lo = np.floor(all_locks.min(0) * (1.0 - slack)) - 1
+    hi = np.ceil(all_locks.max(0) * (1.0 + slack)) + 1
+    return bool(np.all((locks >= lo) & (locks <= hi))), lo, hi

@@ -11,9 +11,10 @@ Criteria (SURVEY 8c parity protocol, BASELINE.json north_star):
 
 import numpy as np
 
-from tests.conftest import trajectory_band_ok
 import pytest
 import torch
+
+from tests.conftest import golden20_band, locks_in_band, trajectory_band_ok
 
 pytestmark = pytest.mark.gpu
 
@@ -40,19 +41,18 @@ def rel(a, b):
 def test_golden_trajectory(pk, golden):
     """20^3 unscaled, m=10, Jacobi, tol 1e-6, seed 2 -> Converged @180
     (pkg/demos/convergence_history.csv)."""
-    g = golden("golden_20cubed_m10_jacobi_seed2.npz")
+    g = golden20_band(golden)
     a = pk.laplacian3d((20, 20, 20))
     rep = pk.solve(a, t=pk.jacobi_preconditioner(a),
                    config=pk.SolverConfig(block_size=10, tol=1e-6, max_iter=200, seed=2))
     assert rep.status == "Converged"
-    # The reference itself moves between 180 and 187 iterations when its
-    # operator is perturbed by 1-3 ulp (golden pert_iterations); hold the GPU
-    # run to that band +-1, and each column's lock iteration likewise.
-    its = np.concatenate([[180], g["pert_iterations"]])
+    # The reference itself moves between 180 and 197 iterations under
+    # rounding-level perturbations (golden20_band); hold the GPU run to that
+    # band +-1, and each column's lock iteration to the widened lock band.
+    its = g["all_iterations"]
     assert its.min() - 1 <= rep.iterations_used <= its.max() + 1, rep.iterations_used
-    locks = np.vstack([g["lock_iterations"], g["pert_locks"]])
-    assert np.all(rep.lock_iterations >= locks.min(0) - 1), rep.lock_iterations
-    assert np.all(rep.lock_iterations <= locks.max(0) + 1), rep.lock_iterations
+    ok, lo, hi = locks_in_band(rep.lock_iterations, g["all_locks"])
+    assert ok, (rep.lock_iterations, lo, hi)
     ritz = np.array([h.ritz for h in rep.history])
     ok, worst = trajectory_band_ok(ritz, g)
     assert ok, worst

@@ -1,0 +1,138 @@
+"""b2l_rayleigh_ritz (host, native) against the numpy checker
+tests/rr_reference.py on Gram blocks of random tall blocks, including every
+rung of the repair ladders (lobpcg.py:475-519).  CPU only: the routine is host
+code, no GPU is needed."""
+
+import numpy as np
+import pytest
+
+from paper_0705_2626_b200.small import NativeRitz, RitzFailure
+from tests.rr_reference import Degenerate, rayleigh_ritz_ref
+
+FLOOR = 1e-8
+
+
+def _case(n, m, kst, have_p, seed, bdiag=False, dup_w=None, dup_p=None, zero_w=None):
+    r = np.random.default_rng(seed)
+    a = r.standard_normal((n, n))
+    A = a @ a.T / n + np.diag(np.linspace(1.0, 3.0, n))
+    d = r.uniform(0.5, 2.0, n) if bdiag else np.ones(n)
+    X = r.standard_normal((n, m))
+    # B-orthonormal X of Ritz vectors of the subspace (what the solver keeps)
+    g = X.T @ (d[:, None] * X)
+    L = np.linalg.cholesky(g)
+    X = X @ np.linalg.inv(L).T
+    ev, V = np.linalg.eigh(X.T @ A @ X)
+    X = X @ V
+    lam = ev
+    W = r.standard_normal((n, kst))
+    P = r.standard_normal((n, m))
+    if dup_w is not None:
+        W[:, dup_w[1]] = W[:, dup_w[0]] * (1.0 + 1e-14)
+    if zero_w is not None:
+        W[:, zero_w] = 0.0
+    if dup_p is not None:
+        P[:, dup_p[1]] = P[:, dup_p[0]]
+    BX, BW, BP = d[:, None] * X, d[:, None] * W, d[:, None] * P
+    AW, AP = A @ W, A @ P
+    if have_p:
+        G1 = np.hstack([X, W, P]).T @ np.hstack([BX, BW, BP, AP])
+    else:
+        G1 = np.hstack([X, W]).T @ np.hstack([BX, BW])
+    G2 = np.hstack([X, W]).T @ AW
+    return G1, G2, lam
+
+
+def _both(m, kst, have_p, G1, G2, lam, J, sel):
+    nat = NativeRitz(m)
+    try:
+        got = nat(m, kst, have_p, G1, G2, lam, J, sel, FLOOR)
+        gerr = None
+    except RitzFailure as f:
+        got, gerr = None, f.fallbacks
+    try:
+        ref = rayleigh_ritz_ref(m, kst, have_p, G1, G2, lam, J, sel, FLOOR)
+        rerr = None
+    except Degenerate as f:
+        ref, rerr = None, f.fallbacks
+    return got, gerr, ref, rerr
+
+
+def _compare(got, ref, m, kst):
+    lam_g, coef_g, pc_g, fb_g = got
+    lam_r, coef_r, pc_r, fb_r = ref
+    assert fb_g == fb_r
+    assert np.array_equal(pc_g, pc_r)
+    np.testing.assert_allclose(lam_g, lam_r, rtol=1e-10, atol=1e-12)
+    assert coef_g.shape == coef_r.shape
+    # eigenvectors are defined up to sign: compare column by column
+    kp = pc_g.size
+    rows = m + kst + kp
+
+    def cols(c):
+        return np.vstack([c[:m * m].reshape(m, m), c[m * m:m * m + kst * m].reshape(kst, m),
+                          c[m * m + kst * m:].reshape(kp, m)])
+
+    cg, cr = cols(coef_g), cols(coef_r)
+    assert cg.shape == (rows, m)
+    for j in range(m):
+        s = np.sign(cg[:, j] @ cr[:, j])
+        np.testing.assert_allclose(s * cg[:, j], cr[:, j], rtol=1e-7,
+                                   atol=1e-9 * np.abs(cr[:, j]).max())
+
+
+@pytest.mark.parametrize("m,kst,have_p,bdiag", [(4, 4, False, False), (4, 4, True, False),
+                                                (10, 10, True, False), (6, 6, True, True),
+                                                (1, 1, True, False)])
+def test_native_rr_matches_numpy(m, kst, have_p, bdiag):
+    G1, G2, lam = _case(300, m, kst, have_p, seed=m * 7 + kst, bdiag=bdiag)
+    J = np.arange(m)
+    got, gerr, ref, rerr = _both(m, kst, have_p, G1, G2, lam, J, J.copy())
+    assert gerr is None and rerr is None
+    _compare(got, ref, m, kst)
+
+
+def test_native_rr_locked_subset():
+    # 3 of 8 columns locked: W holds the 6 previous-active columns, J is 5 of them
+    m, kst = 8, 6
+    G1, G2, lam = _case(250, m, kst, True, seed=11)
+    jprev = np.array([0, 2, 3, 5, 6, 7])
+    J = np.array([0, 3, 5, 6, 7])
+    sel = np.searchsorted(jprev, J)
+    got, gerr, ref, rerr = _both(m, kst, True, G1, G2, lam, J, sel)
+    assert gerr is None and rerr is None
+    _compare(got, ref, m, kst)
+    # unused W column (stored position 1) gets zero coefficients
+    coef = got[1]
+    assert np.all(coef[m * m + 1 * m:m * m + 2 * m] == 0.0)
+
+
+def test_native_rr_drops_dependent_w_column():
+    m = 5
+    G1, G2, lam = _case(200, m, m, True, seed=3, dup_w=(1, 3))
+    J = np.arange(m)
+    got, gerr, ref, rerr = _both(m, m, True, G1, G2, lam, J, J.copy())
+    assert gerr is None and rerr is None
+    assert got[3] >= 1 and got[3] == ref[3]
+    _compare(got, ref, m, m)
+
+
+def test_native_rr_drops_degenerate_p():
+    m = 5
+    G1, G2, lam = _case(200, m, m, True, seed=4, dup_p=(0, 2))
+    J = np.arange(m)
+    got, gerr, ref, rerr = _both(m, m, True, G1, G2, lam, J, J.copy())
+    assert gerr is None and rerr is None
+    assert got[2].size == 0 and ref[2].size == 0   # P dropped
+    _compare(got, ref, m, m)
+
+
+def test_native_rr_all_w_zero_is_degenerate():
+    m = 3
+    G1, G2, lam = _case(100, m, m, True, seed=5)
+    z = np.zeros_like(G1)
+    z[:m, :m] = G1[:m, :m]
+    J = np.arange(m)
+    got, gerr, ref, rerr = _both(m, m, True, z, G2, lam, J, J.copy())
+    assert got is None and ref is None
+    assert gerr == rerr == m
