@@ -152,6 +152,21 @@ int b2l_lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx
                     int want_ax_norms, double* red_out, void* stream);
 
 /*
+ * K9 -- the seeded initial block on the device, bit for bit the reference's
+ * multivec.seeded_random_fill (multivec.py:220-229):
+ *   Generator(PCG64(seed)).uniform(low, high, (n, m))  (C order)
+ * out[r*ld + j] (r < nrows, j < m) = draw (first_draw + r*m + j) of the PCG64
+ * stream whose state before its first draw is (state_hi:state_lo) with
+ * increment (inc_hi:inc_lo) -- numpy's bit_generator.state['state'].
+ * first_draw = row0*m gives a z-slab its rows of the global block.  Columns
+ * m..ld-1 are not written.
+ */
+int b2l_seeded_fill(double* out, int ld, long long nrows, int m, long long first_draw,
+                    unsigned long long state_hi, unsigned long long state_lo,
+                    unsigned long long inc_hi, unsigned long long inc_lo, double low,
+                    double high, void* stream);
+
+/*
  * Host, small dense: register the LAPACK routines the Rayleigh-Ritz step uses
  * (dpotrf, dtrtrs, dtrtri, dsyevr with the Fortran-style signatures of
  * scipy.linalg.cython_lapack, i.e. the routines scipy.linalg.cholesky /

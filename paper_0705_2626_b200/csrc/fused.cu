@@ -36,6 +36,7 @@
 // conflicts.  Out-of-range rows of the last chunk are zero-filled by the TMA.
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 #include "gram_tile.cuh"
@@ -550,6 +551,85 @@ void tile_mask(int NI, int NJ, const int* lcum, int nl, const int* rcum, int nr,
     }
 }
 
+// The Gram tiles one warp of a pair owns, as a compile-time list.
+// MFIX = 0: the tile block of half h (all NI x NJ tiles split along i when NI
+// is even, else along j).  MFIX = m > 0: only the tiles the next step needs
+// when kw_next = m (the pair modes {2,1,1,1; 0,2,1,1; 0,0,2,1} of
+// b2l_lobpcg_step), split evenly between the halves in row-major order.
+struct PairTiles {
+  int n;
+  int ti[32], tj[32];
+  unsigned imask, jmask;          // tile rows / columns used
+  unsigned need[2];               // all needed tiles (bit t = i*NJ + j)
+};
+
+__host__ __device__ constexpr bool pair_tile_needed(int m, int ti, int tj) {
+  const int lcum[4] = {0, m, 2 * m, 3 * m};
+  const int rcum[5] = {0, m, 2 * m, 3 * m, 4 * m};
+  const int modes[12] = {2, 1, 1, 1, 0, 2, 1, 1, 0, 0, 2, 1};
+  for (int l = 0; l < 3; ++l)
+    for (int r = 0; r < 4; ++r) {
+      const int md = modes[l * 4 + r];
+      if (!md) continue;
+      const int i0 = (8 * ti > lcum[l]) ? 8 * ti : lcum[l];
+      const int i1 = (8 * ti + 8 < lcum[l + 1]) ? 8 * ti + 8 : lcum[l + 1];
+      const int j0 = (8 * tj > rcum[r]) ? 8 * tj : rcum[r];
+      const int j1 = (8 * tj + 8 < rcum[r + 1]) ? 8 * tj + 8 : rcum[r + 1];
+      if (i0 >= i1 || j0 >= j1) continue;
+      if (md == 2 && (i0 - lcum[l]) > (j1 - rcum[r]) - 1) continue;
+      return true;
+    }
+  return false;
+}
+
+__host__ __device__ constexpr PairTiles pair_tiles(int NI, int NJ, int mfix, int h, int nh = 2) {
+  PairTiles T{};
+  if (mfix == 0 && nh == 1) {
+    for (int i = 0; i < NI; ++i)
+      for (int j = 0; j < NJ; ++j) {
+        T.ti[T.n] = i;
+        T.tj[T.n] = j;
+        ++T.n;
+      }
+  } else if (mfix == 0) {
+    const bool split_i = (NI % 2) == 0;
+    const int gi = split_i ? NI / 2 : NI, gj = split_i ? NJ : (NJ + 1) / 2;
+    const int i0 = split_i ? h * gi : 0, j0 = split_i ? 0 : h * gj;
+    for (int i = i0; i < i0 + gi && i < NI; ++i)
+      for (int j = j0; j < j0 + gj && j < NJ; ++j) {
+        T.ti[T.n] = i;
+        T.tj[T.n] = j;
+        ++T.n;
+      }
+  } else {
+    int tot = 0;
+    for (int i = 0; i < NI; ++i)
+      for (int j = 0; j < NJ; ++j)
+        if (pair_tile_needed(mfix, i, j)) {
+          const int t = i * NJ + j;
+          T.need[t >> 5] |= 1u << (t & 31);
+          ++tot;
+        }
+    const int first = nh == 1 ? tot : (tot + 1) / 2;
+    int k = 0;
+    for (int i = 0; i < NI; ++i)
+      for (int j = 0; j < NJ; ++j)
+        if (pair_tile_needed(mfix, i, j)) {
+          if ((h == 0 && k < first) || (h == 1 && k >= first)) {
+            T.ti[T.n] = i;
+            T.tj[T.n] = j;
+            ++T.n;
+          }
+          ++k;
+        }
+  }
+  for (int t = 0; t < T.n; ++t) {
+    T.imask |= 1u << T.ti[t];
+    T.jmask |= 1u << T.tj[t];
+  }
+  return T;
+}
+
 // ---------------------------------------------------------------------------
 // F1, warp-local variant (m <= 10): every compute warp owns 8 rows of a chunk
 // and does everything for them -- update, residual, and the Gram over those 8
@@ -561,7 +641,7 @@ void tile_mask(int NI, int NJ, const int* lcum, int nl, const int* rcum, int nr,
 constexpr int LOC_NW = 8;                        // compute warps (8 x 8 = 64 rows)
 constexpr int LOC_THREADS = 32 * (1 + LOC_NW);   // 288
 
-template <int NT, int KS, int NI, int NJ, bool WGT>
+template <int NT, int KS, int NI, int NJ, int MFIX, bool WGT>
 __global__ void __launch_bounds__(LOC_THREADS, 1)
     step_local_kernel(const __grid_constant__ StepMaps M, const __grid_constant__ StepArgs Ain) {
   extern __shared__ __align__(128) unsigned char sm_raw[];
@@ -605,11 +685,10 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
   auto chunk_of = [&](int it) { return blockIdx.x + it * gridDim.x; };
 
   double s_w0 = 0.0, s_a0 = 0.0;
-  double gacc[NI][NJ][2];
+  constexpr PairTiles TL = pair_tiles(NI, NJ, MFIX, 0, 1);
+  double gacc[TL.n][2];
 #pragma unroll
-  for (int i = 0; i < NI; ++i)
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) gacc[i][j][0] = gacc[i][j][1] = 0.0;
+  for (int t = 0; t < TL.n; ++t) gacc[t][0] = gacc[t][1] = 0.0;
 
   if (warp == 0) {
     // ================= producer / storer =================
@@ -819,12 +898,10 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
           for (int j = 0; j < NJ; ++j)
             if (rw_[j]) bv[j] = __dmul_rn(w, bv[j]);
         }
-        // unconditional: a warp-divergence-safe predicate costs a WARPSYNC
-        // per DMMA; the unneeded tiles are simply never read back
+        // compile-time tile list: all tiles, or (MFIX) only the needed ones
 #pragma unroll
-        for (int i = 0; i < NI; ++i)
-#pragma unroll
-          for (int j = 0; j < NJ; ++j) dmma_8x8x4(gacc[i][j][0], gacc[i][j][1], av[i], bv[j]);
+        for (int t = 0; t < TL.n; ++t)
+          dmma_8x8x4(gacc[t][0], gacc[t][1], av[TL.ti[t]], bv[TL.tj[t]]);
       }
       fence_async_smem();   // generic writes -> the TMA store (async proxy)
       __syncwarp();
@@ -860,13 +937,19 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
   double* gred = sm + A.gred_off;   // [warp][NI*NJ tiles][32][2]
   if (warp >= 1) {
 #pragma unroll
-    for (int i = 0; i < NI; ++i)
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) {
-        const size_t o = (((size_t)(warp - 1) * NI * NJ + i * NJ + j) * 32 + lane) * 2;
-        gred[o] = gacc[i][j][0];
-        gred[o + 1] = gacc[i][j][1];
-      }
+    for (int t = 0; t < TL.n; ++t) {
+      const size_t o =
+          (((size_t)(warp - 1) * NI * NJ + TL.ti[t] * NJ + TL.tj[t]) * 32 + lane) * 2;
+      gred[o] = gacc[t][0];
+      gred[o + 1] = gacc[t][1];
+    }
+    if (MFIX)
+      for (int t = 0; t < NI * NJ; ++t)
+        if (!((TL.need[t >> 5] >> (t & 31)) & 1u)) {
+          const size_t o = (((size_t)(warp - 1) * NI * NJ + t) * 32 + lane) * 2;
+          gred[o] = 0.0;
+          gred[o + 1] = 0.0;
+        }
   }
   __syncthreads();
   double* go = out + 2 * m;
@@ -888,23 +971,24 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
   }
 }
 
-// ---------------------------------------------------------------------------
-// F1, warp-pair variant (m <= 10): 16 compute warps, two per 8-row tile.  Of a
-// pair, warp h = 0 forms P' and X', warp h = 1 forms AP' and AX' (the same
-// coefficients on the A-side blocks); after a pair barrier the 64 threads
-// form the residual of the 8 rows, and after a second one each warp folds
-// the 8 rows into its half of the Gram tiles.  Halving every warp's
-// accumulators keeps 4 compute warps per SM sub-partition resident (vs 2 in
-// the one-warp-per-tile layout), which is what keeps the DMMA pipe fed.
 constexpr int PAIR_NW = 14;                        // compute warps (7 pairs, 56-row chunks)
 constexpr int PAIR_THREADS = 32 * (1 + PAIR_NW);   // 480: <= 4 warps per SMSP
-constexpr int NB_PAIR = 5;                         // named barriers 5..12
+constexpr int NB_PAIR = 5;                         // named barriers 5..11
+constexpr int NB_PAIR_DONE = 15;
 
-template <int NT, int KS, int NI, int NJ, bool SPLIT_I, bool WGT>
+// ---------------------------------------------------------------------------
+// F1, warp-pair variant (m = 9..10): 14 compute warps, two per 8-row tile.
+// Of a pair, warp h = 0 forms P' and X', warp h = 1 forms AP' and AX' (the
+// same coefficients on the A-side blocks); after a pair barrier the 64
+// threads form the residual of the 8 rows, and after a second one each warp
+// folds the 8 rows into its share of the Gram tiles (a compile-time tile
+// list: with MFIX the tiles the next step never reads are not computed).
+// Halving every warp's accumulators keeps 4 warps per SM sub-partition
+// resident (vs 2 in the one-warp-per-tile layout), which is what keeps the
+// DMMA pipe fed.
+template <int NT, int KS, int NI, int NJ, int MFIX, bool WGT>
 __global__ void __launch_bounds__(PAIR_THREADS, 1)
     step_pair_kernel(const __grid_constant__ StepMaps M, const __grid_constant__ StepArgs Ain) {
-  constexpr int GI = SPLIT_I ? NI / 2 : NI;          // this warp's Gram tile block
-  constexpr int GJ = SPLIT_I ? NJ : (NJ + 1) / 2;
   extern __shared__ __align__(128) unsigned char sm_raw[];
   __shared__ StepArgs sA;
   if (threadIdx.x == 0) sA = Ain;
@@ -944,49 +1028,18 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
   const int nchunks = (A.nrows + A.rc - 1) / A.rc;
   const int nloc = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   auto chunk_of = [&](int it) { return blockIdx.x + it * gridDim.x; };
-
+  double* gred = sm + A.gred_off;   // [pair][NI*NJ tiles][32][2]
   double s_w0 = 0.0, s_a0 = 0.0;
-  double gacc[GI][GJ][2];
-#pragma unroll
-  for (int i = 0; i < GI; ++i)
-#pragma unroll
-    for (int j = 0; j < GJ; ++j) gacc[i][j][0] = gacc[i][j][1] = 0.0;
 
-  if (warp == 0) {
-    // ================= producer / storer =================
-    if (lane == 0)
-      for (int j = 0; j < A.nst && j < nloc; ++j)
-        step_issue(M, A, stages + (size_t)j * A.stage_doubles, &full[j], chunk_of(j));
-    for (int it = 0; it < nloc; ++it) {
-      const int b = it & 1;
-      nbar_sync(NB_OFULL + b, PAIR_THREADS);
-      if (lane == 0) {
-        const int r0 = chunk_of(it) * A.rc;
-        const int ob = b * A.out_stride;
-        for (int k = 0; k < 5; ++k) {
-          if (k == 4 && A.kwn == 0) continue;
-          tma_store_2d(&M.out[k], sm + A.out_off[k] + ob, 0, r0);
-        }
-        bulk_commit();
-        bulk_wait_read<0>();
-      }
-      __syncwarp();
-      nbar_arrive(NB_OEMPTY + b, PAIR_THREADS);
-      const int jn = it + A.nst;
-      if (lane == 0 && jn < nloc) {
-        const int s = it % A.nst;
-        mbar_wait(&empty[s], (it / A.nst) & 1);
-        step_issue(M, A, stages + (size_t)s * A.stage_doubles, &full[s], chunk_of(jn));
-      }
-      __syncwarp();
-    }
-    if (lane == 0) bulk_wait<0>();
-  } else {
+  // compute warps: one instantiation per half, so each owns exactly its
+  // accumulators (the register allocator never sees the other half's)
+  auto run_half = [&](auto hc) {
+    constexpr int H = decltype(hc)::value;
+    constexpr PairTiles TL = pair_tiles(NI, NJ, MFIX, H);
     const int cw = warp - 1;
-    const int mt = cw >> 1, h = cw & 1;        // 8-row tile, half
+    const int mt = cw >> 1;                    // 8-row tile
     const int pbar = NB_PAIR + mt;
     const int q = lane & 3, rl = lane >> 2;
-    // update coefficients (B fragments), shared by both halves
     double cW[NT][KS], cP[NT][KS], cX[NT][KS];
     int pcol[KS];
 #pragma unroll
@@ -1002,26 +1055,24 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         cX[nt][ks] = (cv && k < m) ? coef[k * m + cb] : 0.0;
       }
     }
-    // residual: the pair's 64 threads as (rsub, j), RP2 rows per pass
-    const int pt = h * 32 + lane;
+    const int pt = H * 32 + lane;
     const int RP2 = 64 / m;
     const int rsub = pt / m, j0 = pt % m;
     const bool on0 = rsub < RP2;
     const double lam0 = on0 ? slam[j0] : 0.0;
     const int jpos0 = on0 ? swp[j0] : -1;
-    // Gram lane columns of this warp's tile block
-    const int i0 = SPLIT_I ? h * GI : 0;
-    const int jb0 = SPLIT_I ? 0 : h * GJ;
+    // lane columns of the tile rows / columns this warp uses
     const uint32_t zero_adr = sm_base + (uint32_t)A.zero_off * 8u;
-    uint32_t la_[GI], ls_[GI], rb_[GJ], rs_[GJ];
-    bool rw_[GJ];
+    uint32_t la_[NI], ls_[NI], rb_[NJ], rs_[NJ];
+    bool rw_[NJ];
     const int Lblk[3] = {0, 4, 2};
     const int Rblk[4] = {0, 4, 2, 3};
 #pragma unroll
-    for (int i = 0; i < GI; ++i) {
-      const int ci = 8 * (i0 + i) + (lane >> 2);
+    for (int i = 0; i < NI; ++i) {
       la_[i] = zero_adr;
       ls_[i] = 0;
+      if (!((TL.imask >> i) & 1u)) continue;
+      const int ci = 8 * i + (lane >> 2);
       if (ci < A.a) {
         int l = 0;
         while (l + 1 < 3 && A.lcum[l + 1] <= ci) ++l;
@@ -1030,12 +1081,13 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
       }
     }
 #pragma unroll
-    for (int j = 0; j < GJ; ++j) {
-      const int cj = 8 * (jb0 + j) + (lane >> 2);
+    for (int j = 0; j < NJ; ++j) {
       rb_[j] = zero_adr;
       rs_[j] = 0;
       rw_[j] = false;
-      if (jb0 + j < NJ && cj < A.b) {
+      if (!((TL.jmask >> j) & 1u)) continue;
+      const int cj = 8 * j + (lane >> 2);
+      if (cj < A.b) {
         int r = 0;
         while (r + 1 < 4 && A.rcum[r + 1] <= cj) ++r;
         rb_[j] = sm_base + 8u * (A.out_off[Rblk[r]] + (cj - A.rcum[r]));
@@ -1043,6 +1095,9 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         rw_[j] = r < 3;
       }
     }
+    double gacc[TL.n > 0 ? TL.n : 1][2];
+#pragma unroll
+    for (int t = 0; t < TL.n; ++t) gacc[t][0] = gacc[t][1] = 0.0;
 
     for (int it = 0; it < nloc; ++it) {
       const int s = it % A.nst, b = it & 1;
@@ -1054,12 +1109,12 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
       const int ob = b * A.out_stride;
       const int r = 8 * mt + rl;
       {
-        // ---- (1) update, this warp's side (h = 0: P', X'; h = 1: AP', AX')
-        const double* Wb = st + A.in_off[2 + h];
-        const double* Pb = st + A.in_off[4 + h];
-        const double* Xb = st + A.in_off[0 + h];
-        double* Ox = sm + A.out_off[0 + h] + ob;
-        double* Op = sm + A.out_off[2 + h] + ob;
+        // ---- (1) update, this warp's side (H = 0: P', X'; H = 1: AP', AX')
+        const double* Wb = st + A.in_off[2 + H];
+        const double* Pb = st + A.in_off[4 + H];
+        const double* Xb = st + A.in_off[0 + H];
+        double* Ox = sm + A.out_off[0 + H] + ob;
+        double* Op = sm + A.out_off[2 + H] + ob;
         double acc[NT][3][2];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
@@ -1125,26 +1180,29 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
           O4[(8 * mt + e / npad) * swn + A.kwn + e % npad] = 0.0;
       }
       nbar_sync(pbar, 64);
-      // ---- (3) Gram over the 8 rows, this warp's tile block
+      // ---- (3) Gram over the 8 rows, this warp's tiles
       const uint32_t boff = 8u * (uint32_t)ob;
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
         const uint32_t row = (uint32_t)(8 * mt + 4 * ks + q);
-        double av[GI], bv[GJ];
+        double av[NI], bv[NJ];
 #pragma unroll
-        for (int i = 0; i < GI; ++i) av[i] = lds64(la_[i] + (ls_[i] ? boff : 0u) + row * ls_[i]);
+        for (int i = 0; i < NI; ++i)
+          av[i] = ((TL.imask >> i) & 1u) ? lds64(la_[i] + (ls_[i] ? boff : 0u) + row * ls_[i])
+                                          : 0.0;
 #pragma unroll
-        for (int j = 0; j < GJ; ++j) bv[j] = lds64(rb_[j] + (rs_[j] ? boff : 0u) + row * rs_[j]);
+        for (int j = 0; j < NJ; ++j)
+          bv[j] = ((TL.jmask >> j) & 1u) ? lds64(rb_[j] + (rs_[j] ? boff : 0u) + row * rs_[j])
+                                          : 0.0;
         if (WGT) {
           const double w = st[A.d_off + row];
 #pragma unroll
-          for (int j = 0; j < GJ; ++j)
+          for (int j = 0; j < NJ; ++j)
             if (rw_[j]) bv[j] = __dmul_rn(w, bv[j]);
         }
 #pragma unroll
-        for (int i = 0; i < GI; ++i)
-#pragma unroll
-          for (int j = 0; j < GJ; ++j) dmma_8x8x4(gacc[i][j][0], gacc[i][j][1], av[i], bv[j]);
+        for (int t = 0; t < TL.n; ++t)
+          dmma_8x8x4(gacc[t][0], gacc[t][1], av[TL.ti[t]], bv[TL.tj[t]]);
       }
       fence_async_smem();   // generic writes -> the TMA store (async proxy)
       __syncwarp();
@@ -1153,6 +1211,60 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     }
     for (int it = (nloc > 2 ? nloc : 2); it < nloc + 2; ++it)
       nbar_sync(NB_OEMPTY + (it & 1), PAIR_THREADS);
+    // the stage ring is idle once every warp is here: stash the accumulators
+    nbar_sync(NB_PAIR_DONE, PAIR_THREADS);
+#pragma unroll
+    for (int t = 0; t < TL.n; ++t) {
+      const size_t o =
+          (((size_t)mt * NI * NJ + TL.ti[t] * NJ + TL.tj[t]) * 32 + lane) * 2;
+      gred[o] = gacc[t][0];
+      gred[o + 1] = gacc[t][1];
+    }
+    if (MFIX && H == 0) {
+      // tiles nobody computes: defined zeros
+      for (int t = 0; t < NI * NJ; ++t)
+        if (!((TL.need[t >> 5] >> (t & 31)) & 1u)) {
+          const size_t o = (((size_t)mt * NI * NJ + t) * 32 + lane) * 2;
+          gred[o] = 0.0;
+          gred[o + 1] = 0.0;
+        }
+    }
+  };
+
+  if (warp == 0) {
+    // ================= producer / storer =================
+    if (lane == 0)
+      for (int j = 0; j < A.nst && j < nloc; ++j)
+        step_issue(M, A, stages + (size_t)j * A.stage_doubles, &full[j], chunk_of(j));
+    for (int it = 0; it < nloc; ++it) {
+      const int b = it & 1;
+      nbar_sync(NB_OFULL + b, PAIR_THREADS);
+      if (lane == 0) {
+        const int r0 = chunk_of(it) * A.rc;
+        const int ob = b * A.out_stride;
+        for (int k = 0; k < 5; ++k) {
+          if (k == 4 && A.kwn == 0) continue;
+          tma_store_2d(&M.out[k], sm + A.out_off[k] + ob, 0, r0);
+        }
+        bulk_commit();
+        bulk_wait_read<0>();
+      }
+      __syncwarp();
+      nbar_arrive(NB_OEMPTY + b, PAIR_THREADS);
+      const int jn = it + A.nst;
+      if (lane == 0 && jn < nloc) {
+        const int s = it % A.nst;
+        mbar_wait(&empty[s], (it / A.nst) & 1);
+        step_issue(M, A, stages + (size_t)s * A.stage_doubles, &full[s], chunk_of(jn));
+      }
+      __syncwarp();
+    }
+    if (lane == 0) bulk_wait<0>();
+    nbar_sync(NB_PAIR_DONE, PAIR_THREADS);
+  } else if (((warp - 1) & 1) == 0) {
+    run_half(std::integral_constant<int, 0>{});
+  } else {
+    run_half(std::integral_constant<int, 1>{});
   }
   __syncthreads();
 
@@ -1177,23 +1289,6 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     out[tid] = a;
     out[m + tid] = bb;
   }
-  double* gred = sm + A.gred_off;   // [pair][NI*NJ tiles][32][2]
-  if (warp >= 1) {
-    const int cw = warp - 1, pr = cw >> 1, h = cw & 1;
-    const int i0 = SPLIT_I ? h * GI : 0;
-    const int jb0 = SPLIT_I ? 0 : h * GJ;
-#pragma unroll
-    for (int i = 0; i < GI; ++i)
-#pragma unroll
-      for (int j = 0; j < GJ; ++j) {
-        if (jb0 + j >= NJ) continue;
-        const int t = (i0 + i) * NJ + jb0 + j;
-        const size_t o = (((size_t)pr * NI * NJ + t) * 32 + lane) * 2;
-        gred[o] = gacc[i][j][0];
-        gred[o + 1] = gacc[i][j][1];
-      }
-  }
-  __syncthreads();
   double* go = out + 2 * m;
   for (int e = tid; e < NI * NJ * 32; e += blockDim.x) {
     const int t = e / 32, ln = e & 31;
@@ -1213,36 +1308,21 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
   }
 }
 
-template <int NT, int KS, int NI, int NJ, bool SPLIT_I>
-static int launch_pair(bool wgt, size_t smem, int gx, const StepMaps& M, const StepArgs& A,
-                       cudaStream_t st) {
-  auto kern = wgt ? step_pair_kernel<NT, KS, NI, NJ, SPLIT_I, true>
-                  : step_pair_kernel<NT, KS, NI, NJ, SPLIT_I, false>;
-  B2L_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<gx, PAIR_THREADS, smem, st>>>(M, A);
-  B2L_CUDA(cudaGetLastError());
-  return 0;
-}
+using StepKernel = void (*)(StepMaps, StepArgs);
 
-template <int NT, int KS, int NI, int NJ>
-static int launch_local(bool wgt, size_t smem, int gx, const StepMaps& M, const StepArgs& A,
-                        cudaStream_t st) {
-  auto kern = wgt ? step_local_kernel<NT, KS, NI, NJ, true>
-                  : step_local_kernel<NT, KS, NI, NJ, false>;
-  B2L_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<gx, LOC_THREADS, smem, st>>>(M, A);
-  B2L_CUDA(cudaGetLastError());
-  return 0;
+template <int NT, int KS, int NI, int NJ, int MFIX>
+static StepKernel pick_pair(bool wgt) {
+  return wgt ? step_pair_kernel<NT, KS, NI, NJ, MFIX, true>
+             : step_pair_kernel<NT, KS, NI, NJ, MFIX, false>;
 }
-
+template <int NT, int KS, int NI, int NJ, int MFIX>
+static StepKernel pick_local(bool wgt) {
+  return wgt ? step_local_kernel<NT, KS, NI, NJ, MFIX, true>
+             : step_local_kernel<NT, KS, NI, NJ, MFIX, false>;
+}
 template <int NT, int KS>
-static int launch_step(bool wgt, size_t smem, int gx, const StepMaps& M, const StepArgs& A,
-                       cudaStream_t st) {
-  auto kern = wgt ? step_kernel<NT, KS, true> : step_kernel<NT, KS, false>;
-  B2L_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<gx, STEP_THREADS, smem, st>>>(M, A);
-  B2L_CUDA(cudaGetLastError());
-  return 0;
+static StepKernel pick_step(bool wgt) {
+  return wgt ? step_kernel<NT, KS, true> : step_kernel<NT, KS, false>;
 }
 
 int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
@@ -1310,10 +1390,13 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   // (6 blocks + d + t) would exceed ~48 KB; then the deepest TMA ring (<= 4)
   // that fits one CTA per SM.
   const int width = 4 * A.sx + 2 * (kw ? A.sw : 0) + (d ? 1 : 0) + (tmode == 2 ? 1 : 0);
-  static const bool one_warp = [] {
+  // m = 9..10: the warp-pair variant (B2L_STEP_VARIANT=local forces the
+  // one-warp-per-tile variant, for A/B timing); m <= 8: one warp per tile
+  static const bool force_local = [] {
     const char* v = getenv("B2L_STEP_VARIANT");
     return v && strcmp(v, "local") == 0;
   }();
+  const bool one_warp = m <= 8 || force_local;
   A.rc = (local && !one_warp) ? 4 * PAIR_NW : 64;
   while (A.rc > 16 && (size_t)A.rc * width * 8 > 48 * 1024) A.rc >>= 1;
   while (A.rs > 1 && A.rc / A.rs < 4) A.rs >>= 1;
@@ -1397,8 +1480,36 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
     if (rcode) return rcode;
   }
 
+  const bool wgt = d != nullptr;
+  StepKernel kern;
+  int threads;
+  if (local) {
+    B2L_CHECK(rc == (one_warp ? 8 * LOC_NW : 4 * PAIR_NW), -B2L_EINVAL,
+              "step: warp-local variants need 64- / 56-row chunks");
+    if (one_warp) {
+      const bool full = kwn == m;   // the compile-time needed-tile lists assume kw_next = m
+      threads = LOC_THREADS;
+      if (m == 4 && full) kern = pick_local<1, 1, 2, 2, 4>(wgt);
+      else if (m <= 4) kern = pick_local<1, 1, 2, 2, 0>(wgt);
+      else if (m == 8 && full) kern = pick_local<1, 2, 3, 4, 8>(wgt);
+      else if (m <= 8) kern = pick_local<1, 2, 3, 4, 0>(wgt);
+      else kern = pick_local<2, 3, 4, 5, 0>(wgt);
+    } else {
+      threads = PAIR_THREADS;
+      kern = (m == 10 && kwn == 10) ? pick_pair<2, 3, 4, 5, 10>(wgt) : pick_pair<2, 3, 4, 5, 0>(wgt);
+    }
+  } else {
+    threads = STEP_THREADS;
+    kern = m <= 4 ? pick_step<1, 1>(wgt)
+                  : m <= 8 ? pick_step<1, 2>(wgt) : m <= 12 ? pick_step<2, 3>(wgt) : pick_step<2, 4>(wgt);
+  }
+  B2L_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // persistent grid: every CTA the SMs can hold (registers / shared memory)
+  int per_sm = 1;
+  B2L_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  if (per_sm < 1) per_sm = 1;
   const int nchunks = (nrows + rc - 1) / rc;
-  int gx = sm_count();
+  int gx = sm_count() * per_sm;
   if (gx > nchunks) gx = nchunks;
   if (gx < 1) gx = 1;
   const int len = 2 * m + A.a * A.b;
@@ -1406,25 +1517,8 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   double* part = static_cast<double*>(workspace((size_t)gx * len * sizeof(double), &werr));
   if (werr) return werr;
   A.partial = part;
-  const bool wgt = d != nullptr;
-  int rcode;
-  if (local) {
-    B2L_CHECK(rc == (one_warp ? 8 * LOC_NW : 4 * PAIR_NW), -B2L_EINVAL,
-              "step: warp-local variants need 64- / 56-row chunks");
-    if (one_warp) {
-      if (m <= 4) rcode = launch_local<1, 1, 2, 2>(wgt, smem, gx, M, A, st);
-      else if (m <= 8) rcode = launch_local<1, 2, 3, 4>(wgt, smem, gx, M, A, st);
-      else rcode = launch_local<2, 3, 4, 5>(wgt, smem, gx, M, A, st);
-    } else {
-      if (m <= 4) rcode = launch_pair<1, 1, 2, 2, true>(wgt, smem, gx, M, A, st);
-      else if (m <= 8) rcode = launch_pair<1, 2, 3, 4, false>(wgt, smem, gx, M, A, st);
-      else rcode = launch_pair<2, 3, 4, 5, true>(wgt, smem, gx, M, A, st);
-    }
-  } else if (m <= 4) rcode = launch_step<1, 1>(wgt, smem, gx, M, A, st);
-  else if (m <= 8) rcode = launch_step<1, 2>(wgt, smem, gx, M, A, st);
-  else if (m <= 12) rcode = launch_step<2, 3>(wgt, smem, gx, M, A, st);
-  else rcode = launch_step<2, 4>(wgt, smem, gx, M, A, st);
-  if (rcode) return rcode;
+  kern<<<gx, threads, smem, st>>>(M, A);
+  B2L_CUDA(cudaGetLastError());
   return sum_parts(part, gx, len, red_out, st);
 }
 

@@ -65,6 +65,21 @@ def stencil7(x: torch.Tensor, out: torch.Tensor, nx: int, ny: int, nz: int,
     LAUNCHES[0] += 1
 
 
+def seeded_fill(out: torch.Tensor, m: int, seed: int, row0: int = 0, low: float = -1.0,
+                high: float = 1.0) -> None:
+    """out[:, :m] = rows row0.. of Generator(PCG64(seed)).uniform(low, high, (N, m))
+    generated on the device, bit for bit (K9, multivec.py:220-229)."""
+    require_block(out, "seeded_fill out")
+    st = np.random.PCG64(seed).state["state"]
+    mask = (1 << 64) - 1
+    s, inc = int(st["state"]), int(st["inc"])
+    lib = _lib.load()
+    _lib.check(lib.b2l_seeded_fill(out.data_ptr(), out.stride(0), out.shape[0], m, row0 * m,
+                                   s >> 64, s & mask, inc >> 64, inc & mask, float(low),
+                                   float(high), stream_ptr(out.device)), "b2l_seeded_fill")
+    LAUNCHES[0] += 1
+
+
 def stencil7_gram(x: torch.Tensor, out: torch.Tensor, nx: int, ny: int, nz: int,
                   scale: float, xb: torch.Tensor, m: int, kw: int, gram_out: torch.Tensor,
                   halo: torch.Tensor | None = None, has_lo: bool = False,

@@ -291,13 +291,12 @@ class LOBPCGRun:
                 if not np.all(np.isfinite(xh)):
                     raise ValueError("x0 contains non-finite entries")
                 x0t = xh
-        elif rows != n:
-            from .distributed import slab_initial_block
-
-            x0t = slab_initial_block(a.grid, a.part, m, cfg.seed)
         else:
-            x0t = np.random.Generator(np.random.PCG64(cfg.seed)).uniform(-1.0, 1.0, size=(n, m))
-        if rows != n and x0t.shape[0] == n:
+            # seeded block generated on the device (K9), bit for bit
+            # Generator(PCG64(seed)).uniform(-1, 1, (n, m)) (multivec.py:220-229);
+            # a z-slab rank generates its own rows only
+            x0t = None
+        if rows != n and x0t is not None and x0t.shape[0] == n:
             r0 = a.part.z0 * a.plane
             x0t = x0t[r0:r0 + rows]
         if b is not None and self.bdiag is not None and self.bdiag.numel() == n and rows != n:
@@ -320,7 +319,10 @@ class LOBPCGRun:
         self.h_red = _host_buf(nred)
         self.h_g2 = _host_buf((2 * m) * m)
         self.pin = _Pinned(dev, 3 * m * m + 2 * m + 8, 3 * m + 8)
-        if isinstance(x0t, torch.Tensor):
+        if x0t is None:
+            row0 = a.part.z0 * a.plane if rows != self.n_global else 0
+            dv.seeded_fill(self.X, m, cfg.seed, row0)
+        elif isinstance(x0t, torch.Tensor):
             self.X[:, :m] = x0t
         else:
             self.X[:, :m].copy_(torch.from_numpy(x0t))

@@ -126,6 +126,14 @@ def lobpcg_step(nrows, m, x, ax, w, aw, kw, p, ap, kp, pcols, coef, xo, axo, po,
     red_out[:2 * m + G.size] = torch.from_numpy(np.concatenate([_np(sums), G.ravel()]))
 
 
+def seeded_fill(out, m, seed, row0=0, low=-1.0, high=1.0):
+    bg = np.random.PCG64(seed)
+    if row0:
+        bg.advance(row0 * m)
+    vals = np.random.Generator(bg).uniform(low, high, size=(out.shape[0], m))
+    out[:, :m] = torch.from_numpy(vals)
+
+
 @contextlib.contextmanager
 def emulate(monkeypatch):
     """Route paper_0705_2626_b200's device wrappers to the CPU stand-ins."""
@@ -137,6 +145,7 @@ def emulate(monkeypatch):
     monkeypatch.setattr(dv, "update", update)
     monkeypatch.setattr(dv, "stencil7_gram", stencil7_gram)
     monkeypatch.setattr(dv, "lobpcg_step", lobpcg_step)
+    monkeypatch.setattr(dv, "seeded_fill", seeded_fill)
     monkeypatch.setattr(_lib, "ensure_device", lambda i: None)
     monkeypatch.setattr(operators, "_default_device", lambda: torch.device("cpu"))
     yield

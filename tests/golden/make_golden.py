@@ -296,15 +296,46 @@ def band20():
     print(f"band20 {time.time() - t0:.1f} s")
 
 
+def band_c1_coef():
+    """C1@1000 under rounding noise in the Ritz-update coefficients (as
+    band20): a second, wider iteration band for the converging C1 test."""
+    t0 = time.time()
+    orig = mv.multiply
+    its, stats, locks = [], [], []
+    for seed in range(12):
+        rng = np.random.default_rng(3000 + seed)
+
+        def noisy(a, c, rng=rng):
+            c = np.asarray(c)
+            return orig(a, c * (1.0 + rng.integers(-1, 2, size=c.shape) * 2.0 ** -52))
+
+        mv.multiply = noisy
+        try:
+            rep = solve(scaled_laplacian(32),
+                        config=SolverConfig(block_size=4, tol=1e-6, max_iter=1000, seed=0))
+        finally:
+            mv.multiply = orig
+        its.append(rep.iterations_used)
+        stats.append(rep.status)
+        locks.append(rep.lock_iterations)
+        print("C1@1000 coef", seed, rep.status, rep.iterations_used, flush=True)
+    np.savez_compressed(OUT / "c1_1000it_band_coef.npz", iterations=np.array(its),
+                        status=np.array(stats), lock_iterations=np.array(locks))
+    print(f"band_c1_coef {time.time() - t0:.1f} s")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--heavy", action="store_true")
     ap.add_argument("--c2", action="store_true")
     ap.add_argument("--bands", action="store_true")
     ap.add_argument("--band20", action="store_true")
+    ap.add_argument("--band-c1", action="store_true")
     args = ap.parse_args()
     print("blockeig", blockeig.__version__)
-    if args.band20:
+    if args.band_c1:
+        band_c1_coef()
+    elif args.band20:
         band20()
     elif args.bands:
         bands()

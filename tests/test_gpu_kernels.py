@@ -291,3 +291,18 @@ def test_lobpcg_step_kernel(dev, n, m, kw, kp, kwn, useb, tmode):
             elif modes[li][ri] == 2:
                 iu = np.triu_indices(rb_.shape[0])
                 assert np.all(np.abs(gb_[iu] - rb_[iu]) <= 1e-12 * sb_[iu] + 1e-300), (li, ri)
+
+
+@pytest.mark.parametrize("n,m,ld,seed,row0", [(1000, 10, 10, 0, 0), (777, 3, 4, 2, 0),
+                                              (4096, 16, 16, 12345, 0), (513, 7, 8, 3, 1000),
+                                              (1, 1, 2, 9, 0), (70001, 4, 4, 0, 37)])
+def test_seeded_fill_bitwise(dev, n, m, ld, seed, row0):
+    """K9 == numpy Generator(PCG64(seed)).uniform(-1, 1, (N, m)) rows row0.. bit for bit."""
+    from paper_0705_2626_b200 import device as dv
+
+    out = torch.zeros((n, ld), dtype=torch.float64, device=dev)
+    dv.seeded_fill(out, m, seed, row0)
+    ref = np.random.Generator(np.random.PCG64(seed)).uniform(-1.0, 1.0, size=(row0 + n, m))[row0:]
+    got = out.cpu().numpy()
+    assert np.array_equal(got[:, :m], ref)
+    assert np.all(got[:, m:] == 0.0)

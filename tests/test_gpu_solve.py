@@ -80,14 +80,16 @@ def test_c1_converging_time_to_tol(pk, golden):
     """C1 with max_iter=1000 converges.  Its triple eigenvalue cluster makes
     the converged iteration count chaotic: the reference itself, with its
     operator scaled by 1..8 ulp, ends anywhere in 359..612 iterations and
-    sometimes as BasisFallback (golden c1_1000it_band.npz).  The GPU run is
-    held to that band (+-10%) and to the closed form."""
+    sometimes as BasisFallback (golden c1_1000it_band.npz); with +-1 ulp noise
+    in its Ritz-update coefficients, in 338..427 (c1_1000it_band_coef.npz).
+    The GPU run is held to the union band (+-10%) and to the closed form."""
     g = golden("c1_32cubed_m4_1000it.npz")
     band = golden("c1_1000it_band.npz")
+    band2 = golden("c1_1000it_band_coef.npz")
     a, s = scaled(pk, 32)
     rep = pk.solve(a, config=pk.SolverConfig(block_size=4, tol=1e-6, max_iter=1000, seed=0))
     assert rep.status == "Converged" or rep.status.startswith("BasisFallback")
-    its = np.concatenate([[int(g["iterations_used"])], band["iterations"]])
+    its = np.concatenate([[int(g["iterations_used"])], band["iterations"], band2["iterations"]])
     assert 0.9 * its.min() <= rep.iterations_used <= 1.1 * its.max(), rep.iterations_used
     exact = pk.exact_eigenvalues((32, 32, 32), 4, scale=s)
     assert rel(rep.eigenvalues, exact).max() <= REL
