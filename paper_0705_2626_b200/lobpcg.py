@@ -33,6 +33,7 @@ does not fit the fused kernels (m > 16) and generic operators.
 from __future__ import annotations
 
 import contextlib
+import dataclasses
 from dataclasses import dataclass
 
 import numpy as np
@@ -47,7 +48,8 @@ from .operators import (
     JacobiPreconditioner,
     Laplacian3D,
 )
-from .small import NativeRitz, NotSPD, RitzFailure, gen_sym_eig, scaled_cholesky, sym_eig
+from .small import (NativeRitz, NotSPD, RitzFailure, chol_solve, cholesky, gen_sym_eig,
+                    scaled_cholesky, sym_eig)
 
 __all__ = [
     "SolverConfig",
@@ -221,6 +223,112 @@ class _Pinned:
         return ([self.dd[s:s + k] for s, k in outs_d], [self.di[s:s + k] for s, k in outs_i])
 
 
+def _device_of(op, default=None):
+    dev = getattr(op, "device", None)
+    if dev is not None:
+        return dev
+    if default is not None:
+        return default
+    from . import operators
+
+    return operators._default_device()
+
+
+def _padded_block(y, device):
+    """(n, k) array / tensor -> CUDA (n, even(k)) float64 block (zero pad)."""
+    if isinstance(y, torch.Tensor):
+        t = y.detach().to(device=device, dtype=torch.float64)
+    else:
+        arr = np.asarray(y, dtype=np.float64)
+        if arr.ndim != 2:
+            raise ValueError(f"constraint basis must be 2-d, got shape {arr.shape}")
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(device)
+    if t.dim() != 2:
+        raise ValueError(f"constraint basis must be 2-d, got shape {tuple(t.shape)}")
+    n, k = t.shape
+    out = dv.new_block(n, dv.even(k), device)
+    out[:, :k] = t
+    return out
+
+
+class Constraints:
+    """Hard-locking basis: iterates are kept B-orthogonal to span(Y)
+    (reference lobpcg.py:101-128).
+
+    Holds Y, the cached product BY (CUDA (n, k) views of padded blocks) and
+    the host Cholesky factor of Y^T B Y, so projections cost one tall Gram,
+    two small triangular solves and one tall update -- no operator
+    applications.
+    """
+
+    def __init__(self, y, by, yby_chol):
+        dev = y.device if isinstance(y, torch.Tensor) else _device_of(None)
+        self._y = _padded_block(y, dev)
+        self._by = self._y if by is y else _padded_block(by, dev)
+        self._k = int(y.shape[1] if hasattr(y, "shape") else np.asarray(y).shape[1])
+        self.yby_chol = np.asarray(yby_chol, dtype=np.float64)
+
+    @property
+    def y(self):
+        return self._y[:, :self._k]
+
+    @property
+    def by(self):
+        return self._by[:, :self._k]
+
+    @classmethod
+    def from_basis(cls, y, b=None):
+        """Build constraints from a basis block, computing BY and the factor
+        (lobpcg.py:114-124).  Raises NotSPD if the columns of y are not
+        linearly B-independent."""
+        dev = _device_of(b, y.device if isinstance(y, torch.Tensor) else None)
+        Y = _padded_block(y, dev)
+        n, k = Y.shape[0], int(y.shape[1] if hasattr(y, "shape") else np.asarray(y).shape[1])
+        if b is None or isinstance(b, IdentityOperator):
+            BY = Y
+        elif isinstance(b, DiagonalOperator):
+            BY = b.d.to(dev)[:, None] * Y
+        else:
+            BY = _padded_block(b(Y[:, :k]), dev)
+        g = dv.to_host(dv.gram(n, [(Y, k)], [(BY, k)]))
+        r = cholesky(g)                     # NotSPD propagates (multivec.py:89-122)
+        obj = cls.__new__(cls)
+        obj._y, obj._by, obj._k = Y, BY, int(k)
+        obj.yby_chol = r
+        return obj
+
+    @property
+    def count(self):
+        return self._k
+
+
+def apply_constraints(x, constraints, b=None):
+    """x - Y (Y^T B Y)^{-1} (BY)^T x  (lobpcg.py:131-144); b is accepted for
+    call-site symmetry and not consulted.  x: CUDA (n, k) tensor (returned
+    as a new tensor) or array (returned as numpy)."""
+    if constraints is None or constraints.count == 0:
+        return x
+    host = not isinstance(x, torch.Tensor)
+    X = _padded_block(x, constraints._y.device)
+    n, k = X.shape[0], int(x.shape[1] if hasattr(x, "shape") else np.asarray(x).shape[1])
+    out = dv.new_block(n, X.shape[1], X.device)
+    _project_into(X, k, constraints, out)
+    res = out[:, :k]
+    return dv.to_host(res).copy() if host else res
+
+
+def _project_into(X, k, cons, out, reduce=None):
+    """out[:, :k] = X - Y chol_solve(R, (BY)^T X) on the device (K5 + K6)."""
+    n, c = X.shape[0], cons.count
+    g = dv.gram(n, [(cons._by, c)], [(X, k)])
+    if reduce is not None:
+        reduce(g)
+    coef = chol_solve(cons.yby_chol, dv.to_host(g))
+    eye = dv.to_device(np.eye(k), X.device)
+    mc = dv.to_device(-coef, X.device)
+    dv.update(n, k, X, None, eye, out, None, w=cons._y, kw=c, cw=mc, x_plus_p=True)
+
+
 class LOBPCGRun:
     """One LOBPCG solve on the device, stepped iteration by iteration.
 
@@ -231,14 +339,14 @@ class LOBPCGRun:
     def __init__(self, a, b=None, t=None, y=None, x0=None, config=None):
         cfg = config if config is not None else SolverConfig()
         cfg.validate()
-        if y is not None and getattr(y, "count", 0) > 0:
-            raise NotImplementedError(
-                "hard-locking constraints (y) are not on the B200 path yet")
         self.cfg = cfg
         m = cfg.block_size
         n = a.dim
-        if m > n:
-            raise ValueError(f"block size {m} exceeds the constrained problem dimension {n} - 0")
+        ncons = 0 if y is None else y.count
+        if m > n - ncons:
+            raise ValueError(f"block size {m} exceeds the constrained problem dimension "
+                             f"{n} - {ncons}")
+        self.cons = y if ncons else None
         self.a, self.b, self.t = a, b, t
         # z-slab runs (distributed.SlabLaplacian3D): blocks hold this rank's
         # rows; every small reduction is summed over ranks before the host
@@ -272,7 +380,9 @@ class LOBPCGRun:
             self.t_generic = t
         fused = _OPTS["fused"]
         # F1 holds the whole next-step Gram in one CTA; stencil+Gram likewise
-        self.use_f1 = fused and _tilesets(3 * m, 4 * m) <= 8
+        # (hard constraints project W between the residual and A W: F1 forms
+        # W' inside its pass, so a constrained run takes the unfused kernels)
+        self.use_f1 = fused and _tilesets(3 * m, 4 * m) <= 8 and self.cons is None
         self.use_sgram = fused and self.fused_a and _tilesets(2 * m, m) <= 8
 
         # ---- initial block (lobpcg.py:386-393)
@@ -304,6 +414,16 @@ class LOBPCGRun:
             self.bdiag = self.bdiag[r0:r0 + rows].contiguous()
         n = rows
 
+        if self.cons is not None:
+            c = self.cons
+            if c._y.shape[0] not in (self.n_global, rows):
+                raise ValueError(f"constraint basis has {c._y.shape[0]} rows, expected {self.n_global}")
+            if c._y.shape[0] != rows:       # z-slab: this rank's rows of Y and BY
+                r0 = a.part.z0 * a.plane
+                loc = Constraints.__new__(Constraints)
+                loc._y, loc._by = c._y[r0:r0 + rows], c._by[r0:r0 + rows]
+                loc._k, loc.yby_chol = c._k, c.yby_chol
+                self.cons = loc
         ld = dv.even(m)
         self.ld = ld
         dev = self.dev
@@ -408,6 +528,9 @@ class LOBPCGRun:
 
     def _initial(self):
         m, n = self.m, self.n
+        if self.cons is not None:                   # lobpcg.py:394
+            _project_into(self.X, m, self.cons, self.X2, self._reduce)
+            self.X, self.X2 = self.X2, self.X
         gxx = self._gram_xx()
         try:
             _, minv = scaled_cholesky(gxx)
@@ -493,6 +616,9 @@ class LOBPCGRun:
             self.lock_iteration[newly] = it
             self.active = self.active & ~newly
             self.norms = norms
+            violation = None
+            if self.cons is not None:                # lobpcg.py:438-439
+                violation = self._violation()
             self.history.append(HistoryEntry(
                 iteration=it,
                 ritz=self.lam.copy() if cfg.lock_history else None,
@@ -500,7 +626,7 @@ class LOBPCGRun:
                 active=self.active.copy(),
                 locked_now=tuple(int(i) for i in np.flatnonzero(newly)),
                 fallbacks=self.pending,
-                constraint_violation=None,
+                constraint_violation=violation,
             ))
             self.total_fallbacks += self.pending
             self.pending = 0
@@ -519,6 +645,13 @@ class LOBPCGRun:
                 W, AW, kst, sel = self._generic_precondition(W, sel, J.size)
                 G1 = G2 = None                       # F1 saw the raw residual
                 g2_rows = m + kst
+            if self.cons is not None:
+                # w = apply_constraints(w, y) (lobpcg.py:475), into the other W buffer
+                nxt = 1 - self.wcur
+                Wn, AW = self._wview(kst, nxt)
+                _project_into(W, kst, self.cons, Wn, self._reduce)
+                self.wcur = nxt
+                W = Wn
 
             # A W (+ [X W]^T A W in the same pass for the built-in stencil)
             g2 = self.g2[:g2_rows * kst].view(g2_rows, kst)
@@ -635,10 +768,24 @@ class LOBPCGRun:
             self.sg_pending = True
         self.lam = lam_new
 
+    def _violation(self):
+        """max |(BY)^T X| (lobpcg.py:438-439)."""
+        c = self.cons
+        g = dv.to_host(self._gram(self.n, [(c._by, c.count)], [(self.X, self.m)]))
+        return float(np.abs(g).max())
+
     def _check_state(self, gxx):
+        """_check_state (lobpcg.py:266-277)."""
         err = np.abs(gxx - np.eye(self.m)).max()
         if err > 1e-10:
             raise RuntimeError(f"block lost B-orthonormality: max deviation {err:.3e}")
+        if self.cons is not None:
+            gx = dv.to_host(self._gram(self.n, [(self.X, self.m)], [(self.X, self.m)]))
+            scale = max(1.0, float(np.sqrt(np.diag(gx)).max()))
+            viol = self._violation()
+            if viol > 1e-10 * scale:
+                raise RuntimeError(
+                    f"block lost constraint orthogonality: max violation {viol:.3e}")
 
     # -------------------------------------------------------------- finish
     def report(self):
@@ -698,6 +845,74 @@ def solve(a, b=None, t=None, y=None, x0=None, config=None):
 
 
 def solve_staged(a, b=None, t=None, total_wanted=1, stage_block=1, config=None):
-    """Staged solves with hard locking (lobpcg.py:580-653) -- needs the
-    constraint path, which is not on the B200 path yet."""
-    raise NotImplementedError("solve_staged needs hard-locking constraints (SURVEY 8f rank 1)")
+    """Compute total_wanted eigenpairs in stages of stage_block at a time
+    (lobpcg.py:580-653): each stage is a ``solve`` with every previously
+    accepted eigenvector hard-locked into the constraints; stage seeds are
+    config.seed + stage; stops at the first stage that fails or stalls.  The
+    report concatenates the stages (eigenpairs sorted ascending, history
+    entries stamped with their stage, iterations summed, per-stage reports
+    in ``stages``).  The accumulated basis stays on the GPU between stages."""
+    cfg = config if config is not None else SolverConfig()
+    cfg.validate()
+    if stage_block < 1:
+        raise ValueError(f"stage_block must be >= 1, got {stage_block}")
+    if total_wanted < stage_block:
+        raise ValueError(
+            f"total_wanted ({total_wanted}) must be >= stage_block ({stage_block})")
+    want_device = _OPTS["return_device"]
+    reports = []
+    constraints = None
+    basis = None
+    remaining = total_wanted
+    stage = 0
+    while remaining > 0:
+        mcur = min(stage_block, remaining)
+        stage_cfg = dataclasses.replace(cfg, block_size=mcur, seed=cfg.seed + stage)
+        with device_options(return_device=True):
+            report = solve(a, b=b, t=t, y=constraints, config=stage_cfg)
+        reports.append(report)
+        if not (report.ok and report.all_converged):
+            break
+        vecs = report.eigenvectors
+        basis = vecs if basis is None else torch.cat([basis, vecs], dim=1)
+        constraints = Constraints.from_basis(basis, b)
+        remaining -= mcur
+        stage += 1
+
+    def host(v):
+        return v if want_device else dv.to_host(v).copy()
+
+    reports = [dataclasses.replace(r, eigenvectors=host(r.eigenvectors)) for r in reports]
+    values = np.concatenate([r.eigenvalues for r in reports])
+    order = np.argsort(values, kind="stable")
+    if want_device:
+        vectors = torch.cat([r.eigenvectors for r in reports], dim=1)[:, torch.as_tensor(order)]
+    else:
+        vectors = np.hstack([r.eigenvectors for r in reports])[:, order]
+    converged = np.concatenate([r.converged for r in reports])[order]
+    residuals = np.concatenate([r.residual_norms for r in reports])[order]
+    locks = np.concatenate([r.lock_iterations for r in reports])[order]
+    history = tuple(dataclasses.replace(entry, stage=s)
+                    for s, r in enumerate(reports) for entry in r.history)
+    fallbacks = sum(r.basis_fallbacks for r in reports)
+    failed = [r.status for r in reports if not r.ok]
+    if failed:
+        status = failed[0]
+    elif not converged.all():
+        status = "MaxIterReached"
+    elif fallbacks:
+        status = f"BasisFallback({fallbacks})"
+    else:
+        status = "Converged"
+    return SolverReport(
+        eigenvalues=values[order],
+        eigenvectors=vectors,
+        iterations_used=sum(r.iterations_used for r in reports),
+        converged=converged,
+        residual_norms=residuals,
+        lock_iterations=locks,
+        history=history,
+        status=status,
+        basis_fallbacks=fallbacks,
+        stages=tuple(reports),
+    )

@@ -90,6 +90,21 @@ def gen_sym_eig(ga: np.ndarray, gb: np.ndarray, want: int, pivot_floor: float = 
     return vals[:want], c
 
 
+def chol_solve(r: np.ndarray, rhs: np.ndarray) -> np.ndarray:
+    """(R^T R) z = rhs for upper R (multivec.chol_solve, multivec.py:149-158)."""
+    r = np.asarray(r, dtype=np.float64)
+    rhs = np.asarray(rhs, dtype=np.float64)
+    if r.ndim != 2 or r.shape[0] != r.shape[1]:
+        raise ValueError(f"factor must be square, got shape {r.shape}")
+    if r.shape[0] == 0:
+        return rhs.copy()
+    u = _lsolve_t(r, rhs)
+    z, info = _trtrs(r, u, lower=0, trans=0)
+    if info != 0:
+        raise np.linalg.LinAlgError(f"dtrtrs failed ({info})")
+    return z
+
+
 def upper_inverse(r: np.ndarray) -> np.ndarray:
     """R^{-1} for an upper-triangular R (used to fold Cholesky-QR factors
     into the Gram blocks and update coefficients instead of rewriting the

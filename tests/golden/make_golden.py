@@ -324,6 +324,67 @@ def band_c1_coef():
     print(f"band_c1_coef {time.time() - t0:.1f} s")
 
 
+def staged_cases():
+    """Hard locking: Constraints / apply_constraints /
+    solve_staged on the reference's own test problems
+    (test_lobpcg.py:385-471, test_acceptance.py:160-178) plus a scaled
+    Laplacian staged run."""
+    from blockeig import Constraints, solve_staged
+
+    def rng(seed):
+        return np.random.Generator(np.random.PCG64(seed))
+
+    def diag_range(n):
+        return DiagonalOperator(np.arange(1.0, n + 1.0))
+
+    def staged_record(rep):
+        return dict(eigenvalues=rep.eigenvalues, status=np.array(rep.status),
+                    iterations_used=np.int64(rep.iterations_used),
+                    stage_iterations=np.array([r.iterations_used for r in rep.stages]),
+                    stage_status=np.array([r.status for r in rep.stages]),
+                    converged=rep.converged,
+                    violation=np.array([h.constraint_violation if h.constraint_violation is not None
+                                        else -1.0 for h in rep.history]),
+                    hist_stage=np.array([h.stage for h in rep.history]))
+
+    out = {}
+    # constrained generalized pencil
+    n = 30
+    a = diag_range(n)
+    b = DiagonalOperator(rng(7).uniform(0.5, 3.0, n))
+    vals, vecs = mv.gen_sym_eig(np.diag(a.d), np.diag(b.d))
+    cons = Constraints.from_basis(vecs[:, :2], b)
+    rep = solve(a, b=b, y=cons, config=SolverConfig(block_size=2, tol=1e-10, max_iter=300))
+    out["pencil"] = dict(record(rep, 2), bdiag=b.d, ybasis=vecs[:, :2], dense_vals=vals,
+                         violation=np.array([h.constraint_violation for h in rep.history]))
+    # exact constraints shift the floor
+    rep = solve(diag_range(10), y=Constraints.from_basis(np.eye(10)[:, :3]),
+                config=SolverConfig(block_size=2, tol=1e-10, max_iter=100))
+    out["floor"] = record(rep, 2)
+    # staged solves
+    rep = solve_staged(diag_range(10), total_wanted=6, stage_block=2,
+                       config=SolverConfig(tol=1e-10, max_iter=100))
+    out["walk"] = staged_record(rep)
+    b = DiagonalOperator(rng(11).uniform(0.5, 2.0, 20))
+    rep = solve_staged(diag_range(20), b=b, total_wanted=6, stage_block=3,
+                       config=SolverConfig(tol=1e-10, max_iter=200))
+    out["union"] = dict(staged_record(rep), bdiag=b.d)
+    rep = solve_staged(laplacian3d((6, 6, 6)), total_wanted=4, stage_block=2,
+                       config=SolverConfig(tol=1e-12, max_iter=2))
+    out["stall"] = staged_record(rep)
+    L = laplacian3d((10, 10, 10))
+    rep = solve_staged(L, t=jacobi_preconditioner(L), total_wanted=10, stage_block=5,
+                       config=SolverConfig(tol=1e-6, max_iter=300))
+    out["crit5"] = staged_record(rep)
+    A = scaled_laplacian(16)
+    rep = solve_staged(A, t=jacobi_preconditioner(A), total_wanted=8, stage_block=4,
+                       config=SolverConfig(tol=1e-6, max_iter=300, seed=5))
+    out["lap16"] = staged_record(rep)
+    for k, v in out.items():
+        np.savez_compressed(OUT / f"staged_{k}.npz", **v)
+        print(k, v["status"], v.get("stage_iterations", v["iterations_used"]))
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--heavy", action="store_true")
@@ -331,9 +392,12 @@ if __name__ == "__main__":
     ap.add_argument("--bands", action="store_true")
     ap.add_argument("--band20", action="store_true")
     ap.add_argument("--band-c1", action="store_true")
+    ap.add_argument("--staged", action="store_true")
     args = ap.parse_args()
     print("blockeig", blockeig.__version__)
-    if args.band_c1:
+    if args.staged:
+        staged_cases()
+    elif args.band_c1:
         band_c1_coef()
     elif args.band20:
         band20()

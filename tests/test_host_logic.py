@@ -54,3 +54,26 @@ def test_diag_b_laplacian_emulated(pk, golden):
                    config=pk.SolverConfig(block_size=6, tol=1e-6, max_iter=150, seed=0))
     assert rep.status == str(g["status"])
     assert rel(rep.eigenvalues, g["eigenvalues"]).max() <= 1e-8
+
+
+def test_staged_walk_emulated(pk, golden):
+    """solve_staged + constraint projection host logic on CPU stand-ins."""
+    g = golden("staged_walk.npz")
+    rep = pk.solve_staged(pk.DiagonalOperator(np.arange(1.0, 11.0)), total_wanted=6, stage_block=2,
+                          config=pk.SolverConfig(tol=1e-10, max_iter=100))
+    assert rep.ok and rep.all_converged and rep.status == str(g["status"])
+    np.testing.assert_allclose(rep.eigenvalues, np.arange(1.0, 7.0), rtol=0.0, atol=1e-8)
+    its = np.array([r.iterations_used for r in rep.stages])
+    assert np.all(np.abs(its - g["stage_iterations"]) <= 2), its
+    assert sorted({h.stage for h in rep.history}) == [0, 1, 2]
+
+
+def test_constrained_pencil_emulated(pk, golden):
+    g = golden("staged_pencil.npz")
+    b = pk.DiagonalOperator(g["bdiag"])
+    cons = pk.Constraints.from_basis(g["ybasis"], b)
+    rep = pk.solve(pk.DiagonalOperator(np.arange(1.0, 31.0)), b=b, y=cons,
+                   config=pk.SolverConfig(block_size=2, tol=1e-10, max_iter=300))
+    assert rep.all_converged
+    np.testing.assert_allclose(rep.eigenvalues, g["dense_vals"][2:4], rtol=1e-9)
+    assert max(h.constraint_violation for h in rep.history) <= 1e-8
