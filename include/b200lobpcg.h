@@ -122,6 +122,8 @@ int b2l_update(int nrows, int m, const double* x, const double* ax, int ldx,
  *   out = A in  (as b2l_stencil7)   and
  *   gram_out ((m + kw) x kw, row-major, device) = [X[:, :m] ; in[:, :kw]]^T out[:, :kw]
  * X is an (n, ldx) block of the same grid rows.  A W is never re-read.
+ * m = 0 (x may be NULL): gram_out = in^T out (kw x kw) -- the curvatures
+ * p_j^T A p_j of the column-batched PCG (b2l_pcg_*).
  */
 int b2l_stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
                       const double* halo, int has_lo, int has_hi, double scale,
@@ -165,6 +167,41 @@ int b2l_seeded_fill(double* out, int ld, long long nrows, int m, long long first
                     unsigned long long state_hi, unsigned long long state_lo,
                     unsigned long long inc_hi, unsigned long long inc_lo, double low,
                     double high, void* stream);
+
+/*
+ * Inner-PCG preconditioner, column-batched (reference operators.py:341-427,
+ * pcg_solve / InnerPCGPreconditioner): the k columns of an (n, ld) block run
+ * pcg_solve side by side, each with its own scalars, all kept on the device.
+ * M (the PCG's own preconditioner): tmode 0 identity, 1 scalar tinv, 2 row
+ * vector tvec (Jacobi), 3 z = M r supplied by the caller in the block z.
+ *   init      : x = 0, r = b, p = M b ; sums_out = [b^T b | r^T M r]     (2k)
+ *   (A p and pap_j = p_j^T A p_j: b2l_stencil7_gram with m = 0, or any
+ *    operator + b2l_gram)
+ *   update    : alpha_j = rz_j / pap_j ; x += alpha p ; r -= alpha A p ;
+ *               sums_out = [r^T M r | r^T r] (tmode 3: [0 | r^T r]);
+ *               *err |= 1 if a live column has pap <= 0 or non-finite
+ *               (the reference's PCGBreakdown)
+ *   dot       : tmode 3 only: sums_out = [r^T z | r^T r]
+ *   direction : a column stops when ||r|| <= rtol ||b|| (rtol > 0) or
+ *               r^T M r == 0; live columns get p = M r + (rz_next / rz) p;
+ *               done_next / rz_next are the next step's flags / rz.
+ * Columns with b = 0 or done[j] != 0 are left untouched.  Elementwise
+ * arithmetic rounds like numpy (product, then sum); reductions are
+ * deterministic.
+ */
+int b2l_pcg_init(int nrows, int k, const double* b, int ldb, double* x, double* r, double* p,
+                 int ld, const double* z, int tmode, double tinv, const double* tvec,
+                 double* sums_out, void* stream);
+int b2l_pcg_update(int nrows, int k, double* x, double* r, const double* p, const double* ap,
+                   int ld, const double* pap, int pap_stride, const double* rz,
+                   const double* bb, const int* done, int tmode, double tinv,
+                   const double* tvec, double* sums_out, int* err, void* stream);
+int b2l_pcg_dot(int nrows, int k, const double* r, const double* z, int ld, const double* bb,
+                const int* done, double* sums_out, void* stream);
+int b2l_pcg_direction(int nrows, int k, const double* r, double* p, int ld, const double* z,
+                      int tmode, double tinv, const double* tvec, const double* rz,
+                      const double* sums, const double* bb, double rtol, const int* done,
+                      int* done_next, double* rz_next, void* stream);
 
 /*
  * Host, small dense: register the LAPACK routines the Rayleigh-Ritz step uses

@@ -58,6 +58,19 @@ SIGNATURES = {
     "b2l_seeded_fill": (C.c_int, [C.c_void_p, C.c_int, C.c_longlong, C.c_int, C.c_longlong,
                                   C.c_ulonglong, C.c_ulonglong, C.c_ulonglong, C.c_ulonglong,
                                   C.c_double, C.c_double, C.c_void_p]),
+    "b2l_pcg_init": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_double,
+                               C.c_void_p, C.c_void_p, C.c_void_p]),
+    "b2l_pcg_update": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_void_p]),
+    "b2l_pcg_dot": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                              C.c_void_p, C.c_void_p, C.c_void_p]),
+    "b2l_pcg_direction": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                    C.c_void_p, C.c_int, C.c_double, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_void_p]),
     "b2l_set_lapack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "b2l_rayleigh_ritz": (C.c_int, [C.c_int, C.c_int, C.c_int, c_dp, C.c_int, c_dp, c_dp,
                                     c_ip, C.c_int, c_ip, C.c_double, c_dp, c_dp, c_ip, c_ip,

@@ -149,10 +149,13 @@ __global__ void __launch_bounds__(256, 2)
       mbar_expect_tx(&xbar[sl], G.x_bytes);
       tma_load_4d(xbuf(sl), &tx_map, &xbar[sl], 0, tx0, ty0, z);
     };
+    const bool have_x = G.m > 0;   // m = 0: W^T AW only (PCG curvatures)
     if (tid == 0) {
       for (int q = 0; q < NST && q < nplanes; ++q) issue(q);
-      issue_x(z0);
-      if (z0 + 1 < z1) issue_x(z0 + 1);
+      if (have_x) {
+        issue_x(z0);
+        if (z0 + 1 < z1) issue_x(z0 + 1);
+      }
     }
     double prev[EPT], cur[EPT];
     mbar_wait(&bar[0], 0);
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(256, 2)
       // ---- Gram over this warp's rows (points); the lane reads only rows
       // its own warp wrote, so no CTA barrier is needed before it
       const int xs = (z - z0) & 1;
-      mbar_wait(&xbar[xs], ((z - z0) >> 1) & 1);
+      if (have_x) mbar_wait(&xbar[xs], ((z - z0) >> 1) & 1);
       const double* Xb = xbuf(xs);
 #pragma unroll
       for (int gi = 0; gi < GPW; ++gi)
@@ -229,7 +232,7 @@ __global__ void __launch_bounds__(256, 2)
         bulk_commit();
         bulk_wait_read<2>();   // output slots are triple buffered
         if (q + NST < nplanes) issue(q + NST);
-        if (z + 2 < z1) issue_x(z + 2);
+        if (have_x && z + 2 < z1) issue_x(z + 2);
       }
     }
     if (tid == 0) bulk_wait<0>();
@@ -309,9 +312,10 @@ int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
                   const double* x, int ldx, int m, int kw, double* gram_out,
                   cudaStream_t st) {
   B2L_CHECK(nx > 0 && ny > 0 && nz > 0, -B2L_EINVAL, "stencil: empty grid");
-  B2L_CHECK(ld >= 2 && (ld % 2) == 0 && ldx >= 2 && (ldx % 2) == 0, -B2L_EINVAL,
+  B2L_CHECK(ld >= 2 && (ld % 2) == 0 && (m == 0 || (ldx >= 2 && (ldx % 2) == 0)), -B2L_EINVAL,
             "stencil: ld and ldx must be even (16-B rows for TMA)");
-  B2L_CHECK(kw >= 1 && kw <= ld && m >= 1 && m <= ldx, -B2L_EINVAL, "stencil: bad m / kw");
+  B2L_CHECK(kw >= 1 && kw <= ld && m >= 0 && m <= ldx && (m == 0 || x), -B2L_EINVAL,
+            "stencil: bad m / kw");
   B2L_CHECK(in != out, -B2L_EINVAL, "stencil: in-place apply not supported");
   B2L_CHECK(!(has_lo || has_hi) || halo != nullptr, -B2L_EINVAL,
             "stencil: halo flags set without a halo buffer");
@@ -321,6 +325,7 @@ int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
     if (rc) return rc;
     const HostBlock L[2] = {{x, ldx, m}, {in, ld, kw}};
     const HostBlock R[1] = {{out, ld, kw}};
+    if (m == 0) return gram(nx * ny * nz, L + 1, 1, R, 1, 0u, nullptr, nullptr, gram_out, st);
     return gram(nx * ny * nz, L, 2, R, 1, 0u, nullptr, nullptr, gram_out, st);
   }
   SGramGeom G{};
@@ -338,7 +343,7 @@ int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
   auto need = [&](int ty) {
     const size_t stg = (((size_t)(TX + 2) * (ty + 2) * ld * 8) + 127) & ~(size_t)127;
     const size_t ob = (((size_t)TX * ty * ld * 8) + 127) & ~(size_t)127;
-    const size_t xb = (((size_t)TX * ty * ldx * 8) + 127) & ~(size_t)127;
+    const size_t xb = m ? ((((size_t)TX * ty * ldx * 8) + 127) & ~(size_t)127) : 0;
     return 3 * stg + 3 * ob + 2 * xb + 128;
   };
   // 8 warps x GPW groups of 8 points per tile; the largest tile that keeps
@@ -368,7 +373,7 @@ int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
   g.stage_bytes = (uint32_t)((TX + 2) * (TY + 2) * ld * 8);
   g.stage_stride = (g.stage_bytes + 127u) & ~127u;
   g.out_stride = ((uint32_t)(TX * TY * ld * 8) + 127u) & ~127u;
-  G.x_bytes = (uint32_t)(TX * TY * ldx * 8);
+  G.x_bytes = m ? (uint32_t)(TX * TY * ldx * 8) : 0u;
   G.x_stride = (G.x_bytes + 127u) & ~127u;
   size_t smem = need(TY);
   const int NI = (2 * ld + 7) / 8, NJ = (ld + 7) / 8;
@@ -398,8 +403,12 @@ int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
   if (rc) return rc;
   rc = encode_tmap_4d(&tout, out, ld, nx, ny, nz, ld, TX, TY, 1);
   if (rc) return rc;
-  rc = encode_tmap_4d(&txm, x, ldx, nx, ny, nz, ldx, TX, TY, 1);
-  if (rc) return rc;
+  if (m) {
+    rc = encode_tmap_4d(&txm, x, ldx, nx, ny, nz, ldx, TX, TY, 1);
+    if (rc) return rc;
+  } else {
+    txm = tout;   // never loaded
+  }
   if (halo) {
     rc = encode_tmap_4d(&thalo, halo, ld, nx, ny, 2, ld, TX + 2, TY + 2, 1);
     if (rc) return rc;

@@ -92,7 +92,8 @@ def stencil7_gram(x: torch.Tensor, out: torch.Tensor, nx: int, ny: int, nz: int,
     _lib.check(lib.b2l_stencil7_gram(
         x.data_ptr(), out.data_ptr(), nx, ny, nz, ld,
         halo.data_ptr() if halo is not None else None, int(has_lo), int(has_hi),
-        float(scale), xb.data_ptr(), xb.stride(0), int(m), int(kw), gram_out.data_ptr(),
+        float(scale), xb.data_ptr() if xb is not None else None,
+        xb.stride(0) if xb is not None else 0, int(m), int(kw), gram_out.data_ptr(),
         stream_ptr(x.device)), "b2l_stencil7_gram")
     LAUNCHES[0] += 2
 
@@ -180,6 +181,52 @@ def update(nrows: int, m: int, x, ax, cx, xo, axo, w=None, aw=None, kw=0, cw=Non
         ptr(xo), ptr(axo), xo.stride(0), ptr(po), ptr(apo),
         po.stride(0) if po is not None else 0, int(bool(x_plus_p)),
         stream_ptr(x.device)), "b2l_update")
+    LAUNCHES[0] += 1
+
+
+# ------------------------------------------------ column-batched PCG (K10)
+
+
+def _p(t):
+    return t.data_ptr() if t is not None else None
+
+
+def pcg_init(nrows, k, b, x, r, p, z, tmode, tinv, tvec, sums_out):
+    lib = _lib.load()
+    _lib.check(lib.b2l_pcg_init(nrows, k, b.data_ptr(), b.stride(0), x.data_ptr(),
+                                r.data_ptr(), p.data_ptr(), x.stride(0), _p(z), int(tmode),
+                                float(tinv), _p(tvec), sums_out.data_ptr(),
+                                stream_ptr(x.device)), "b2l_pcg_init")
+    LAUNCHES[0] += 2
+
+
+def pcg_update(nrows, k, x, r, p, ap, pap, pap_stride, rz, bb, done, tmode, tinv, tvec,
+               sums_out, err):
+    lib = _lib.load()
+    _lib.check(lib.b2l_pcg_update(nrows, k, x.data_ptr(), r.data_ptr(), p.data_ptr(),
+                                  ap.data_ptr(), x.stride(0), pap.data_ptr(), int(pap_stride),
+                                  rz.data_ptr(), bb.data_ptr(), done.data_ptr(), int(tmode),
+                                  float(tinv), _p(tvec), sums_out.data_ptr(), err.data_ptr(),
+                                  stream_ptr(x.device)), "b2l_pcg_update")
+    LAUNCHES[0] += 2
+
+
+def pcg_dot(nrows, k, r, z, bb, done, sums_out):
+    lib = _lib.load()
+    _lib.check(lib.b2l_pcg_dot(nrows, k, r.data_ptr(), z.data_ptr(), r.stride(0),
+                               bb.data_ptr(), done.data_ptr(), sums_out.data_ptr(),
+                               stream_ptr(r.device)), "b2l_pcg_dot")
+    LAUNCHES[0] += 2
+
+
+def pcg_direction(nrows, k, r, p, z, tmode, tinv, tvec, rz, sums, bb, rtol, done, done_next,
+                  rz_next):
+    lib = _lib.load()
+    _lib.check(lib.b2l_pcg_direction(nrows, k, r.data_ptr(), p.data_ptr(), r.stride(0), _p(z),
+                                     int(tmode), float(tinv), _p(tvec), rz.data_ptr(),
+                                     sums.data_ptr(), bb.data_ptr(), float(rtol),
+                                     done.data_ptr(), done_next.data_ptr(), rz_next.data_ptr(),
+                                     stream_ptr(r.device)), "b2l_pcg_direction")
     LAUNCHES[0] += 1
 
 

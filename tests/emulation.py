@@ -104,7 +104,7 @@ def update(nrows, m, x, ax, cx, xo, axo, w=None, aw=None, kw=0, cw=None, p=None,
 def stencil7_gram(x, out, nx, ny, nz, scale, xb, m, kw, gram_out, halo=None, has_lo=False,
                   has_hi=False):
     stencil7(x, out, nx, ny, nz, scale, halo, has_lo, has_hi)
-    L = np.hstack([_np(xb)[:, :m], _np(x)[:, :kw]])
+    L = np.hstack([_np(xb)[:, :m], _np(x)[:, :kw]]) if m else _np(x)[:, :kw]
     gram_out.copy_(torch.from_numpy(L.T @ _np(out)[:, :kw]))
 
 
@@ -134,6 +134,64 @@ def seeded_fill(out, m, seed, row0=0, low=-1.0, high=1.0):
     out[:, :m] = torch.from_numpy(vals)
 
 
+def _tapply(tmode, tinv, tvec, v):
+    if tmode == 1:
+        return tinv * v
+    if tmode == 2:
+        return _np(tvec)[:, None] * v
+    return v
+
+
+def pcg_init(nrows, k, b, x, r, p, z, tmode, tinv, tvec, sums_out):
+    bv = _np(b)[:, :k]
+    zv = _np(z)[:, :k] if tmode == 3 else _tapply(tmode, tinv, tvec, bv)
+    x[:, :k] = 0.0
+    r[:, :k] = torch.from_numpy(bv.copy())
+    p[:, :k] = torch.from_numpy(np.ascontiguousarray(zv))
+    sums_out[:] = torch.from_numpy(np.concatenate([(bv * bv).sum(0), (bv * zv).sum(0)]))
+
+
+def pcg_update(nrows, k, x, r, p, ap, pap, pap_stride, rz, bb, done, tmode, tinv, tvec,
+               sums_out, err):
+    papv = _np(pap).ravel()[::pap_stride][:k]
+    live = (_np(done)[:k] == 0) & (_np(bb)[:k] != 0.0)
+    if np.any(live & (~(papv > 0) | ~np.isfinite(papv))):
+        err[0] = 1
+    alpha = np.where(live, _np(rz)[:k] / np.where(live, papv, 1.0), 0.0)
+    X, R, P, AP = (_np(t)[:, :k] for t in (x, r, p, ap))
+    Xn = np.where(live, X + alpha * P, X)
+    Rn = np.where(live, R - alpha * AP, R)
+    x[:, :k] = torch.from_numpy(np.ascontiguousarray(Xn))
+    r[:, :k] = torch.from_numpy(np.ascontiguousarray(Rn))
+    s0 = np.where(live, (Rn * _tapply(tmode, tinv, tvec, Rn)).sum(0), 0.0) if tmode != 3 else np.zeros(k)
+    s1 = np.where(live, (Rn * Rn).sum(0), 0.0)
+    sums_out[:] = torch.from_numpy(np.concatenate([s0, s1]))
+
+
+def pcg_dot(nrows, k, r, z, bb, done, sums_out):
+    live = (_np(done)[:k] == 0) & (_np(bb)[:k] != 0.0)
+    R, Z = _np(r)[:, :k], _np(z)[:, :k]
+    sums_out[:] = torch.from_numpy(np.concatenate([np.where(live, (R * Z).sum(0), 0.0),
+                                                   np.where(live, (R * R).sum(0), 0.0)]))
+
+
+def pcg_direction(nrows, k, r, p, z, tmode, tinv, tvec, rz, sums, bb, rtol, done, done_next,
+                  rz_next):
+    sv = _np(sums)
+    rzn, rr = sv[:k], sv[k:2 * k]
+    bbv, rzv = _np(bb)[:k], _np(rz)[:k]
+    stop = (_np(done)[:k] != 0) | (bbv == 0.0)
+    if rtol > 0:
+        stop |= np.sqrt(rr) <= rtol * np.sqrt(bbv)
+    stop |= rzn == 0.0
+    done_next[:k] = torch.from_numpy(stop.astype(np.int32))
+    rz_next[:k] = torch.from_numpy(np.where(stop, rzv, rzn))
+    R, P = _np(r)[:, :k], _np(p)[:, :k]
+    Z = _np(z)[:, :k] if tmode == 3 else _tapply(tmode, tinv, tvec, R)
+    beta = np.where(stop, 0.0, rzn / np.where(stop, 1.0, rzv))
+    p[:, :k] = torch.from_numpy(np.ascontiguousarray(np.where(stop, P, Z + beta * P)))
+
+
 @contextlib.contextmanager
 def emulate(monkeypatch):
     """Route paper_0705_2626_b200's device wrappers to the CPU stand-ins."""
@@ -146,6 +204,8 @@ def emulate(monkeypatch):
     monkeypatch.setattr(dv, "stencil7_gram", stencil7_gram)
     monkeypatch.setattr(dv, "lobpcg_step", lobpcg_step)
     monkeypatch.setattr(dv, "seeded_fill", seeded_fill)
+    for name in ("pcg_init", "pcg_update", "pcg_dot", "pcg_direction"):
+        monkeypatch.setattr(dv, name, globals()[name])
     monkeypatch.setattr(_lib, "ensure_device", lambda i: None)
     monkeypatch.setattr(operators, "_default_device", lambda: torch.device("cpu"))
     yield

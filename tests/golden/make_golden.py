@@ -385,6 +385,50 @@ def staged_cases():
         print(k, v["status"], v.get("stage_iterations", v["iterations_used"]))
 
 
+def pcg_cases():
+    """Inner-PCG preconditioner: pcg_solve vectors,
+    breakdown, and the reference demo's outer-iteration table
+    (pkg/demos/preconditioner_quality.csv), re-run here to confirm it."""
+    from blockeig import PCGBreakdown, inner_pcg_preconditioner, pcg_solve
+
+    L = laplacian3d((8, 9, 7))
+    jac = jacobi_preconditioner(L)
+    b = np.random.Generator(np.random.PCG64(21)).standard_normal(L.dim)
+    out = {"b": b}
+    for name, m in (("none", None), ("jacobi", jac)):
+        for it in (1, 5, 30):
+            out[f"x_{name}_{it}"] = pcg_solve(L, m, b, it, 0.0)
+        out[f"x_{name}_rtol"] = pcg_solve(L, m, b, 200, 1e-6)
+    d = DiagonalOperator(np.linspace(-1.0, 3.0, 50))
+    try:
+        pcg_solve(d, None, np.ones(50), 10)
+        out["breakdown"] = np.array(0)
+    except PCGBreakdown:
+        out["breakdown"] = np.array(1)
+    # the demo's table
+    rows = (REF / "demos" / "preconditioner_quality.csv").read_text().splitlines()[1:]
+    steps = np.array([int(r.split(",")[0]) for r in rows])
+    outer = np.array([int(r.split(",")[1]) for r in rows])
+    a = laplacian3d((20, 20, 20))
+    jacobi = jacobi_preconditioner(a)
+    rerun = []
+    for k in steps:
+        t = jacobi if k == 0 else inner_pcg_preconditioner(a, jacobi, int(k))
+        rep = solve(a, t=t, config=SolverConfig(block_size=1, tol=1e-6, max_iter=600, seed=2,
+                                                lock_history=False))
+        rerun.append(rep.iterations_used)
+        print("demo", k, rep.iterations_used, rep.status, flush=True)
+    assert np.array_equal(np.array(rerun), outer), (rerun, outer)
+    out["demo_steps"], out["demo_outer"] = steps, outer
+    # block case: scaled 24^3, m = 4, 5 inner Jacobi-PCG steps
+    A = scaled_laplacian(24)
+    t = inner_pcg_preconditioner(A, jacobi_preconditioner(A), 5)
+    rep = solve(A, t=t, config=SolverConfig(block_size=4, tol=1e-6, max_iter=200, seed=1))
+    print("block", rep.status, rep.iterations_used, flush=True)
+    out.update({f"block_{k}": v for k, v in record(rep, 4).items()})
+    np.savez_compressed(OUT / "pcg_cases.npz", **out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--heavy", action="store_true")
@@ -393,9 +437,12 @@ if __name__ == "__main__":
     ap.add_argument("--band20", action="store_true")
     ap.add_argument("--band-c1", action="store_true")
     ap.add_argument("--staged", action="store_true")
+    ap.add_argument("--pcg", action="store_true")
     args = ap.parse_args()
     print("blockeig", blockeig.__version__)
-    if args.staged:
+    if args.pcg:
+        pcg_cases()
+    elif args.staged:
         staged_cases()
     elif args.band_c1:
         band_c1_coef()

@@ -77,3 +77,18 @@ def test_constrained_pencil_emulated(pk, golden):
     assert rep.all_converged
     np.testing.assert_allclose(rep.eigenvalues, g["dense_vals"][2:4], rtol=1e-9)
     assert max(h.constraint_violation for h in rep.history) <= 1e-8
+
+
+def test_pcg_emulated(pk, golden):
+    """Host control of the column-batched PCG (device scalars, stop flags)
+    on CPU stand-ins, against the reference's pcg_solve vectors."""
+    g = golden("pcg_cases.npz")
+    L = pk.laplacian3d((8, 9, 7))
+    for name, m in (("none", None), ("jacobi", pk.jacobi_preconditioner(L))):
+        for it in (1, 5, 30):
+            x = pk.pcg_solve(L, m, g["b"], it, 0.0)
+            ref = g[f"x_{name}_{it}"]
+            np.testing.assert_allclose(x, ref, rtol=0, atol=1e-10 * np.abs(ref).max())
+        x = pk.pcg_solve(L, m, g["b"], 200, 1e-6)
+        np.testing.assert_allclose(x, g[f"x_{name}_rtol"], rtol=0,
+                                   atol=1e-10 * np.abs(g[f"x_{name}_rtol"]).max())
