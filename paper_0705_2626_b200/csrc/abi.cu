@@ -108,9 +108,98 @@ static int ensure_encode() {
   return 0;
 }
 
+// Encoded maps are cached per thread (the solver alternates between a few
+// ping-ponged buffers, so a launch usually re-uses all of its maps): the key
+// is the full encoding input, so a hit is exactly the map the driver would
+// produce.
+namespace {
+struct MapKey {
+  const void* base;
+  uint64_t dims[4];
+  uint32_t box[4];
+  int rank;
+  bool operator==(const MapKey& o) const {
+    if (base != o.base || rank != o.rank) return false;
+    for (int i = 0; i < 4; ++i)
+      if (dims[i] != o.dims[i] || box[i] != o.box[i]) return false;
+    return true;
+  }
+};
+struct MapCache {
+  static constexpr int N = 64;
+  MapKey key[N];
+  CUtensorMap map[N];
+  int used = 0, next = 0;
+  const CUtensorMap* find(const MapKey& k) const {
+    for (int i = 0; i < used; ++i)
+      if (key[i] == k) return &map[i];
+    return nullptr;
+  }
+  void put(const MapKey& k, const CUtensorMap& m) {
+    key[next] = k;
+    map[next] = m;
+    next = (next + 1) % N;
+    if (used < N) ++used;
+  }
+};
+thread_local MapCache g_maps;
+}  // namespace
+
+namespace {
+struct PrepEntry {
+  const void* kern;
+  size_t smem;
+  int threads, dev, per_sm;
+};
+struct SmemEntry {   // largest dynamic smem opted in so far, per kernel/device
+  const void* kern;
+  int dev;
+  size_t smem;
+};
+thread_local PrepEntry g_prep[64];
+thread_local int g_prep_used = 0, g_prep_next = 0;
+thread_local SmemEntry g_smem[64];
+thread_local int g_smem_used = 0;
+}  // namespace
+
+int prepare_kernel(const void* kern, size_t smem, int threads, int* per_sm) {
+  int dev = 0;
+  B2L_CUDA(cudaGetDevice(&dev));
+  // opt-in limit only ever grows: a smaller launch later stays valid
+  int si = -1;
+  for (int i = 0; i < g_smem_used; ++i)
+    if (g_smem[i].kern == kern && g_smem[i].dev == dev) si = i;
+  if (si < 0 || g_smem[si].smem < smem) {
+    B2L_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (si >= 0) g_smem[si].smem = smem;
+    else if (g_smem_used < 64) g_smem[g_smem_used++] = SmemEntry{kern, dev, smem};
+  }
+  if (!per_sm) return 0;
+  for (int i = 0; i < g_prep_used; ++i) {
+    const PrepEntry& e = g_prep[i];
+    if (e.kern == kern && e.smem == smem && e.threads == threads && e.dev == dev) {
+      *per_sm = e.per_sm;
+      return 0;
+    }
+  }
+  int n = 1;
+  B2L_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem));
+  if (n < 1) n = 1;
+  g_prep[g_prep_next] = PrepEntry{kern, smem, threads, dev, n};
+  g_prep_next = (g_prep_next + 1) % 64;
+  if (g_prep_used < 64) ++g_prep_used;
+  *per_sm = n;
+  return 0;
+}
+
 int encode_tmap_4d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1,
                    uint64_t d2, uint64_t d3, uint32_t b0, uint32_t b1,
                    uint32_t b2, uint32_t b3) {
+  const MapKey key{base, {d0, d1, d2, d3}, {b0, b1, b2, b3}, 4};
+  if (const CUtensorMap* hit = g_maps.find(key)) {
+    *map = *hit;
+    return 0;
+  }
   if (int rc = ensure_encode()) return rc;
   cuuint64_t dims[4] = {d0, d1, d2, d3};
   cuuint64_t strides[3] = {d0 * 8, d0 * d1 * 8, d0 * d1 * d2 * 8};
@@ -122,6 +211,7 @@ int encode_tmap_4d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   B2L_CHECK(r == CUDA_SUCCESS, -B2L_EDRIVER,
             "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
+  g_maps.put(key, *map);
   return 0;
 }
 
@@ -130,6 +220,11 @@ int encode_tmap_4d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1,
 // clipped on store).
 int encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
                    uint32_t box_cols, uint32_t box_rows) {
+  const MapKey key{base, {cols, rows, 0, 0}, {box_cols, box_rows, 0, 0}, 2};
+  if (const CUtensorMap* hit = g_maps.find(key)) {
+    *map = *hit;
+    return 0;
+  }
   if (int rc = ensure_encode()) return rc;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 8};
@@ -141,6 +236,7 @@ int encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t r
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   B2L_CHECK(r == CUDA_SUCCESS, -B2L_EDRIVER,
             "cuTensorMapEncodeTiled(2d) failed (code " + std::to_string((int)r) + ")");
+  g_maps.put(key, *map);
   return 0;
 }
 

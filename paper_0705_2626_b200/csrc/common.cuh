@@ -48,6 +48,10 @@ enum : int {
 // driven by one host thread / one stream per device.
 void* workspace(size_t bytes, int* err);
 int sm_count();
+// cudaFuncSetAttribute(max dynamic smem) + occupancy query, cached per
+// (kernel, smem, threads): both are host API round trips on every launch
+// otherwise.  per_sm may be null.
+int prepare_kernel(const void* kern, size_t smem, int threads, int* per_sm);
 // out[e] = sum over parts c of partial[c * len + e] (fixed order, deterministic)
 int sum_parts(const double* partial, int nparts, int len, double* out, cudaStream_t st);
 

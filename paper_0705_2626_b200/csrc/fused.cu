@@ -1503,11 +1503,10 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
     kern = m <= 4 ? pick_step<1, 1>(wgt)
                   : m <= 8 ? pick_step<1, 2>(wgt) : m <= 12 ? pick_step<2, 3>(wgt) : pick_step<2, 4>(wgt);
   }
-  B2L_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // persistent grid: every CTA the SMs can hold (registers / shared memory)
   int per_sm = 1;
-  B2L_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
-  if (per_sm < 1) per_sm = 1;
+  if (int rc = prepare_kernel(reinterpret_cast<const void*>(kern), smem, threads, &per_sm))
+    return rc;
   const int nchunks = (nrows + rc - 1) / rc;
   int gx = sm_count() * per_sm;
   if (gx > nchunks) gx = nchunks;

@@ -183,8 +183,8 @@ static int launch_stencil_t(const StencilPlan& p, const CUtensorMap& tin,
                             const CUtensorMap& thalo, const CUtensorMap& tout,
                             cudaStream_t st) {
   auto kern = stencil7_kernel<EPT, NST>;
-  B2L_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)p.smem));
+  if (int rc = prepare_kernel(reinterpret_cast<const void*>(kern), p.smem, 256, nullptr))
+    return rc;
   kern<<<p.grid, 256, p.smem, st>>>(tin, thalo, tout, p.g);
   B2L_CUDA(cudaGetLastError());
   return 0;

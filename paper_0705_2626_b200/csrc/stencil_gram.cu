@@ -289,7 +289,7 @@ static int launch_sgram_t(const StencilPlan& p, size_t smem, const CUtensorMap& 
                           const CUtensorMap& thalo, const CUtensorMap& tout,
                           const CUtensorMap& txm, const SGramGeom& G, cudaStream_t st) {
   auto kern = stencil7_gram_kernel<LD, GPW, 3>;
-  B2L_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (int rc = prepare_kernel(reinterpret_cast<const void*>(kern), smem, 256, nullptr)) return rc;
   kern<<<p.grid, 256, smem, st>>>(tin, thalo, tout, txm, p.g, G);
   B2L_CUDA(cudaGetLastError());
   return 0;

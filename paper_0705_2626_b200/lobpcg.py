@@ -200,9 +200,14 @@ class _Pinned:
         self.di = torch.empty(ni, dtype=torch.int32, device=dev)
         self.hd_np = self.hd.numpy()
         self.hi_np = self.hi.numpy()
+        self._views = {}
 
     def upload(self, dparts, iparts):
-        """Pack float64 / int32 arrays, one H2D copy each; returns device views."""
+        """Pack float64 / int32 arrays, one H2D copy each; returns device views.
+
+        The pinned staging is reused by the next call: the stream orders the
+        copy before any later host write only because every caller
+        synchronises the stream once per iteration (LOBPCGRun.step)."""
         outs_d, outs_i = [], []
         o = 0
         for a in dparts:
@@ -211,7 +216,7 @@ class _Pinned:
             outs_d.append((o, a.size))
             o += a.size
         if o:
-            self.dd[:o].copy_(self.hd[:o], non_blocking=True)
+            self._copy(self.dd, self.hd, o)
         oi = 0
         for a in iparts:
             a = np.asarray(a, dtype=np.int32).ravel()
@@ -219,8 +224,19 @@ class _Pinned:
             outs_i.append((oi, a.size))
             oi += a.size
         if oi:
-            self.di[:oi].copy_(self.hi[:oi], non_blocking=True)
-        return ([self.dd[s:s + k] for s, k in outs_d], [self.di[s:s + k] for s, k in outs_i])
+            self._copy(self.di, self.hi, oi)
+        return ([self._view(self.dd, s, k) for s, k in outs_d],
+                [self._view(self.di, s, k) for s, k in outs_i])
+
+    def _view(self, buf, s, k):
+        key = (id(buf), s, k)
+        v = self._views.get(key)
+        if v is None:
+            v = self._views[key] = buf[s:s + k]
+        return v
+
+    def _copy(self, dst, src, count):
+        self._view(dst, 0, count).copy_(self._view(src, 0, count), non_blocking=True)
 
 
 def _device_of(op, default=None):
@@ -438,6 +454,14 @@ class LOBPCGRun:
         self.g2 = torch.zeros((2 * m) * m, dtype=torch.float64, device=dev)
         self.h_red = _host_buf(nred)
         self.h_g2 = _host_buf((2 * m) * m)
+        self.h_red_np = self.h_red.numpy()
+        self.h_g2_np = self.h_g2.numpy()
+        self._wviews = {}
+        self._triu = np.triu_indices(m)
+        self._eye_triu = np.eye(m)[self._triu]
+        self._tol_vec = np.full(m, cfg.tol)
+        self._iota = np.arange(m)
+        self._iota32 = np.arange(m, dtype=np.int32)
         self.pin = _Pinned(dev, 3 * m * m + 2 * m + 8, 3 * m + 8)
         if x0t is None:
             row0 = a.part.z0 * a.plane if rows != self.n_global else 0
@@ -482,9 +506,14 @@ class LOBPCGRun:
         return ((1 << nblocks) - 1) if self.bdiag is not None else 0
 
     def _wview(self, k, which=None):
-        buf = self.Wbufs[self.wcur if which is None else which]
-        ldw = dv.even(k)
-        return dv.view_block(buf, self.n, ldw), dv.view_block(self.AWbuf, self.n, ldw)
+        key = (self.wcur if which is None else which, k)
+        v = self._wviews.get(key)
+        if v is None:
+            buf = self.Wbufs[key[0]]
+            ldw = dv.even(k)
+            v = (dv.view_block(buf, self.n, ldw), dv.view_block(self.AWbuf, self.n, ldw))
+            self._wviews[key] = v
+        return v
 
     def _fetch(self, dev_t, host_t, count):
         """D2H of the first `count` doubles through pinned memory (syncs)."""
@@ -573,18 +602,24 @@ class LOBPCGRun:
                     self.h_g2[:g2_rows * kst].copy_(self.g2[:g2_rows * kst], non_blocking=True)
                 if self.dev.type == "cuda":
                     torch.cuda.current_stream(self.dev).synchronize()
-                red = self.h_red[:nred].numpy().copy()
+                # views of the pinned staging buffers (rewritten only after
+                # the next synchronisation)
+                red = self.h_red_np[:nred]
                 sums = red[:2 * m]
                 G1 = red[2 * m:].reshape(a, b)
-                gxx = _mirror_upper(G1[:m, :m])
+                gxx = None
                 if self.sg_pending:
-                    G2 = self.h_g2[:g2_rows * kst].numpy().copy().reshape(g2_rows, kst)
+                    G2 = self.h_g2_np[:g2_rows * kst].reshape(g2_rows, kst)
             else:
                 gxx = self._gram_xx()
             self.f1_pending = False
             self.sg_pending = False
-            # drift check (lobpcg.py:419-428)
-            drift = np.abs(gxx - np.eye(m)).max()
+            # drift check (lobpcg.py:419-428): max |X^T B X - I| over the
+            # upper triangle (the Gram is symmetric)
+            gu = G1[:m, :m] if gxx is None else gxx
+            drift = float(np.abs(gu[self._triu] - self._eye_triu).max())
+            if gxx is None and (drift > DRIFT_LIMIT or cfg.check_invariants):
+                gxx = _mirror_upper(gu)
             if drift > DRIFT_LIMIT:
                 try:
                     self._refresh_ritz(gxx)
@@ -611,7 +646,7 @@ class LOBPCGRun:
             if cfg.relative_tol:
                 thresholds = cfg.tol * np.sqrt(sums[m:2 * m])
             else:
-                thresholds = np.full(m, cfg.tol)
+                thresholds = self._tol_vec
             newly = self.active & (norms < thresholds)
             self.lock_iteration[newly] = it
             self.active = self.active & ~newly
@@ -624,7 +659,7 @@ class LOBPCGRun:
                 ritz=self.lam.copy() if cfg.lock_history else None,
                 residual_norms=norms.copy() if cfg.lock_history else None,
                 active=self.active.copy(),
-                locked_now=tuple(int(i) for i in np.flatnonzero(newly)),
+                locked_now=tuple(int(i) for i in np.flatnonzero(newly)) if newly.any() else (),
                 fallbacks=self.pending,
                 constraint_violation=violation,
             ))
@@ -640,7 +675,8 @@ class LOBPCGRun:
                 self._check_state(gxx)
 
             J = np.flatnonzero(self.active)
-            sel = np.searchsorted(jprev, J)          # W columns of J
+            # W columns of J
+            sel = self._iota[:kst] if J.size == kst else np.searchsorted(jprev, J)
             if self.t_generic is not None:
                 W, AW, kst, sel = self._generic_precondition(W, sel, J.size)
                 G1 = G2 = None                       # F1 saw the raw residual
@@ -729,8 +765,11 @@ class LOBPCGRun:
 
         if self.use_f1:
             # next iteration's W holds the current active set J
-            wpos = np.full(m, -1, dtype=np.int32)
-            wpos[J] = np.arange(J.size, dtype=np.int32)
+            if J.size == m:
+                wpos = self._iota32
+            else:
+                wpos = np.full(m, -1, dtype=np.int32)
+                wpos[J] = np.arange(J.size, dtype=np.int32)
             (coef_d, lam_d), (pc_d, wpos_d) = self.pin.upload(
                 [coef, lam_new],
                 [pcols if kp else np.zeros(1, np.int32), wpos])
