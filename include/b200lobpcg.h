@@ -107,7 +107,8 @@ int b2l_residual(int nrows, int m, const double* x, const double* ax, int ldx,
  *   X'  = X Cx (+ P' if x_plus_p)      AX' = AX Cx (+ AP')
  * cx (m x m), cw (kw x m), cp (kp x m) row-major device matrices; pcols
  * (kp ints) device.  ax/axo/aw/ap may be NULL (no A side); po/apo NULL skips
- * writing P'.  Outputs must not alias inputs.
+ * writing P'.  x = NULL (cx ignored, no A side): xo = W Cw + P Cp, the plain
+ * block product multivec.multiply.  Outputs must not alias inputs.
  */
 int b2l_update(int nrows, int m, const double* x, const double* ax, int ldx,
                const double* cx, const double* w, const double* aw, int ldw, int kw,

@@ -514,7 +514,8 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs A) {
   double* scp = scw + A.kw * A.m;
   int* spc = reinterpret_cast<int*>(scp + A.kp * A.m);
   const int tid = threadIdx.x;
-  for (int i = tid; i < A.m * A.m; i += blockDim.x) scx[i] = A.cx[i];
+  if (A.x)
+    for (int i = tid; i < A.m * A.m; i += blockDim.x) scx[i] = A.cx[i];
   for (int i = tid; i < A.kw * A.m; i += blockDim.x) scw[i] = A.cw[i];
   for (int i = tid; i < A.kp * A.m; i += blockDim.x) scp[i] = A.cp[i];
   for (int i = tid; i < A.kp; i += blockDim.x) spc[i] = A.pcols[i];
@@ -543,9 +544,13 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs A) {
     }
     {
       double xs = 0.0;
-      const double* xr = A.x + (size_t)r * A.ldx;
-      for (int i = 0; i < A.m; ++i) xs = fma(xr[i], scx[i * A.m + c], xs);
-      if (A.x_plus_p) xs = __dadd_rn(xs, pn);
+      if (A.x) {
+        const double* xr = A.x + (size_t)r * A.ldx;
+        for (int i = 0; i < A.m; ++i) xs = fma(xr[i], scx[i * A.m + c], xs);
+        if (A.x_plus_p) xs = __dadd_rn(xs, pn);
+      } else {
+        xs = pn;   // no X term: X' = P'
+      }
       A.xo[(size_t)r * A.ldo + c] = xs;
       if (padx)
         for (int e = A.m; e < A.ldo; ++e) A.xo[(size_t)r * A.ldo + e] = 0.0;
@@ -584,10 +589,13 @@ int update(int nrows, int m, const double* x, const double* ax, int ldx,
            int ldo, double* po, double* apo, int ldpo, int x_plus_p,
            cudaStream_t st) {
   B2L_CHECK(m >= 1 && m <= 256, -B2L_EINVAL, "update: 1 <= m <= 256");
-  B2L_CHECK(ldx >= m && ldo >= m, -B2L_EINVAL, "update: ld < m");
+  B2L_CHECK((!x || ldx >= m) && ldo >= m, -B2L_EINVAL, "update: ld < m");
   B2L_CHECK(kw >= 0 && kp >= 0, -B2L_EINVAL, "update: negative block width");
   B2L_CHECK(!ax || axo, -B2L_EINVAL, "update: A-side input without output");
   B2L_CHECK(x != xo && (!ax || ax != axo), -B2L_EINVAL, "update: in-place not supported");
+  B2L_CHECK(x || (!ax && kw + kp > 0), -B2L_EINVAL,
+            "update: without x, only X' = W Cw + P Cp (no A side) is defined");
+  B2L_CHECK(!x || cx, -B2L_EINVAL, "update: x without cx");
   UpdArgs A{};
   A.nrows = nrows;
   A.m = m;

@@ -175,12 +175,12 @@ def update(nrows: int, m: int, x, ax, cx, xo, axo, w=None, aw=None, kw=0, cw=Non
         return t.data_ptr() if t is not None else None
 
     _lib.check(lib.b2l_update(
-        nrows, m, ptr(x), ptr(ax), x.stride(0), ptr(cx),
+        nrows, m, ptr(x), ptr(ax), x.stride(0) if x is not None else 0, ptr(cx),
         ptr(w), ptr(aw), w.stride(0) if w is not None else 0, int(kw), ptr(cw),
         ptr(p), ptr(ap), p.stride(0) if p is not None else 0, ptr(pcols), int(kp), ptr(cp),
         ptr(xo), ptr(axo), xo.stride(0), ptr(po), ptr(apo),
         po.stride(0) if po is not None else 0, int(bool(x_plus_p)),
-        stream_ptr(x.device)), "b2l_update")
+        stream_ptr(xo.device)), "b2l_update")
     LAUNCHES[0] += 1
 
 

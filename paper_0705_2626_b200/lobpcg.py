@@ -318,6 +318,38 @@ class Constraints:
         return self._k
 
 
+def b_orthonormalize(x, bx, pivot_floor=0.0):
+    """B-orthonormalize a block (lobpcg.py:147-179): returns (x', bx', r)
+    with x'^T bx' = I and x ~ x' r (r upper, the column scaling included).
+    Columns are scaled to unit B-norm before the Cholesky factorisation;
+    raises NotSPD(pivot) for a nonpositive / non-finite B-norm or a pivot at
+    or below pivot_floor.  On the device: one Gram (K5), the small factor on
+    the host, one update (K6) per block; bx may alias x (B = I).  CUDA
+    tensors in -> CUDA tensors out; arrays in -> arrays out."""
+    host = not isinstance(x, torch.Tensor)
+    shared = bx is x
+    dev = x.device if not host else _device_of(None)
+    X = _padded_block(x, dev)
+    BX = X if shared else _padded_block(bx, dev)
+    n = X.shape[0]
+    k = int(x.shape[1] if hasattr(x, "shape") else np.asarray(x).shape[1])
+    g = _mirror_upper(dv.to_host(dv.gram(n, [(X, k)], [(BX, k)], pair_mode=_UPPER)))
+    reff, inv = scaled_cholesky(g, pivot_floor)
+    M = dv.to_device(inv, dev)
+    XO = dv.new_block(n, X.shape[1], dev)
+    dv.update(n, k, X, None, M, XO, None)
+    if shared:
+        BXO = XO
+    else:
+        BXO = dv.new_block(n, X.shape[1], dev)
+        dv.update(n, k, BX, None, M, BXO, None)
+    xo, bxo = XO[:, :k], BXO[:, :k]
+    if host:
+        xo = dv.to_host(xo).copy()
+        bxo = xo if shared else dv.to_host(bxo).copy()
+    return xo, bxo, reff
+
+
 def apply_constraints(x, constraints, b=None):
     """x - Y (Y^T B Y)^{-1} (BY)^T x  (lobpcg.py:131-144); b is accepted for
     call-site symmetry and not consulted.  x: CUDA (n, k) tensor (returned

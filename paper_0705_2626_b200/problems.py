@@ -14,7 +14,10 @@ import numpy as np
 
 from .operators import Grid3D
 
-__all__ = ["AnalyticSpectrum", "analytic_spectrum", "exact_eigenvalues"]
+__all__ = ["AnalyticSpectrum", "analytic_spectrum", "exact_eigenvalues", "dense_matrix",
+           "dense_oracle_spectrum", "DENSE_ORACLE_LIMIT"]
+
+DENSE_ORACLE_LIMIT = 600   # problems.py:26
 
 
 @dataclass(frozen=True)
@@ -53,3 +56,21 @@ def exact_eigenvalues(grid, m, scale=1.0):
     if not 1 <= m <= grid.n:
         raise ValueError(f"m must be in 1..{grid.n}, got {m}")
     return analytic_spectrum(grid, limit=m).values[:m].copy() * scale
+
+
+def dense_matrix(op):
+    """Dense matrix of an operator: op applied to the identity's columns
+    (problems.py:95-98).  Host numpy (n, n)."""
+    y = op(np.eye(op.dim))
+    return y.detach().cpu().numpy() if hasattr(y, "detach") else np.asarray(y, dtype=np.float64)
+
+
+def dense_oracle_spectrum(op, n_limit=DENSE_ORACLE_LIMIT):
+    """All eigenvalues ascending by brute force (problems.py:101-113); the
+    dimension is capped (default 600), as in the reference."""
+    if op.dim > n_limit:
+        raise ValueError(f"operator dimension {op.dim} exceeds the dense oracle limit {n_limit}")
+    from .small import sym_eig
+
+    values, _ = sym_eig(dense_matrix(op))
+    return values
