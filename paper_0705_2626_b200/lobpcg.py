@@ -442,12 +442,12 @@ class LOBPCGRun:
                 if not bool(torch.isfinite(x0t).all()):
                     raise ValueError("x0 contains non-finite entries")
             else:
-                xh = np.array(x0, dtype=np.float64, copy=True)
+                # no host copy (the block is copied to the device below) and
+                # the finiteness check runs on the device after the upload
+                xh = np.asarray(x0, dtype=np.float64)
                 # a z-slab run also accepts this rank's rows only
                 if xh.shape not in ((n, m), (rows, m)):
                     raise ValueError(f"x0 has shape {xh.shape}, expected ({n}, {m})")
-                if not np.all(np.isfinite(xh)):
-                    raise ValueError("x0 contains non-finite entries")
                 x0t = xh
         else:
             # seeded block generated on the device (K9), bit for bit
@@ -501,7 +501,9 @@ class LOBPCGRun:
         elif isinstance(x0t, torch.Tensor):
             self.X[:, :m] = x0t
         else:
-            self.X[:, :m].copy_(torch.from_numpy(x0t))
+            self.X[:, :m].copy_(torch.from_numpy(np.ascontiguousarray(x0t)))
+            if not bool(torch.isfinite(self.X[:, :m]).all()):
+                raise ValueError("x0 contains non-finite entries")
 
         self.active = np.ones(m, dtype=bool)
         self.lock_iteration = np.full(m, -1, dtype=np.int64)
