@@ -233,6 +233,63 @@ int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, int ldg1,
                       const int* sel, double pivot_floor, double* lam_out, double* coef_out,
                       int* pcols_out, int* kp_out, int* fallbacks_out);
 
+/*
+ * Steady-state iteration, host driven natively (lobpcg.py:418-540 when the
+ * previous step ran b2l_lobpcg_step + b2l_stencil7_gram): one stream
+ * synchronisation fetching red_dev (2m + a*b, a = 2m + kst, b = 3m + kst) and
+ * g2_dev ((m + kst) x kst) into the pinned h_red / h_g2; the drift test; the
+ * lock test (updates active, lock_iteration; writes norms, newly); the
+ * Rayleigh-Ritz step (b2l_rayleigh_ritz); the upload of coefficients,
+ * Ritz values, pcols and wpos (through the pinned h_stage (>= 3m^2 + m
+ * doubles) / h_istage (>= 2m ints) into coef_dev / lam_dev / pcols_dev
+ * (>= 2m ints: pcols then wpos)); then the launches of the next
+ * b2l_lobpcg_step (x,ax,p,ap,w_cur -> x2,ax2,p2,ap2,w_next) and
+ * b2l_stencil7_gram (w_next -> aw, g2_dev = [x2 ; w_next]^T aw).
+ * Returns B2L_ITER_OK (next passes queued; lam_next, k_next, kp, fallbacks
+ * set), B2L_ITER_DRIFT (nothing changed but drift and the fetched h_red /
+ * h_g2: the caller repairs), B2L_ITER_DONE (lock test applied, loop over),
+ * -1003 (B2L_EDEGENERATE, lock test applied) or another negative error.
+ */
+#define B2L_ITER_OK 0
+#define B2L_ITER_DRIFT 1
+#define B2L_ITER_DONE 2
+
+typedef struct {
+  int n, m, ldx;                      /* rows, block size, leading dim of X-like blocks */
+  int nx, ny, nz;                     /* grid of the built-in stencil */
+  double scale;                       /* stencil scale s */
+  int tmode;                          /* preconditioner: 0 none, 1 scalar, 2 vector */
+  double tinv;
+  const double* tvec;
+  const double* bdiag;                /* diag(B) or NULL */
+  double tol;
+  int relative_tol, max_iter;
+  double drift_limit, pivot_floor;
+  double *x, *ax, *p, *ap;            /* current blocks (device) */
+  double *x2, *ax2, *p2, *ap2;        /* next blocks (device) */
+  double *w_cur, *w_next, *aw;        /* W buffers and the AW buffer (device) */
+  double *red_dev, *g2_dev;           /* reductions of F1 / the stencil pass (device) */
+  double *coef_dev, *lam_dev;         /* device staging */
+  int* pcols_dev;                     /* device staging, 2m ints */
+  double *h_red, *h_g2, *h_stage;     /* pinned host */
+  int* h_istage;                      /* pinned host */
+  double* lam;                        /* (m) current Ritz values (host) */
+  unsigned char* active;              /* (m) in/out */
+  long long* lock_iteration;          /* (m) in/out */
+  int it, have_p, kst;                /* iteration, P valid, stored W columns */
+  void* stream;
+  double* norms;                      /* out (m) */
+  unsigned char* newly;               /* out (m) */
+  double* lam_next;                   /* out (m) */
+  double drift;                       /* out */
+  int fallbacks, k_next, kp;          /* out */
+} b2l_iter_state;
+
+int b2l_fast_iteration(b2l_iter_state* state);
+
+/* sizeof(b2l_iter_state) as compiled into the library (binding checks). */
+int b2l_iter_state_size(void);
+
 #ifdef __cplusplus
 }
 #endif

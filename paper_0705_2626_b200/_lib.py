@@ -24,6 +24,34 @@ class b2l_block(C.Structure):
     _fields_ = [("ptr", C.c_void_p), ("ld", C.c_int), ("cols", C.c_int)]
 
 
+class b2l_iter_state(C.Structure):
+    """Mirror of b2l_iter_state (include/b200lobpcg.h), field for field."""
+
+    _fields_ = [
+        ("n", C.c_int), ("m", C.c_int), ("ldx", C.c_int),
+        ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int),
+        ("scale", C.c_double),
+        ("tmode", C.c_int), ("tinv", C.c_double), ("tvec", C.c_void_p), ("bdiag", C.c_void_p),
+        ("tol", C.c_double), ("relative_tol", C.c_int), ("max_iter", C.c_int),
+        ("drift_limit", C.c_double), ("pivot_floor", C.c_double),
+        ("x", C.c_void_p), ("ax", C.c_void_p), ("p", C.c_void_p), ("ap", C.c_void_p),
+        ("x2", C.c_void_p), ("ax2", C.c_void_p), ("p2", C.c_void_p), ("ap2", C.c_void_p),
+        ("w_cur", C.c_void_p), ("w_next", C.c_void_p), ("aw", C.c_void_p),
+        ("red_dev", C.c_void_p), ("g2_dev", C.c_void_p),
+        ("coef_dev", C.c_void_p), ("lam_dev", C.c_void_p), ("pcols_dev", C.c_void_p),
+        ("h_red", C.c_void_p), ("h_g2", C.c_void_p), ("h_stage", C.c_void_p),
+        ("h_istage", C.c_void_p),
+        ("lam", C.c_void_p), ("active", C.c_void_p), ("lock_iteration", C.c_void_p),
+        ("it", C.c_int), ("have_p", C.c_int), ("kst", C.c_int),
+        ("stream", C.c_void_p),
+        ("norms", C.c_void_p), ("newly", C.c_void_p), ("lam_next", C.c_void_p),
+        ("drift", C.c_double),
+        ("fallbacks", C.c_int), ("k_next", C.c_int), ("kp", C.c_int),
+    ]
+
+
+ITER_OK, ITER_DRIFT, ITER_DONE = 0, 1, 2
+
 # name -> (restype, argtypes); every exported symbol of include/b200lobpcg.h
 SIGNATURES = {
     "b2l_last_error": (C.c_char_p, []),
@@ -71,6 +99,8 @@ SIGNATURES = {
                                     C.c_void_p, C.c_int, C.c_double, C.c_void_p, C.c_void_p,
                                     C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                                     C.c_void_p, C.c_void_p, C.c_void_p]),
+    "b2l_fast_iteration": (C.c_int, [C.POINTER(b2l_iter_state)]),
+    "b2l_iter_state_size": (C.c_int, []),
     "b2l_set_lapack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "b2l_rayleigh_ritz": (C.c_int, [C.c_int, C.c_int, C.c_int, c_dp, C.c_int, c_dp, c_dp,
                                     c_ip, C.c_int, c_ip, C.c_double, c_dp, c_dp, c_ip, c_ip,
@@ -105,6 +135,8 @@ def load():
             fn.argtypes = args
         if lib.b2l_abi_version() != ABI_VERSION:
             raise ImportError("libb200lobpcg ABI version mismatch; rebuild")
+        if lib.b2l_iter_state_size() != C.sizeof(b2l_iter_state):
+            raise ImportError("b2l_iter_state layout mismatch between _lib.py and the library")
         _register_lapack(lib)
         _lib = lib
         return lib

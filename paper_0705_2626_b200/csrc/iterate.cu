@@ -1,0 +1,125 @@
+// Steady-state LOBPCG iteration driven natively (host side of one step of
+// reference lobpcg.py:418-540 when the previous step ran the fused passes):
+//   fetch F1's reductions and the stencil pass's [X W]^T A W (one
+//   synchronisation) -> drift test -> lock test -> Rayleigh-Ritz with the
+//   repair ladders (b2l_rayleigh_ritz) -> upload of the coefficients ->
+//   launch of the next F1 (b2l_lobpcg_step) and stencil pass
+//   (b2l_stencil7_gram).
+// Same decisions, same order as the Python driver (paper_0705_2626_b200/
+// lobpcg.py, LOBPCGRun.step); the Python side keeps every other path (first
+// iteration, drift repair, callbacks, constraints, z-slabs) and records the
+// history from the outputs.
+#include <cmath>
+#include <vector>
+
+#include "../../include/b200lobpcg.h"
+#include "common.cuh"
+
+namespace b2l {
+int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx, const double* w,
+                const double* aw, int ldw, int kw, const double* p, const double* ap, int kp,
+                const int* pcols, const double* coef, double* xo, double* axo, double* po,
+                double* apo, const double* lam, const double* d, int tmode, double tinv,
+                const double* tvec, const int* wpos, int kwn, double* wo, int ldwn, int want_ax,
+                double* red_out, cudaStream_t st);
+int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
+                  const double* halo, int has_lo, int has_hi, double scale, const double* x,
+                  int ldx, int m, int kw, double* gram_out, cudaStream_t st);
+}  // namespace b2l
+
+using namespace b2l;
+
+namespace {
+inline int even(int k) { return k < 2 ? 2 : k + (k & 1); }
+}  // namespace
+
+extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
+  if (!s || s->m < 1 || s->kst < 1 || s->kst > s->m)
+    return fail(-B2L_EINVAL, "fast_iteration: bad state");
+  const int m = s->m, kst = s->kst;
+  cudaStream_t st = (cudaStream_t)s->stream;
+  const int a = 2 * m + kst, b = 3 * m + kst;
+  const size_t nred = (size_t)2 * m + (size_t)a * b;
+  const size_t ng2 = (size_t)(m + kst) * kst;
+
+  // ---- one synchronisation: F1's reductions + the stencil pass's Gram
+  B2L_CUDA(cudaMemcpyAsync(s->h_red, s->red_dev, nred * sizeof(double), cudaMemcpyDeviceToHost,
+                           st));
+  B2L_CUDA(cudaMemcpyAsync(s->h_g2, s->g2_dev, ng2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  B2L_CUDA(cudaStreamSynchronize(st));
+  const double* sums = s->h_red;
+  const double* G1 = s->h_red + 2 * m;
+
+  // ---- drift (lobpcg.py:419-428): max |X^T B X - I| over the upper triangle
+  double drift = 0.0;
+  for (int i = 0; i < m; ++i)
+    for (int j = i; j < m; ++j) {
+      const double v = std::fabs(G1[(size_t)i * b + j] - (i == j ? 1.0 : 0.0));
+      if (!(v <= drift)) drift = v;   // NaN-propagating max
+    }
+  s->drift = drift;
+  if (!(drift <= s->drift_limit)) return B2L_ITER_DRIFT;
+
+  // ---- lock test (lobpcg.py:429-437)
+  std::vector<int> jprev, jact;
+  for (int j = 0; j < m; ++j)
+    if (s->active[j]) jprev.push_back(j);
+  if ((int)jprev.size() != kst) return fail(-B2L_EINVAL, "fast_iteration: kst != |active|");
+  for (int j = 0; j < m; ++j) {
+    const double nrm = std::sqrt(sums[j]);
+    const double thr = s->relative_tol ? s->tol * std::sqrt(sums[m + j]) : s->tol;
+    s->norms[j] = nrm;
+    const bool lock = s->active[j] && nrm < thr;
+    s->newly[j] = lock ? 1 : 0;
+    if (lock) {
+      s->lock_iteration[j] = s->it;
+      s->active[j] = 0;
+    }
+  }
+  for (int j = 0; j < m; ++j)
+    if (s->active[j]) jact.push_back(j);
+  if (jact.empty() || s->it == s->max_iter) return B2L_ITER_DONE;
+
+  // ---- Rayleigh-Ritz (lobpcg.py:475-519) on the fetched Grams
+  const int kj = (int)jact.size();
+  std::vector<int> sel(kj);
+  for (int q = 0, t = 0; q < kj; ++q) {
+    while (jprev[t] != jact[q]) ++t;
+    sel[q] = t;
+  }
+  double* coef = s->h_stage;                        // [Cx | Cw | Cp]
+  double* lam_next = s->h_stage + (size_t)3 * m * m;
+  int* pcols = s->h_istage;
+  int* wpos = s->h_istage + m;
+  int kp = 0, fb = 0;
+  const int rc = b2l_rayleigh_ritz(m, kst, s->have_p, G1, b, s->h_g2, s->lam, jact.data(), kj,
+                                   sel.data(), s->pivot_floor, lam_next, coef, pcols, &kp, &fb);
+  s->fallbacks = fb;
+  if (rc) return rc;
+  for (int j = 0; j < m; ++j) {
+    wpos[j] = -1;
+    s->lam_next[j] = lam_next[j];
+  }
+  for (int q = 0; q < kj; ++q) wpos[jact[q]] = q;
+  s->kp = kp;
+  s->k_next = kj;
+
+  // ---- uploads + the next fused passes
+  const size_t ncoef = (size_t)m * m + (size_t)kst * m + (size_t)kp * m;
+  B2L_CUDA(cudaMemcpyAsync(s->coef_dev, coef, ncoef * sizeof(double), cudaMemcpyHostToDevice, st));
+  B2L_CUDA(cudaMemcpyAsync(s->lam_dev, lam_next, m * sizeof(double), cudaMemcpyHostToDevice, st));
+  B2L_CUDA(cudaMemcpyAsync(s->pcols_dev, pcols, (size_t)2 * m * sizeof(int),
+                           cudaMemcpyHostToDevice, st));
+  int r = lobpcg_step(s->n, m, s->x, s->ax, s->ldx, s->w_cur, s->aw, even(kst), kst,
+                      kp ? s->p : nullptr, kp ? s->ap : nullptr, kp, s->pcols_dev, s->coef_dev,
+                      s->x2, s->ax2, s->p2, s->ap2, s->lam_dev, s->bdiag, s->tmode, s->tinv,
+                      s->tvec, s->pcols_dev + m, kj, s->w_next, even(kj), s->relative_tol,
+                      s->red_dev, st);
+  if (r) return r;
+  r = stencil7_gram(s->w_next, s->aw, s->nx, s->ny, s->nz, even(kj), nullptr, 0, 0, s->scale,
+                    s->x2, s->ldx, m, kj, s->g2_dev, st);
+  if (r) return r;
+  return B2L_ITER_OK;
+}
+
+extern "C" int b2l_iter_state_size(void) { return (int)sizeof(b2l_iter_state); }

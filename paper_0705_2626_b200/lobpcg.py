@@ -33,6 +33,7 @@ does not fit the fused kernels (m > 16) and generic operators.
 from __future__ import annotations
 
 import contextlib
+import ctypes
 import dataclasses
 from dataclasses import dataclass
 
@@ -521,6 +522,7 @@ class LOBPCGRun:
         self.sg_pending = False    # self.g2 / AW hold the stencil pass for this step
 
         self._initial()
+        self._native_setup()
 
     # ------------------------------------------------------------ helpers
     def _reduce(self, t):
@@ -609,12 +611,120 @@ class LOBPCGRun:
         self._rotate_x(q)
         self.lam = lam
 
+    # ---------------------------------------------------- native fast path
+    def _native_setup(self):
+        """b2l_fast_iteration drives the steady state when every piece of the
+        step is one of the fused kernels (built-in stencil, diagonal or no B,
+        Jacobi/identity T, no constraints, one GPU)."""
+        cfg, m = self.cfg, self.m
+        self._native = None
+        if not (self.dev.type == "cuda" and self.use_f1 and self.use_sgram and self.fused_a
+                and self._allreduce is None and self.t_generic is None and self.cons is None
+                and not cfg.check_invariants and cfg.verbosity < 2):
+            return
+        dev = self.dev
+        st = _lib.b2l_iter_state()
+        g = self.a.grid
+        st.n, st.m, st.ldx = self.n, m, self.ld
+        st.nx, st.ny, st.nz, st.scale = g.nx, g.ny, g.nz, self.a.scale
+        st.tmode, st.tinv = self.tmode, self.tinv
+        st.tvec = self.tvec.data_ptr() if self.tvec is not None else None
+        st.bdiag = self.bdiag.data_ptr() if self.bdiag is not None else None
+        st.tol, st.relative_tol, st.max_iter = cfg.tol, int(cfg.relative_tol), cfg.max_iter
+        st.drift_limit, st.pivot_floor = DRIFT_LIMIT, PIVOT_FLOOR
+        self._n_coef = torch.empty(3 * m * m, dtype=torch.float64, device=dev)
+        self._n_lam = torch.empty(m, dtype=torch.float64, device=dev)
+        self._n_pcols = torch.empty(2 * m, dtype=torch.int32, device=dev)
+        self._n_stage = _host_buf(3 * m * m + m)
+        self._n_istage = _host_buf(2 * m, torch.int32)
+        st.aw = self.AWbuf.data_ptr()
+        st.red_dev, st.g2_dev = self.red.data_ptr(), self.g2.data_ptr()
+        st.coef_dev, st.lam_dev = self._n_coef.data_ptr(), self._n_lam.data_ptr()
+        st.pcols_dev = self._n_pcols.data_ptr()
+        st.h_red, st.h_g2 = self.h_red.data_ptr(), self.h_g2.data_ptr()
+        st.h_stage, st.h_istage = self._n_stage.data_ptr(), self._n_istage.data_ptr()
+        self._n_norms = np.zeros(m)
+        self._n_newly = np.zeros(m, dtype=bool)
+        self._n_lamnext = np.zeros(m)
+        st.norms = self._n_norms.ctypes.data
+        st.newly = self._n_newly.ctypes.data
+        st.lam_next = self._n_lamnext.ctypes.data
+        self._native = st
+
+    def _native_step(self):
+        """One steady-state iteration in b2l_fast_iteration.  Returns the
+        step() result, or None when the drift test needs the repair path."""
+        st, cfg, m = self._native, self.cfg, self.m
+        lam = np.ascontiguousarray(self.lam, dtype=np.float64)
+        active = np.ascontiguousarray(self.active, dtype=bool)
+        self.lam, self.active = lam, active
+        kst = int(active.sum())
+        st.x, st.ax, st.p, st.ap = (t.data_ptr() for t in (self.X, self.AX, self.P, self.AP))
+        st.x2, st.ax2, st.p2, st.ap2 = (t.data_ptr() for t in (self.X2, self.AX2, self.P2,
+                                                                  self.AP2))
+        st.w_cur = self.Wbufs[self.wcur].data_ptr()
+        st.w_next = self.Wbufs[1 - self.wcur].data_ptr()
+        st.lam = lam.ctypes.data
+        st.active = active.ctypes.data
+        st.lock_iteration = self.lock_iteration.ctypes.data
+        st.it, st.have_p, st.kst = self.it, int(self.have_p), kst
+        st.stream = torch.cuda.current_stream(self.dev).cuda_stream
+        lib = _lib.load()
+        rc = lib.b2l_fast_iteration(ctypes.byref(st))
+        if rc == _lib.ITER_DRIFT:
+            return None
+        if rc < 0 and rc != _lib.EDEGENERATE:
+            _lib.check(rc, "b2l_fast_iteration")
+        it = self.it
+        norms = self._n_norms.copy()
+        newly = self._n_newly
+        self.norms = norms
+        self.f1_pending = self.sg_pending = False
+        self.history.append(HistoryEntry(
+            iteration=it,
+            ritz=lam.copy() if cfg.lock_history else None,
+            residual_norms=norms.copy() if cfg.lock_history else None,
+            active=active.copy(),
+            locked_now=tuple(int(i) for i in np.flatnonzero(newly)) if newly.any() else (),
+            fallbacks=self.pending,
+            constraint_violation=None,
+        ))
+        self.total_fallbacks += self.pending
+        self.pending = 0
+        if rc == _lib.ITER_DONE:
+            self.done = True
+            return False
+        if rc == _lib.EDEGENERATE:
+            self.pending += st.fallbacks
+            self.failure = "BasisDegeneracy"
+            self.done = True
+            return False
+        # ITER_OK: the next F1 and stencil pass are queued
+        self.pending += st.fallbacks
+        self.X, self.X2 = self.X2, self.X
+        self.AX, self.AX2 = self.AX2, self.AX
+        self.P, self.P2 = self.P2, self.P
+        self.AP, self.AP2 = self.AP2, self.AP
+        self.have_p = True
+        self.wcur = 1 - self.wcur
+        self.lam = self._n_lamnext.copy()
+        self.f1_pending = self.sg_pending = True
+        self.it += 1
+        return True
+
     # ---------------------------------------------------------- iteration
     def step(self):
         """One pass of the hot loop body (lobpcg.py:418-540).  Returns False
         once the loop has exited (converged, max_iter or failure)."""
         if self.done:
             return False
+        fetched = False
+        if self._native is not None and self.f1_pending and self.sg_pending \
+                and _OPTS["timer"] is None:
+            res = self._native_step()
+            if res is not None:
+                return res
+            fetched = True            # drift: the reductions are in h_red / h_g2
         cfg, m, n = self.cfg, self.m, self.n
         it = self.it
         try:
@@ -629,13 +739,15 @@ class LOBPCGRun:
                 # [X W]^T A W.  One host synchronisation for both.
                 a, b = 2 * m + kst, 3 * m + kst
                 nred = 2 * m + a * b
-                self._reduce(self.red[:nred])
-                self.h_red[:nred].copy_(self.red[:nred], non_blocking=True)
-                if self.sg_pending:
-                    self._reduce(self.g2[:g2_rows * kst])
-                    self.h_g2[:g2_rows * kst].copy_(self.g2[:g2_rows * kst], non_blocking=True)
-                if self.dev.type == "cuda":
-                    torch.cuda.current_stream(self.dev).synchronize()
+                if not fetched:
+                    self._reduce(self.red[:nred])
+                    self.h_red[:nred].copy_(self.red[:nred], non_blocking=True)
+                    if self.sg_pending:
+                        self._reduce(self.g2[:g2_rows * kst])
+                        self.h_g2[:g2_rows * kst].copy_(self.g2[:g2_rows * kst],
+                                                        non_blocking=True)
+                    if self.dev.type == "cuda":
+                        torch.cuda.current_stream(self.dev).synchronize()
                 # views of the pinned staging buffers (rewritten only after
                 # the next synchronisation)
                 red = self.h_red_np[:nred]

@@ -107,3 +107,12 @@ def test_exact_eigenvalues_match_oracle_closed_form():
     s = float(129 ** 2)
     np.testing.assert_allclose(exact_eigenvalues((128,) * 3, 10, scale=s)[0],
                                s * 12 * np.sin(np.pi / 258) ** 2, rtol=1e-14)
+
+
+def test_iter_state_layout_matches_library():
+    import ctypes
+
+    from paper_0705_2626_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.b2l_iter_state_size() == ctypes.sizeof(_lib.b2l_iter_state)
