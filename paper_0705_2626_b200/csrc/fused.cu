@@ -1029,7 +1029,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
   const int nloc = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   auto chunk_of = [&](int it) { return blockIdx.x + it * gridDim.x; };
   double* gred = sm + A.gred_off;   // [pair][NI*NJ tiles][32][2]
-  double s_w0 = 0.0, s_a0 = 0.0;
+  double s_w0 = 0.0, s_a0 = 0.0, s_w1 = 0.0, s_a1 = 0.0;   // per-lane column partials
 
   // compute warps: one instantiation per half, so each owns exactly its
   // accumulators (the register allocator never sees the other half's)
@@ -1040,27 +1040,36 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     const int mt = cw >> 1;                    // 8-row tile
     const int pbar = NB_PAIR + mt;
     const int q = lane & 3, rl = lane >> 2;
-    double cW[NT][KS], cP[NT][KS], cX[NT][KS];
+    // this warp's output column tile: nt = H (columns 8H .. 8H+7)
+    static_assert(NT == 2, "the warp pair splits the update by column tile");
+    double cW[KS], cP[KS], cX[KS];
     int pcol[KS];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const int k = 4 * ks + q;
       pcol[ks] = k < A.kp ? spc[k] : 0;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int cb = 8 * nt + rl;
-        const bool cv = cb < m;
-        cW[nt][ks] = (cv && k < A.kw) ? coef[m * m + k * m + cb] : 0.0;
-        cP[nt][ks] = (cv && k < A.kp) ? coef[m * m + A.kw * m + k * m + cb] : 0.0;
-        cX[nt][ks] = (cv && k < m) ? coef[k * m + cb] : 0.0;
-      }
+      const int cb = 8 * H + rl;
+      const bool cv = cb < m;
+      cW[ks] = (cv && k < A.kw) ? coef[m * m + k * m + cb] : 0.0;
+      cP[ks] = (cv && k < A.kp) ? coef[m * m + A.kw * m + k * m + cb] : 0.0;
+      cX[ks] = (cv && k < m) ? coef[k * m + cb] : 0.0;
     }
-    const int pt = H * 32 + lane;
-    const int RP2 = 64 / m;
-    const int rsub = pt / m, j0 = pt % m;
-    const bool on0 = rsub < RP2;
-    const double lam0 = on0 ? slam[j0] : 0.0;
-    const int jpos0 = on0 ? swp[j0] : -1;
+    // residual columns of this lane: c = 8H + 2q + e (fragment layout of C)
+    double lamc[2];
+    int wposc[2];
+    bool colok[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = 8 * H + 2 * q + e;
+      colok[e] = c < m;
+      lamc[e] = colok[e] ? slam[c] : 0.0;
+      wposc[e] = colok[e] ? swp[c] : -1;
+    }
+    const bool weighted = A.d != nullptr, want_ax = A.want_ax != 0;
+    const int tmode = A.tmode;
+    const double tinv = A.tinv;
+    const int npad = swn - A.kwn;
+    double s_w[2] = {0.0, 0.0}, s_a[2] = {0.0, 0.0};
     // lane columns of the tile rows / columns this warp uses
     const uint32_t zero_adr = sm_base + (uint32_t)A.zero_off * 8u;
     uint32_t la_[NI], ls_[NI], rb_[NJ], rs_[NJ];
@@ -1109,75 +1118,73 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
       const int ob = b * A.out_stride;
       const int r = 8 * mt + rl;
       {
-        // ---- (1) update, this warp's side (H = 0: P', X'; H = 1: AP', AX')
-        const double* Wb = st + A.in_off[2 + H];
-        const double* Pb = st + A.in_off[4 + H];
-        const double* Xb = st + A.in_off[0 + H];
-        double* Ox = sm + A.out_off[0 + H] + ob;
-        double* Op = sm + A.out_off[2 + H] + ob;
-        double acc[NT][3][2];
+        // ---- (1) update of this warp's column tile, all six products, and
+        // (2) the next residual straight from the accumulators
+        const double* W = st + A.in_off[2];
+        const double* AW = st + A.in_off[3];
+        const double* P = st + A.in_off[4];
+        const double* AP = st + A.in_off[5];
+        const double* X = st + A.in_off[0];
+        const double* AX = st + A.in_off[1];
+        double acc[6][2];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) acc[nt][c][0] = acc[nt][c][1] = 0.0;
+        for (int c = 0; c < 6; ++c) acc[c][0] = acc[c][1] = 0.0;
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int k = 4 * ks + q;
-          const double wv = k < A.kw ? Wb[r * sw + k] : 0.0;
-          const double pv = k < A.kp ? Pb[r * sx + pcol[ks]] : 0.0;
-          const double xv = k < m ? Xb[r * sx + k] : 0.0;
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            dmma_8x8x4(acc[nt][0][0], acc[nt][0][1], wv, cW[nt][ks]);
-            dmma_8x8x4(acc[nt][1][0], acc[nt][1][1], pv, cP[nt][ks]);
-            dmma_8x8x4(acc[nt][2][0], acc[nt][2][1], xv, cX[nt][ks]);
-          }
+          const bool kw_ok = k < A.kw, kp_ok = k < A.kp, km_ok = k < m;
+          const double wv = kw_ok ? W[r * sw + k] : 0.0;
+          const double awv = kw_ok ? AW[r * sw + k] : 0.0;
+          const double pv = kp_ok ? P[r * sx + pcol[ks]] : 0.0;
+          const double apv = kp_ok ? AP[r * sx + pcol[ks]] : 0.0;
+          const double xv = km_ok ? X[r * sx + k] : 0.0;
+          const double axv = km_ok ? AX[r * sx + k] : 0.0;
+          dmma_8x8x4(acc[0][0], acc[0][1], wv, cW[ks]);
+          dmma_8x8x4(acc[1][0], acc[1][1], awv, cW[ks]);
+          dmma_8x8x4(acc[2][0], acc[2][1], pv, cP[ks]);
+          dmma_8x8x4(acc[3][0], acc[3][1], apv, cP[ks]);
+          dmma_8x8x4(acc[4][0], acc[4][1], xv, cX[ks]);
+          dmma_8x8x4(acc[5][0], acc[5][1], axv, cX[ks]);
         }
         const bool bw = A.kw > 0, bp = A.kp > 0;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int co = 8 * nt + 2 * q;
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const double pn = (bw && bp) ? __dadd_rn(acc[nt][0][e], acc[nt][1][e])
-                                         : (bw ? acc[nt][0][e] : acc[nt][1][e]);
-            if (co + e < A.ldx) {
-              Ox[r * sx + co + e] = __dadd_rn(acc[nt][2][e], pn);
-              Op[r * sx + co + e] = pn;
-            }
-          }
-        }
-      }
-      nbar_sync(pbar, 64);
-      // ---- (2) residual of the 8 rows (both warps of the pair)
-      {
-        const double* O0 = sm + A.out_off[0] + ob;
-        const double* O1 = sm + A.out_off[1] + ob;
+        double* O0 = sm + A.out_off[0] + ob;
+        double* O1 = sm + A.out_off[1] + ob;
+        double* O2 = sm + A.out_off[2] + ob;
+        double* O3 = sm + A.out_off[3] + ob;
         double* O4 = sm + A.out_off[4] + ob;
-        if (on0) {
-          double sw_ = 0.0, sa_ = 0.0;
-          for (int rr = rsub; rr < 8; rr += RP2) {
-            const int row = 8 * mt + rr;
-            double wv = 0.0;
-            if (row < nvalid) {
-              const double xv = O0[row * sx + j0];
-              const double av = O1[row * sx + j0];
-              const double bx = A.d ? __dmul_rn(st[A.d_off + row], xv) : xv;
-              const double wf = __dsub_rn(av, __dmul_rn(bx, lam0));
-              sw_ = fma(wf, wf, sw_);
-              if (A.want_ax) sa_ = fma(av, av, sa_);
-              wv = wf;
-              if (A.tmode == 1) wv = __dmul_rn(A.tinv, wf);
-              else if (A.tmode == 2) wv = __dmul_rn(st[A.t_off + row], wf);
-            }
-            if (jpos0 >= 0) O4[row * swn + jpos0] = wv;
+        const double dr = weighted ? st[A.d_off + r] : 1.0;
+        const double tr = tmode == 2 ? st[A.t_off + r] : tinv;
+        const int co = 8 * H + 2 * q;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double pn = (bw && bp) ? __dadd_rn(acc[0][e], acc[2][e])
+                                       : (bw ? acc[0][e] : acc[2][e]);
+          const double apn = (bw && bp) ? __dadd_rn(acc[1][e], acc[3][e])
+                                        : (bw ? acc[1][e] : acc[3][e]);
+          const double xn = __dadd_rn(acc[4][e], pn);
+          const double axn = __dadd_rn(acc[5][e], apn);
+          if (co + e < A.ldx) {
+            O0[r * sx + co + e] = xn;
+            O1[r * sx + co + e] = axn;
+            O2[r * sx + co + e] = pn;
+            O3[r * sx + co + e] = apn;
           }
-          s_w0 += sw_;
-          s_a0 += sa_;
+          if (colok[e]) {
+            // W'_j = T (AX'_j - BX'_j lam_j) (lobpcg.py:429-430, :466-467)
+            const double bx = weighted ? __dmul_rn(dr, xn) : xn;
+            const double wf = __dsub_rn(axn, __dmul_rn(bx, lamc[e]));
+            s_w[e] = fma(wf, wf, s_w[e]);
+            if (want_ax) s_a[e] = fma(axn, axn, s_a[e]);
+            const double wv = tmode == 0 ? wf : __dmul_rn(tr, wf);
+            if (wposc[e] >= 0) O4[r * swn + wposc[e]] = wv;
+          }
         }
-        const int npad = swn - A.kwn;
-        for (int e = pt; e < 8 * npad; e += 64)
-          O4[(8 * mt + e / npad) * swn + A.kwn + e % npad] = 0.0;
+        // W' padding columns (kw_next .. ldw_next-1) of this warp's rows
+        if (H == 1)
+          for (int e = lane; e < 8 * npad; e += 32) {
+            const int rr = e / npad;
+            O4[(8 * mt + rr) * swn + A.kwn + (e - rr * npad)] = 0.0;
+          }
       }
       nbar_sync(pbar, 64);
       // ---- (3) Gram over the 8 rows, this warp's tiles
@@ -1211,6 +1218,10 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     }
     for (int it = (nloc > 2 ? nloc : 2); it < nloc + 2; ++it)
       nbar_sync(NB_OEMPTY + (it & 1), PAIR_THREADS);
+    s_w0 = s_w[0];
+    s_w1 = s_w[1];
+    s_a0 = s_a[0];
+    s_a1 = s_a[1];
     // the stage ring is idle once every warp is here: stash the accumulators
     nbar_sync(NB_PAIR_DONE, PAIR_THREADS);
 #pragma unroll
@@ -1268,23 +1279,27 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
   }
   __syncthreads();
 
-  // ---- CTA reductions (fixed order over pairs / threads)
+  // ---- CTA reductions (fixed order over pairs / rows)
   double* red = sm + A.red_off;
-  const int NL = PAIR_NW * 32;
+  const int NL = PAIR_NW * 64;      // [warp][lane][e]
   if (warp >= 1) {
-    const int o = (warp - 1) * 32 + lane;
+    const int o = ((warp - 1) * 32 + lane) * 2;
     red[o] = s_w0;
+    red[o + 1] = s_w1;
     red[NL + o] = s_a0;
+    red[NL + o + 1] = s_a1;
   }
   __syncthreads();
   double* out = A.partial + (size_t)blockIdx.x * (2 * m + A.a * A.b);
   if (tid < m) {
+    // column j lives in warp half H = j / 8, lanes with (lane & 3) = (j % 8) / 2, e = j % 2
+    const int H = tid >> 3, qq = (tid & 7) >> 1, e = tid & 1;
     double a = 0.0, bb = 0.0;
-    const int RP2 = 64 / m;
     for (int p = 0; p < PAIR_NW / 2; ++p)
-      for (int r_ = 0; r_ < RP2; ++r_) {
-        a += red[p * 64 + r_ * m + tid];
-        bb += red[NL + p * 64 + r_ * m + tid];
+      for (int g = 0; g < 8; ++g) {
+        const int o = (((2 * p + H) * 32) + 4 * g + qq) * 2 + e;
+        a += red[o];
+        bb += red[NL + o];
       }
     out[tid] = a;
     out[m + tid] = bb;
@@ -1444,7 +1459,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.bar_off = off;
   off += 16;  // mbarriers
   A.red_off = off;
-  const size_t red1 = (size_t)4 * STEP_NU * 32;
+  const size_t red1 = (size_t)4 * 32 * (PAIR_NW > STEP_NU ? PAIR_NW : STEP_NU);
   const size_t red2 = local ? (size_t)LOC_NW * lNI * lNJ * 64 : (size_t)A.TS * A.rs * 8 * 64;
   // the Gram item reduction reuses the (idle) stage ring after the loop
   if (red2 <= (size_t)A.nst * A.stage_doubles) {
