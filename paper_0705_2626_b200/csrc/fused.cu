@@ -684,7 +684,9 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
   const int nloc = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   auto chunk_of = [&](int it) { return blockIdx.x + it * gridDim.x; };
 
-  double s_w0 = 0.0, s_a0 = 0.0;
+  double s_w[NT][2], s_a[NT][2];   // per-lane residual-norm partials (columns 8nt + 2q + e)
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) s_w[nt][0] = s_w[nt][1] = s_a[nt][0] = s_a[nt][1] = 0.0;
   constexpr PairTiles TL = pair_tiles(NI, NJ, MFIX, 0, 1);
   double gacc[TL.n][2];
 #pragma unroll
@@ -738,12 +740,21 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
         cX[nt][ks] = (cv && k < m) ? coef[k * m + cb] : 0.0;
       }
     }
-    // residual lanes (m <= 10 < 32): lane = (rsub, j)
-    const int RP = 32 / m;
-    const int rsub = lane / m, j0 = lane % m;
-    const bool on0 = rsub < RP;
-    const double lam0 = on0 ? slam[j0] : 0.0;
-    const int jpos0 = on0 ? swp[j0] : -1;
+    // residual columns of this lane: c = 8 nt + 2q + e (fragment layout of C)
+    double lamc[NT][2];
+    int wposc[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * nt + 2 * q + e;
+        lamc[nt][e] = c < m ? slam[c] : 0.0;
+        wposc[nt][e] = c < m ? swp[c] : -1;
+      }
+    const bool weighted = A.d != nullptr, want_ax = A.want_ax != 0;
+    const int tmode = A.tmode;
+    const double tinv = A.tinv;
+    const int npad = swn - A.kwn;
     // Gram lane columns: L = [X' W' P'] (a cols), R = [X' W' P' AP'] (b cols)
     const uint32_t zero_adr = sm_base + (uint32_t)A.zero_off * 8u;
     uint32_t la_[NI], ls_[NI], rb_[NJ], rs_[NJ];
@@ -835,6 +846,8 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
           }
         }
         const bool bw = A.kw > 0, bp = A.kp > 0;
+        const double dr = weighted ? st[A.d_off + r] : 1.0;
+        const double tr = tmode == 2 ? st[A.t_off + r] : tinv;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const int co = 8 * nt + 2 * q;
@@ -844,42 +857,29 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
                                          : (bw ? acc[nt][0][e] : acc[nt][2][e]);
             const double apn = (bw && bp) ? __dadd_rn(acc[nt][1][e], acc[nt][3][e])
                                           : (bw ? acc[nt][1][e] : acc[nt][3][e]);
+            const double xn = __dadd_rn(acc[nt][4][e], pn);
+            const double axn = __dadd_rn(acc[nt][5][e], apn);
             if (co + e < A.ldx) {
-              O0[r * sx + co + e] = __dadd_rn(acc[nt][4][e], pn);
-              O1[r * sx + co + e] = __dadd_rn(acc[nt][5][e], apn);
+              O0[r * sx + co + e] = xn;
+              O1[r * sx + co + e] = axn;
               O2[r * sx + co + e] = pn;
               O3[r * sx + co + e] = apn;
+            }
+            if (co + e < m) {
+              // ---- (2) W'_j = T (AX'_j - BX'_j lam_j) from the accumulators
+              const double bx = weighted ? __dmul_rn(dr, xn) : xn;
+              const double wf = __dsub_rn(axn, __dmul_rn(bx, lamc[nt][e]));
+              s_w[nt][e] = fma(wf, wf, s_w[nt][e]);
+              if (want_ax) s_a[nt][e] = fma(axn, axn, s_a[nt][e]);
+              const double wv = tmode == 0 ? wf : __dmul_rn(tr, wf);
+              if (wposc[nt][e] >= 0) O4[r * swn + wposc[nt][e]] = wv;
             }
           }
         }
       }
-      __syncwarp();
-      // ---- (2) residual of the 8 rows
-      if (on0) {
-        double sw_ = 0.0, sa_ = 0.0;
-        for (int rr = rsub; rr < 8; rr += RP) {
-          const int row = 8 * mt + rr;
-          double wv = 0.0;
-          if (row < nvalid) {
-            const double xv = O0[row * sx + j0];
-            const double av = O1[row * sx + j0];
-            const double bx = A.d ? __dmul_rn(st[A.d_off + row], xv) : xv;
-            const double wf = __dsub_rn(av, __dmul_rn(bx, lam0));
-            sw_ = fma(wf, wf, sw_);
-            if (A.want_ax) sa_ = fma(av, av, sa_);
-            wv = wf;
-            if (A.tmode == 1) wv = __dmul_rn(A.tinv, wf);
-            else if (A.tmode == 2) wv = __dmul_rn(st[A.t_off + row], wf);
-          }
-          if (jpos0 >= 0) O4[row * swn + jpos0] = wv;
-        }
-        s_w0 += sw_;
-        s_a0 += sa_;
-      }
-      {
-        const int npad = swn - A.kwn;
-        for (int e = lane; e < 8 * npad; e += 32)
-          O4[(8 * mt + e / npad) * swn + A.kwn + e % npad] = 0.0;
+      for (int e = lane; e < 8 * npad; e += 32) {
+        const int rr = e / npad;
+        O4[(8 * mt + rr) * swn + A.kwn + (e - rr * npad)] = 0.0;
       }
       __syncwarp();
       // ---- (3) Gram over the 8 rows, every needed tile
@@ -913,23 +913,29 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
   }
   __syncthreads();
 
-  // ---- CTA reductions (fixed order over compute warps / lanes)
+  // ---- CTA reductions (fixed order over compute warps / rows)
   double* red = sm + A.red_off;
-  const int NL = LOC_NW * 32;
+  const int NL = LOC_NW * 32 * 2 * NT;    // [warp][lane][nt][e]
   if (warp >= 1) {
-    const int o = (warp - 1) * 32 + lane;
-    red[o] = s_w0;
-    red[NL + o] = s_a0;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int o = (((warp - 1) * 32 + lane) * NT + nt) * 2 + e;
+        red[o] = s_w[nt][e];
+        red[NL + o] = s_a[nt][e];
+      }
   }
   __syncthreads();
   double* out = A.partial + (size_t)blockIdx.x * (2 * m + A.a * A.b);
   if (tid < m) {
+    const int nt = tid >> 3, qq = (tid & 7) >> 1, e = tid & 1;
     double a = 0.0, bb = 0.0;
-    const int RP = 32 / m;
     for (int w = 0; w < LOC_NW; ++w)
-      for (int r_ = 0; r_ < RP; ++r_) {
-        a += red[w * 32 + r_ * m + tid];
-        bb += red[NL + w * 32 + r_ * m + tid];
+      for (int g = 0; g < 8; ++g) {
+        const int o = (((w * 32) + 4 * g + qq) * NT + nt) * 2 + e;
+        a += red[o];
+        bb += red[NL + o];
       }
     out[tid] = a;
     out[m + tid] = bb;
