@@ -8,11 +8,15 @@
 // rewritten).  Everything here is O(m^3) on <= 3m x 3m matrices; it sits on
 // the critical path between two device passes, which is why it is native.
 //
-// LAPACK: the caller registers dpotrf / dtrtrs / dtrtri / dsyevr with the
-// Fortran-style C signatures of scipy.linalg.cython_lapack (the routines
-// scipy.linalg.cholesky / solve_triangular / eigh -- the reference's calls --
-// run), see b2l_set_lapack.  The small matrix products are plain loops.
+// The small dense algebra (Cholesky in the reference's row-by-row form,
+// triangular solves, the symmetric eigensolver) is native by default.  With
+// B2L_RR_LAPACK=1 it runs through LAPACK routines the caller registered with
+// b2l_set_lapack (dpotrf / dtrtrs / dtrtri / dsyevr, Fortran-style C
+// signatures of scipy.linalg.cython_lapack: the routines the reference's
+// scipy calls run).  The small matrix products are plain loops.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -69,9 +73,184 @@ Mat transpose(const Mat& x) {
   return z;
 }
 
+// The small dense algebra runs natively by default (n <= 3m <= 48: library
+// call overheads dominate LAPACK here, and dsyevr on 30 x 30 costs ~2x the
+// native tridiagonal QL).  B2L_RR_LAPACK=1 routes it through the registered
+// LAPACK routines instead (same factorisations, LAPACK rounding).
+bool use_lapack() {
+  static const bool on = [] {
+    const char* v = getenv("B2L_RR_LAPACK");
+    return v && v[0] == '1';
+  }();
+  return on && g_potrf != nullptr;
+}
+
+// Symmetric eigensolver (tred2 / tql2 scheme): Householder reduction with the
+// transform accumulated, implicit QL with shifts, ascending sort.
+// a: n x n (lda = n) symmetric, overwritten by the eigenvectors; d: values; e: work (n)
+int symeig_ql(int n, double* a, double* d, double* e) {
+  auto A = [&](int i, int j) -> double& { return a[i + (size_t)j * n]; };
+  // --- Householder tridiagonalisation (rows n-1 .. 1)
+  for (int i = n - 1; i > 0; --i) {
+    const int l = i - 1;
+    double h = 0.0, scale = 0.0;
+    if (l > 0) {
+      for (int k = 0; k <= l; ++k) scale += std::fabs(A(i, k));
+      if (scale == 0.0) {
+        e[i] = A(i, l);
+      } else {
+        for (int k = 0; k <= l; ++k) {
+          A(i, k) /= scale;
+          h += A(i, k) * A(i, k);
+        }
+        double f = A(i, l);
+        double g = f >= 0.0 ? -std::sqrt(h) : std::sqrt(h);
+        e[i] = scale * g;
+        h -= f * g;
+        A(i, l) = f - g;
+        f = 0.0;
+        for (int j = 0; j <= l; ++j) {
+          A(j, i) = A(i, j) / h;
+          double gg = 0.0;
+          for (int k = 0; k <= j; ++k) gg += A(j, k) * A(i, k);
+          for (int k = j + 1; k <= l; ++k) gg += A(k, j) * A(i, k);
+          e[j] = gg / h;
+          f += e[j] * A(i, j);
+        }
+        const double hh = f / (h + h);
+        for (int j = 0; j <= l; ++j) {
+          const double ff = A(i, j);
+          const double gg = e[j] - hh * ff;
+          e[j] = gg;
+          for (int k = 0; k <= j; ++k) A(j, k) -= ff * e[k] + gg * A(i, k);
+        }
+      }
+    } else {
+      e[i] = A(i, l);
+    }
+    d[i] = h;
+  }
+  d[0] = 0.0;
+  e[0] = 0.0;
+  // --- accumulate the transformations
+  for (int i = 0; i < n; ++i) {
+    const int l = i - 1;
+    if (d[i] != 0.0) {
+      for (int j = 0; j <= l; ++j) {
+        double g = 0.0;
+        for (int k = 0; k <= l; ++k) g += A(i, k) * A(k, j);
+        for (int k = 0; k <= l; ++k) A(k, j) -= g * A(k, i);
+      }
+    }
+    d[i] = A(i, i);
+    A(i, i) = 1.0;
+    for (int j = 0; j <= l; ++j) A(j, i) = A(i, j) = 0.0;
+  }
+  // --- implicit QL on the tridiagonal (d, e)
+  for (int i = 1; i < n; ++i) e[i - 1] = e[i];
+  e[n - 1] = 0.0;
+  for (int l = 0; l < n; ++l) {
+    int iter = 0, mm;
+    do {
+      for (mm = l; mm < n - 1; ++mm) {
+        const double dd = std::fabs(d[mm]) + std::fabs(d[mm + 1]);
+        if (std::fabs(e[mm]) <= 2.220446049250313e-16 * dd) break;
+      }
+      if (mm != l) {
+        if (++iter > 60) return 1;
+        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+        double r = std::hypot(g, 1.0);
+        g = d[mm] - d[l] + e[l] / (g + (g >= 0.0 ? std::fabs(r) : -std::fabs(r)));
+        double s = 1.0, c = 1.0, p = 0.0;
+        int i;
+        for (i = mm - 1; i >= l; --i) {
+          double f = s * e[i];
+          const double b = c * e[i];
+          e[i + 1] = (r = std::hypot(f, g));
+          if (r == 0.0) {
+            d[i + 1] -= p;
+            e[mm] = 0.0;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = d[i + 1] - p;
+          r = (d[i] - g) * s + 2.0 * c * b;
+          d[i + 1] = g + (p = s * r);
+          g = c * r - b;
+          for (int k = 0; k < n; ++k) {
+            f = A(k, i + 1);
+            A(k, i + 1) = s * A(k, i) + c * f;
+            A(k, i) = c * A(k, i) - s * f;
+          }
+        }
+        if (r == 0.0 && i >= l) continue;
+        d[l] -= p;
+        e[l] = g;
+        e[mm] = 0.0;
+      }
+    } while (mm != l);
+  }
+  // --- ascending order (selection sort, vectors follow)
+  for (int i = 0; i < n - 1; ++i) {
+    int k = i;
+    for (int j = i + 1; j < n; ++j)
+      if (d[j] < d[k]) k = j;
+    if (k != i) {
+      std::swap(d[i], d[k]);
+      for (int r = 0; r < n; ++r) std::swap(A(r, i), A(r, k));
+    }
+  }
+  return 0;
+}
+
+// Upper R with g = R^T R from g's upper triangle, row by row as the
+// reference's multivec.cholesky (multivec.py:89-122): pivot d_j = g_jj -
+// sum_k r_kj^2 must be finite and > floor * g_jj, else NotSPD(j).
+Mat cholesky_native(const Mat& g, double floor_) {
+  const int k = g.r;
+  Mat r(k, k);
+  for (int j = 0; j < k; ++j) {
+    double d = g(j, j);
+    for (int t = 0; t < j; ++t) d -= r(t, j) * r(t, j);
+    if (!(d > floor_ * g(j, j)) || !std::isfinite(d)) throw NotSPD{j};
+    const double rjj = std::sqrt(d);
+    r(j, j) = rjj;
+    for (int c = j + 1; c < k; ++c) {
+      double v = g(j, c);
+      for (int t = 0; t < j; ++t) v -= r(t, j) * r(t, c);
+      r(j, c) = v / rjj;
+    }
+  }
+  return r;
+}
+
+// R^{-T} b (trans: forward substitution with R^T) or R^{-1} b (back substitution)
+Mat trsolve_native(const Mat& r, const Mat& b, bool trans) {
+  const int n = r.r;
+  Mat x = b;
+  for (int c = 0; c < b.c; ++c) {
+    if (trans) {
+      for (int i = 0; i < n; ++i) {
+        double v = x(i, c);
+        for (int t = 0; t < i; ++t) v -= r(t, i) * x(t, c);
+        x(i, c) = v / r(i, i);
+      }
+    } else {
+      for (int i = n - 1; i >= 0; --i) {
+        double v = x(i, c);
+        for (int t = i + 1; t < n; ++t) v -= r(i, t) * x(t, c);
+        x(i, c) = v / r(i, i);
+      }
+    }
+  }
+  return x;
+}
+
 // Upper R with g = R^T R from g's upper triangle; a pivot <= floor * g_jj (or
 // non-finite) throws NotSPD(j)  (small.cholesky; multivec.py:89-122).
 Mat cholesky(const Mat& g, double floor_) {
+  if (!use_lapack()) return cholesky_native(g, floor_);
   const int k = g.r;
   Mat r = g;
   if (k == 0) return r;
@@ -92,6 +271,7 @@ Mat cholesky(const Mat& g, double floor_) {
 
 // R^{-T} b (trans) or R^{-1} b for upper R
 Mat trsolve(const Mat& r, const Mat& b, bool trans) {
+  if (!use_lapack()) return trsolve_native(r, b, trans);
   Mat x = b;
   if (r.r == 0 || b.c == 0) return x;
   char uplo = 'U', tr = trans ? 'T' : 'N', diag = 'N';
@@ -103,6 +283,11 @@ Mat trsolve(const Mat& r, const Mat& b, bool trans) {
 }
 
 Mat upper_inverse(const Mat& r) {
+  if (!use_lapack()) {
+    Mat eye(r.r, r.r);
+    for (int i = 0; i < r.r; ++i) eye(i, i) = 1.0;
+    return trsolve_native(r, eye, false);
+  }
   Mat inv = r;
   if (r.r == 0) return inv;
   char uplo = 'U', diag = 'N';
@@ -147,6 +332,17 @@ void gen_sym_eig(const Mat& ga_in, const Mat& gb, int want, double floor_, doubl
   Mat ts(d, d);
   for (int j = 0; j < d; ++j)
     for (int i = 0; i < d; ++i) ts(i, j) = 0.5 * (t(i, j) + t(j, i));
+  if (!use_lapack()) {
+    std::vector<double> dv(d), ev(d);
+    if (d > 0 && symeig_ql(d, ts.p(), dv.data(), ev.data()) != 0)
+      throw LapackError{"tql2 (no convergence)", 1};
+    Mat v(d, want);
+    for (int j = 0; j < want; ++j)
+      for (int i = 0; i < d; ++i) v(i, j) = ts(i, j);
+    *c_out = trsolve(r, v, false);
+    for (int j = 0; j < want; ++j) vals_out[j] = dv[j];
+    return;
+  }
   // dsyevr, range 'A', upper, abstol 0 (scipy.linalg.eigh defaults)
   char jobz = 'V', range = 'A', uplo = 'U';
   int n = d, lda = d, il = 1, iu = d, mfound = 0, ldz = d, info = 0;
@@ -184,7 +380,6 @@ extern "C" int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, i
                                  const int* sel, double pivot_floor, double* lam_out,
                                  double* coef_out, int* pcols_out, int* kp_out,
                                  int* fallbacks_out) {
-  if (!g_potrf) return fail(-B2L_EINVAL, "rayleigh_ritz: LAPACK not registered (b2l_set_lapack)");
   if (m < 1 || kst < 0 || kj < 1 || kj > kst || kj > m || !g1 || !g2 || !lam || !jact || !sel)
     return fail(-B2L_EINVAL, "rayleigh_ritz: bad arguments");
   const int rW = m, rP = m + kst;
