@@ -59,6 +59,7 @@ struct StepArgs {
   int nrows, m, ldx;
   int kw, kp, kwn;
   int sx, sw, swn;      // shared-memory row strides (X-like, W, W')
+  int ldwn;             // W' leading dimension in HBM (its columns kwn..ldwn-1 are zeroed)
   const double* d;      // diag(B) or null
   const double* tvec;
   const double* coef;   // [Cx m*m | Cw kw*m | Cp kp*m]
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
           }
         }
         // zero W' pad columns kwn..swn-1 of the 8 rows
-        const int npad = swn - A.kwn;
+        const int npad = A.ldwn - A.kwn;
         for (int e = lane; e < 8 * npad; e += 32)
           O4[(8 * mt + e / npad) * swn + A.kwn + e % npad] = 0.0;
       }
@@ -754,7 +755,7 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
     const bool weighted = A.d != nullptr, want_ax = A.want_ax != 0;
     const int tmode = A.tmode;
     const double tinv = A.tinv;
-    const int npad = swn - A.kwn;
+    const int npad = A.ldwn - A.kwn;
     // Gram lane columns: L = [X' W' P'] (a cols), R = [X' W' P' AP'] (b cols)
     const uint32_t zero_adr = sm_base + (uint32_t)A.zero_off * 8u;
     uint32_t la_[NI], ls_[NI], rb_[NJ], rs_[NJ];
@@ -1074,7 +1075,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     const bool weighted = A.d != nullptr, want_ax = A.want_ax != 0;
     const int tmode = A.tmode;
     const double tinv = A.tinv;
-    const int npad = swn - A.kwn;
+    const int npad = A.ldwn - A.kwn;
     double s_w[2] = {0.0, 0.0}, s_a[2] = {0.0, 0.0};
     // lane columns of the tile rows / columns this warp uses
     const uint32_t zero_adr = sm_base + (uint32_t)A.zero_off * 8u;
@@ -1372,6 +1373,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.sx = smem_stride(ldx);
   A.sw = kw ? smem_stride(ldw) : 4;
   A.swn = smem_stride(kwn ? ldwn : 2);
+  A.ldwn = kwn ? ldwn : 2;
   A.d = d;
   A.tvec = tvec;
   A.coef = coef;
