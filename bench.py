@@ -323,11 +323,18 @@ def run_gpu(args):
                 "kernels": per,
                 "stencil_frac_of_8TBs": per.get("stencil", {}).get("gbs", 0.0) / 8000.0}
 
-    # ---- e2e through the public API on host buffers
+    # ---- e2e through the public API on host buffers: X0 from pinned host
+    # memory, eigenvectors back to host memory, both inside the timed call.
+    # One short untimed warm-up solve first (same shapes: it primes the
+    # caching host/device allocators, the tensor-map and kernel caches).
+    x0_host = torch.from_numpy(np.ascontiguousarray(x0)).pin_memory()
+    warm_cfg = pk.SolverConfig(block_size=M_BLOCK, tol=TOL, max_iter=3, seed=SEED)
+    del run, run2
+    pk.solve(A, t=T, x0=x0_host, config=warm_cfg)
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    rep = pk.solve(A, t=T, x0=x0, config=cfg)
+    rep = pk.solve(A, t=T, x0=x0_host, config=cfg)
     vecs = rep.eigenvectors  # numpy: D2H inside solve()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0

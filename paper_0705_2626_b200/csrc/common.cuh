@@ -163,7 +163,7 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 // doubles per half-warp) hit 16 distinct bank pairs.  The TMA box is this
 // wide; the columns past `ld` are out of bounds, zero-filled on load and
 // clipped on store.
-__host__ __device__ inline int smem_stride(int ld) {
+__host__ __device__ constexpr inline int smem_stride(int ld) {
   int s = ld < 4 ? 4 : ld;
   while ((s & 15) != 4 && (s & 15) != 12) ++s;
   return s;

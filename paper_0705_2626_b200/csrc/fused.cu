@@ -979,8 +979,12 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
 }
 
 constexpr int PAIR_NW = 14;                        // compute warps (7 pairs, 56-row chunks)
-constexpr int PAIR_THREADS = 32 * (1 + PAIR_NW);   // 480: <= 4 warps per SMSP
+constexpr int PAIR_THREADS = 32 * (2 + PAIR_NW);   // 512: loader + 14 compute + storer warps
+constexpr int PAIR_BAR = 32 * (1 + PAIR_NW);       // output-buffer barriers: compute + storer
+constexpr int PAIR_NOB = 3;                        // output buffers
+constexpr int NB_POFULL = 1;                       // named barriers 1..3
 constexpr int NB_PAIR = 5;                         // named barriers 5..11
+constexpr int NB_POEMPTY = 12;                     // named barriers 12..14
 constexpr int NB_PAIR_DONE = 15;
 
 // ---------------------------------------------------------------------------
@@ -1013,15 +1017,21 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int m = A.m;
-  const int sx = A.sx, sw = A.sw, swn = A.swn;
-  const int ncoef = m * m + A.kw * m + A.kp * m;
+  // MFIX > 0: the full-block step (kw = kp = kw_next = m = MFIX, every column
+  // active, so P and W' columns are the identity maps): every size, stride
+  // and predicate below is a compile-time constant
+  constexpr bool FIX = MFIX > 0;
+  constexpr int SF = FIX ? smem_stride(MFIX) : 4;
+  const int m = FIX ? MFIX : A.m;
+  const int kw = FIX ? MFIX : A.kw, kp = FIX ? MFIX : A.kp;
+  const int sx = FIX ? SF : A.sx, sw = FIX ? SF : A.sw, swn = FIX ? SF : A.swn;
+  const int ncoef = m * m + kw * m + kp * m;
   for (int i = tid; i < ncoef; i += blockDim.x) coef[i] = A.coef[i];
   for (int i = tid; i < m; i += blockDim.x) {
     slam[i] = A.lam[i];
     swp[i] = A.wpos[i];
   }
-  for (int i = tid; i < A.kp; i += blockDim.x) spc[i] = A.pcols[i];
+  for (int i = tid; i < kp; i += blockDim.x) spc[i] = A.pcols[i];
   for (int i = tid; i < 16; i += blockDim.x) sm[A.zero_off + i] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < A.nst; ++s) {
@@ -1054,11 +1064,11 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const int k = 4 * ks + q;
-      pcol[ks] = k < A.kp ? spc[k] : 0;
+      pcol[ks] = FIX ? k : (k < kp ? spc[k] : 0);
       const int cb = 8 * H + rl;
       const bool cv = cb < m;
-      cW[ks] = (cv && k < A.kw) ? coef[m * m + k * m + cb] : 0.0;
-      cP[ks] = (cv && k < A.kp) ? coef[m * m + A.kw * m + k * m + cb] : 0.0;
+      cW[ks] = (cv && k < kw) ? coef[m * m + k * m + cb] : 0.0;
+      cP[ks] = (cv && k < kp) ? coef[m * m + kw * m + k * m + cb] : 0.0;
       cX[ks] = (cv && k < m) ? coef[k * m + cb] : 0.0;
     }
     // residual columns of this lane: c = 8H + 2q + e (fragment layout of C)
@@ -1070,12 +1080,13 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
       const int c = 8 * H + 2 * q + e;
       colok[e] = c < m;
       lamc[e] = colok[e] ? slam[c] : 0.0;
-      wposc[e] = colok[e] ? swp[c] : -1;
+      wposc[e] = colok[e] ? (FIX ? c : swp[c]) : -1;
     }
     const bool weighted = A.d != nullptr, want_ax = A.want_ax != 0;
     const int tmode = A.tmode;
     const double tinv = A.tinv;
-    const int npad = A.ldwn - A.kwn;
+    const int npad = FIX ? 0 : A.ldwn - A.kwn;
+    const int ldx = FIX ? MFIX : A.ldx;
     double s_w[2] = {0.0, 0.0}, s_a[2] = {0.0, 0.0};
     // lane columns of the tile rows / columns this warp uses
     const uint32_t zero_adr = sm_base + (uint32_t)A.zero_off * 8u;
@@ -1115,12 +1126,11 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
 #pragma unroll
     for (int t = 0; t < TL.n; ++t) gacc[t][0] = gacc[t][1] = 0.0;
 
+    int s = 0, b = 0;
+    uint32_t phase = 0;
     for (int it = 0; it < nloc; ++it) {
-      const int s = it % A.nst, b = it & 1;
-      const int r0 = chunk_of(it) * A.rc;
-      const int nvalid = min(A.rc, A.nrows - r0);
-      if (it >= 2) nbar_sync(NB_OEMPTY + b, PAIR_THREADS);
-      mbar_wait(&full[s], (it / A.nst) & 1);
+      if (it >= PAIR_NOB) nbar_sync(NB_POEMPTY + b, PAIR_BAR);
+      mbar_wait(&full[s], phase);
       const double* st = stages + (size_t)s * A.stage_doubles;
       const int ob = b * A.out_stride;
       const int r = 8 * mt + rl;
@@ -1139,7 +1149,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int k = 4 * ks + q;
-          const bool kw_ok = k < A.kw, kp_ok = k < A.kp, km_ok = k < m;
+          const bool kw_ok = k < kw, kp_ok = k < kp, km_ok = k < m;
           const double wv = kw_ok ? W[r * sw + k] : 0.0;
           const double awv = kw_ok ? AW[r * sw + k] : 0.0;
           const double pv = kp_ok ? P[r * sx + pcol[ks]] : 0.0;
@@ -1153,7 +1163,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
           dmma_8x8x4(acc[4][0], acc[4][1], xv, cX[ks]);
           dmma_8x8x4(acc[5][0], acc[5][1], axv, cX[ks]);
         }
-        const bool bw = A.kw > 0, bp = A.kp > 0;
+        const bool bw = kw > 0, bp = kp > 0;
         double* O0 = sm + A.out_off[0] + ob;
         double* O1 = sm + A.out_off[1] + ob;
         double* O2 = sm + A.out_off[2] + ob;
@@ -1170,7 +1180,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
                                         : (bw ? acc[1][e] : acc[3][e]);
           const double xn = __dadd_rn(acc[4][e], pn);
           const double axn = __dadd_rn(acc[5][e], apn);
-          if (co + e < A.ldx) {
+          if (co + e < ldx) {
             O0[r * sx + co + e] = xn;
             O1[r * sx + co + e] = axn;
             O2[r * sx + co + e] = pn;
@@ -1190,8 +1200,14 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         if (H == 1)
           for (int e = lane; e < 8 * npad; e += 32) {
             const int rr = e / npad;
-            O4[(8 * mt + rr) * swn + A.kwn + (e - rr * npad)] = 0.0;
+            O4[(8 * mt + rr) * swn + (FIX ? MFIX : A.kwn) + (e - rr * npad)] = 0.0;
           }
+      }
+      // the stage is free once the update has read it (the B-weighted Gram
+      // still reads d from it): the loader refills it while the Gram runs
+      if (!WGT) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
       }
       nbar_sync(pbar, 64);
       // ---- (3) Gram over the 8 rows, this warp's tiles
@@ -1220,11 +1236,16 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
       }
       fence_async_smem();   // generic writes -> the TMA store (async proxy)
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      nbar_arrive(NB_OFULL + b, PAIR_THREADS);
+      if (WGT && lane == 0) mbar_arrive(&empty[s]);
+      nbar_arrive(NB_POFULL + b, PAIR_BAR);
+      if (++s == A.nst) {
+        s = 0;
+        phase ^= 1u;
+      }
+      if (++b == PAIR_NOB) b = 0;
     }
-    for (int it = (nloc > 2 ? nloc : 2); it < nloc + 2; ++it)
-      nbar_sync(NB_OEMPTY + (it & 1), PAIR_THREADS);
+    for (int it = (nloc > PAIR_NOB ? nloc : PAIR_NOB); it < nloc + PAIR_NOB; ++it)
+      nbar_sync(NB_POEMPTY + it % PAIR_NOB, PAIR_BAR);
     s_w0 = s_w[0];
     s_w1 = s_w[1];
     s_a0 = s_a[0];
@@ -1250,13 +1271,20 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
   };
 
   if (warp == 0) {
-    // ================= producer / storer =================
+    // ================= loader: refills a stage as soon as it is released
     if (lane == 0)
-      for (int j = 0; j < A.nst && j < nloc; ++j)
-        step_issue(M, A, stages + (size_t)j * A.stage_doubles, &full[j], chunk_of(j));
+      for (int j = 0; j < nloc; ++j) {
+        const int s = j % A.nst;
+        if (j >= A.nst) mbar_wait(&empty[s], (j / A.nst - 1) & 1);
+        step_issue(M, A, stages + (size_t)s * A.stage_doubles, &full[s], chunk_of(j));
+      }
+    __syncwarp();
+    nbar_sync(NB_PAIR_DONE, PAIR_THREADS);
+  } else if (warp == PAIR_NW + 1) {
+    // ================= storer: TMA stores of each finished output buffer
     for (int it = 0; it < nloc; ++it) {
-      const int b = it & 1;
-      nbar_sync(NB_OFULL + b, PAIR_THREADS);
+      const int b = it % PAIR_NOB;
+      nbar_sync(NB_POFULL + b, PAIR_BAR);
       if (lane == 0) {
         const int r0 = chunk_of(it) * A.rc;
         const int ob = b * A.out_stride;
@@ -1268,16 +1296,10 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         bulk_wait_read<0>();
       }
       __syncwarp();
-      nbar_arrive(NB_OEMPTY + b, PAIR_THREADS);
-      const int jn = it + A.nst;
-      if (lane == 0 && jn < nloc) {
-        const int s = it % A.nst;
-        mbar_wait(&empty[s], (it / A.nst) & 1);
-        step_issue(M, A, stages + (size_t)s * A.stage_doubles, &full[s], chunk_of(jn));
-      }
-      __syncwarp();
+      nbar_arrive(NB_POEMPTY + b, PAIR_BAR);
     }
     if (lane == 0) bulk_wait<0>();
+    __syncwarp();
     nbar_sync(NB_PAIR_DONE, PAIR_THREADS);
   } else if (((warp - 1) & 1) == 0) {
     run_half(std::integral_constant<int, 0>{});
@@ -1289,7 +1311,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
   // ---- CTA reductions (fixed order over pairs / rows)
   double* red = sm + A.red_off;
   const int NL = PAIR_NW * 64;      // [warp][lane][e]
-  if (warp >= 1) {
+  if (warp >= 1 && warp <= PAIR_NW) {
     const int o = ((warp - 1) * 32 + lane) * 2;
     red[o] = s_w0;
     red[o + 1] = s_w1;
@@ -1440,11 +1462,15 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.stage_doubles = (off + 15) & ~15;
   const int tile_x = (rc * A.sx + 15) & ~15;
   const int tile_w = (rc * A.swn + 15) & ~15;
+  // output buffers: 3 for the warp-pair variant (separate storer warp), else 2
+  const bool pair = local && !one_warp;
+  const int nob = pair ? PAIR_NOB : 2;
   {
-    const size_t tail = (size_t)2 * (4 * tile_x + tile_w) + (m * m + kw * m + kp * m) + 3 * m +
-                        64 + (size_t)4 * STEP_NU * 32 + 64;
+    const size_t tail = (size_t)nob * (4 * tile_x + tile_w) + (m * m + kw * m + kp * m) + 3 * m +
+                        64 + (pair ? 0 : (size_t)4 * STEP_NU * 32) + 64;
+    const size_t budget = pair ? 224 * 1024 : 200 * 1024;
     A.nst = 4;
-    while (A.nst > 2 && ((size_t)A.nst * A.stage_doubles + tail) * 8 > 200 * 1024) --A.nst;
+    while (A.nst > 2 && ((size_t)A.nst * A.stage_doubles + tail) * 8 > budget) --A.nst;
   }
   off = A.nst * A.stage_doubles;
   for (int b = 0; b < 4; ++b) {
@@ -1454,7 +1480,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.out_off[4] = off;
   off += tile_w;
   A.out_stride = off - A.out_off[0];
-  off += A.out_stride;  // second output buffer
+  off += (nob - 1) * A.out_stride;  // the other output buffers
   A.coef_off = off;
   off += (m * m + kw * m + kp * m + 1) & ~1;
   A.lam_off = off;
@@ -1469,8 +1495,12 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.red_off = off;
   const size_t red1 = (size_t)4 * 32 * (PAIR_NW > STEP_NU ? PAIR_NW : STEP_NU);
   const size_t red2 = local ? (size_t)LOC_NW * lNI * lNJ * 64 : (size_t)A.TS * A.rs * 8 * 64;
-  // the Gram item reduction reuses the (idle) stage ring after the loop
-  if (red2 <= (size_t)A.nst * A.stage_doubles) {
+  // the Gram item reduction reuses the (idle) stage ring after the loop; the
+  // pair variant also puts the column-norm partials there
+  if (pair && red2 + red1 <= (size_t)A.nst * A.stage_doubles) {
+    A.gred_off = 0;
+    A.red_off = (int)((red2 + 15) & ~(size_t)15);
+  } else if (red2 <= (size_t)A.nst * A.stage_doubles) {
     A.gred_off = 0;
     off += (int)red1;
   } else {
@@ -1519,7 +1549,11 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
       else kern = pick_local<2, 3, 4, 5, 0>(wgt);
     } else {
       threads = PAIR_THREADS;
-      kern = (m == 10 && kwn == 10) ? pick_pair<2, 3, 4, 5, 10>(wgt) : pick_pair<2, 3, 4, 5, 0>(wgt);
+      // the full-block specialisation: every column active (P and W' column
+      // maps are then the identity), unpadded leading dimensions
+      const bool full = m == 10 && kw == 10 && kp == 10 && kwn == 10 && ldx == 10 && ldw == 10 &&
+                        ldwn == 10;
+      kern = full ? pick_pair<2, 3, 4, 5, 10>(wgt) : pick_pair<2, 3, 4, 5, 0>(wgt);
     }
   } else {
     threads = STEP_THREADS;

@@ -9,7 +9,9 @@
 // lobpcg.py, LOBPCGRun.step); the Python side keeps every other path (first
 // iteration, drift repair, callbacks, constraints, z-slabs) and records the
 // history from the outputs.
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/b200lobpcg.h"
@@ -31,7 +33,29 @@ using namespace b2l;
 
 namespace {
 inline int even(int k) { return k < 2 ? 2 : k + (k & 1); }
+
+// Host-side phase timer of b2l_fast_iteration (B2L_ITER_PROFILE=1):
+// [0] calls, [1] enqueue of the fetch, [2] wait in the synchronisation,
+// [3] drift + lock tests, [4] Rayleigh-Ritz, [5] uploads + launches (us).
+double g_prof[6];
+const bool g_prof_on = [] {
+  const char* v = getenv("B2L_ITER_PROFILE");
+  return v && v[0] == '1';
+}();
+inline double now_us() {
+  return std::chrono::duration<double, std::micro>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
 }  // namespace
+
+extern "C" int b2l_iter_profile(double* out, int reset) {
+  if (out)
+    for (int i = 0; i < 6; ++i) out[i] = g_prof[i];
+  if (reset)
+    for (int i = 0; i < 6; ++i) g_prof[i] = 0.0;
+  return g_prof_on ? 1 : 0;
+}
 
 extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
   if (!s || s->m < 1 || s->kst < 1 || s->kst > s->m)
@@ -42,11 +66,21 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
   const size_t nred = (size_t)2 * m + (size_t)a * b;
   const size_t ng2 = (size_t)(m + kst) * kst;
 
+  double t0 = g_prof_on ? now_us() : 0.0, t1 = 0.0;
+  auto mark = [&](int slot) {
+    if (!g_prof_on) return;
+    t1 = now_us();
+    g_prof[slot] += t1 - t0;
+    t0 = t1;
+  };
+  if (g_prof_on) g_prof[0] += 1.0;
   // ---- one synchronisation: F1's reductions + the stencil pass's Gram
   B2L_CUDA(cudaMemcpyAsync(s->h_red, s->red_dev, nred * sizeof(double), cudaMemcpyDeviceToHost,
                            st));
   B2L_CUDA(cudaMemcpyAsync(s->h_g2, s->g2_dev, ng2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  mark(1);
   B2L_CUDA(cudaStreamSynchronize(st));
+  mark(2);
   const double* sums = s->h_red;
   const double* G1 = s->h_red + 2 * m;
 
@@ -80,6 +114,7 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
     if (s->active[j]) jact.push_back(j);
   if (jact.empty() || s->it == s->max_iter) return B2L_ITER_DONE;
 
+  mark(3);
   // ---- Rayleigh-Ritz (lobpcg.py:475-519) on the fetched Grams
   const int kj = (int)jact.size();
   std::vector<int> sel(kj);
@@ -95,6 +130,7 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
   const int rc = b2l_rayleigh_ritz(m, kst, s->have_p, G1, b, s->h_g2, s->lam, jact.data(), kj,
                                    sel.data(), s->pivot_floor, lam_next, coef, pcols, &kp, &fb);
   s->fallbacks = fb;
+  mark(4);
   if (rc) return rc;
   for (int j = 0; j < m; ++j) {
     wpos[j] = -1;
@@ -119,6 +155,7 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
   r = stencil7_gram(s->w_next, s->aw, s->nx, s->ny, s->nz, even(kj), nullptr, 0, 0, s->scale,
                     s->x2, s->ldx, m, kj, s->g2_dev, st);
   if (r) return r;
+  mark(5);
   return B2L_ITER_OK;
 }
 

@@ -21,6 +21,14 @@
 
 #include "common.cuh"
 
+// phase timers for the standalone host harness (tools/rr_harness.cu); empty
+// in the library
+#ifdef B2L_RR_PROF
+#define RR_MARK(k) rr_mark(k)
+#else
+#define RR_MARK(k) ((void)0)
+#endif
+
 namespace b2l {
 namespace {
 
@@ -85,11 +93,24 @@ bool use_lapack() {
   return on && g_potrf != nullptr;
 }
 
-// Symmetric eigensolver (tred2 / tql2 scheme): Householder reduction with the
-// transform accumulated, implicit QL with shifts, ascending sort.
-// a: n x n (lda = n) symmetric, overwritten by the eigenvectors; d: values; e: work (n)
-int symeig_ql(int n, double* a, double* d, double* e) {
+// Symmetric eigensolver (tred2 / tql2 scheme) for the `want` smallest pairs:
+// Householder reduction with the transform accumulated (Q), implicit QL with
+// shifts on the tridiagonal WITHOUT touching vectors -- each plane rotation is
+// logged instead -- then the wanted eigenvectors Q G_1 ... G_K e_k are formed
+// by replaying the log backwards on unit vectors (two entries per rotation).
+// Same eigenvalues as the classic tql2 (identical scalar recurrence), the
+// eigenvectors equal to rounding, at O(n^2 + K want) instead of O(K n) for
+// the rotations (K ~ 1.5 n^2 / 2 rotations; 30 x 30: ~6x fewer flops there).
+// a: n x n (lda = n) symmetric (destroyed); vals (want) ascending; vecs
+// (n x want, column-major).  Ascending order as a stable selection sort.
+int symeig_ql(int n, double* a, int want, double* vals, double* vecs) {
   auto A = [&](int i, int j) -> double& { return a[i + (size_t)j * n]; };
+  thread_local std::vector<double> dbuf, ebuf, rs, rc;
+  thread_local std::vector<int> ri, perm;
+  dbuf.assign(n, 0.0);
+  ebuf.assign(n, 0.0);
+  double* d = dbuf.data();
+  double* e = ebuf.data();
   // --- Householder tridiagonalisation (rows n-1 .. 1)
   for (int i = n - 1; i > 0; --i) {
     const int l = i - 1;
@@ -132,7 +153,8 @@ int symeig_ql(int n, double* a, double* d, double* e) {
   }
   d[0] = 0.0;
   e[0] = 0.0;
-  // --- accumulate the transformations
+  RR_MARK(7);
+  // --- accumulate the transformations (Q in a)
   for (int i = 0; i < n; ++i) {
     const int l = i - 1;
     if (d[i] != 0.0) {
@@ -146,9 +168,13 @@ int symeig_ql(int n, double* a, double* d, double* e) {
     A(i, i) = 1.0;
     for (int j = 0; j <= l; ++j) A(j, i) = A(i, j) = 0.0;
   }
-  // --- implicit QL on the tridiagonal (d, e)
+  RR_MARK(8);
+  // --- implicit QL on the tridiagonal (d, e); rotations logged
+  ri.clear();
+  rs.clear();
+  rc.clear();
   for (int i = 1; i < n; ++i) e[i - 1] = e[i];
-  e[n - 1] = 0.0;
+  if (n > 0) e[n - 1] = 0.0;
   for (int l = 0; l < n; ++l) {
     int iter = 0, mm;
     do {
@@ -166,23 +192,24 @@ int symeig_ql(int n, double* a, double* d, double* e) {
         for (i = mm - 1; i >= l; --i) {
           double f = s * e[i];
           const double b = c * e[i];
-          e[i + 1] = (r = std::hypot(f, g));
+          // |(f, g)| without hypot's overflow guard: f and g are bounded by
+          // the matrix norm, far from the fp64 range limits here
+          e[i + 1] = (r = std::sqrt(f * f + g * g));
           if (r == 0.0) {
             d[i + 1] -= p;
             e[mm] = 0.0;
             break;
           }
-          s = f / r;
-          c = g / r;
+          const double rinv = 1.0 / r;
+          s = f * rinv;
+          c = g * rinv;
           g = d[i + 1] - p;
           r = (d[i] - g) * s + 2.0 * c * b;
           d[i + 1] = g + (p = s * r);
           g = c * r - b;
-          for (int k = 0; k < n; ++k) {
-            f = A(k, i + 1);
-            A(k, i + 1) = s * A(k, i) + c * f;
-            A(k, i) = c * A(k, i) - s * f;
-          }
+          ri.push_back(i);
+          rs.push_back(s);
+          rc.push_back(c);
         }
         if (r == 0.0 && i >= l) continue;
         d[l] -= p;
@@ -191,14 +218,47 @@ int symeig_ql(int n, double* a, double* d, double* e) {
       }
     } while (mm != l);
   }
-  // --- ascending order (selection sort, vectors follow)
-  for (int i = 0; i < n - 1; ++i) {
+  RR_MARK(9);
+  // --- ascending order: selection sort on (value, column) pairs
+  perm.resize(n);
+  for (int i = 0; i < n; ++i) perm[i] = i;
+  for (int i = 0; i < n - 1 && i < want; ++i) {
     int k = i;
     for (int j = i + 1; j < n; ++j)
       if (d[j] < d[k]) k = j;
     if (k != i) {
       std::swap(d[i], d[k]);
-      for (int r = 0; r < n; ++r) std::swap(A(r, i), A(r, k));
+      std::swap(perm[i], perm[k]);
+    }
+  }
+  // --- wanted vectors: Y = G_1 ... G_K [e_perm(0) .. e_perm(want-1)] with the
+  // log replayed backwards on all wanted columns at once (Y row-major n x
+  // want: a rotation updates two contiguous rows), then V = Q Y
+  thread_local std::vector<double> ybuf;
+  ybuf.assign((size_t)n * want, 0.0);
+  double* Y = ybuf.data();
+  for (int w = 0; w < want; ++w) {
+    vals[w] = d[w];
+    Y[(size_t)perm[w] * want + w] = 1.0;
+  }
+  for (int t = (int)ri.size() - 1; t >= 0; --t) {
+    double* y0 = Y + (size_t)ri[t] * want;
+    double* y1 = y0 + want;
+    const double s = rs[t], c = rc[t];
+    for (int w = 0; w < want; ++w) {
+      const double yi = y0[w], yj = y1[w];
+      y0[w] = c * yi + s * yj;
+      y1[w] = c * yj - s * yi;
+    }
+  }
+  for (int w = 0; w < want; ++w) {
+    double* v = vecs + (size_t)w * n;
+    for (int r = 0; r < n; ++r) v[r] = 0.0;
+    for (int k = 0; k < n; ++k) {
+      const double yk = Y[(size_t)k * want + w];
+      if (yk == 0.0) continue;
+      const double* q = a + (size_t)k * n;
+      for (int r = 0; r < n; ++r) v[r] += q[r] * yk;
     }
   }
   return 0;
@@ -327,22 +387,77 @@ void gen_sym_eig(const Mat& ga_in, const Mat& gb, int want, double floor_, doubl
   for (int j = 0; j < d; ++j)
     for (int i = 0; i <= j; ++i) ga(i, j) = ga(j, i) = ga_in(i, j);
   Mat r = cholesky(gb, floor_);
+  RR_MARK(4);   // pencil Cholesky
+  if (!use_lapack()) {
+    // M = R^-T ga R^-1 through the explicit inverse: row-oriented loops whose
+    // inner index runs over independent entries (the substitution form is a
+    // chain of dependent dot products, latency-bound at these sizes)
+    thread_local std::vector<double> ri_, t_, m_;
+    ri_.assign((size_t)d * d, 0.0);   // R^-1, row-major upper
+    t_.assign((size_t)d * d, 0.0);    // ga R^-1, row-major
+    m_.assign((size_t)d * d, 0.0);    // column-major (symeig_ql layout)
+    double* Ri = ri_.data();
+    for (int i = d - 1; i >= 0; --i) {
+      const double inv = 1.0 / r(i, i);
+      double* row = Ri + (size_t)i * d;
+      row[i] = inv;
+      for (int t = i + 1; t < d; ++t) {
+        const double rit = r(i, t);
+        const double* rt = Ri + (size_t)t * d;
+        for (int j = t; j < d; ++j) row[j] -= rit * rt[j];
+      }
+      for (int j = i + 1; j < d; ++j) row[j] *= inv;
+    }
+    double* T = t_.data();
+    for (int i = 0; i < d; ++i) {
+      double* ti = T + (size_t)i * d;
+      for (int k = 0; k < d; ++k) {
+        const double g = ga(i, k);
+        const double* rk = Ri + (size_t)k * d;
+        for (int j = k; j < d; ++j) ti[j] += g * rk[j];
+      }
+    }
+    // M(i, j) = sum_k Ri(k, i) T(k, j), k <= i; symmetrised as the reference
+    thread_local std::vector<double> u_;
+    u_.assign((size_t)d * d, 0.0);
+    double* U = u_.data();   // row-major full product
+    for (int i = 0; i < d; ++i) {
+      double* ui = U + (size_t)i * d;
+      for (int k = 0; k <= i; ++k) {
+        const double rki = Ri[(size_t)k * d + i];
+        const double* tk = T + (size_t)k * d;
+        for (int j = 0; j < d; ++j) ui[j] += rki * tk[j];
+      }
+    }
+    double* M = m_.data();
+    for (int j = 0; j < d; ++j)
+      for (int i = 0; i < d; ++i)
+        M[i + (size_t)j * d] = 0.5 * (U[(size_t)i * d + j] + U[(size_t)j * d + i]);
+    thread_local std::vector<double> v_;
+    v_.assign((size_t)d * want, 0.0);
+    RR_MARK(5);   // R^-T A R^-1
+    if (d > 0 && symeig_ql(d, M, want, vals_out, v_.data()) != 0)
+      throw LapackError{"tql2 (no convergence)", 1};
+    RR_MARK(6);   // symmetric eigensolve
+    // C = R^-1 V
+    Mat c(d, want);
+    for (int w = 0; w < want; ++w) {
+      const double* v = v_.data() + (size_t)w * d;
+      for (int i = 0; i < d; ++i) {
+        const double* ri = Ri + (size_t)i * d;
+        double s = 0.0;
+        for (int k = i; k < d; ++k) s += ri[k] * v[k];
+        c(i, w) = s;
+      }
+    }
+    *c_out = std::move(c);
+    return;
+  }
   Mat t = trsolve(r, ga, true);
   t = trsolve(r, transpose(t), true);
   Mat ts(d, d);
   for (int j = 0; j < d; ++j)
     for (int i = 0; i < d; ++i) ts(i, j) = 0.5 * (t(i, j) + t(j, i));
-  if (!use_lapack()) {
-    std::vector<double> dv(d), ev(d);
-    if (d > 0 && symeig_ql(d, ts.p(), dv.data(), ev.data()) != 0)
-      throw LapackError{"tql2 (no convergence)", 1};
-    Mat v(d, want);
-    for (int j = 0; j < want; ++j)
-      for (int i = 0; i < d; ++i) v(i, j) = ts(i, j);
-    *c_out = trsolve(r, v, false);
-    for (int j = 0; j < want; ++j) vals_out[j] = dv[j];
-    return;
-  }
   // dsyevr, range 'A', upper, abstol 0 (scipy.linalg.eigh defaults)
   char jobz = 'V', range = 'A', uplo = 'U';
   int n = d, lda = d, il = 1, iu = d, mfound = 0, ldz = d, info = 0;
@@ -386,6 +501,7 @@ extern "C" int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, i
   const int cW = m, cP = m + kst, cAP = 2 * m + kst;
   auto G1 = [&](int i, int j) { return g1[(size_t)i * ldg1 + j]; };
   auto G2 = [&](int i, int j) { return g2[(size_t)i * kst + j]; };
+  RR_MARK(-1);
   int pending = 0;
   *fallbacks_out = 0;
   *kp_out = 0;
@@ -429,6 +545,7 @@ extern "C" int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, i
         pending += 1;
       }
     }
+    RR_MARK(0);   // W and P Cholesky-QR
     auto block1 = [&](int r0, const int* ri, int nr, int c0, const int* ci, int nc) {
       Mat z(nr, nc);
       for (int b = 0; b < nc; ++b)
@@ -492,8 +609,10 @@ extern "C" int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, i
           for (int i = 0; i < kp; ++i) ga(o + i, o + j) = app(i, j);
         }
       }
+      RR_MARK(1);   // blocks + pencil assembly
       try {
         gen_sym_eig(ga, gb, m, pivot_floor, vals.data(), &c);
+        RR_MARK(2);   // generalized eigensolve
         break;
       } catch (const NotSPD& e) {
         pending += 1;
@@ -541,6 +660,7 @@ extern "C" int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, i
     for (int j = 0; j < m; ++j) lam_out[j] = vals[j];
     *kp_out = kp;
     *fallbacks_out = pending;
+    RR_MARK(3);   // coefficient folding
     return 0;
   } catch (const LapackError& e) {
     return fail(-B2L_ELAPACK, std::string("rayleigh_ritz: ") + e.what + " info " +
