@@ -239,12 +239,14 @@ int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, int ldg1,
  * synchronisation fetching red_dev (2m + a*b, a = 2m + kst, b = 3m + kst) and
  * g2_dev ((m + kst) x kst) into the pinned h_red / h_g2; the drift test; the
  * lock test (updates active, lock_iteration; writes norms, newly); the
- * Rayleigh-Ritz step (b2l_rayleigh_ritz); the upload of coefficients,
- * Ritz values, pcols and wpos (through the pinned h_stage (>= 3m^2 + m
- * doubles) / h_istage (>= 2m ints) into coef_dev / lam_dev / pcols_dev
- * (>= 2m ints: pcols then wpos)); then the launches of the next
- * b2l_lobpcg_step (x,ax,p,ap,w_cur -> x2,ax2,p2,ap2,w_next) and
- * b2l_stencil7_gram (w_next -> aw, g2_dev = [x2 ; w_next]^T aw).
+ * Rayleigh-Ritz step (b2l_rayleigh_ritz, output staged in the pinned
+ * h_stage (>= 3m^2 + m doubles) / h_istage (>= 2m ints)); then the launches
+ * of the next b2l_lobpcg_step (x,ax,p,ap,w_cur -> x2,ax2,p2,ap2,w_next; the
+ * coefficients, Ritz values, pcols and wpos travel by value in the launch)
+ * and b2l_stencil7_gram (w_next -> aw, [x2 ; w_next]^T aw).  Their
+ * reductions are written straight into h_red / h_g2 when those are
+ * device-mapped pinned buffers (red_on_host = 1), else into red_dev / g2_dev
+ * and copied at the next call.  coef_dev / lam_dev / pcols_dev are unused.
  * Returns B2L_ITER_OK (next passes queued; lam_next, k_next, kp, fallbacks
  * set), B2L_ITER_DRIFT (nothing changed but drift and the fetched h_red /
  * h_g2: the caller repairs), B2L_ITER_DONE (lock test applied, loop over),
@@ -283,6 +285,10 @@ typedef struct {
   double* lam_next;                   /* out (m) */
   double drift;                       /* out */
   int fallbacks, k_next, kp;          /* out */
+  int red_on_host;                    /* in/out: 1 when the queued passes write
+                                         h_red / h_g2 directly (mapped pinned
+                                         memory); the caller sets 0 whenever it
+                                         queued the passes itself */
 } b2l_iter_state;
 
 int b2l_fast_iteration(b2l_iter_state* state);

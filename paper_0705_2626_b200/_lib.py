@@ -47,6 +47,7 @@ class b2l_iter_state(C.Structure):
         ("norms", C.c_void_p), ("newly", C.c_void_p), ("lam_next", C.c_void_p),
         ("drift", C.c_double),
         ("fallbacks", C.c_int), ("k_next", C.c_int), ("kp", C.c_int),
+        ("red_on_host", C.c_int),
     ]
 
 

@@ -41,7 +41,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
                 double* xo, double* axo, double* po, double* apo, const double* lam,
                 const double* d, int tmode, double tinv, const double* tvec,
                 const int* wpos, int kwn, double* wo, int ldwn, int want_ax,
-                double* red_out, cudaStream_t st);
+                double* red_out, cudaStream_t st, const StepHostCoef* hc);
 
 static thread_local std::string g_err;
 
@@ -318,7 +318,7 @@ int b2l_lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx
                     int want_ax_norms, double* red_out, void* stream) {
   return lobpcg_step(nrows, m, x, ax, ldx, w, aw, ldw, kw, p, ap, kp, pcols, coef, xo, axo, po,
                      apo, lam, bdiag, tmode, tinv, tvec, wpos, kw_next, w_next, ldw_next,
-                     want_ax_norms, red_out, static_cast<cudaStream_t>(stream));
+                     want_ax_norms, red_out, static_cast<cudaStream_t>(stream), nullptr);
 }
 
 }  // extern "C"

@@ -52,6 +52,13 @@ int sm_count();
 // (kernel, smem, threads): both are host API round trips on every launch
 // otherwise.  per_sm may be null.
 int prepare_kernel(const void* kern, size_t smem, int threads, int* per_sm);
+// Host-side Rayleigh-Ritz output handed to the F1 launch by value (no H2D copy)
+struct StepHostCoef {
+  const double* coef;   // [Cx m*m | Cw kw*m | Cp kp*m]
+  const double* lam;    // m
+  const int* pcols;     // kp
+  const int* wpos;      // m
+};
 // out[e] = sum over parts c of partial[c * len + e] (fixed order, deterministic)
 int sum_parts(const double* partial, int nparts, int len, double* out, cudaStream_t st);
 

@@ -87,6 +87,16 @@ struct StepArgs {
   double* partial;      // [gridDim.x][2m + a*b]
 };
 
+// Coefficients passed by value in the launch (kernel parameter space) instead
+// of through an H2D copy: the steady-state driver (b2l_fast_iteration) hands
+// its host-side Rayleigh-Ritz output straight to the launch.  Used when
+// StepArgs::coef is null.
+struct StepCoef {
+  double c[3 * 16 * 16];   // [Cx m*m | Cw kw*m | Cp kp*m]
+  double lam[16];
+  int pcols[16], wpos[16];
+};
+
 __device__ __forceinline__ void nbar_sync(int id, int count) {
   asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -133,7 +143,8 @@ __device__ __forceinline__ void step_issue(const StepMaps& M, const StepArgs& A,
 // WGT: B = diag(d) weights the B-Gram blocks.
 template <int NT, int KS, bool WGT>
 __global__ void __launch_bounds__(STEP_THREADS, 1)
-    step_kernel(const __grid_constant__ StepMaps M, const __grid_constant__ StepArgs Ain) {
+    step_kernel(const __grid_constant__ StepMaps M, const __grid_constant__ StepArgs Ain,
+                    const __grid_constant__ StepCoef Cf) {
   extern __shared__ __align__(128) unsigned char sm_raw[];
   // The parameters (1.7 KB with the tensor maps) overflow the constant cache
   // when the hot loops re-read fields: keep a shared copy.
@@ -156,12 +167,13 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
   const int m = A.m;
   const int sx = A.sx, sw = A.sw, swn = A.swn;
   const int ncoef = m * m + A.kw * m + A.kp * m;
-  for (int i = tid; i < ncoef; i += blockDim.x) coef[i] = A.coef[i];
+  const bool inl = A.coef == nullptr;
+  for (int i = tid; i < ncoef; i += blockDim.x) coef[i] = inl ? Cf.c[i] : A.coef[i];
   for (int i = tid; i < m; i += blockDim.x) {
-    slam[i] = A.lam[i];
-    swp[i] = A.wpos[i];
+    slam[i] = inl ? Cf.lam[i] : A.lam[i];
+    swp[i] = inl ? Cf.wpos[i] : A.wpos[i];
   }
-  for (int i = tid; i < A.kp; i += blockDim.x) spc[i] = A.pcols[i];
+  for (int i = tid; i < A.kp; i += blockDim.x) spc[i] = inl ? Cf.pcols[i] : A.pcols[i];
   for (int i = tid; i < 16; i += blockDim.x) sm[A.zero_off + i] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < A.nst; ++s) {
@@ -644,7 +656,8 @@ constexpr int LOC_THREADS = 32 * (1 + LOC_NW);   // 288
 
 template <int NT, int KS, int NI, int NJ, int MFIX, bool WGT>
 __global__ void __launch_bounds__(LOC_THREADS, 1)
-    step_local_kernel(const __grid_constant__ StepMaps M, const __grid_constant__ StepArgs Ain) {
+    step_local_kernel(const __grid_constant__ StepMaps M, const __grid_constant__ StepArgs Ain,
+                    const __grid_constant__ StepCoef Cf) {
   extern __shared__ __align__(128) unsigned char sm_raw[];
   __shared__ StepArgs sA;
   if (threadIdx.x == 0) sA = Ain;
@@ -665,12 +678,13 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
   const int m = A.m;
   const int sx = A.sx, sw = A.sw, swn = A.swn;
   const int ncoef = m * m + A.kw * m + A.kp * m;
-  for (int i = tid; i < ncoef; i += blockDim.x) coef[i] = A.coef[i];
+  const bool inl = A.coef == nullptr;
+  for (int i = tid; i < ncoef; i += blockDim.x) coef[i] = inl ? Cf.c[i] : A.coef[i];
   for (int i = tid; i < m; i += blockDim.x) {
-    slam[i] = A.lam[i];
-    swp[i] = A.wpos[i];
+    slam[i] = inl ? Cf.lam[i] : A.lam[i];
+    swp[i] = inl ? Cf.wpos[i] : A.wpos[i];
   }
-  for (int i = tid; i < A.kp; i += blockDim.x) spc[i] = A.pcols[i];
+  for (int i = tid; i < A.kp; i += blockDim.x) spc[i] = inl ? Cf.pcols[i] : A.pcols[i];
   for (int i = tid; i < 16; i += blockDim.x) sm[A.zero_off + i] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < A.nst; ++s) {
@@ -999,7 +1013,8 @@ constexpr int NB_PAIR_DONE = 15;
 // DMMA pipe fed.
 template <int NT, int KS, int NI, int NJ, int MFIX, bool WGT>
 __global__ void __launch_bounds__(PAIR_THREADS, 1)
-    step_pair_kernel(const __grid_constant__ StepMaps M, const __grid_constant__ StepArgs Ain) {
+    step_pair_kernel(const __grid_constant__ StepMaps M, const __grid_constant__ StepArgs Ain,
+                    const __grid_constant__ StepCoef Cf) {
   extern __shared__ __align__(128) unsigned char sm_raw[];
   __shared__ StepArgs sA;
   if (threadIdx.x == 0) sA = Ain;
@@ -1026,12 +1041,13 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
   const int kw = FIX ? MFIX : A.kw, kp = FIX ? MFIX : A.kp;
   const int sx = FIX ? SF : A.sx, sw = FIX ? SF : A.sw, swn = FIX ? SF : A.swn;
   const int ncoef = m * m + kw * m + kp * m;
-  for (int i = tid; i < ncoef; i += blockDim.x) coef[i] = A.coef[i];
+  const bool inl = A.coef == nullptr;
+  for (int i = tid; i < ncoef; i += blockDim.x) coef[i] = inl ? Cf.c[i] : A.coef[i];
   for (int i = tid; i < m; i += blockDim.x) {
-    slam[i] = A.lam[i];
-    swp[i] = A.wpos[i];
+    slam[i] = inl ? Cf.lam[i] : A.lam[i];
+    swp[i] = inl ? Cf.wpos[i] : A.wpos[i];
   }
-  for (int i = tid; i < kp; i += blockDim.x) spc[i] = A.pcols[i];
+  for (int i = tid; i < kp; i += blockDim.x) spc[i] = inl ? Cf.pcols[i] : A.pcols[i];
   for (int i = tid; i < 16; i += blockDim.x) sm[A.zero_off + i] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < A.nst; ++s) {
@@ -1352,7 +1368,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
   }
 }
 
-using StepKernel = void (*)(StepMaps, StepArgs);
+using StepKernel = void (*)(StepMaps, StepArgs, StepCoef);
 
 template <int NT, int KS, int NI, int NJ, int MFIX>
 static StepKernel pick_pair(bool wgt) {
@@ -1375,7 +1391,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
                 double* xo, double* axo, double* po, double* apo, const double* lam,
                 const double* d, int tmode, double tinv, const double* tvec,
                 const int* wpos, int kwn, double* wo, int ldwn, int want_ax,
-                double* red_out, cudaStream_t st) {
+                double* red_out, cudaStream_t st, const StepHostCoef* hc) {
   B2L_CHECK(m >= 1 && m <= 16, -B2L_EINVAL, "step: 1 <= m <= 16 (larger blocks: b2l_update)");
   B2L_CHECK(nrows >= 1, -B2L_EINVAL, "step: empty block");
   B2L_CHECK(ldx >= m && (ldx & 1) == 0, -B2L_EINVAL, "step: ldx must be even and >= m");
@@ -1402,6 +1418,21 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.pcols = pcols;
   A.wpos = wpos;
   A.lam = lam;
+  // host coefficients travel in the launch itself (hc: b2l_fast_iteration)
+  static StepCoef cf;   // the launch copies it; one host thread drives a context
+  if (hc) {
+    const int nc = m * m + kw * m + kp * m;
+    for (int i = 0; i < nc; ++i) cf.c[i] = hc->coef[i];
+    for (int i = 0; i < m; ++i) {
+      cf.lam[i] = hc->lam[i];
+      cf.wpos[i] = hc->wpos[i];
+    }
+    for (int i = 0; i < kp; ++i) cf.pcols[i] = hc->pcols[i];
+    A.coef = nullptr;
+    A.lam = nullptr;
+    A.pcols = nullptr;
+    A.wpos = nullptr;
+  }
   A.tmode = tmode;
   A.tinv = tinv;
   A.want_ax = want_ax;
@@ -1573,7 +1604,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   double* part = static_cast<double*>(workspace((size_t)gx * len * sizeof(double), &werr));
   if (werr) return werr;
   A.partial = part;
-  kern<<<gx, threads, smem, st>>>(M, A);
+  kern<<<gx, threads, smem, st>>>(M, A, cf);
   B2L_CUDA(cudaGetLastError());
   return sum_parts(part, gx, len, red_out, st);
 }

@@ -23,7 +23,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx, co
                 const int* pcols, const double* coef, double* xo, double* axo, double* po,
                 double* apo, const double* lam, const double* d, int tmode, double tinv,
                 const double* tvec, const int* wpos, int kwn, double* wo, int ldwn, int want_ax,
-                double* red_out, cudaStream_t st);
+                double* red_out, cudaStream_t st, const StepHostCoef* hc);
 int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
                   const double* halo, int has_lo, int has_hi, double scale, const double* x,
                   int ldx, int m, int kw, double* gram_out, cudaStream_t st);
@@ -48,6 +48,25 @@ inline double now_us() {
       .count();
 }
 }  // namespace
+
+// Device address of a pinned host buffer (cudaHostGetDevicePointer), cached
+// for the last two buffers; null when it is not device-mapped (then copied).
+double* mapped(double* h) {
+  static double* hs[2] = {nullptr, nullptr};
+  static double* ds[2] = {nullptr, nullptr};
+  for (int i = 0; i < 2; ++i)
+    if (hs[i] == h) return ds[i];
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) {
+    cudaGetLastError();
+    d = nullptr;
+  }
+  hs[1] = hs[0];
+  ds[1] = ds[0];
+  hs[0] = h;
+  ds[0] = static_cast<double*>(d);
+  return ds[0];
+}
 
 extern "C" int b2l_iter_profile(double* out, int reset) {
   if (out)
@@ -74,12 +93,18 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
     t0 = t1;
   };
   if (g_prof_on) g_prof[0] += 1.0;
-  // ---- one synchronisation: F1's reductions + the stencil pass's Gram
-  B2L_CUDA(cudaMemcpyAsync(s->h_red, s->red_dev, nred * sizeof(double), cudaMemcpyDeviceToHost,
-                           st));
-  B2L_CUDA(cudaMemcpyAsync(s->h_g2, s->g2_dev, ng2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  // ---- one synchronisation: F1's reductions + the stencil pass's Gram.  The
+  // passes this function queued wrote them straight into the pinned h_red /
+  // h_g2 (device-mapped); passes queued elsewhere left them on the device.
+  if (!s->red_on_host) {
+    B2L_CUDA(cudaMemcpyAsync(s->h_red, s->red_dev, nred * sizeof(double), cudaMemcpyDeviceToHost,
+                             st));
+    B2L_CUDA(cudaMemcpyAsync(s->h_g2, s->g2_dev, ng2 * sizeof(double), cudaMemcpyDeviceToHost,
+                             st));
+  }
   mark(1);
   B2L_CUDA(cudaStreamSynchronize(st));
+  s->red_on_host = 0;
   mark(2);
   const double* sums = s->h_red;
   const double* G1 = s->h_red + 2 * m;
@@ -140,21 +165,29 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
   s->kp = kp;
   s->k_next = kj;
 
-  // ---- uploads + the next fused passes
-  const size_t ncoef = (size_t)m * m + (size_t)kst * m + (size_t)kp * m;
-  B2L_CUDA(cudaMemcpyAsync(s->coef_dev, coef, ncoef * sizeof(double), cudaMemcpyHostToDevice, st));
-  B2L_CUDA(cudaMemcpyAsync(s->lam_dev, lam_next, m * sizeof(double), cudaMemcpyHostToDevice, st));
-  B2L_CUDA(cudaMemcpyAsync(s->pcols_dev, pcols, (size_t)2 * m * sizeof(int),
-                           cudaMemcpyHostToDevice, st));
+  // ---- the next fused passes: coefficients by value in the F1 launch (no
+  // H2D copies), reductions written into the mapped pinned buffers (no D2H)
+  double* red_h = mapped(s->h_red);
+  double* g2_h = mapped(s->h_g2);
+  const StepHostCoef hc{coef, lam_next, pcols, wpos};
   int r = lobpcg_step(s->n, m, s->x, s->ax, s->ldx, s->w_cur, s->aw, even(kst), kst,
-                      kp ? s->p : nullptr, kp ? s->ap : nullptr, kp, s->pcols_dev, s->coef_dev,
-                      s->x2, s->ax2, s->p2, s->ap2, s->lam_dev, s->bdiag, s->tmode, s->tinv,
-                      s->tvec, s->pcols_dev + m, kj, s->w_next, even(kj), s->relative_tol,
-                      s->red_dev, st);
+                      kp ? s->p : nullptr, kp ? s->ap : nullptr, kp, nullptr, nullptr,
+                      s->x2, s->ax2, s->p2, s->ap2, nullptr, s->bdiag, s->tmode, s->tinv,
+                      s->tvec, nullptr, kj, s->w_next, even(kj), s->relative_tol,
+                      red_h ? red_h : s->red_dev, st, &hc);
   if (r) return r;
   r = stencil7_gram(s->w_next, s->aw, s->nx, s->ny, s->nz, even(kj), nullptr, 0, 0, s->scale,
-                    s->x2, s->ldx, m, kj, s->g2_dev, st);
+                    s->x2, s->ldx, m, kj, g2_h ? g2_h : s->g2_dev, st);
   if (r) return r;
+  // the next call skips its D2H copies only when both landed on the host
+  if (red_h && !g2_h)
+    B2L_CUDA(cudaMemcpyAsync(s->h_g2, s->g2_dev, (size_t)(m + kj) * kj * sizeof(double),
+                             cudaMemcpyDeviceToHost, st));
+  if (!red_h && g2_h)
+    B2L_CUDA(cudaMemcpyAsync(s->h_red, s->red_dev,
+                             (2 * (size_t)m + (size_t)(2 * m + kj) * (3 * m + kj)) * sizeof(double),
+                             cudaMemcpyDeviceToHost, st));
+  s->red_on_host = (red_h || g2_h) ? 1 : 0;
   mark(5);
   return B2L_ITER_OK;
 }

@@ -133,6 +133,20 @@ __global__ void __launch_bounds__(256)
 
 // ------------------------------------------------------------------ host
 
+// z-chunk length for `tiles` xy tiles on `slots` resident CTAs.  A CTA pays a
+// pipeline fill (two halo planes + the ring latency) per chunk, which
+// measured costlier than a partly idle wave (C2, 128 tiles on 296 slots:
+// chunks of 64 planes 138 us, 26 planes 148 us, 8 planes 161 us,
+// tools/sweep_sgram.py), so: the longest chunks that still give every
+// resident slot at most one CTA (one wave), chunks of >= 4 planes.
+int choose_zchunk(int tiles, int nz, int slots) {
+  int zs = tiles >= slots ? 1 : slots / tiles;
+  if (zs < 1) zs = 1;
+  int c = (nz + zs - 1) / zs;
+  if (c < 4) c = nz < 4 ? nz : 4;
+  return c;
+}
+
 int plan_stencil(int nx, int ny, int nz, int ld, StencilPlan* p) {
   StencilGeom& g = p->g;
   g.nx = nx;
@@ -166,14 +180,8 @@ int plan_stencil(int nx, int ny, int nz, int ld, StencilPlan* p) {
   B2L_CHECK(smem <= 227 * 1024, -B2L_EINVAL,
             "stencil tile does not fit in shared memory (ld too large)");
   p->smem = smem;
-  const int target = 4 * sm_count();
-  int zsplit = (target + tiles - 1) / tiles;
-  int maxsplit = nz / 8;
-  if (maxsplit < 1) maxsplit = 1;
-  if (zsplit > maxsplit) zsplit = maxsplit;
-  if (zsplit < 1) zsplit = 1;
-  g.zchunk = (nz + zsplit - 1) / zsplit;
-  zsplit = (nz + g.zchunk - 1) / g.zchunk;
+  g.zchunk = choose_zchunk(tiles, nz, 2 * sm_count());
+  const int zsplit = (nz + g.zchunk - 1) / g.zchunk;
   p->grid = dim3(tiles, zsplit, 1);
   return 0;
 }

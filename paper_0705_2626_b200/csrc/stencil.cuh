@@ -28,5 +28,6 @@ struct StencilPlan {
 };
 
 int plan_stencil(int nx, int ny, int nz, int ld, StencilPlan* p);
+int choose_zchunk(int tiles, int nz, int slots);
 
 }  // namespace b2l

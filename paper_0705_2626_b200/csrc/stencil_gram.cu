@@ -10,6 +10,8 @@
 // its own Gram accumulators on the fp64 tensor cores (DMMA) -- no hand-off
 // between warps, one CTA barrier per plane (output tiles triple buffered, X
 // boxes double buffered).  A W is never re-read from HBM.
+#include <cstdlib>
+
 #include "gram_tile.cuh"
 #include "stencil.cuh"
 
@@ -29,7 +31,7 @@ struct SGramGeom {
 // warp.  Every per-lane offset is precomputed once, so the plane loop is
 // branch free: the stencil chains of a lane's EPT elements interleave and the
 // Gram loads of all its rows issue ahead of the DMMAs.
-template <int LD, int GPW, int NST>
+template <int LD, int GPW, int NST, int NOB>
 __global__ void __launch_bounds__(256, 2)
     stencil7_gram_kernel(const __grid_constant__ CUtensorMap tin,
                          const __grid_constant__ CUtensorMap thalo,
@@ -48,10 +50,10 @@ __global__ void __launch_bounds__(256, 2)
     return reinterpret_cast<double*>(base + NST * g.stage_stride + i * g.out_stride);
   };
   auto xbuf = [&](int i) -> double* {
-    return reinterpret_cast<double*>(base + NST * g.stage_stride + 3 * g.out_stride +
+    return reinterpret_cast<double*>(base + NST * g.stage_stride + NOB * g.out_stride +
                                      i * G.x_stride);
   };
-  uint64_t* bar = reinterpret_cast<uint64_t*>(base + NST * g.stage_stride + 3 * g.out_stride +
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + NST * g.stage_stride + NOB * g.out_stride +
                                               2 * G.x_stride);
   uint64_t* xbar = bar + NST;
 
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(256, 2)
       mbar_wait(&bar[sn], ((q + 1) / NST) & 1);
       const double* P = stage(q % NST);
       const double* N = stage(sn);
-      double* O = outbuf((z - z0) % 3);
+      double* O = outbuf((z - z0) % NOB);
       // ---- stencil, reference operation order, no FMA contraction
 #pragma unroll
       for (int i = 0; i < EPT; ++i) {
@@ -230,7 +232,7 @@ __global__ void __launch_bounds__(256, 2)
         fence_async_smem();
         tma_store_4d(&tout, O, 0, tx0, ty0, z);
         bulk_commit();
-        bulk_wait_read<2>();   // output slots are triple buffered
+        bulk_wait_read<NOB - 1>();   // NOB output slots
         if (q + NST < nplanes) issue(q + NST);
         if (have_x && z + 2 < z1) issue_x(z + 2);
       }
@@ -288,7 +290,9 @@ template <int LD, int GPW>
 static int launch_sgram_t(const StencilPlan& p, size_t smem, const CUtensorMap& tin,
                           const CUtensorMap& thalo, const CUtensorMap& tout,
                           const CUtensorMap& txm, const SGramGeom& G, cudaStream_t st) {
-  auto kern = stencil7_gram_kernel<LD, GPW, 3>;
+  // a 4-deep plane ring with double-buffered outputs when it fits two CTAs
+  // per SM (more loads in flight), else 3 + 3
+  auto kern = p.nst == 4 ? stencil7_gram_kernel<LD, GPW, 4, 2> : stencil7_gram_kernel<LD, GPW, 3, 3>;
   if (int rc = prepare_kernel(reinterpret_cast<const void*>(kern), smem, 256, nullptr)) return rc;
   kern<<<p.grid, 256, smem, st>>>(tin, thalo, tout, txm, p.g, G);
   B2L_CUDA(cudaGetLastError());
@@ -346,6 +350,12 @@ int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
     const size_t xb = m ? ((((size_t)TX * ty * ldx * 8) + 127) & ~(size_t)127) : 0;
     return 3 * stg + 3 * ob + 2 * xb + 128;
   };
+  auto need4 = [&](int ty) {
+    const size_t stg = (((size_t)(TX + 2) * (ty + 2) * ld * 8) + 127) & ~(size_t)127;
+    const size_t ob = (((size_t)TX * ty * ld * 8) + 127) & ~(size_t)127;
+    const size_t xb = m ? ((((size_t)TX * ty * ldx * 8) + 127) & ~(size_t)127) : 0;
+    return 4 * stg + 2 * ob + 2 * xb + 128;
+  };
   // 8 warps x GPW groups of 8 points per tile; the largest tile that keeps
   // two CTAs resident per SM (<= ~110 KB shared memory) wins
   int gpw = 0, TY = 1;
@@ -376,18 +386,21 @@ int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
   G.x_bytes = m ? (uint32_t)(TX * TY * ldx * 8) : 0u;
   G.x_stride = (G.x_bytes + 127u) & ~127u;
   size_t smem = need(TY);
+  p.nst = 3;
+  if (need4(TY) <= 110 * 1024) {
+    p.nst = 4;
+    smem = need4(TY);
+  }
   const int NI = (2 * ld + 7) / 8, NJ = (ld + 7) / 8;
   const size_t red = (size_t)8 * NI * NJ * 64 * 8;
   if (red > smem) smem = red + 128;
   B2L_CHECK(smem <= 227 * 1024, -B2L_EINVAL, "stencil_gram: tile does not fit");
-  const int target = 4 * sm_count();
-  int zsplit = (target + tiles - 1) / tiles;
-  int maxsplit = nz / 8;
-  if (maxsplit < 1) maxsplit = 1;
-  if (zsplit > maxsplit) zsplit = maxsplit;
-  if (zsplit < 1) zsplit = 1;
-  g.zchunk = (nz + zsplit - 1) / zsplit;
-  zsplit = (nz + g.zchunk - 1) / g.zchunk;
+  g.zchunk = choose_zchunk(tiles, nz, 2 * sm_count());   // two CTAs per SM
+  if (const char* zc = getenv("B2L_SGRAM_ZCHUNK")) {     // tuning override
+    const int v = atoi(zc);
+    if (v >= 1) g.zchunk = v < nz ? v : nz;
+  }
+  const int zsplit = (nz + g.zchunk - 1) / g.zchunk;
   p.grid = dim3(tiles, zsplit, 1);
   g.has_lo = has_lo;
   g.has_hi = has_hi;
