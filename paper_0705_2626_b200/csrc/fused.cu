@@ -595,7 +595,8 @@ __host__ __device__ constexpr bool pair_tile_needed(int m, int ti, int tj) {
   return false;
 }
 
-__host__ __device__ constexpr PairTiles pair_tiles(int NI, int NJ, int mfix, int h, int nh = 2) {
+__host__ __device__ constexpr PairTiles pair_tiles(int NI, int NJ, int mfix, int h, int nh = 2,
+                                                   int first_h0 = -1) {
   PairTiles T{};
   if (mfix == 0 && nh == 1) {
     for (int i = 0; i < NI; ++i)
@@ -623,7 +624,7 @@ __host__ __device__ constexpr PairTiles pair_tiles(int NI, int NJ, int mfix, int
           T.need[t >> 5] |= 1u << (t & 31);
           ++tot;
         }
-    const int first = nh == 1 ? tot : (tot + 1) / 2;
+    const int first = nh == 1 ? tot : (first_h0 >= 0 ? first_h0 : (tot + 1) / 2);
     int k = 0;
     for (int i = 0; i < NI; ++i)
       for (int j = 0; j < NJ; ++j)
@@ -992,6 +993,9 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
   }
 }
 
+#ifndef B2L_TAIL_DFMA   // full-block tail columns on DFMA (0: DMMA, for A/B timing)
+#define B2L_TAIL_DFMA 1
+#endif
 constexpr int PAIR_NW = 14;                        // compute warps (7 pairs, 56-row chunks)
 constexpr int PAIR_THREADS = 32 * (2 + PAIR_NW);   // 512: loader + 14 compute + storer warps
 constexpr int PAIR_BAR = 32 * (1 + PAIR_NW);       // output-buffer barriers: compute + storer
@@ -1068,6 +1072,9 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
   // accumulators (the register allocator never sees the other half's)
   auto run_half = [&](auto hc) {
     constexpr int H = decltype(hc)::value;
+    // even split of the Gram tiles: the pair barrier makes the chunk's path
+    // max(update) + max(Gram), so moving tiles to the lighter half 1 (DFMA
+    // tail update) does not pay (measured: 4/10 and 5/9 splits slower)
     constexpr PairTiles TL = pair_tiles(NI, NJ, MFIX, H);
     const int cw = warp - 1;
     const int mt = cw >> 1;                    // 8-row tile
@@ -1080,6 +1087,11 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const int k = 4 * ks + q;
+      if (FIX && H == 1 && B2L_TAIL_DFMA) {   // tail columns on DFMA: coefficients from smem
+        cW[ks] = cP[ks] = cX[ks] = 0.0;
+        pcol[ks] = 0;
+        continue;
+      }
       pcol[ks] = FIX ? k : (k < kp ? spc[k] : 0);
       const int cb = 8 * H + rl;
       const bool cv = cb < m;
@@ -1159,6 +1171,48 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         const double* AP = st + A.in_off[5];
         const double* X = st + A.in_off[0];
         const double* AX = st + A.in_off[1];
+        // per lane: the two columns co, co+1 of P', AP', X', AX'
+        double pn_[2], apn_[2], xn_[2], axn_[2];
+        const bool bw = kw > 0, bp = kp > 0;
+        if constexpr (FIX && H == 1 && B2L_TAIL_DFMA) {
+          // full block, columns 8..MFIX-1 (2 at MFIX = 10): DFMA instead of a
+          // 75%-empty DMMA column tile.  Lane (row rl, q) forms column
+          // 8 + (q & 1) of the P side (q < 2: W, P, X) or the A side (q >= 2:
+          // AW, AP, AX); the four values of a row are then gathered in its
+          // q = 0 lane, the lane the DMMA layout gives columns 8, 9.
+          static_assert(MFIX == 0 || MFIX == 10, "tail-column update assumes two tail columns");
+          const int c = 8 + (q & 1);
+          const bool aside = q >= 2;
+          const double* D1 = (aside ? AW : W) + r * SF;
+          const double* D2 = (aside ? AP : P) + r * SF;
+          const double* D3 = (aside ? AX : X) + r * SF;
+          const double* cw = coef + MFIX * MFIX + c;
+          const double* cp = coef + 2 * MFIX * MFIX + c;
+          const double* cx = coef + c;
+          double sw_ = 0.0, sp_ = 0.0, sx_ = 0.0;
+#pragma unroll
+          for (int k = 0; k < MFIX; k += 2) {
+            const double2 w2 = *reinterpret_cast<const double2*>(D1 + k);
+            const double2 p2 = *reinterpret_cast<const double2*>(D2 + k);
+            const double2 x2 = *reinterpret_cast<const double2*>(D3 + k);
+            sw_ = fma(w2.x, cw[k * MFIX], sw_);
+            sp_ = fma(p2.x, cp[k * MFIX], sp_);
+            sx_ = fma(x2.x, cx[k * MFIX], sx_);
+            sw_ = fma(w2.y, cw[(k + 1) * MFIX], sw_);
+            sp_ = fma(p2.y, cp[(k + 1) * MFIX], sp_);
+            sx_ = fma(x2.y, cx[(k + 1) * MFIX], sx_);
+          }
+          const double pv = __dadd_rn(sw_, sp_);
+          const double xv = __dadd_rn(sx_, pv);
+          pn_[0] = pv;
+          xn_[0] = xv;
+          pn_[1] = __shfl_down_sync(0xffffffffu, pv, 1);
+          xn_[1] = __shfl_down_sync(0xffffffffu, xv, 1);
+          apn_[0] = __shfl_down_sync(0xffffffffu, pv, 2);
+          axn_[0] = __shfl_down_sync(0xffffffffu, xv, 2);
+          apn_[1] = __shfl_down_sync(0xffffffffu, pv, 3);
+          axn_[1] = __shfl_down_sync(0xffffffffu, xv, 3);
+        } else {
         double acc[6][2];
 #pragma unroll
         for (int c = 0; c < 6; ++c) acc[c][0] = acc[c][1] = 0.0;
@@ -1179,7 +1233,14 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
           dmma_8x8x4(acc[4][0], acc[4][1], xv, cX[ks]);
           dmma_8x8x4(acc[5][0], acc[5][1], axv, cX[ks]);
         }
-        const bool bw = kw > 0, bp = kp > 0;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          pn_[e] = (bw && bp) ? __dadd_rn(acc[0][e], acc[2][e]) : (bw ? acc[0][e] : acc[2][e]);
+          apn_[e] = (bw && bp) ? __dadd_rn(acc[1][e], acc[3][e]) : (bw ? acc[1][e] : acc[3][e]);
+          xn_[e] = __dadd_rn(acc[4][e], pn_[e]);
+          axn_[e] = __dadd_rn(acc[5][e], apn_[e]);
+        }
+        }
         double* O0 = sm + A.out_off[0] + ob;
         double* O1 = sm + A.out_off[1] + ob;
         double* O2 = sm + A.out_off[2] + ob;
@@ -1190,12 +1251,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         const int co = 8 * H + 2 * q;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const double pn = (bw && bp) ? __dadd_rn(acc[0][e], acc[2][e])
-                                       : (bw ? acc[0][e] : acc[2][e]);
-          const double apn = (bw && bp) ? __dadd_rn(acc[1][e], acc[3][e])
-                                        : (bw ? acc[1][e] : acc[3][e]);
-          const double xn = __dadd_rn(acc[4][e], pn);
-          const double axn = __dadd_rn(acc[5][e], apn);
+          const double pn = pn_[e], apn = apn_[e], xn = xn_[e], axn = axn_[e];
           if (co + e < ldx) {
             O0[r * sx + co + e] = xn;
             O1[r * sx + co + e] = axn;
