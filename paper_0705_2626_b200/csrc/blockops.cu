@@ -14,6 +14,8 @@
 //
 // Every reduction is deterministic: CTA partials in a fixed row assignment,
 // then a fixed-order second stage over CTAs.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "gram_tile.cuh"
 
@@ -582,6 +584,259 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs A) {
   }
 }
 
+
+// -------------------------------------------------------------------------
+// K6 for large blocks (16 < m <= 64): the same products on the fp64 tensor
+// cores.  Out (rows x m) = In (rows x K) C (K x m) is a tall-skinny GEMM
+// whose C is tiny and shared by every row: the coefficients sit in shared
+// memory for the whole kernel, row chunks of the six input blocks stream
+// through a TMA double buffer (one producer warp), and compute warp j owns
+// output columns 8j..8j+7 of every chunk (DMMA m8n8k4: A = 8 data rows x 4,
+// B = 4 coefficient rows x 8).  P_J Cp is formed as P Cp^ with Cp^ the m x m
+// scatter of Cp's rows to the pcols positions (zero rows elsewhere), so the
+// column gather needs no data movement.  Shared rows are padded to
+// smem_stride(ld) (TMA out-of-bounds columns read as zero): conflict-free
+// fragment loads.  Reference: lobpcg.py:520-540, multivec.multiply :74-86.
+constexpr int UM_R = 16;                     // rows per chunk (two 8-row tiles)
+constexpr int UM_NW = 8;                     // compute warps = 64 / 8 column tiles
+constexpr int UM_THREADS = 32 * (UM_NW + 1);
+constexpr int UM_NST = 2;
+constexpr int UM_CS = 68;                    // coefficient row stride (smem_stride(64))
+
+struct UmArgs {
+  int nrows, m, kw, kp;
+  int kx4, kw4, kp4;                         // K extents rounded up to 4
+  int sx, sw, sp;                            // shared row strides of X-, W-, P-like blocks
+  int ldo, ldpo;
+  int x_plus_p, has_x, has_ax, has_p_out, has_ap_out;
+  int in_off[6];                             // X AX W AW P AP, doubles within a stage
+  int stage_doubles;
+  uint32_t stage_tx;
+  int coef_off;                              // Cx | Cw | Cp^ (doubles)
+  int bar_off;
+  const double* cx;
+  const double* cw;
+  const double* cp;
+  const int* pcols;
+  double* xo;
+  double* axo;
+  double* po;
+  double* apo;
+};
+struct UmMaps {
+  CUtensorMap in[6];
+};
+
+__global__ void __launch_bounds__(UM_THREADS, 1)
+    update_mma_kernel(const __grid_constant__ UmMaps M, const __grid_constant__ UmArgs A) {
+  extern __shared__ __align__(128) unsigned char um_raw[];
+  double* sm = reinterpret_cast<double*>(um_raw);
+  double* Cx = sm + A.coef_off;
+  double* Cw = Cx + A.kx4 * UM_CS;
+  double* Cp = Cw + A.kw4 * UM_CS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + A.bar_off);
+  uint64_t* empty = full + UM_NST;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = A.m;
+  for (int i = tid; i < A.kx4 * UM_CS; i += blockDim.x) {
+    const int k = i / UM_CS, c = i - k * UM_CS;
+    Cx[i] = (A.has_x && k < m && c < m) ? A.cx[k * m + c] : 0.0;
+  }
+  for (int i = tid; i < A.kw4 * UM_CS; i += blockDim.x) {
+    const int k = i / UM_CS, c = i - k * UM_CS;
+    Cw[i] = (k < A.kw && c < m) ? A.cw[k * m + c] : 0.0;
+  }
+  for (int i = tid; i < A.kp4 * UM_CS; i += blockDim.x) {
+    const int k = i / UM_CS, c = i - k * UM_CS;
+    double v = 0.0;
+    if (c < m)
+      for (int q = 0; q < A.kp; ++q)
+        if (A.pcols[q] == k) v = A.cp[q * m + c];
+    Cp[i] = v;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < UM_NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], UM_NW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int nchunks = (A.nrows + UM_R - 1) / UM_R;
+  const int nloc = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const bool on[6] = {A.has_x != 0, A.has_ax != 0, A.kw > 0, A.kw > 0 && A.has_ax != 0,
+                      A.kp > 0, A.kp > 0 && A.has_ax != 0};
+
+  if (warp == UM_NW) {
+    // ---- producer
+    if (lane == 0)
+      for (int it = 0; it < nloc; ++it) {
+        const int s = it % UM_NST;
+        if (it >= UM_NST) mbar_wait(&empty[s], (it / UM_NST - 1) & 1);
+        double* st = sm + (size_t)s * A.stage_doubles;
+        const int r0 = (blockIdx.x + it * gridDim.x) * UM_R;
+        mbar_expect_tx(&full[s], A.stage_tx);
+        for (int b = 0; b < 6; ++b)
+          if (on[b]) tma_load_2d(st + A.in_off[b], &M.in[b], &full[s], 0, r0);
+      }
+    return;
+  }
+
+  // ---- compute warp: output column tile j = warp
+  const int j = warp;
+  const int ra = lane >> 2, qa = lane & 3;        // A fragment: row, k
+  const int bk = lane & 3, bn = lane >> 2;        // B fragment: k, column
+  const double* cxl = Cx + bk * UM_CS + 8 * j + bn;
+  const double* cwl = Cw + bk * UM_CS + 8 * j + bn;
+  const double* cpl = Cp + bk * UM_CS + 8 * j + bn;
+  const int col = 8 * j + 2 * qa;                 // accumulator columns col, col + 1
+  const bool have_pw = A.kw > 0 || A.kp > 0;
+  for (int it = 0; it < nloc; ++it) {
+    const int s = it % UM_NST;
+    mbar_wait(&full[s], (it / UM_NST) & 1);
+    const double* st = sm + (size_t)s * A.stage_doubles;
+    const double* X = st + A.in_off[0] + ra * A.sx + qa;
+    const double* AX = st + A.in_off[1] + ra * A.sx + qa;
+    const double* W = st + A.in_off[2] + ra * A.sw + qa;
+    const double* AW = st + A.in_off[3] + ra * A.sw + qa;
+    const double* P = st + A.in_off[4] + ra * A.sp + qa;
+    const double* AP = st + A.in_off[5] + ra * A.sp + qa;
+    double pacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, apacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    double xacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, axacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    const bool hax = A.has_ax != 0;
+    for (int k = 0; k < A.kw4; k += 4) {
+      const double b = cwl[k * UM_CS];
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt) {
+        dmma_8x8x4(pacc[rt][0], pacc[rt][1], W[8 * rt * A.sw + k], b);
+        if (hax) dmma_8x8x4(apacc[rt][0], apacc[rt][1], AW[8 * rt * A.sw + k], b);
+      }
+    }
+    for (int k = 0; k < A.kp4 && A.kp > 0; k += 4) {
+      const double b = cpl[k * UM_CS];
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt) {
+        dmma_8x8x4(pacc[rt][0], pacc[rt][1], P[8 * rt * A.sp + k], b);
+        if (hax) dmma_8x8x4(apacc[rt][0], apacc[rt][1], AP[8 * rt * A.sp + k], b);
+      }
+    }
+    if (A.has_x)
+      for (int k = 0; k < A.kx4; k += 4) {
+        const double b = cxl[k * UM_CS];
+#pragma unroll
+        for (int rt = 0; rt < 2; ++rt) {
+          dmma_8x8x4(xacc[rt][0], xacc[rt][1], X[8 * rt * A.sx + k], b);
+          if (hax) dmma_8x8x4(axacc[rt][0], axacc[rt][1], AX[8 * rt * A.sx + k], b);
+        }
+      }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cta(&empty[s]);
+    const int r0 = (blockIdx.x + it * gridDim.x) * UM_R;
+#pragma unroll
+    for (int rt = 0; rt < 2; ++rt) {
+      const int row = r0 + 8 * rt + ra;
+      if (row >= A.nrows) continue;
+      double xv[2], av[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        xv[e] = !A.has_x ? pacc[rt][e]
+                         : (A.x_plus_p && have_pw ? __dadd_rn(xacc[rt][e], pacc[rt][e])
+                                                  : xacc[rt][e]);
+        av[e] = A.x_plus_p && have_pw ? __dadd_rn(axacc[rt][e], apacc[rt][e]) : axacc[rt][e];
+      }
+      if (col < A.ldo) {
+        *reinterpret_cast<double2*>(A.xo + (size_t)row * A.ldo + col) = make_double2(xv[0], xv[1]);
+        if (hax && A.axo)
+          *reinterpret_cast<double2*>(A.axo + (size_t)row * A.ldo + col) =
+              make_double2(av[0], av[1]);
+      }
+      if (col < A.ldpo) {
+        if (A.has_p_out)
+          *reinterpret_cast<double2*>(A.po + (size_t)row * A.ldpo + col) =
+              make_double2(pacc[rt][0], pacc[rt][1]);
+        if (A.has_ap_out)
+          *reinterpret_cast<double2*>(A.apo + (size_t)row * A.ldpo + col) =
+              make_double2(apacc[rt][0], apacc[rt][1]);
+      }
+    }
+  }
+}
+
+static int update_mma(int nrows, int m, const double* x, const double* ax, int ldx,
+                      const double* cx, const double* w, const double* aw, int ldw, int kw,
+                      const double* cw, const double* p, const double* ap, int ldp,
+                      const int* pcols, int kp, const double* cp, double* xo, double* axo,
+                      int ldo, double* po, double* apo, int ldpo, int x_plus_p,
+                      cudaStream_t st) {
+  UmArgs A{};
+  A.nrows = nrows;
+  A.m = m;
+  A.kw = kw;
+  A.kp = kp;
+  auto r4 = [](int v) { return (v + 3) & ~3; };
+  A.kx4 = r4(m);
+  A.kw4 = r4(kw);
+  A.kp4 = kp ? r4(m) : 0;
+  A.sx = smem_stride(ldx > 0 ? ldx : 2);
+  A.sw = smem_stride(kw ? ldw : 2);
+  A.sp = smem_stride(kp ? ldp : 2);
+  A.ldo = ldo;
+  A.ldpo = ldpo;
+  A.x_plus_p = x_plus_p;
+  A.has_x = x != nullptr;
+  A.has_ax = ax != nullptr;
+  A.has_p_out = po != nullptr;
+  A.has_ap_out = apo != nullptr && ax != nullptr;
+  A.cx = cx;
+  A.cw = cw;
+  A.cp = cp;
+  A.pcols = pcols;
+  A.xo = xo;
+  A.axo = axo;
+  A.po = po;
+  A.apo = apo;
+  const int sin_[6] = {A.sx, A.sx, A.sw, A.sw, A.sp, A.sp};
+  const bool on[6] = {x != nullptr, ax != nullptr, kw > 0, kw > 0 && ax != nullptr, kp > 0,
+                      kp > 0 && ax != nullptr};
+  int off = 0;
+  A.stage_tx = 0;
+  for (int b = 0; b < 6; ++b) {
+    A.in_off[b] = off;
+    if (on[b]) {
+      off += ((UM_R * sin_[b]) + 15) & ~15;
+      A.stage_tx += (uint32_t)(UM_R * sin_[b] * 8);
+    }
+  }
+  A.stage_doubles = off;
+  off *= UM_NST;
+  A.coef_off = off;
+  off += (A.kx4 + A.kw4 + A.kp4) * UM_CS;
+  off = (off + 15) & ~15;
+  A.bar_off = off;
+  off += 2 * UM_NST;
+  const size_t smem = (size_t)off * 8 + 64;
+  B2L_CHECK(smem <= 227 * 1024, -B2L_EINVAL, "update: block too large for the MMA kernel");
+  UmMaps M;
+  const double* ins[6] = {x, ax, w, aw, p, ap};
+  const int lds[6] = {ldx, ldx, ldw, ldw, ldp, ldp};
+  for (int b = 0; b < 6; ++b) {
+    if (!on[b]) {
+      M.in[b] = M.in[0];
+      continue;
+    }
+    if (int rc = encode_tmap_2d(&M.in[b], ins[b], lds[b], nrows, sin_[b], UM_R)) return rc;
+  }
+  if (int rc = prepare_kernel(reinterpret_cast<const void*>(update_mma_kernel), smem, UM_THREADS,
+                              nullptr))
+    return rc;
+  const int nchunks = (nrows + UM_R - 1) / UM_R;
+  int grid = sm_count();
+  if (grid > nchunks) grid = nchunks;
+  update_mma_kernel<<<grid, UM_THREADS, smem, st>>>(M, A);
+  B2L_CUDA(cudaGetLastError());
+  return 0;
+}
+
 int update(int nrows, int m, const double* x, const double* ax, int ldx,
            const double* cx, const double* w, const double* aw, int ldw, int kw,
            const double* cw, const double* p, const double* ap, int ldp,
@@ -596,6 +851,16 @@ int update(int nrows, int m, const double* x, const double* ax, int ldx,
   B2L_CHECK(x || (!ax && kw + kp > 0), -B2L_EINVAL,
             "update: without x, only X' = W Cw + P Cp (no A side) is defined");
   B2L_CHECK(!x || cx, -B2L_EINVAL, "update: x without cx");
+  // 16 < m <= 64 with TMA-compatible (even) leading dimensions: fp64 tensor cores
+  static const bool scalar_only = [] {
+    const char* v = getenv("B2L_UPDATE_SCALAR");
+    return v && v[0] == '1';
+  }();
+  if (!scalar_only && m > 16 && m <= 64 && (!x || (ldx % 2) == 0) && (kw == 0 || (ldw % 2) == 0) &&
+      (kp == 0 || (ldp % 2) == 0) && (ldo % 2) == 0 && (!po || (ldpo % 2) == 0) &&
+      (x || !ax))
+    return update_mma(nrows, m, x, ax, ldx, cx, w, aw, ldw, kw, cw, p, ap, ldp, pcols, kp, cp, xo,
+                      axo, ldo, po, apo, ldpo, x_plus_p, st);
   UpdArgs A{};
   A.nrows = nrows;
   A.m = m;

@@ -177,7 +177,9 @@ def test_residual_kernel(dev, m, tmode, useb):
         assert np.all(got[:, kw] == 0.0)
 
 
-@pytest.mark.parametrize("m,kw,kp", [(10, 10, 10), (10, 7, 7), (4, 3, 0), (16, 16, 9), (64, 40, 40)])
+@pytest.mark.parametrize("m,kw,kp", [(10, 10, 10), (10, 7, 7), (4, 3, 0), (16, 16, 9), (64, 40, 40),
+                                    (64, 64, 64), (64, 63, 0), (24, 24, 24), (33, 20, 11),
+                                    (17, 5, 17)])
 def test_update_kernel(dev, m, kw, kp):
     from paper_0705_2626_b200 import device as dv
 
@@ -306,3 +308,26 @@ def test_seeded_fill_bitwise(dev, n, m, ld, seed, row0):
     got = out.cpu().numpy()
     assert np.array_equal(got[:, :m], ref)
     assert np.all(got[:, m:] == 0.0)
+
+
+@pytest.mark.parametrize("m", [10, 40, 64])
+def test_update_rotation_only(dev, m):
+    """X' = X M without W / P terms, with and without the A side (the
+    initial-block and drift-repair rotations, lobpcg.py:280-296, :398)."""
+    from paper_0705_2626_b200 import device as dv
+
+    n = 10007
+    r = rng(7 * m)
+    X, AX = r.standard_normal((n, m)), r.standard_normal((n, m))
+    M = r.standard_normal((m, m))
+    tX, tAX = blk(X, dev), blk(AX, dev)
+    c = torch.from_numpy(M).to(dev)
+    for with_ax in (True, False):
+        xo = torch.full_like(tX, np.nan)
+        axo = torch.full_like(tX, np.nan) if with_ax else None
+        dv.update(n, m, tX, tAX if with_ax else None, c, xo, axo)
+        np.testing.assert_allclose(xo.cpu().numpy()[:, :m], X @ M, rtol=1e-12,
+                                   atol=1e-12 * np.abs(X @ M).max())
+        if with_ax:
+            np.testing.assert_allclose(axo.cpu().numpy()[:, :m], AX @ M, rtol=1e-12,
+                                       atol=1e-12 * np.abs(AX @ M).max())
