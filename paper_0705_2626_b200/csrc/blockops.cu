@@ -207,6 +207,231 @@ struct HostBlock {
   int ld, cols;
 };
 
+
+// -------------------------------------------------------------------------
+// K5 for large Grams (the m = 64 pencil of C5: [X W P]^T [BX BW BP AP] is
+// 24 x 32 tiles of 8x8, ~490 needed): every warp owns a 4x4 block of needed
+// tiles (16 DMMA per 8 fragment loads, accumulators in registers for the
+// whole pass), the needed tile blocks are split over gridDim.y CTA groups,
+// row chunks of every block stream through a TMA ring (2-D tile loads with
+// padded shared rows -> conflict-free fragment loads) filled by one producer
+// warp with full / empty mbarriers, no CTA-wide barrier in the loop.  CTAs
+// of one row range but different tile groups run side by side, so the
+// re-reads of a chunk hit L2.  Deterministic like K5: per-CTA partials,
+// fixed-order second stage.
+constexpr int GB_TI = 4, GB_TJ = 4, GB_MAXW = 12, GB_MAXBLK = 64;
+
+struct GbArgs {
+  int nrows, rc, nst;
+  int nu;
+  int ubase[GRAM_MAXU];        // stage offsets (doubles)
+  int ustr[GRAM_MAXU];         // shared row strides
+  int a, b, nl, nr;
+  int lu[GRAM_MAXL], lcum[GRAM_MAXL + 1];
+  int ru[GRAM_MAXR], rcum[GRAM_MAXR + 1];
+  unsigned rw_mask;
+  const double* d;
+  int dbase;
+  int stage_doubles;
+  uint32_t stage_tx;
+  int wpc, nblk, nzero;
+  unsigned short blk[GB_MAXBLK];     // (ti0 << 8) | tj0 of needed 4x4 tile blocks
+  unsigned short bmask[GB_MAXBLK];   // needed tiles inside the block, bit i*4+j
+  unsigned short zblk[GB_MAXBLK];    // tile blocks nobody computes (zeroed)
+  double* partial;                   // [gridDim.x][a*b]
+};
+struct GbMaps {
+  CUtensorMap u[GRAM_MAXU];
+};
+
+__global__ void __launch_bounds__(32 * (GB_MAXW + 1), 1)
+    gram_big_kernel(const __grid_constant__ GbMaps M, const __grid_constant__ GbArgs A) {
+  extern __shared__ __align__(128) unsigned char gb_raw[];
+  double* stages = reinterpret_cast<double*>(gb_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(gb_raw + (size_t)A.nst * A.stage_doubles * 8);
+  uint64_t* empty = full + 4;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < A.nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], A.wpc);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int nchunks = (A.nrows + A.rc - 1) / A.rc;
+  const int nloc = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  double* out = A.partial + (size_t)blockIdx.x * A.a * A.b;
+
+  if (warp == A.wpc) {
+    // ---- producer
+    if (lane == 0)
+      for (int it = 0; it < nloc; ++it) {
+        const int s = it % A.nst;
+        if (it >= A.nst) mbar_wait(&empty[s], (it / A.nst - 1) & 1);
+        double* st = stages + (size_t)s * A.stage_doubles;
+        const int r0 = (blockIdx.x + it * gridDim.x) * A.rc;
+        const int nvalid = min(A.rc, A.nrows - r0);
+        uint32_t tx = A.stage_tx;
+        bool dbulk = false;
+        if (A.d) {
+          dbulk = (nvalid % 2) == 0;
+          if (dbulk) tx += (uint32_t)nvalid * 8u;
+          else
+            for (int e = 0; e < nvalid; ++e) st[A.dbase + e] = A.d[r0 + e];
+          for (int e = nvalid; e < A.rc; ++e) st[A.dbase + e] = 0.0;
+          fence_async_smem();
+        }
+        mbar_expect_tx(&full[s], tx);
+        for (int u = 0; u < A.nu; ++u) tma_load_2d(st + A.ubase[u], &M.u[u], &full[s], 0, r0);
+        if (dbulk) bulk_load(st + A.dbase, A.d + r0, (uint32_t)nvalid * 8u, &full[s]);
+      }
+  } else if (warp < A.wpc) {
+    const int bi = blockIdx.y * A.wpc + warp;
+    const bool act = bi < A.nblk;
+    const int ti0 = act ? (A.blk[bi] >> 8) : 0, tj0 = act ? (A.blk[bi] & 255) : 0;
+    const unsigned mask = act ? A.bmask[bi] : 0u;
+    LaneCol la[GB_TI], lb[GB_TJ];
+#pragma unroll
+    for (int i = 0; i < GB_TI; ++i) {
+      const int ci = 8 * (ti0 + i) + (lane >> 2);
+      la[i] = LaneCol{0, 0, false, false};
+      if (act && ci < A.a) {
+        int l = 0;
+        while (l + 1 < A.nl && A.lcum[l + 1] <= ci) ++l;
+        la[i] = LaneCol{A.ubase[A.lu[l]] + (ci - A.lcum[l]), A.ustr[A.lu[l]], true, false};
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < GB_TJ; ++j) {
+      const int cj = 8 * (tj0 + j) + (lane >> 2);
+      lb[j] = LaneCol{0, 0, false, false};
+      if (act && cj < A.b) {
+        int r = 0;
+        while (r + 1 < A.nr && A.rcum[r + 1] <= cj) ++r;
+        lb[j] = LaneCol{A.ubase[A.ru[r]] + (cj - A.rcum[r]), A.ustr[A.ru[r]], true,
+                        ((A.rw_mask >> r) & 1u) != 0};
+      }
+    }
+    WarpGram<GB_TI, GB_TJ> g;
+    g.zero();
+    for (int it = 0; it < nloc; ++it) {
+      const int s = it % A.nst;
+      mbar_wait(&full[s], (it / A.nst) & 1);
+      const double* st = stages + (size_t)s * A.stage_doubles;
+      if (mask) g.run(st, la, lb, A.d ? st + A.dbase : nullptr, 0, A.rc, mask, DenseRows());
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&empty[s]);
+    }
+    if (act) {
+#pragma unroll
+      for (int i = 0; i < GB_TI; ++i)
+#pragma unroll
+        for (int j = 0; j < GB_TJ; ++j) {
+          const int row = 8 * (ti0 + i) + (lane >> 2);
+          const int col = 8 * (tj0 + j) + 2 * (lane & 3);
+          if (row < A.a) {
+            if (col < A.b) out[(size_t)row * A.b + col] = g.acc[i][j][0];
+            if (col + 1 < A.b) out[(size_t)row * A.b + col + 1] = g.acc[i][j][1];
+          }
+        }
+    }
+  }
+  // tile blocks nobody computes: defined zeros (group 0 of every row range)
+  if (blockIdx.y == 0)
+    for (int e = tid; e < A.nzero * 256; e += blockDim.x) {
+      const int zb = e >> 8, t = e & 255;
+      const int row = 8 * (A.zblk[zb] >> 8) + (t >> 4);
+      const int col = 8 * (A.zblk[zb] & 255) + (t & 15) * 2;
+      for (int c = col; c < col + 2; ++c)
+        if (row < A.a && c < A.b) out[(size_t)row * A.b + c] = 0.0;
+    }
+}
+
+// The large-Gram path of gram(): returns 1 when the shapes do not qualify.
+static int gram_big(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr,
+                    unsigned rw_mask, const double* d, const GramArgs& G, double* out,
+                    cudaStream_t st) {
+  GbArgs A{};
+  A.nrows = nrows;
+  A.nu = G.nu;
+  A.a = G.a;
+  A.b = G.b;
+  A.nl = nl;
+  A.nr = nr;
+  for (int l = 0; l < nl; ++l) A.lu[l] = G.lu[l];
+  for (int l = 0; l <= nl; ++l) A.lcum[l] = G.lcum[l];
+  for (int r = 0; r < nr; ++r) A.ru[r] = G.ru[r];
+  for (int r = 0; r <= nr; ++r) A.rcum[r] = G.rcum[r];
+  A.rw_mask = rw_mask;
+  A.d = rw_mask ? d : nullptr;
+  // needed 4x4 tile blocks
+  const int bI = (G.NI + GB_TI - 1) / GB_TI, bJ = (G.NJ + GB_TJ - 1) / GB_TJ;
+  for (int bi = 0; bi < bI; ++bi)
+    for (int bj = 0; bj < bJ; ++bj) {
+      unsigned msk = 0;
+      for (int i = 0; i < GB_TI; ++i)
+        for (int j = 0; j < GB_TJ; ++j) {
+          const int ti = GB_TI * bi + i, tj = GB_TJ * bj + j;
+          if (ti < G.NI && tj < G.NJ) {
+            const int t = ti * G.NJ + tj;
+            if ((G.tmask[t >> 5] >> (t & 31)) & 1u) msk |= 1u << (i * GB_TJ + j);
+          }
+        }
+      const unsigned short code = (unsigned short)(((GB_TI * bi) << 8) | (GB_TJ * bj));
+      if (msk) {
+        if (A.nblk >= GB_MAXBLK) return 1;
+        A.blk[A.nblk] = code;
+        A.bmask[A.nblk++] = (unsigned short)msk;
+      } else {
+        if (A.nzero >= GB_MAXBLK) return 1;
+        A.zblk[A.nzero++] = code;
+      }
+    }
+  const int gy = (A.nblk + GB_MAXW - 1) / GB_MAXW;
+  A.wpc = (A.nblk + gy - 1) / gy;
+  // stage: padded rows of every distinct block (+ the weights)
+  int width = 0;
+  for (int u = 0; u < A.nu; ++u) {
+    A.ustr[u] = smem_stride(G.uld[u]);
+    width += A.ustr[u];
+  }
+  A.rc = 64;
+  while (A.rc > 8 && (size_t)A.rc * (width + 1) * 8 * 3 > 200 * 1024) A.rc >>= 1;
+  int off = 0;
+  A.stage_tx = 0;
+  for (int u = 0; u < A.nu; ++u) {
+    A.ubase[u] = off;
+    off += (A.rc * A.ustr[u] + 15) & ~15;
+    A.stage_tx += (uint32_t)(A.rc * A.ustr[u] * 8);
+  }
+  A.dbase = off;
+  off += A.d ? ((A.rc + 15) & ~15) : 0;
+  A.stage_doubles = off;
+  A.nst = (size_t)off * 8 * 3 <= 200 * 1024 ? 3 : 2;
+  const size_t smem = (size_t)A.nst * off * 8 + 128;
+  if (smem > 227 * 1024) return 1;
+  GbMaps Mp;
+  for (int u = 0; u < A.nu; ++u)
+    if (int rc = encode_tmap_2d(&Mp.u[u], G.up[u], G.uld[u], nrows, A.ustr[u], A.rc)) return rc;
+  const int threads = 32 * (A.wpc + 1);
+  int per_sm = 1;
+  if (int rc = prepare_kernel(reinterpret_cast<const void*>(gram_big_kernel), smem, threads,
+                              &per_sm))
+    return rc;
+  const int nchunks = (nrows + A.rc - 1) / A.rc;
+  int gx = (sm_count() * per_sm) / gy;
+  if (gx > nchunks) gx = nchunks;
+  if (gx < 1) gx = 1;
+  int werr = 0;
+  double* part = static_cast<double*>(workspace((size_t)gx * A.a * A.b * sizeof(double), &werr));
+  if (werr) return werr;
+  A.partial = part;
+  gram_big_kernel<<<dim3(gx, gy), threads, smem, st>>>(Mp, A);
+  B2L_CUDA(cudaGetLastError());
+  return sum_parts(part, gx, A.a * A.b, out, st);
+}
+
 // pair_mode[l*nr + r]: 0 = block pair not needed, 1 = full, 2 = upper
 // triangle only (a symmetric diagonal pair).  nullptr = all full.
 int gram(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr,
@@ -282,6 +507,20 @@ int gram(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr,
         A.tmask[t >> 5] |= 1u << (t & 31);
       }
     }
+  // large Grams (> 96 needed 8x8 tiles, e.g. the m = 64 pencil): 4x4 tile
+  // blocks per warp, TMA ring, producer warp (gram_big)
+  {
+    int need = 0;
+    for (int t = 0; t < A.NI * A.NJ; ++t) need += (A.tmask[t >> 5] >> (t & 31)) & 1u;
+    static const bool small_only = [] {
+      const char* v = getenv("B2L_GRAM_SMALL");
+      return v && v[0] == '1';
+    }();
+    if (need > 96 && nrows > 0 && !small_only) {
+      const int rc = gram_big(nrows, L, nl, R, nr, rw_mask, d, A, out, st);
+      if (rc != 1) return rc;
+    }
+  }
   A.tsI = (A.NI + GT_TI - 1) / GT_TI;
   A.tsJ = (A.NJ + GT_TJ - 1) / GT_TJ;
   const int TS = A.tsI * A.tsJ;

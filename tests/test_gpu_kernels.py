@@ -96,7 +96,9 @@ def test_stencil_halo_planes(dev):
 
 
 @pytest.mark.parametrize("n,cols", [(1000, (4, 4, 4)), (65537, (10, 9, 10)), (3, (2, 1, 2)),
-                                    (200000, (16, 16, 16)), (5000, (64, 13, 64))])
+                                    (200000, (16, 16, 16)), (5000, (64, 13, 64)),
+                                    (30011, (64, 64, 64)), (7, (64, 64, 64)),
+                                    (100003, (48, 33, 48))])
 def test_gram_multiblock(dev, n, cols):
     from paper_0705_2626_b200 import device as dv
 
