@@ -43,10 +43,19 @@
 
 namespace b2l {
 
-constexpr int STEP_NU = 8;                                  // update warps
-constexpr int STEP_NG = 3;                                  // Gram warps
+#ifndef B2L_STEP_NU
+#define B2L_STEP_NU 4
+#endif
+#ifndef B2L_STEP_NG
+#define B2L_STEP_NG 6
+#endif
+// 4 update + 6 Gram warps: at m = 16 the Gram (~40 needed 8x8 tiles, 80
+// DMMA per 8 rows) outweighs the update (48 DMMA per 8 rows); 8 + 3 left the
+// Gram warps 4x more loaded (C3 step 10.2 -> 8.7 ms; 6 + 5, 5 + 6 slower)
+constexpr int STEP_NU = B2L_STEP_NU;                        // update warps
+constexpr int STEP_NG = B2L_STEP_NG;                        // Gram warps
 constexpr int STEP_GI = 2;                                  // Gram items per Gram warp
-constexpr int STEP_THREADS = 32 * (1 + STEP_NU + STEP_NG);  // 416
+constexpr int STEP_THREADS = 32 * (1 + STEP_NU + STEP_NG);  // 352
 constexpr int NB_OFULL = 1;                                 // named barriers 1,2
 constexpr int NB_OEMPTY = 3;                                // named barriers 3,4
 
