@@ -227,12 +227,16 @@ __global__ void __launch_bounds__(256, 2)
                   if (t == sa) dmma_8x8x4(gacc[t][i][j][0], gacc[t][i][j][1], av[i], bv[j]);
               }
         }
+      // The next plane writes output slot (z + 1) % NOB, last stored for
+      // plane z + 1 - NOB: its TMA store must have read the slot before the
+      // barrier releases the writers (a wait after the barrier would let the
+      // other threads overwrite it while thread 0 still waits).
+      if (tid == 0) bulk_wait_read<NOB - 2>();
       __syncthreads();
       if (tid == 0) {
         fence_async_smem();
         tma_store_4d(&tout, O, 0, tx0, ty0, z);
         bulk_commit();
-        bulk_wait_read<NOB - 1>();   // NOB output slots
         if (q + NST < nplanes) issue(q + NST);
         if (have_x && z + 2 < z1) issue_x(z + 2);
       }
