@@ -304,6 +304,10 @@ int b2l_iter_state_size(void);
  */
 int b2l_iter_profile(double* out, int reset);
 
+/* Number of kernels this library has launched in the process (all entry
+ * points, including the ones b2l_fast_iteration queues). */
+long long b2l_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

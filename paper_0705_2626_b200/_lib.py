@@ -103,6 +103,7 @@ SIGNATURES = {
     "b2l_fast_iteration": (C.c_int, [C.POINTER(b2l_iter_state)]),
     "b2l_iter_state_size": (C.c_int, []),
     "b2l_iter_profile": (C.c_int, [C.POINTER(C.c_double), C.c_int]),
+    "b2l_launch_count": (C.c_longlong, []),
     "b2l_set_lapack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "b2l_rayleigh_ritz": (C.c_int, [C.c_int, C.c_int, C.c_int, c_dp, C.c_int, c_dp, c_dp,
                                     c_ip, C.c_int, c_ip, C.c_double, c_dp, c_dp, c_ip, c_ip,

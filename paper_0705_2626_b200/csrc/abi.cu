@@ -1,5 +1,6 @@
 // C ABI of libb200lobpcg.so -- see include/b200lobpcg.h for the contract and
 // the reference interface each entry point replaces.
+#include <atomic>
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -57,6 +58,9 @@ struct DevWs {
 };
 static DevWs g_ws[64];
 static int g_sms[64];
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void* workspace(size_t bytes, int* err) {
   int dev = 0;
@@ -245,6 +249,8 @@ int encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t r
 using namespace b2l;
 
 extern "C" {
+
+long long b2l_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char* b2l_last_error(void) { return g_err.c_str(); }
 

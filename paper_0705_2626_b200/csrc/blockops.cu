@@ -428,6 +428,7 @@ static int gram_big(int nrows, const HostBlock* L, int nl, const HostBlock* R, i
   if (werr) return werr;
   A.partial = part;
   gram_big_kernel<<<dim3(gx, gy), threads, smem, st>>>(Mp, A);
+  count_launch();
   B2L_CUDA(cudaGetLastError());
   return sum_parts(part, gx, A.a * A.b, out, st);
 }
@@ -576,6 +577,7 @@ int gram(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr,
   B2L_CUDA(cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   gram_kernel<<<dim3(gx, gy), GRAM_THREADS, smem, st>>>(A);
+  count_launch();
   B2L_CUDA(cudaGetLastError());
   const int tot = A.a * A.b;
   return sum_parts(part, gx, tot, out, st);
@@ -679,6 +681,7 @@ __global__ void __launch_bounds__(1024) sum_parts_kernel(const double* partial, 
 int sum_parts(const double* partial, int nparts, int len, double* out, cudaStream_t st) {
   if (len <= 0) return 0;
   sum_parts_kernel<<<(len + 31) / 32, dim3(32, 32), 0, st>>>(partial, nparts, len, out);
+  count_launch();
   B2L_CUDA(cudaGetLastError());
   return 0;
 }
@@ -717,6 +720,7 @@ int residual(int nrows, int m, const double* x, const double* ax, int ldx,
   A.partial = part;
   const size_t smem = (size_t)2 * A.rp * m * sizeof(double);
   resid_kernel<<<blocks, 256, smem, st>>>(A);
+  count_launch();
   B2L_CUDA(cudaGetLastError());
   return sum_parts(part, blocks, 2 * m, sums_out, st);
 }
@@ -1072,6 +1076,7 @@ static int update_mma(int nrows, int m, const double* x, const double* ax, int l
   int grid = sm_count();
   if (grid > nchunks) grid = nchunks;
   update_mma_kernel<<<grid, UM_THREADS, smem, st>>>(M, A);
+  count_launch();
   B2L_CUDA(cudaGetLastError());
   return 0;
 }
@@ -1135,6 +1140,7 @@ int update(int nrows, int m, const double* x, const double* ax, int ldx,
   B2L_CUDA(cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   update_kernel<<<blocks, 256, smem, st>>>(A);
+  count_launch();
   B2L_CUDA(cudaGetLastError());
   return 0;
 }

@@ -52,6 +52,8 @@ int sm_count();
 // (kernel, smem, threads): both are host API round trips on every launch
 // otherwise.  per_sm may be null.
 int prepare_kernel(const void* kern, size_t smem, int threads, int* per_sm);
+// every kernel launch of the library is counted (b2l_launch_count)
+void count_launch();
 // Host-side Rayleigh-Ritz output handed to the F1 launch by value (no H2D copy)
 struct StepHostCoef {
   const double* coef;   // [Cx m*m | Cw kw*m | Cp kp*m]

@@ -1670,6 +1670,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   if (werr) return werr;
   A.partial = part;
   kern<<<gx, threads, smem, st>>>(M, A, cf);
+  count_launch();
   B2L_CUDA(cudaGetLastError());
   return sum_parts(part, gx, len, red_out, st);
 }

@@ -160,6 +160,7 @@ int pcg_launch(int phase, PcgArgs& A, cudaStream_t st, double* sums_out) {
   const size_t smem = (size_t)2 * A.rp * A.k * sizeof(double);
   if (phase == 2) {
     pcg_direction_kernel<<<blocks, 256, 0, st>>>(A);
+    count_launch();
     B2L_CUDA(cudaGetLastError());
     return 0;
   }
@@ -168,9 +169,9 @@ int pcg_launch(int phase, PcgArgs& A, cudaStream_t st, double* sums_out) {
       static_cast<double*>(workspace((size_t)blocks * 2 * A.k * sizeof(double), &werr));
   if (werr) return werr;
   A.partial = part;
-  if (phase == 0) pcg_init_kernel<<<blocks, 256, smem, st>>>(A);
-  else if (phase == 1) pcg_update_kernel<<<blocks, 256, smem, st>>>(A);
-  else pcg_dot_kernel<<<blocks, 256, smem, st>>>(A);
+  if (phase == 0) { pcg_init_kernel<<<blocks, 256, smem, st>>>(A); count_launch(); }
+  else if (phase == 1) { pcg_update_kernel<<<blocks, 256, smem, st>>>(A); count_launch(); }
+  else { pcg_dot_kernel<<<blocks, 256, smem, st>>>(A); count_launch(); }
   B2L_CUDA(cudaGetLastError());
   return sum_parts(part, blocks, 2 * A.k, sums_out, st);
 }

@@ -109,6 +109,7 @@ extern "C" int b2l_seeded_fill(double* out, int ld, long long nrows, int m, long
   const long long nw = (total + per_warp - 1) / per_warp;
   const long long blocks = (nw + 7) / 8;
   seeded_fill_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(A);
+  count_launch();
   B2L_CUDA(cudaGetLastError());
   return 0;
 }

@@ -64,13 +64,17 @@ struct LapackError {
 };
 
 Mat matmul(const Mat& x, const Mat& y) {
+  // column-major j-k-i order: the inner loop runs down contiguous columns of
+  // z and x (vectorisable, cache-friendly at the 192 x 192 sizes of m = 64)
   Mat z(x.r, y.c);
-  for (int j = 0; j < y.c; ++j)
-    for (int i = 0; i < x.r; ++i) {
-      double s = 0.0;
-      for (int k = 0; k < x.c; ++k) s += x(i, k) * y(k, j);
-      z(i, j) = s;
+  for (int j = 0; j < y.c; ++j) {
+    double* zc = z.p() + (size_t)j * z.r;
+    for (int k = 0; k < x.c; ++k) {
+      const double ykj = y(k, j);
+      const double* xc = x.a.data() + (size_t)k * x.r;
+      for (int i = 0; i < x.r; ++i) zc[i] += xc[i] * ykj;
     }
+  }
   return z;
 }
 
@@ -85,12 +89,18 @@ Mat transpose(const Mat& x) {
 // call overheads dominate LAPACK here, and dsyevr on 30 x 30 costs ~2x the
 // native tridiagonal QL).  B2L_RR_LAPACK=1 routes it through the registered
 // LAPACK routines instead (same factorisations, LAPACK rounding).
+// B2L_RR_LAPACK=1: always LAPACK; =0: never; unset: LAPACK for pencils
+// larger than 64 (m > 21; the blocked, vectorised routines win there: 192 x
+// 192 at m = 64 ~2x faster than the native scalar code), native below.
+int g_rr_dim = 0;   // dimension of the pencil being solved (set per call)
 bool use_lapack() {
-  static const bool on = [] {
+  static const int mode = [] {
     const char* v = getenv("B2L_RR_LAPACK");
-    return v && v[0] == '1';
+    return v ? (v[0] == '1' ? 1 : 0) : -1;
   }();
-  return on && g_potrf != nullptr;
+  if (g_potrf == nullptr) return false;
+  if (mode >= 0) return mode == 1;
+  return g_rr_dim > 64;
 }
 
 // Symmetric eigensolver (tred2 / tql2 scheme) for the `want` smallest pairs:
@@ -497,6 +507,7 @@ extern "C" int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, i
                                  int* fallbacks_out) {
   if (m < 1 || kst < 0 || kj < 1 || kj > kst || kj > m || !g1 || !g2 || !lam || !jact || !sel)
     return fail(-B2L_EINVAL, "rayleigh_ritz: bad arguments");
+  g_rr_dim = m + kst + (have_p ? kj : 0);
   const int rW = m, rP = m + kst;
   const int cW = m, cP = m + kst, cAP = 2 * m + kst;
   auto G1 = [&](int i, int j) { return g1[(size_t)i * ldg1 + j]; };

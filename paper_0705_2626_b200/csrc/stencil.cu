@@ -194,6 +194,7 @@ static int launch_stencil_t(const StencilPlan& p, const CUtensorMap& tin,
   if (int rc = prepare_kernel(reinterpret_cast<const void*>(kern), p.smem, 256, nullptr))
     return rc;
   kern<<<p.grid, 256, p.smem, st>>>(tin, thalo, tout, p.g);
+  count_launch();
   B2L_CUDA(cudaGetLastError());
   return 0;
 }

@@ -299,6 +299,7 @@ static int launch_sgram_t(const StencilPlan& p, size_t smem, const CUtensorMap& 
   auto kern = p.nst == 4 ? stencil7_gram_kernel<LD, GPW, 4, 2> : stencil7_gram_kernel<LD, GPW, 3, 3>;
   if (int rc = prepare_kernel(reinterpret_cast<const void*>(kern), smem, 256, nullptr)) return rc;
   kern<<<p.grid, 256, smem, st>>>(tin, thalo, tout, txm, p.g, G);
+  count_launch();
   B2L_CUDA(cudaGetLastError());
   return 0;
 }

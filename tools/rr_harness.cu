@@ -37,7 +37,7 @@ int main(int argc, char** argv) {
     std::vector<double> lo(m), coef(3 * m * m);
     std::vector<int> pc(2 * m);
     int kp, fb;
-    const int reps = 5000;
+    const int reps = m >= 32 ? 50 : 5000;
     for (int r = 0; r < 200; ++r)
       b2l_rayleigh_ritz(m, m, 1, g1.data(), (int)hd[2], g2.data(), lam.data(), j.data(), m,
                         j.data(), 1e-8, lo.data(), coef.data(), pc.data(), &kp, &fb);
