@@ -1042,6 +1042,10 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
   int* swp = spc + A.kp;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + A.bar_off);
   uint64_t* empty = full + 4;
+  // output buffer b free again: the storer's arrival after its TMA store has
+  // read the buffer (an mbarrier, so compute warps wait individually instead
+  // of meeting at a CTA-wide named barrier every chunk)
+  uint64_t* oempty = full + 8;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -1067,6 +1071,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], PAIR_NW);
     }
+    for (int b = 0; b < PAIR_NOB; ++b) mbar_init(&oempty[b], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -1164,9 +1169,9 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     for (int t = 0; t < TL.n; ++t) gacc[t][0] = gacc[t][1] = 0.0;
 
     int s = 0, b = 0;
-    uint32_t phase = 0;
+    uint32_t phase = 0, ophase = 0;
     for (int it = 0; it < nloc; ++it) {
-      if (it >= PAIR_NOB) nbar_sync(NB_POEMPTY + b, PAIR_BAR);
+      if (it >= PAIR_NOB) mbar_wait(&oempty[b], ophase);
       mbar_wait(&full[s], phase);
       const double* st = stages + (size_t)s * A.stage_doubles;
       const int ob = b * A.out_stride;
@@ -1323,10 +1328,11 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         s = 0;
         phase ^= 1u;
       }
-      if (++b == PAIR_NOB) b = 0;
+      if (++b == PAIR_NOB) {
+        b = 0;
+        if (it + 1 > PAIR_NOB) ophase ^= 1u;
+      }
     }
-    for (int it = (nloc > PAIR_NOB ? nloc : PAIR_NOB); it < nloc + PAIR_NOB; ++it)
-      nbar_sync(NB_POEMPTY + it % PAIR_NOB, PAIR_BAR);
     s_w0 = s_w[0];
     s_w1 = s_w[1];
     s_a0 = s_a[0];
@@ -1375,9 +1381,9 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         }
         bulk_commit();
         bulk_wait_read<0>();
+        mbar_arrive(&oempty[b]);
       }
       __syncwarp();
-      nbar_arrive(NB_POEMPTY + b, PAIR_BAR);
     }
     if (lane == 0) bulk_wait<0>();
     __syncwarp();
