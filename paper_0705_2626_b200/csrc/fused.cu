@@ -55,7 +55,7 @@ namespace b2l {
 constexpr int STEP_NU = B2L_STEP_NU;                        // update warps
 constexpr int STEP_NG = B2L_STEP_NG;                        // Gram warps
 constexpr int STEP_GI = 2;                                  // Gram items per Gram warp
-constexpr int STEP_THREADS = 32 * (1 + STEP_NU + STEP_NG);  // 352
+constexpr int STEP_THREADS = 32 * (2 + STEP_NU + STEP_NG);  // 384: loader, update, Gram, storer
 constexpr int NB_OFULL = 1;                                 // named barriers 1,2
 constexpr int NB_OEMPTY = 3;                                // named barriers 3,4
 
@@ -170,6 +170,8 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
   int* swp = spc + A.kp;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + A.bar_off);
   uint64_t* empty = full + 4;
+  uint64_t* ofull = full + 8;    // output buffer b written (update warps arrive)
+  uint64_t* oempty = full + 10;  // buffer b read by its TMA store and the Gram warps
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -188,6 +190,10 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
     for (int s = 0; s < A.nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], STEP_NU + STEP_NG);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ofull[b], STEP_NU);
+      mbar_init(&oempty[b], 1 + STEP_NG);
     }
     fence_mbar_init();
   }
@@ -208,14 +214,19 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
   const int gw = warp - 1 - STEP_NU;
 
   if (warp == 0) {
-    // ================= producer / storer =================
+    // ================= loader: refills a stage as soon as it is released
     if (lane == 0)
-      for (int j = 0; j < A.nst && j < nloc; ++j)
-        step_issue(M, A, stages + (size_t)j * A.stage_doubles, &full[j], chunk_of(j));
-    for (int it = 0; it < nloc; ++it) {
-      const int b = it & 1;
-      nbar_sync(NB_OFULL + b, STEP_THREADS);
-      if (lane == 0) {
+      for (int j = 0; j < nloc; ++j) {
+        const int s = j % A.nst;
+        if (j >= A.nst) mbar_wait(&empty[s], (j / A.nst - 1) & 1);
+        step_issue(M, A, stages + (size_t)s * A.stage_doubles, &full[s], chunk_of(j));
+      }
+  } else if (warp == 1 + STEP_NU + STEP_NG) {
+    // ================= storer (mbarrier hand-offs: no CTA-wide barrier)
+    if (lane == 0) {
+      for (int it = 0; it < nloc; ++it) {
+        const int b = it & 1;
+        mbar_wait(&ofull[b], (it >> 1) & 1);
         const int r0 = chunk_of(it) * A.rc;
         const int ob = b * A.out_stride;
         for (int k = 0; k < 5; ++k) {
@@ -224,18 +235,10 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
         }
         bulk_commit();
         bulk_wait_read<0>();           // release the buffer once read
+        mbar_arrive(&oempty[b]);
       }
-      __syncwarp();
-      nbar_arrive(NB_OEMPTY + b, STEP_THREADS);
-      const int jn = it + A.nst;       // refill the stage chunk `it` used
-      if (lane == 0 && jn < nloc) {
-        const int s = it % A.nst;
-        mbar_wait(&empty[s], (it / A.nst) & 1);
-        step_issue(M, A, stages + (size_t)s * A.stage_doubles, &full[s], chunk_of(jn));
-      }
-      __syncwarp();
+      bulk_wait<0>();
     }
-    if (lane == 0) bulk_wait<0>();
   } else if (warp <= STEP_NU) {
     // ================= update + residual =================
     const int wu = warp - 1;
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
       const int s = it % A.nst, b = it & 1;
       const int r0 = chunk_of(it) * A.rc;
       const int nvalid = min(A.rc, A.nrows - r0);
-      if (it >= 2) nbar_sync(NB_OEMPTY + b, STEP_THREADS);
+      if (it >= 2) mbar_wait(&oempty[b], ((it >> 1) - 1) & 1);
       mbar_wait(&full[s], (it / A.nst) & 1);
       const double* st = stages + (size_t)s * A.stage_doubles;
       const double* X = st + A.in_off[0];
@@ -374,12 +377,11 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
       }
       fence_async_smem();   // generic writes -> the TMA store (async proxy)
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      nbar_arrive(NB_OFULL + b, STEP_THREADS);
+      if (lane == 0) {
+        mbar_arrive(&empty[s]);
+        mbar_arrive(&ofull[b]);
+      }
     }
-    // balance the output-buffer barrier: consume the last two phases
-    for (int it = (nloc > 2 ? nloc : 2); it < nloc + 2; ++it)
-      nbar_sync(NB_OEMPTY + (it & 1), STEP_THREADS);
   } else {
     // ================= Gram of the finished output buffers =================
     // item = (tile block ts, row slice sl); warp gw owns items gw, gw + NG.
@@ -444,7 +446,7 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
       const int r0 = chunk_of(it) * A.rc;
       const int nvalid = min(A.rc, A.nrows - r0);
       const int nv4 = (nvalid + 3) & ~3;
-      nbar_sync(NB_OFULL + b, STEP_THREADS);
+      mbar_wait(&ofull[b], (it >> 1) & 1);
       const uint32_t boff = 8u * (uint32_t)(b * A.out_stride);
       const double* dst_ = stages + (size_t)s * A.stage_doubles + A.d_off;
 #pragma unroll
@@ -475,8 +477,10 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      nbar_arrive(NB_OEMPTY + b, STEP_THREADS);
+      if (lane == 0) {
+        mbar_arrive(&empty[s]);
+        mbar_arrive(&oempty[b]);
+      }
     }
   }
   __syncthreads();
@@ -514,7 +518,7 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
   __syncthreads();
   // ---- Gram: per item, fixed-order sum over row slices
   double* gred = sm + A.gred_off;  // [item][8 tiles][32 lanes][2]
-  if (gw >= 0) {
+  if (gw >= 0 && gw < STEP_NG) {
 #pragma unroll
     for (int u = 0; u < STEP_GI; ++u) {
       const int item = gw + u * STEP_NG;
@@ -662,7 +666,7 @@ __host__ __device__ constexpr PairTiles pair_tiles(int NI, int NJ, int mfix, int
 // full) and producer -> warp (buffer empty).  8 warps keep the fp64 tensor
 // pipe busy without the load imbalance of a separate Gram warp group.
 constexpr int LOC_NW = 8;                        // compute warps (8 x 8 = 64 rows)
-constexpr int LOC_THREADS = 32 * (1 + LOC_NW);   // 288
+constexpr int LOC_THREADS = 32 * (2 + LOC_NW);   // 320: loader + 8 compute + storer
 
 template <int NT, int KS, int NI, int NJ, int MFIX, bool WGT>
 __global__ void __launch_bounds__(LOC_THREADS, 1)
@@ -682,6 +686,8 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
   int* swp = spc + A.kp;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + A.bar_off);
   uint64_t* empty = full + 4;
+  uint64_t* ofull = full + 8;    // output buffer b written (compute warps arrive)
+  uint64_t* oempty = full + 10;  // output buffer b read by its TMA store (storer arrives)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -701,6 +707,10 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], LOC_NW);
     }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ofull[b], LOC_NW);
+      mbar_init(&oempty[b], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -718,14 +728,19 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
   for (int t = 0; t < TL.n; ++t) gacc[t][0] = gacc[t][1] = 0.0;
 
   if (warp == 0) {
-    // ================= producer / storer =================
+    // ================= loader: refills a stage as soon as it is released
     if (lane == 0)
-      for (int j = 0; j < A.nst && j < nloc; ++j)
-        step_issue(M, A, stages + (size_t)j * A.stage_doubles, &full[j], chunk_of(j));
-    for (int it = 0; it < nloc; ++it) {
-      const int b = it & 1;
-      nbar_sync(NB_OFULL + b, LOC_THREADS);
-      if (lane == 0) {
+      for (int j = 0; j < nloc; ++j) {
+        const int s = j % A.nst;
+        if (j >= A.nst) mbar_wait(&empty[s], (j / A.nst - 1) & 1);
+        step_issue(M, A, stages + (size_t)s * A.stage_doubles, &full[s], chunk_of(j));
+      }
+  } else if (warp == LOC_NW + 1) {
+    // ================= storer (mbarrier hand-offs: no CTA-wide barrier)
+    if (lane == 0) {
+      for (int it = 0; it < nloc; ++it) {
+        const int b = it & 1;
+        mbar_wait(&ofull[b], (it >> 1) & 1);
         const int r0 = chunk_of(it) * A.rc;
         const int ob = b * A.out_stride;
         for (int k = 0; k < 5; ++k) {
@@ -734,18 +749,10 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
         }
         bulk_commit();
         bulk_wait_read<0>();
+        mbar_arrive(&oempty[b]);
       }
-      __syncwarp();
-      nbar_arrive(NB_OEMPTY + b, LOC_THREADS);
-      const int jn = it + A.nst;
-      if (lane == 0 && jn < nloc) {
-        const int s = it % A.nst;
-        mbar_wait(&empty[s], (it / A.nst) & 1);
-        step_issue(M, A, stages + (size_t)s * A.stage_doubles, &full[s], chunk_of(jn));
-      }
-      __syncwarp();
+      bulk_wait<0>();
     }
-    if (lane == 0) bulk_wait<0>();
   } else {
     const int mt = warp - 1;                   // this warp's 8-row tile
     const int q = lane & 3, rl = lane >> 2;
@@ -827,7 +834,7 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
       const int s = it % A.nst, b = it & 1;
       const int r0 = chunk_of(it) * A.rc;
       const int nvalid = min(A.rc, A.nrows - r0);
-      if (it >= 2) nbar_sync(NB_OEMPTY + b, LOC_THREADS);
+      if (it >= 2) mbar_wait(&oempty[b], ((it >> 1) - 1) & 1);
       mbar_wait(&full[s], (it / A.nst) & 1);
       const double* st = stages + (size_t)s * A.stage_doubles;
       const double* X = st + A.in_off[0];
@@ -930,18 +937,18 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
       }
       fence_async_smem();   // generic writes -> the TMA store (async proxy)
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      nbar_arrive(NB_OFULL + b, LOC_THREADS);
+      if (lane == 0) {
+        mbar_arrive(&empty[s]);
+        mbar_arrive(&ofull[b]);
+      }
     }
-    for (int it = (nloc > 2 ? nloc : 2); it < nloc + 2; ++it)
-      nbar_sync(NB_OEMPTY + (it & 1), LOC_THREADS);
   }
   __syncthreads();
 
   // ---- CTA reductions (fixed order over compute warps / rows)
   double* red = sm + A.red_off;
   const int NL = LOC_NW * 32 * 2 * NT;    // [warp][lane][nt][e]
-  if (warp >= 1) {
+  if (warp >= 1 && warp <= LOC_NW) {
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -966,7 +973,7 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
     out[m + tid] = bb;
   }
   double* gred = sm + A.gred_off;   // [warp][NI*NJ tiles][32][2]
-  if (warp >= 1) {
+  if (warp >= 1 && warp <= LOC_NW) {
 #pragma unroll
     for (int t = 0; t < TL.n; ++t) {
       const size_t o =
