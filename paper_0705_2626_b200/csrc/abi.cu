@@ -42,7 +42,8 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
                 double* xo, double* axo, double* po, double* apo, const double* lam,
                 const double* d, int tmode, double tinv, const double* tvec,
                 const int* wpos, int kwn, double* wo, int ldwn, int want_ax,
-                double* red_out, cudaStream_t st, const StepHostCoef* hc);
+                double* red_out, cudaStream_t st, const StepHostCoef* hc,
+                StepDeferred* defer);
 
 static thread_local std::string g_err;
 
@@ -56,16 +57,16 @@ struct DevWs {
   void* ptr = nullptr;
   size_t bytes = 0;
 };
-static DevWs g_ws[64];
+static DevWs g_ws[64][2];
 static int g_sms[64];
 
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-void* workspace(size_t bytes, int* err) {
+void* workspace(size_t bytes, int* err, int slot) {
   int dev = 0;
   cudaGetDevice(&dev);
-  DevWs& w = g_ws[dev & 63];
+  DevWs& w = g_ws[dev & 63][slot & 1];
   if (w.bytes < bytes) {
     // growth is rare (first call per shape); keep it stream-safe by syncing
     if (w.ptr) {
@@ -324,7 +325,8 @@ int b2l_lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx
                     int want_ax_norms, double* red_out, void* stream) {
   return lobpcg_step(nrows, m, x, ax, ldx, w, aw, ldw, kw, p, ap, kp, pcols, coef, xo, axo, po,
                      apo, lam, bdiag, tmode, tinv, tvec, wpos, kw_next, w_next, ldw_next,
-                     want_ax_norms, red_out, static_cast<cudaStream_t>(stream), nullptr);
+                     want_ax_norms, red_out, static_cast<cudaStream_t>(stream), nullptr,
+                     nullptr);
 }
 
 }  // extern "C"

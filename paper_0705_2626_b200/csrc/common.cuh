@@ -46,7 +46,15 @@ enum : int {
 // One growable device scratch buffer per device (CTA partials of the
 // deterministic two-stage reductions).  Stream-ordered: the library is
 // driven by one host thread / one stream per device.
-void* workspace(size_t bytes, int* err);
+// slot 1 holds F1's partials while the stencil pass (slot 0) runs beside their
+// reduction (b2l_fast_iteration)
+void* workspace(size_t bytes, int* err, int slot = 0);
+// F1's second reduction stage, left to the caller when requested
+struct StepDeferred {
+  const double* part = nullptr;
+  int nparts = 0, len = 0;
+  double* out = nullptr;
+};
 int sm_count();
 // cudaFuncSetAttribute(max dynamic smem) + occupancy query, cached per
 // (kernel, smem, threads): both are host API round trips on every launch

@@ -1467,7 +1467,8 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
                 double* xo, double* axo, double* po, double* apo, const double* lam,
                 const double* d, int tmode, double tinv, const double* tvec,
                 const int* wpos, int kwn, double* wo, int ldwn, int want_ax,
-                double* red_out, cudaStream_t st, const StepHostCoef* hc) {
+                double* red_out, cudaStream_t st, const StepHostCoef* hc,
+                StepDeferred* defer) {
   B2L_CHECK(m >= 1 && m <= 16, -B2L_EINVAL, "step: 1 <= m <= 16 (larger blocks: b2l_update)");
   B2L_CHECK(nrows >= 1, -B2L_EINVAL, "step: empty block");
   B2L_CHECK(ldx >= m && (ldx & 1) == 0, -B2L_EINVAL, "step: ldx must be even and >= m");
@@ -1677,12 +1678,20 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   if (gx < 1) gx = 1;
   const int len = 2 * m + A.a * A.b;
   int werr = 0;
-  double* part = static_cast<double*>(workspace((size_t)gx * len * sizeof(double), &werr));
+  double* part = static_cast<double*>(
+      workspace((size_t)gx * len * sizeof(double), &werr, defer ? 1 : 0));
   if (werr) return werr;
   A.partial = part;
   kern<<<gx, threads, smem, st>>>(M, A, cf);
   count_launch();
   B2L_CUDA(cudaGetLastError());
+  if (defer) {   // the caller reduces (on a side stream, beside the stencil pass)
+    defer->part = part;
+    defer->nparts = gx;
+    defer->len = len;
+    defer->out = red_out;
+    return 0;
+  }
   return sum_parts(part, gx, len, red_out, st);
 }
 

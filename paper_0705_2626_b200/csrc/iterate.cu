@@ -23,7 +23,8 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx, co
                 const int* pcols, const double* coef, double* xo, double* axo, double* po,
                 double* apo, const double* lam, const double* d, int tmode, double tinv,
                 const double* tvec, const int* wpos, int kwn, double* wo, int ldwn, int want_ax,
-                double* red_out, cudaStream_t st, const StepHostCoef* hc);
+                double* red_out, cudaStream_t st, const StepHostCoef* hc,
+                StepDeferred* defer);
 int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
                   const double* halo, int has_lo, int has_hi, double scale, const double* x,
                   int ldx, int m, int kw, double* gram_out, cudaStream_t st);
@@ -48,6 +49,30 @@ inline double now_us() {
       .count();
 }
 }  // namespace
+
+// A non-blocking side stream + fork/join events per device (lazily created;
+// null if creation fails, then everything stays on the caller's stream).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  bool tried = false;
+};
+SideStream* side_stream() {
+  static SideStream g[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  SideStream& x = g[dev & 63];
+  if (!x.tried) {
+    x.tried = true;
+    if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      x.s = nullptr;
+    }
+  }
+  return x.s ? &x : nullptr;
+}
 
 // Device address of a pinned host buffer (cudaHostGetDevicePointer), cached
 // for the last two buffers; null when it is not device-mapped (then copied).
@@ -170,15 +195,28 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
   double* red_h = mapped(s->h_red);
   double* g2_h = mapped(s->h_g2);
   const StepHostCoef hc{coef, lam_next, pcols, wpos};
+  // F1's second reduction stage runs on a side stream beside the stencil
+  // pass (it only feeds the host); the main stream joins it before the next
+  // synchronisation
+  StepDeferred dfr;
+  SideStream* side = side_stream();
   int r = lobpcg_step(s->n, m, s->x, s->ax, s->ldx, s->w_cur, s->aw, even(kst), kst,
                       kp ? s->p : nullptr, kp ? s->ap : nullptr, kp, nullptr, nullptr,
                       s->x2, s->ax2, s->p2, s->ap2, nullptr, s->bdiag, s->tmode, s->tinv,
                       s->tvec, nullptr, kj, s->w_next, even(kj), s->relative_tol,
-                      red_h ? red_h : s->red_dev, st, &hc);
+                      red_h ? red_h : s->red_dev, st, &hc, side ? &dfr : nullptr);
   if (r) return r;
+  if (side) {
+    B2L_CUDA(cudaEventRecord(side->fork, st));
+    B2L_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
+    r = sum_parts(dfr.part, dfr.nparts, dfr.len, dfr.out, side->s);
+    if (r) return r;
+    B2L_CUDA(cudaEventRecord(side->join, side->s));
+  }
   r = stencil7_gram(s->w_next, s->aw, s->nx, s->ny, s->nz, even(kj), nullptr, 0, 0, s->scale,
                     s->x2, s->ldx, m, kj, g2_h ? g2_h : s->g2_dev, st);
   if (r) return r;
+  if (side) B2L_CUDA(cudaStreamWaitEvent(st, side->join, 0));
   // the next call skips its D2H copies only when both landed on the host
   if (red_h && !g2_h)
     B2L_CUDA(cudaMemcpyAsync(s->h_g2, s->g2_dev, (size_t)(m + kj) * kj * sizeof(double),
