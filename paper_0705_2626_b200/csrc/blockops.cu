@@ -315,11 +315,49 @@ __global__ void __launch_bounds__(32 * (GB_MAXW + 1), 1)
     }
     WarpGram<GB_TI, GB_TJ> g;
     g.zero();
+    // Branch-free inner loop: all 16 tiles of the block are accumulated (the
+    // few unneeded ones are never read), lanes whose column lies beyond the
+    // Gram read a valid smem column instead (their products land only in
+    // accumulator rows / columns the output loop skips), and the loads walk
+    // fixed per-lane offsets -- no predicated mma (no WARPSYNC per DMMA).
+    const int q = lane & 3;
+    int aoff[GB_TI], astr[GB_TI], boff[GB_TJ], bstr[GB_TJ];
+    bool bw[GB_TJ];
+#pragma unroll
+    for (int i = 0; i < GB_TI; ++i) {
+      aoff[i] = la[i].ok ? la[i].off + q * la[i].str : A.ubase[0];
+      astr[i] = la[i].ok ? 4 * la[i].str : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < GB_TJ; ++j) {
+      boff[j] = lb[j].ok ? lb[j].off + q * lb[j].str : A.ubase[0];
+      bstr[j] = lb[j].ok ? 4 * lb[j].str : 0;
+      bw[j] = lb[j].ok && lb[j].weighted;
+    }
     for (int it = 0; it < nloc; ++it) {
       const int s = it % A.nst;
       mbar_wait(&full[s], (it / A.nst) & 1);
       const double* st = stages + (size_t)s * A.stage_doubles;
-      if (mask) g.run(st, la, lb, A.d ? st + A.dbase : nullptr, 0, A.rc, mask, DenseRows());
+      if (mask) {
+        const double* dw = A.d ? st + A.dbase + q : nullptr;
+#pragma unroll 2
+        for (int r = 0; r < A.rc; r += 4) {
+          const int k4 = r >> 2;
+          double av[GB_TI], bv[GB_TJ];
+#pragma unroll
+          for (int i = 0; i < GB_TI; ++i) av[i] = st[aoff[i] + k4 * astr[i]];
+          const double w = dw ? dw[r] : 1.0;
+#pragma unroll
+          for (int j = 0; j < GB_TJ; ++j) {
+            const double v = st[boff[j] + k4 * bstr[j]];
+            bv[j] = bw[j] ? __dmul_rn(w, v) : v;
+          }
+#pragma unroll
+          for (int i = 0; i < GB_TI; ++i)
+#pragma unroll
+            for (int j = 0; j < GB_TJ; ++j) dmma_8x8x4(g.acc[i][j][0], g.acc[i][j][1], av[i], bv[j]);
+        }
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive_cta(&empty[s]);
     }
