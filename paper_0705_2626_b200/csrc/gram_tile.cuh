@@ -25,7 +25,8 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 
 // Per-lane view of one 8-column slab of L or R: the lane's column lives at
 // smem offset `off` (doubles, relative to the row-0 base of its block) with
-// row stride `str`; `ok` is false for padding columns beyond the matrix.
+// row stride `str`; `ok` is false for padding columns beyond the matrix (then
+// off = str = 0: a valid dummy element, see WarpGram::run).
 struct LaneCol {
   int off;
   int str;
@@ -61,19 +62,23 @@ struct WarpGram {
     for (int r = r0; r < r1; r += 4) {
       const int rr = rowmap(r + q);
       double av[TI], bv[TJ];
+      // branch free: a lane whose column lies beyond the Gram (ok = false)
+      // reads the valid element its {off, str} = {0, 0} points at, and its
+      // products land only in accumulator rows / columns the caller never
+      // writes out; every tile is accumulated (unneeded ones are never read),
+      // so no predicated mma (a WARPSYNC per DMMA) is emitted
 #pragma unroll
-      for (int i = 0; i < TI; ++i) av[i] = a[i].ok ? base[a[i].off + rr * a[i].str] : 0.0;
+      for (int i = 0; i < TI; ++i) av[i] = base[a[i].off + rr * a[i].str];
       const double w = d ? d[r + q] : 1.0;
 #pragma unroll
       for (int j = 0; j < TJ; ++j) {
-        double v = b[j].ok ? base[b[j].off + rr * b[j].str] : 0.0;
+        const double v = base[b[j].off + rr * b[j].str];
         bv[j] = b[j].weighted ? __dmul_rn(w, v) : v;
       }
 #pragma unroll
       for (int i = 0; i < TI; ++i)
 #pragma unroll
-        for (int j = 0; j < TJ; ++j)
-          if (mask & (1u << (i * TJ + j))) dmma_8x8x4(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+        for (int j = 0; j < TJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
     }
   }
 };
