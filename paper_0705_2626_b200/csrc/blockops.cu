@@ -15,6 +15,7 @@
 // Every reduction is deterministic: CTA partials in a fixed row assignment,
 // then a fixed-order second stage over CTAs.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "gram_tile.cuh"
@@ -1043,6 +1044,89 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
   }
 }
 
+
+// -------------------------------------------------------------------------
+// K6 for small blocks (m <= 16): one thread per row, the row's outputs in
+// registers (MT >= m columns), inputs read element by element (L1-cached:
+// a warp's 32 rows are contiguous), coefficients broadcast from shared
+// memory.  The scalar update_kernel kept one thread per (row, column) and
+// re-read the row m times; this is the memory-bound form (repairs, the
+// initial block, the exit refresh and the unfused paths at m <= 16).
+template <int MT>
+__global__ void __launch_bounds__(256) update_row_kernel(UpdArgs A) {
+  extern __shared__ double usm[];
+  double* scx = usm;
+  double* scw = scx + MT * MT;
+  double* scp = scw + MT * MT;
+  const int tid = threadIdx.x;
+  const int m = A.m;
+  // zero-padded MT x MT coefficient blocks; Cp rows scattered to pcols
+  for (int i = tid; i < 3 * MT * MT; i += blockDim.x) usm[i] = 0.0;
+  __syncthreads();
+  if (A.x)
+    for (int i = tid; i < m * m; i += blockDim.x) scx[(i / m) * MT + i % m] = A.cx[i];
+  for (int i = tid; i < A.kw * m; i += blockDim.x) scw[(i / m) * MT + i % m] = A.cw[i];
+  for (int i = tid; i < A.kp * m; i += blockDim.x) scp[A.pcols[i / m] * MT + i % m] = A.cp[i];
+  __syncthreads();
+  const bool haveP = (A.kw + A.kp) > 0;
+  for (int r = blockIdx.x * blockDim.x + tid; r < A.nrows; r += gridDim.x * blockDim.x) {
+#pragma unroll 1
+    for (int side = 0; side < 2; ++side) {
+      const bool aside = side == 1;
+      if (aside && !A.ax) break;
+      double pn[MT], xs[MT];
+#pragma unroll
+      for (int c = 0; c < MT; ++c) pn[c] = xs[c] = 0.0;
+      if (haveP) {
+        const double* wr = (aside ? A.aw : A.w) + (size_t)r * A.ldw;
+        for (int k = 0; k < A.kw; ++k) {
+          const double v = wr[k];
+#pragma unroll
+          for (int c = 0; c < MT; ++c) pn[c] = fma(v, scw[k * MT + c], pn[c]);
+        }
+        if (A.kp) {
+          double pp[MT];
+#pragma unroll
+          for (int c = 0; c < MT; ++c) pp[c] = 0.0;
+          const double* pr = (aside ? A.ap : A.p) + (size_t)r * A.ldp;
+          for (int k = 0; k < m; ++k) {
+            const double v = pr[k];
+#pragma unroll
+            for (int c = 0; c < MT; ++c) pp[c] = fma(v, scp[k * MT + c], pp[c]);
+          }
+#pragma unroll
+          for (int c = 0; c < MT; ++c) pn[c] = A.kw ? __dadd_rn(pn[c], pp[c]) : pp[c];
+        }
+      }
+      if (A.x) {
+        const double* xr = (aside ? A.ax : A.x) + (size_t)r * A.ldx;
+        for (int k = 0; k < m; ++k) {
+          const double v = xr[k];
+#pragma unroll
+          for (int c = 0; c < MT; ++c) xs[c] = fma(v, scx[k * MT + c], xs[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < MT; ++c)
+          if (A.x_plus_p && haveP) xs[c] = __dadd_rn(xs[c], pn[c]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < MT; ++c) xs[c] = pn[c];
+      }
+      double* xo = (aside ? A.axo : A.xo) + (size_t)r * A.ldo;
+#pragma unroll
+      for (int c = 0; c < MT; ++c)
+        if (c < A.ldo) xo[c] = c < m ? xs[c] : 0.0;
+      double* po = aside ? A.apo : A.po;
+      if (haveP && po) {
+        po += (size_t)r * A.ldpo;
+#pragma unroll
+        for (int c = 0; c < MT; ++c)
+          if (c < A.ldpo) po[c] = c < m ? pn[c] : 0.0;
+      }
+    }
+  }
+}
+
 static int update_mma(int nrows, int m, const double* x, const double* ax, int ldx,
                       const double* cx, const double* w, const double* aw, int ldw, int kw,
                       const double* cw, const double* p, const double* ap, int ldp,
@@ -1169,6 +1253,24 @@ int update(int nrows, int m, const double* x, const double* ax, int ldx,
   A.apo = apo;
   A.ldpo = ldpo;
   A.x_plus_p = x_plus_p;
+  const int mt_r = m <= 4 ? 4 : (m <= 8 ? 8 : (m <= 10 ? 10 : 16));
+  if (m <= 16 && !scalar_only && ldo <= mt_r && (!po || ldpo <= mt_r)) {
+    // one thread per row (memory-bound form); MT = the next of 4 / 8 / 10 / 16
+    const int blocks_r = (int)(((size_t)nrows + 255) / 256);
+    int grid_r = blocks_r < 8 * sm_count() ? blocks_r : 8 * sm_count();
+    if (grid_r < 1) grid_r = 1;
+    auto launch = [&](auto mt) {
+      constexpr int MT = decltype(mt)::value;
+      update_row_kernel<MT><<<grid_r, 256, 3 * MT * MT * sizeof(double), st>>>(A);
+      count_launch();
+    };
+    if (m <= 4) launch(std::integral_constant<int, 4>{});
+    else if (m <= 8) launch(std::integral_constant<int, 8>{});
+    else if (m <= 10) launch(std::integral_constant<int, 10>{});
+    else launch(std::integral_constant<int, 16>{});
+    B2L_CUDA(cudaGetLastError());
+    return 0;
+  }
   const size_t smem = (size_t)(m * m + kw * m + kp * m) * sizeof(double) + kp * sizeof(int) + 16;
   B2L_CHECK(smem <= 227 * 1024, -B2L_EINVAL, "update: coefficients too large");
   int blocks = (nrows + A.rp - 1) / A.rp;
