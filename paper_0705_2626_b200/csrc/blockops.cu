@@ -556,7 +556,11 @@ int gram(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr,
       const char* v = getenv("B2L_GRAM_SMALL");
       return v && v[0] == '1';
     }();
-    if (need > 96 && nrows > 0 && !small_only) {
+    // ... and any Gram over wide blocks (ld >= 32): the small kernel stages
+    // dense rows, whose 8-B fragment loads then fall on a few banks
+    int maxld = 0;
+    for (int u = 0; u < A.nu; ++u) maxld = A.uld[u] > maxld ? A.uld[u] : maxld;
+    if ((need > 96 || maxld >= 32) && nrows > 0 && !small_only) {
       const int rc = gram_big(nrows, L, nl, R, nr, rw_mask, d, A, out, st);
       if (rc != 1) return rc;
     }
