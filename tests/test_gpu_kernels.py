@@ -181,7 +181,7 @@ def test_residual_kernel(dev, m, tmode, useb):
 
 @pytest.mark.parametrize("m,kw,kp", [(10, 10, 10), (10, 7, 7), (4, 3, 0), (16, 16, 9), (64, 40, 40),
                                     (64, 64, 64), (64, 63, 0), (24, 24, 24), (33, 20, 11),
-                                    (17, 5, 17)])
+                                    (17, 5, 17), (1, 1, 1), (3, 3, 2), (13, 11, 6), (15, 15, 0)])
 def test_update_kernel(dev, m, kw, kp):
     from paper_0705_2626_b200 import device as dv
 
@@ -312,7 +312,7 @@ def test_seeded_fill_bitwise(dev, n, m, ld, seed, row0):
     assert np.all(got[:, m:] == 0.0)
 
 
-@pytest.mark.parametrize("m", [10, 40, 64])
+@pytest.mark.parametrize("m", [1, 5, 10, 16, 40, 64])
 def test_update_rotation_only(dev, m):
     """X' = X M without W / P terms, with and without the A side (the
     initial-block and drift-repair rotations, lobpcg.py:280-296, :398)."""
