@@ -578,11 +578,12 @@ int gram(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr,
     A.rs = 1;
   }
   const int gy = (TS + A.ts_per_cta - 1) / A.ts_per_cta;
-  // rows per chunk: the largest power of two whose stage stays <= ~40 KB
+  // rows per chunk: the largest power of two whose stage stays <= ~24 KB, so
+  // a 3-deep ring leaves room for the two CTAs per SM the grid assumes
   int width = A.d ? 1 : 0;
   for (int u = 0; u < A.nu; ++u) width += A.uld[u];
   A.rc = 256;
-  while (A.rc > 16 && (size_t)A.rc * width * 8 > 40 * 1024) A.rc >>= 1;
+  while (A.rc > 16 && (size_t)A.rc * width * 8 > 24 * 1024) A.rc >>= 1;
   while (A.rs > 1 && A.rc / A.rs < 4) A.rs >>= 1;
   int off = 0;
   for (int u = 0; u < A.nu; ++u) {
