@@ -18,18 +18,23 @@
 // once and written once per iteration; the only other pass is the stencil
 // (stencil.cu), which also produces [X' W']^T A W'.
 //
-// Warp-specialised pipeline (no CTA-wide barrier inside the chunk loop):
-//   warp 0         TMA producer + storer (lane 0 issues): refills the NST-deep
-//                  input ring and stores each finished output buffer;
-//   warps 1..8     update + residual, one 8-row tile (all columns) per warp,
-//                  so the residual of a row needs no other warp; the update
-//                  coefficients live in registers for the whole kernel;
-//   warps 9..12    Gram of the finished output buffer (double buffered),
-//                  overlapping the update of the next chunk; each warp owns
-//                  up to two (tile block, row slice) items.
-// Handoffs: mbarriers for TMA (full[s]) and stage reuse (empty[s]); hardware
-// named barriers (sleeping, not polling) for output buffer full / empty.
-//
+// Three warp-specialised variants (persistent grid, one CTA per SM):
+//   step_pair_kernel  (m = 9..10; C2): loader warp (TMA loads into a 4-deep
+//       ring; a stage comes back as soon as the update has read it), 7 warp
+//       pairs, storer warp (TMA stores of triple-buffered outputs).  Warp 0 of
+//       a pair forms columns 0-7 on DMMA, warp 1 the two tail columns on DFMA;
+//       after a pair barrier each folds the 8 rows into half the needed Gram
+//       tiles.  Output buffers come back through an mbarrier the storer
+//       arrives on (compute warps never meet at a CTA-wide barrier).  The
+//       full block (every column active) is a compile-time specialisation.
+//   step_local_kernel (m <= 8; C1, C4): loader, 8 compute warps (one 8-row
+//       tile each: update, residual and the whole Gram in registers), storer;
+//       mbarrier hand-offs.
+//   step_kernel       (11 <= m <= 16; C3): one producer/storer warp, 4 update
+//       warps, 6 Gram warps folding the finished output buffer while the next
+//       chunk is updated; named barriers for the double-buffered outputs.
+// Input stages: mbarriers full[s] (TMA) / empty[s] (consumers).
+
 // Shared-memory rows are padded to smem_stride(ld) doubles (4 or 12 mod 16):
 // the TMA box is wider than the block's row, the extra columns are zero-filled
 // on load and clipped on store, and the DMMA fragment loads are free of bank
