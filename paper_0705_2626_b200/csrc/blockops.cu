@@ -10,7 +10,11 @@
 //                   (lobpcg.py:520-540; multivec.py:74-86), with the Cholesky
 //                   factors of W and P folded into Cw/Cp on the host so W and P
 //                   are never rewritten (replaces tri_solve_right,
-//                   multivec.py:125-146)
+//                   multivec.py:125-146): one thread per row for m <= 16,
+//                   DMMA with resident coefficients for 16 < m <= 64, a scalar
+//                   fallback otherwise
+//   K5 for wide / large Grams (gram_big): 4x4 tile blocks per warp, padded
+//                   TMA rows, producer warp (the m = 64 pencil of C5)
 //
 // Every reduction is deterministic: CTA partials in a fixed row assignment,
 // then a fixed-order second stage over CTAs.

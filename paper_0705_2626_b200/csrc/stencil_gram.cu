@@ -8,8 +8,10 @@
 // plane it computes the stencil for all columns of its points (bitwise the
 // reference's operation order) and immediately folds those 8-point rows into
 // its own Gram accumulators on the fp64 tensor cores (DMMA) -- no hand-off
-// between warps, one CTA barrier per plane (output tiles triple buffered, X
-// boxes double buffered).  A W is never re-read from HBM.
+// between warps, one CTA barrier per plane (a 4-deep plane ring with double-
+// buffered output tiles when two CTAs fit per SM, else 3 + 3; X boxes double
+// buffered; the slot a plane writes is released by its TMA store's read
+// before that barrier).  A W is never re-read from HBM.
 #include <cstdlib>
 
 #include "gram_tile.cuh"
