@@ -213,6 +213,13 @@ int b2l_pcg_direction(int nrows, int k, const double* r, double* p, int ld, cons
 int b2l_set_lapack(void* dpotrf, void* dtrtrs, void* dtrtri, void* dsyevr);
 
 /*
+ * Host, small dense: optionally register BLAS dgemm (Fortran-style signature
+ * of scipy.linalg.cython_blas) for the block products of large pencils
+ * (m >= 32); null keeps the native loops.
+ */
+int b2l_set_blas(void* dgemm);
+
+/*
  * Host, small dense -- the Rayleigh-Ritz step of one iteration with the
  * reference's repair ladders (lobpcg.py:475-519; b_orthonormalize :147-200;
  * rayleigh_ritz :299-340 on the projected blocks), given the device Grams:

@@ -105,6 +105,7 @@ SIGNATURES = {
     "b2l_iter_profile": (C.c_int, [C.POINTER(C.c_double), C.c_int]),
     "b2l_launch_count": (C.c_longlong, []),
     "b2l_set_lapack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "b2l_set_blas": (C.c_int, [C.c_void_p]),
     "b2l_rayleigh_ritz": (C.c_int, [C.c_int, C.c_int, C.c_int, c_dp, C.c_int, c_dp, c_dp,
                                     c_ip, C.c_int, c_ip, C.c_double, c_dp, c_dp, c_ip, c_ip,
                                     c_ip]),
@@ -162,6 +163,10 @@ def _register_lapack(lib) -> None:
     for name in ("dpotrf", "dtrtrs", "dtrtri", "dsyevr"):
         cap = caps[name]
         ptrs.append(get(cap, getname(cap)))
+    from scipy.linalg import cython_blas
+
+    bcap = cython_blas.__pyx_capi__["dgemm"]
+    lib.b2l_set_blas(get(bcap, getname(bcap)))
     rc = lib.b2l_set_lapack(*ptrs)
     if rc != 0:
         raise ImportError("b2l_set_lapack failed: " + lib.b2l_last_error().decode())

@@ -63,7 +63,21 @@ struct LapackError {
   int info;
 };
 
+// optional BLAS dgemm (Fortran signature of scipy.linalg.cython_blas) for
+// the larger pencils (m = 64: 64 x 64 blocks)
+using dgemm_t = void(char*, char*, int*, int*, int*, double*, const double*, int*, const double*,
+                     int*, double*, double*, int*);
+dgemm_t* g_dgemm = nullptr;
+
 Mat matmul(const Mat& x, const Mat& y) {
+  if (g_dgemm && x.r * x.c * y.c >= 32 * 32 * 32) {
+    Mat z(x.r, y.c);
+    char n = 'N';
+    int mm = x.r, nn = y.c, kk = x.c, lda = x.r, ldb = y.r, ldc = z.r;
+    double one = 1.0, zero = 0.0;
+    g_dgemm(&n, &n, &mm, &nn, &kk, &one, x.a.data(), &lda, y.a.data(), &ldb, &zero, z.p(), &ldc);
+    return z;
+  }
   // column-major j-k-i order: the inner loop runs down contiguous columns of
   // z and x (vectorisable, cache-friendly at the 192 x 192 sizes of m = 64)
   Mat z(x.r, y.c);
@@ -489,6 +503,11 @@ void gen_sym_eig(const Mat& ga_in, const Mat& gb, int want, double floor_, doubl
 }  // namespace b2l
 
 using namespace b2l;
+
+extern "C" int b2l_set_blas(void* dgemm) {
+  g_dgemm = reinterpret_cast<dgemm_t*>(dgemm);
+  return 0;
+}
 
 extern "C" int b2l_set_lapack(void* dpotrf, void* dtrtrs, void* dtrtri, void* dsyevr) {
   if (!dpotrf || !dtrtrs || !dtrtri || !dsyevr)
