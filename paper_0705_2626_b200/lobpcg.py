@@ -484,8 +484,11 @@ class LOBPCGRun:
         self.AWbuf = torch.zeros(n * ld, dtype=torch.float64, device=dev)
         self.sums = torch.zeros(2 * m, dtype=torch.float64, device=dev)
         nred = 2 * m + (3 * m) * (4 * m)
-        self.red = torch.zeros(nred, dtype=torch.float64, device=dev)
-        self.g2 = torch.zeros((2 * m) * m, dtype=torch.float64, device=dev)
+        # F1's reductions and the stencil pass's Gram share one buffer, so a
+        # z-slab run sums both over the ranks with a single all-reduce
+        self._redg2 = torch.zeros(nred + (2 * m) * m, dtype=torch.float64, device=dev)
+        self.red = self._redg2[:nred]
+        self.g2 = self._redg2[nred:]
         self.h_red = _host_buf(nred)
         self.h_g2 = _host_buf((2 * m) * m)
         self.h_red_np = self.h_red.numpy()
@@ -740,10 +743,16 @@ class LOBPCGRun:
                 a, b = 2 * m + kst, 3 * m + kst
                 nred = 2 * m + a * b
                 if not fetched:
-                    self._reduce(self.red[:nred])
+                    if self.sg_pending and self._allreduce is not None:
+                        # one all-reduce over [red | g2] (the unused tail of
+                        # red between nred and its capacity rides along)
+                        self._reduce(self._redg2[:self.red.numel() + g2_rows * kst])
+                    else:
+                        self._reduce(self.red[:nred])
+                        if self.sg_pending:
+                            self._reduce(self.g2[:g2_rows * kst])
                     self.h_red[:nred].copy_(self.red[:nred], non_blocking=True)
                     if self.sg_pending:
-                        self._reduce(self.g2[:g2_rows * kst])
                         self.h_g2[:g2_rows * kst].copy_(self.g2[:g2_rows * kst],
                                                         non_blocking=True)
                     if self.dev.type == "cuda":
