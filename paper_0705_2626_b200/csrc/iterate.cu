@@ -18,6 +18,10 @@
 #include "common.cuh"
 
 namespace b2l {
+int rr_begin_tls(int m, int kst, int have_p, const double* g1, int ldg1, const int* jact, int kj,
+                 const int* sel, double pivot_floor, int* fallbacks_out);
+int rr_finish_tls(const double* g2, const double* lam, double* lam_out, double* coef_out,
+                  int* pcols_out, int* kp_out, int* fallbacks_out);
 int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx, const double* w,
                 const double* aw, int ldw, int kw, const double* p, const double* ap, int kp,
                 const int* pcols, const double* coef, double* xo, double* axo, double* po,
@@ -128,8 +132,26 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
                              st));
   }
   mark(1);
-  B2L_CUDA(cudaStreamSynchronize(st));
+  // red_on_host == 2: F1's reductions went through the side stream into the
+  // mapped h_red -- wait only for them (the stencil pass, which produces A W
+  // and h_g2, may still run) and do the G1-only half of the Rayleigh-Ritz
+  // step meanwhile; the main stream is synchronised before the G2 half.
+  SideStream* side0 = side_stream();
+  const bool early = s->red_on_host == 2 && side0 != nullptr;
+  if (early) {
+    B2L_CUDA(cudaEventSynchronize(side0->join));
+  } else {
+    B2L_CUDA(cudaStreamSynchronize(st));
+  }
   s->red_on_host = 0;
+  bool main_synced = !early;
+  auto sync_main = [&]() -> int {
+    if (!main_synced) {
+      B2L_CUDA(cudaStreamSynchronize(st));
+      main_synced = true;
+    }
+    return 0;
+  };
   mark(2);
   const double* sums = s->h_red;
   const double* G1 = s->h_red + 2 * m;
@@ -142,13 +164,19 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
       if (!(v <= drift)) drift = v;   // NaN-propagating max
     }
   s->drift = drift;
-  if (!(drift <= s->drift_limit)) return B2L_ITER_DRIFT;
+  if (!(drift <= s->drift_limit)) {
+    if (int r = sync_main()) return r;   // the caller reads h_g2 too
+    return B2L_ITER_DRIFT;
+  }
 
   // ---- lock test (lobpcg.py:429-437)
   std::vector<int> jprev, jact;
   for (int j = 0; j < m; ++j)
     if (s->active[j]) jprev.push_back(j);
-  if ((int)jprev.size() != kst) return fail(-B2L_EINVAL, "fast_iteration: kst != |active|");
+  if ((int)jprev.size() != kst) {
+    sync_main();
+    return fail(-B2L_EINVAL, "fast_iteration: kst != |active|");
+  }
   for (int j = 0; j < m; ++j) {
     const double nrm = std::sqrt(sums[j]);
     const double thr = s->relative_tol ? s->tol * std::sqrt(sums[m + j]) : s->tol;
@@ -162,7 +190,10 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
   }
   for (int j = 0; j < m; ++j)
     if (s->active[j]) jact.push_back(j);
-  if (jact.empty() || s->it == s->max_iter) return B2L_ITER_DONE;
+  if (jact.empty() || s->it == s->max_iter) {
+    if (int r = sync_main()) return r;
+    return B2L_ITER_DONE;
+  }
 
   mark(3);
   // ---- Rayleigh-Ritz (lobpcg.py:475-519) on the fetched Grams
@@ -177,8 +208,10 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
   int* pcols = s->h_istage;
   int* wpos = s->h_istage + m;
   int kp = 0, fb = 0;
-  const int rc = b2l_rayleigh_ritz(m, kst, s->have_p, G1, b, s->h_g2, s->lam, jact.data(), kj,
-                                   sel.data(), s->pivot_floor, lam_next, coef, pcols, &kp, &fb);
+  int rc = rr_begin_tls(m, kst, s->have_p, G1, b, jact.data(), kj, sel.data(), s->pivot_floor,
+                        &fb);
+  if (int r = sync_main()) return r;   // G2 = [X ; W]^T A W has landed
+  if (!rc) rc = rr_finish_tls(s->h_g2, s->lam, lam_next, coef, pcols, &kp, &fb);
   s->fallbacks = fb;
   mark(4);
   if (rc) return rc;
@@ -225,7 +258,9 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
     B2L_CUDA(cudaMemcpyAsync(s->h_red, s->red_dev,
                              (2 * (size_t)m + (size_t)(2 * m + kj) * (3 * m + kj)) * sizeof(double),
                              cudaMemcpyDeviceToHost, st));
-  s->red_on_host = (red_h || g2_h) ? 1 : 0;
+  // 2: both reductions land in mapped memory, F1's through the side stream
+  // (the next call may then start on G1 before the stencil pass is done)
+  s->red_on_host = (red_h && g2_h && side) ? 2 : ((red_h || g2_h) ? 1 : 0);
   mark(5);
   return B2L_ITER_OK;
 }

@@ -402,36 +402,54 @@ Mat scaled_cholesky_inv(const Mat& g, double floor_) {
   return upper_inverse(r);
 }
 
-// Smallest `want` pairs of ga c = lam gb c via gb = R^T R (small.gen_sym_eig,
-// multivec.py:174-211); only upper triangles are read.
-void gen_sym_eig(const Mat& ga_in, const Mat& gb, int want, double floor_, double* vals_out,
-                 Mat* c_out) {
+// gb = R^T R (small.gen_sym_eig, multivec.py:174-211): the factor half of the
+// generalized eigensolve -- it is all the repair ladder needs (NotSPD comes
+// from here), and it only involves B-Gram blocks, so b2l_fast_iteration runs
+// it while the stencil pass that produces A W is still on the GPU.
+struct PencilFactor {
+  Mat r;                   // upper Cholesky factor of gb
+  std::vector<double> Ri;  // R^-1 row-major upper (native path)
+  int d = 0;
+};
+
+void pencil_factor(const Mat& gb, double floor_, PencilFactor& f) {
+  f.d = gb.r;
+  f.r = cholesky(gb, floor_);
+  RR_MARK(4);   // pencil Cholesky
+  f.Ri.clear();
+  if (use_lapack()) return;
+  const int d = f.d;
+  f.Ri.assign((size_t)d * d, 0.0);
+  double* Ri = f.Ri.data();
+  for (int i = d - 1; i >= 0; --i) {
+    const double inv = 1.0 / f.r(i, i);
+    double* row = Ri + (size_t)i * d;
+    row[i] = inv;
+    for (int t = i + 1; t < d; ++t) {
+      const double rit = f.r(i, t);
+      const double* rt = Ri + (size_t)t * d;
+      for (int j = t; j < d; ++j) row[j] -= rit * rt[j];
+    }
+    for (int j = i + 1; j < d; ++j) row[j] *= inv;
+  }
+}
+
+// Smallest `want` pairs of ga c = lam gb c given gb's factor; only the upper
+// triangle of ga is read.
+void pencil_solve(const Mat& ga_in, const PencilFactor& f, int want, double* vals_out,
+                  Mat* c_out) {
   const int d = ga_in.r;
   Mat ga(d, d);
   for (int j = 0; j < d; ++j)
     for (int i = 0; i <= j; ++i) ga(i, j) = ga(j, i) = ga_in(i, j);
-  Mat r = cholesky(gb, floor_);
-  RR_MARK(4);   // pencil Cholesky
-  if (!use_lapack()) {
+  if (!f.Ri.empty()) {
     // M = R^-T ga R^-1 through the explicit inverse: row-oriented loops whose
     // inner index runs over independent entries (the substitution form is a
     // chain of dependent dot products, latency-bound at these sizes)
-    thread_local std::vector<double> ri_, t_, m_;
-    ri_.assign((size_t)d * d, 0.0);   // R^-1, row-major upper
+    const double* Ri = f.Ri.data();
+    thread_local std::vector<double> t_, m_, u_, v_;
     t_.assign((size_t)d * d, 0.0);    // ga R^-1, row-major
     m_.assign((size_t)d * d, 0.0);    // column-major (symeig_ql layout)
-    double* Ri = ri_.data();
-    for (int i = d - 1; i >= 0; --i) {
-      const double inv = 1.0 / r(i, i);
-      double* row = Ri + (size_t)i * d;
-      row[i] = inv;
-      for (int t = i + 1; t < d; ++t) {
-        const double rit = r(i, t);
-        const double* rt = Ri + (size_t)t * d;
-        for (int j = t; j < d; ++j) row[j] -= rit * rt[j];
-      }
-      for (int j = i + 1; j < d; ++j) row[j] *= inv;
-    }
     double* T = t_.data();
     for (int i = 0; i < d; ++i) {
       double* ti = T + (size_t)i * d;
@@ -442,7 +460,6 @@ void gen_sym_eig(const Mat& ga_in, const Mat& gb, int want, double floor_, doubl
       }
     }
     // M(i, j) = sum_k Ri(k, i) T(k, j), k <= i; symmetrised as the reference
-    thread_local std::vector<double> u_;
     u_.assign((size_t)d * d, 0.0);
     double* U = u_.data();   // row-major full product
     for (int i = 0; i < d; ++i) {
@@ -457,7 +474,6 @@ void gen_sym_eig(const Mat& ga_in, const Mat& gb, int want, double floor_, doubl
     for (int j = 0; j < d; ++j)
       for (int i = 0; i < d; ++i)
         M[i + (size_t)j * d] = 0.5 * (U[(size_t)i * d + j] + U[(size_t)j * d + i]);
-    thread_local std::vector<double> v_;
     v_.assign((size_t)d * want, 0.0);
     RR_MARK(5);   // R^-T A R^-1
     if (d > 0 && symeig_ql(d, M, want, vals_out, v_.data()) != 0)
@@ -469,14 +485,15 @@ void gen_sym_eig(const Mat& ga_in, const Mat& gb, int want, double floor_, doubl
       const double* v = v_.data() + (size_t)w * d;
       for (int i = 0; i < d; ++i) {
         const double* ri = Ri + (size_t)i * d;
-        double s = 0.0;
-        for (int k = i; k < d; ++k) s += ri[k] * v[k];
-        c(i, w) = s;
+        double acc = 0.0;
+        for (int k = i; k < d; ++k) acc += ri[k] * v[k];
+        c(i, w) = acc;
       }
     }
     *c_out = std::move(c);
     return;
   }
+  const Mat& r = f.r;
   Mat t = trsolve(r, ga, true);
   t = trsolve(r, transpose(t), true);
   Mat ts(d, d);
@@ -519,60 +536,76 @@ extern "C" int b2l_set_lapack(void* dpotrf, void* dtrtrs, void* dtrtri, void* ds
   return 0;
 }
 
-extern "C" int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, int ldg1,
-                                 const double* g2, const double* lam, const int* jact, int kj,
-                                 const int* sel, double pivot_floor, double* lam_out,
-                                 double* coef_out, int* pcols_out, int* kp_out,
-                                 int* fallbacks_out) {
-  if (m < 1 || kst < 0 || kj < 1 || kj > kst || kj > m || !g1 || !g2 || !lam || !jact || !sel)
+namespace b2l {
+
+struct RRPlan;
+inline RRPlan*& rr_tls_plan() {
+  thread_local RRPlan* p = nullptr;
+  return p;
+}
+
+// State between the two halves of the Rayleigh-Ritz step.
+struct RRPlan {
+  int m = 0, kst = 0, kj = 0, nw = 0, pending = 0;
+  bool use_p = false;
+  Mat mw, mp;
+  std::vector<int> wcols, jact;
+  Mat gXAP, gWAP, gPAP;   // A-side blocks that come from G1
+  PencilFactor fac;       // of the final gb (after the repair ladder)
+};
+
+// First half (G1 only: B-Gram blocks and A P): Cholesky-QR of W and P with
+// their ladders, gb and its factor with the pencil ladder (lobpcg.py:475-519).
+int rr_begin(RRPlan& P, int m, int kst, int have_p, const double* g1, int ldg1, const int* jact,
+             int kj, const int* sel, double pivot_floor, int* fallbacks_out) {
+  if (m < 1 || kst < 0 || kj < 1 || kj > kst || kj > m || !g1 || !jact || !sel)
     return fail(-B2L_EINVAL, "rayleigh_ritz: bad arguments");
   g_rr_dim = m + kst + (have_p ? kj : 0);
   const int rW = m, rP = m + kst;
   const int cW = m, cP = m + kst, cAP = 2 * m + kst;
   auto G1 = [&](int i, int j) { return g1[(size_t)i * ldg1 + j]; };
-  auto G2 = [&](int i, int j) { return g2[(size_t)i * kst + j]; };
   RR_MARK(-1);
-  int pending = 0;
+  P = RRPlan{};
+  P.m = m;
+  P.kst = kst;
+  P.kj = kj;
+  P.jact.assign(jact, jact + kj);
   *fallbacks_out = 0;
-  *kp_out = 0;
   try {
     // W: Cholesky-QR with column dropping on the J sub-block (lobpcg.py:475-481)
     std::vector<int> keep(kj);
     for (int i = 0; i < kj; ++i) keep[i] = i;
-    Mat mw;
     while (!keep.empty()) {
       const int k = (int)keep.size();
       Mat gww(k, k);
       for (int b = 0; b < k; ++b)
         for (int a = 0; a < k; ++a) gww(a, b) = G1(rW + sel[keep[a]], cW + sel[keep[b]]);
       try {
-        mw = scaled_cholesky_inv(gww, pivot_floor);
+        P.mw = scaled_cholesky_inv(gww, pivot_floor);
         break;
       } catch (const NotSPD& e) {
         keep.erase(keep.begin() + e.pivot);
       }
     }
-    pending += kj - (int)keep.size();
+    P.pending += kj - (int)keep.size();
     if (keep.empty()) {
-      *fallbacks_out = pending;
+      *fallbacks_out = P.pending;
       return fail(-B2L_EDEGENERATE, "BasisDegeneracy");
     }
-    const int nw = (int)keep.size();
-    std::vector<int> wcols(nw);
-    for (int i = 0; i < nw; ++i) wcols[i] = sel[keep[i]];
+    P.nw = (int)keep.size();
+    P.wcols.resize(P.nw);
+    for (int i = 0; i < P.nw; ++i) P.wcols[i] = sel[keep[i]];
 
     // P_J: Cholesky-QR with floor; NotSPD drops P (lobpcg.py:484-494)
-    Mat mp;
-    bool use_p = false;
     if (have_p) {
       Mat gpp(kj, kj);
       for (int b = 0; b < kj; ++b)
         for (int a = 0; a < kj; ++a) gpp(a, b) = G1(rP + jact[a], cP + jact[b]);
       try {
-        mp = scaled_cholesky_inv(gpp, pivot_floor);
-        use_p = true;
+        P.mp = scaled_cholesky_inv(gpp, pivot_floor);
+        P.use_p = true;
       } catch (const NotSPD&) {
-        pending += 1;
+        P.pending += 1;
       }
     }
     RR_MARK(0);   // W and P Cholesky-QR
@@ -582,96 +615,121 @@ extern "C" int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, i
         for (int a = 0; a < nr; ++a) z(a, b) = G1(r0 + (ri ? ri[a] : a), c0 + ci[b]);
       return z;
     };
-    Mat gXAW(m, nw), gWAW(nw, nw);
-    for (int b = 0; b < nw; ++b) {
-      for (int a = 0; a < m; ++a) gXAW(a, b) = G2(a, wcols[b]);
-      for (int a = 0; a < nw; ++a) gWAW(a, b) = G2(m + wcols[a], wcols[b]);
-    }
-    Mat gXBW = block1(0, nullptr, m, cW, wcols.data(), nw);
-    Mat gXAP, gWAP, gXBP, gWBP, gPAP;
+    const int nw = P.nw;
+    Mat gXBW = block1(0, nullptr, m, cW, P.wcols.data(), nw);
+    Mat gXBP, gWBP;
     if (have_p) {
-      gXAP = block1(0, nullptr, m, cAP, jact, kj);
-      gWAP = block1(rW, wcols.data(), nw, cAP, jact, kj);
+      P.gXAP = block1(0, nullptr, m, cAP, jact, kj);
+      P.gWAP = block1(rW, P.wcols.data(), nw, cAP, jact, kj);
       gXBP = block1(0, nullptr, m, cP, jact, kj);
-      gWBP = block1(rW, wcols.data(), nw, cP, jact, kj);
-      gPAP = block1(rP, jact, kj, cAP, jact, kj);
+      gWBP = block1(rW, P.wcols.data(), nw, cP, jact, kj);
+      P.gPAP = block1(rP, jact, kj, cAP, jact, kj);
     }
-
-    // Rayleigh-Ritz with the repair ladder (lobpcg.py:501-519)
-    Mat c;
-    std::vector<double> vals(m);
+    // the pencil's B side and its repair ladder (lobpcg.py:501-519): NotSPD
+    // drops P, then a W column, then fails
     while (true) {
-      const int kw = mw.c;
-      const int kp = use_p ? kj : 0;
+      const int kw = P.mw.c;
+      const int kp = P.use_p ? kj : 0;
       const int d = m + kw + kp;
-      Mat ga(d, d), gb(d, d);
-      for (int i = 0; i < m; ++i) {
-        ga(i, i) = lam[i];
-        gb(i, i) = 1.0;
-      }
-      const Mat mwT = transpose(mw);
-      const Mat aww = matmul(matmul(mwT, gWAW), mw);
-      const Mat axw = matmul(gXAW, mw), bxw = matmul(gXBW, mw);
+      Mat gb(d, d);
+      for (int i = 0; i < m; ++i) gb(i, i) = 1.0;
+      const Mat mwT = transpose(P.mw);
+      const Mat bxw = matmul(gXBW, P.mw);
       for (int j = 0; j < kw; ++j) {
         gb(m + j, m + j) = 1.0;
-        for (int i = 0; i < kw; ++i) ga(m + i, m + j) = aww(i, j);
-        for (int i = 0; i < m; ++i) {
-          ga(i, m + j) = axw(i, j);
-          gb(i, m + j) = bxw(i, j);
-        }
+        for (int i = 0; i < m; ++i) gb(i, m + j) = bxw(i, j);
       }
       if (kp) {
-        const Mat mpT = transpose(mp);
-        const Mat axp = matmul(gXAP, mp), bxp = matmul(gXBP, mp);
-        const Mat awp = matmul(matmul(mwT, gWAP), mp), bwp = matmul(matmul(mwT, gWBP), mp);
-        const Mat app = matmul(matmul(mpT, gPAP), mp);
+        const Mat bxp = matmul(gXBP, P.mp);
+        const Mat bwp = matmul(matmul(mwT, gWBP), P.mp);
         const int o = m + kw;
         for (int j = 0; j < kp; ++j) {
           gb(o + j, o + j) = 1.0;
-          for (int i = 0; i < m; ++i) {
-            ga(i, o + j) = axp(i, j);
-            gb(i, o + j) = bxp(i, j);
-          }
-          for (int i = 0; i < kw; ++i) {
-            ga(m + i, o + j) = awp(i, j);
-            gb(m + i, o + j) = bwp(i, j);
-          }
-          for (int i = 0; i < kp; ++i) ga(o + i, o + j) = app(i, j);
+          for (int i = 0; i < m; ++i) gb(i, o + j) = bxp(i, j);
+          for (int i = 0; i < kw; ++i) gb(m + i, o + j) = bwp(i, j);
         }
       }
-      RR_MARK(1);   // blocks + pencil assembly
+      RR_MARK(1);   // blocks + pencil assembly (B side)
       try {
-        gen_sym_eig(ga, gb, m, pivot_floor, vals.data(), &c);
-        RR_MARK(2);   // generalized eigensolve
+        pencil_factor(gb, pivot_floor, P.fac);
         break;
       } catch (const NotSPD& e) {
-        pending += 1;
-        if (use_p) {
-          use_p = false;
+        P.pending += 1;
+        if (P.use_p) {
+          P.use_p = false;
         } else if (m <= e.pivot && e.pivot < m + kw && kw > 1) {
-          Mat mw2(mw.r, kw - 1);
+          Mat mw2(P.mw.r, kw - 1);
           int jj = 0;
           for (int j = 0; j < kw; ++j) {
             if (j == e.pivot - m) continue;
-            for (int i = 0; i < mw.r; ++i) mw2(i, jj) = mw(i, j);
+            for (int i = 0; i < P.mw.r; ++i) mw2(i, jj) = P.mw(i, j);
             ++jj;
           }
-          mw = mw2;
+          P.mw = mw2;
         } else {
-          *fallbacks_out = pending;
+          *fallbacks_out = P.pending;
           return fail(-B2L_EDEGENERATE, "BasisDegeneracy");
         }
       }
     }
+    *fallbacks_out = P.pending;
+    return 0;
+  } catch (const LapackError& e) {
+    return fail(-B2L_ELAPACK, std::string("rayleigh_ritz: ") + e.what + " info " +
+                                   std::to_string(e.info));
+  } catch (const std::bad_alloc&) {
+    return fail(-B2L_ENOMEM, "rayleigh_ritz: out of host memory");
+  }
+}
+
+// Second half (needs G2 = [X ; W]^T A W): the pencil's A side, the
+// eigensolve on the factor of the first half, the coefficient folding.
+int rr_finish(RRPlan& P, const double* g2, const double* lam, double* lam_out, double* coef_out,
+              int* pcols_out, int* kp_out, int* fallbacks_out) {
+  if (!g2 || !lam) return fail(-B2L_EINVAL, "rayleigh_ritz: bad arguments");
+  const int m = P.m, kst = P.kst, kj = P.kj, nw = P.nw;
+  auto G2 = [&](int i, int j) { return g2[(size_t)i * kst + j]; };
+  try {
+    Mat gXAW(m, nw), gWAW(nw, nw);
+    for (int b = 0; b < nw; ++b) {
+      for (int a = 0; a < m; ++a) gXAW(a, b) = G2(a, P.wcols[b]);
+      for (int a = 0; a < nw; ++a) gWAW(a, b) = G2(m + P.wcols[a], P.wcols[b]);
+    }
+    const int kw = P.mw.c;
+    const int kp = P.use_p ? kj : 0;
+    const int d = m + kw + kp;
+    Mat ga(d, d);
+    for (int i = 0; i < m; ++i) ga(i, i) = lam[i];
+    const Mat mwT = transpose(P.mw);
+    const Mat aww = matmul(matmul(mwT, gWAW), P.mw);
+    const Mat axw = matmul(gXAW, P.mw);
+    for (int j = 0; j < kw; ++j) {
+      for (int i = 0; i < kw; ++i) ga(m + i, m + j) = aww(i, j);
+      for (int i = 0; i < m; ++i) ga(i, m + j) = axw(i, j);
+    }
+    if (kp) {
+      const Mat mpT = transpose(P.mp);
+      const Mat axp = matmul(P.gXAP, P.mp);
+      const Mat awp = matmul(matmul(mwT, P.gWAP), P.mp);
+      const Mat app = matmul(matmul(mpT, P.gPAP), P.mp);
+      const int o = m + kw;
+      for (int j = 0; j < kp; ++j) {
+        for (int i = 0; i < m; ++i) ga(i, o + j) = axp(i, j);
+        for (int i = 0; i < kw; ++i) ga(m + i, o + j) = awp(i, j);
+        for (int i = 0; i < kp; ++i) ga(o + i, o + j) = app(i, j);
+      }
+    }
+    Mat c;
+    std::vector<double> vals(m);
+    pencil_solve(ga, P.fac, m, vals.data(), &c);
+    RR_MARK(2);   // generalized eigensolve
     // fold the orthonormalization into raw-block coefficients
-    const int kw = mw.c;
-    const int kp = use_p ? kj : 0;
     Mat cw(kw, m), cp(kp, m);
     for (int j = 0; j < m; ++j) {
       for (int i = 0; i < kw; ++i) cw(i, j) = c(m + i, j);
       for (int i = 0; i < kp; ++i) cp(i, j) = c(m + kw + i, j);
     }
-    const Mat cwr = matmul(mw, cw);   // nw x m -> rows wcols of the kst x m block
+    const Mat cwr = matmul(P.mw, cw);   // nw x m -> rows wcols of the kst x m block
     double* cx_o = coef_out;
     double* cw_o = coef_out + (size_t)m * m;
     double* cp_o = cw_o + (size_t)kst * m;
@@ -679,17 +737,17 @@ extern "C" int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, i
       for (int j = 0; j < m; ++j) cx_o[(size_t)i * m + j] = c(i, j);
     for (size_t e = 0; e < (size_t)kst * m; ++e) cw_o[e] = 0.0;
     for (int i = 0; i < nw; ++i)
-      for (int j = 0; j < m; ++j) cw_o[(size_t)wcols[i] * m + j] = cwr(i, j);
+      for (int j = 0; j < m; ++j) cw_o[(size_t)P.wcols[i] * m + j] = cwr(i, j);
     if (kp) {
-      const Mat cpr = matmul(mp, cp);
+      const Mat cpr = matmul(P.mp, cp);
       for (int i = 0; i < kp; ++i) {
-        pcols_out[i] = jact[i];
+        pcols_out[i] = P.jact[i];
         for (int j = 0; j < m; ++j) cp_o[(size_t)i * m + j] = cpr(i, j);
       }
     }
     for (int j = 0; j < m; ++j) lam_out[j] = vals[j];
     *kp_out = kp;
-    *fallbacks_out = pending;
+    *fallbacks_out = P.pending;
     RR_MARK(3);   // coefficient folding
     return 0;
   } catch (const LapackError& e) {
@@ -698,4 +756,34 @@ extern "C" int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, i
   } catch (const std::bad_alloc&) {
     return fail(-B2L_ENOMEM, "rayleigh_ritz: out of host memory");
   }
+}
+
+// The two halves on a per-thread plan (b2l_fast_iteration).
+int rr_begin_tls(int m, int kst, int have_p, const double* g1, int ldg1, const int* jact, int kj,
+                 const int* sel, double pivot_floor, int* fallbacks_out) {
+  thread_local RRPlan plan_;
+  rr_tls_plan() = &plan_;
+  return rr_begin(plan_, m, kst, have_p, g1, ldg1, jact, kj, sel, pivot_floor, fallbacks_out);
+}
+int rr_finish_tls(const double* g2, const double* lam, double* lam_out, double* coef_out,
+                  int* pcols_out, int* kp_out, int* fallbacks_out) {
+  RRPlan* p = rr_tls_plan();
+  if (!p) return fail(-B2L_EINVAL, "rayleigh_ritz: finish without begin");
+  return rr_finish(*p, g2, lam, lam_out, coef_out, pcols_out, kp_out, fallbacks_out);
+}
+
+}  // namespace b2l
+
+extern "C" int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, int ldg1,
+                                 const double* g2, const double* lam, const int* jact, int kj,
+                                 const int* sel, double pivot_floor, double* lam_out,
+                                 double* coef_out, int* pcols_out, int* kp_out,
+                                 int* fallbacks_out) {
+  if (!g2 || !lam) return fail(-B2L_EINVAL, "rayleigh_ritz: bad arguments");
+  thread_local RRPlan plan;
+  *kp_out = 0;
+  const int rc = rr_begin(plan, m, kst, have_p, g1, ldg1, jact, kj, sel, pivot_floor,
+                          fallbacks_out);
+  if (rc) return rc;
+  return rr_finish(plan, g2, lam, lam_out, coef_out, pcols_out, kp_out, fallbacks_out);
 }
