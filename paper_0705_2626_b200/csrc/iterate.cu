@@ -59,6 +59,7 @@ inline double now_us() {
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  const void* owner = nullptr;   // the iteration state whose F1 `join` marks
   bool tried = false;
 };
 SideStream* side_stream() {
@@ -137,7 +138,7 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
   // and h_g2, may still run) and do the G1-only half of the Rayleigh-Ritz
   // step meanwhile; the main stream is synchronised before the G2 half.
   SideStream* side0 = side_stream();
-  const bool early = s->red_on_host == 2 && side0 != nullptr;
+  const bool early = s->red_on_host == 2 && side0 != nullptr && side0->owner == s;
   if (early) {
     B2L_CUDA(cudaEventSynchronize(side0->join));
   } else {
@@ -245,6 +246,7 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
     r = sum_parts(dfr.part, dfr.nparts, dfr.len, dfr.out, side->s);
     if (r) return r;
     B2L_CUDA(cudaEventRecord(side->join, side->s));
+    side->owner = s;
   }
   r = stencil7_gram(s->w_next, s->aw, s->nx, s->ny, s->nz, even(kj), nullptr, 0, 0, s->scale,
                     s->x2, s->ldx, m, kj, g2_h ? g2_h : s->g2_dev, st);
