@@ -238,3 +238,33 @@ def test_relative_tol_and_history_flags(pk):
     assert rep.all_converged
     assert all(h.ritz is None for h in rep.history)
     np.testing.assert_allclose(rep.eigenvalues, pk.exact_eigenvalues((6, 6, 6), 3), rtol=1e-8)
+
+
+def test_interleaved_runs_match_solo_runs(pk):
+    """Two LOBPCGRun objects stepped alternately (they share the library's
+    side stream, workspaces and caches) give the same histories as when each
+    runs alone."""
+    from paper_0705_2626_b200 import lobpcg as lb
+
+    def make(N, m, seed):
+        a, _ = scaled(pk, N)
+        cfg = pk.SolverConfig(block_size=m, tol=1e-8, max_iter=30, seed=seed)
+        return lambda: lb.LOBPCGRun(a, t=pk.jacobi_preconditioner(a), config=cfg)
+
+    mk1, mk2 = make(24, 10, 1), make(20, 8, 2)
+    solo = []
+    for mk in (mk1, mk2):
+        r = mk()
+        while r.step():
+            pass
+        solo.append(np.array([h.ritz for h in r.history]))
+    r1, r2 = mk1(), mk2()
+    more1 = more2 = True
+    while more1 or more2:
+        if more1:
+            more1 = r1.step()
+        if more2:
+            more2 = r2.step()
+    for r, ref in zip((r1, r2), solo):
+        got = np.array([h.ritz for h in r.history])
+        assert got.shape == ref.shape and np.array_equal(got, ref)
