@@ -241,6 +241,20 @@ int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, int ldg1,
                       int* pcols_out, int* kp_out, int* fallbacks_out);
 
 /*
+ * The same step in two halves on a per-thread plan, so a caller can run the
+ * first while the pass producing g2 (A W) is still on the GPU:
+ *   _begin: the G1-only half -- W / P Cholesky-QR with their ladders, the
+ *           pencil's B side, its Cholesky factor and repair ladder;
+ *   _finish: the pencil's A side from g2, the eigensolve, the coefficients.
+ * Arguments and return codes as b2l_rayleigh_ritz (kst is the g2 row stride).
+ */
+int b2l_rayleigh_ritz_begin(int m, int kst, int have_p, const double* g1, int ldg1,
+                            const int* jact, int kj, const int* sel, double pivot_floor,
+                            int* fallbacks_out);
+int b2l_rayleigh_ritz_finish(const double* g2, const double* lam, double* lam_out,
+                             double* coef_out, int* pcols_out, int* kp_out, int* fallbacks_out);
+
+/*
  * Steady-state iteration, host driven natively (lobpcg.py:418-540 when the
  * previous step ran b2l_lobpcg_step + b2l_stencil7_gram): one stream
  * synchronisation fetching red_dev (2m + a*b, a = 2m + kst, b = 3m + kst) and

@@ -106,6 +106,10 @@ SIGNATURES = {
     "b2l_launch_count": (C.c_longlong, []),
     "b2l_set_lapack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "b2l_set_blas": (C.c_int, [C.c_void_p]),
+    "b2l_rayleigh_ritz_begin": (C.c_int, [C.c_int, C.c_int, C.c_int, c_dp, C.c_int, c_ip, C.c_int,
+                                          c_ip, C.c_double, C.POINTER(C.c_int)]),
+    "b2l_rayleigh_ritz_finish": (C.c_int, [c_dp, c_dp, c_dp, c_dp, c_ip, C.POINTER(C.c_int),
+                                           C.POINTER(C.c_int)]),
     "b2l_rayleigh_ritz": (C.c_int, [C.c_int, C.c_int, C.c_int, c_dp, C.c_int, c_dp, c_dp,
                                     c_ip, C.c_int, c_ip, C.c_double, c_dp, c_dp, c_ip, c_ip,
                                     c_ip]),

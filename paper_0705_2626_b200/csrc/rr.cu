@@ -774,6 +774,19 @@ int rr_finish_tls(const double* g2, const double* lam, double* lam_out, double* 
 
 }  // namespace b2l
 
+extern "C" int b2l_rayleigh_ritz_begin(int m, int kst, int have_p, const double* g1, int ldg1,
+                                       const int* jact, int kj, const int* sel,
+                                       double pivot_floor, int* fallbacks_out) {
+  return rr_begin_tls(m, kst, have_p, g1, ldg1, jact, kj, sel, pivot_floor, fallbacks_out);
+}
+
+extern "C" int b2l_rayleigh_ritz_finish(const double* g2, const double* lam, double* lam_out,
+                                        double* coef_out, int* pcols_out, int* kp_out,
+                                        int* fallbacks_out) {
+  *kp_out = 0;
+  return rr_finish_tls(g2, lam, lam_out, coef_out, pcols_out, kp_out, fallbacks_out);
+}
+
 extern "C" int b2l_rayleigh_ritz(int m, int kst, int have_p, const double* g1, int ldg1,
                                  const double* g2, const double* lam, const int* jact, int kj,
                                  const int* sel, double pivot_floor, double* lam_out,

@@ -491,6 +491,7 @@ class LOBPCGRun:
         self.g2 = self._redg2[nred:]
         self.h_red = _host_buf(nred)
         self.h_g2 = _host_buf((2 * m) * m)
+        self.h_g1 = _host_buf((3 * m) * (4 * m))
         self.h_red_np = self.h_red.numpy()
         self.h_g2_np = self.h_g2.numpy()
         self._wviews = {}
@@ -846,10 +847,12 @@ class LOBPCGRun:
 
             # A W (+ [X W]^T A W in the same pass for the built-in stencil)
             g2 = self.g2[:g2_rows * kst].view(g2_rows, kst)
-            if G2 is None:
-                self._launch_aw(W, AW, kst, g2)
             G1dev = None
             if G1 is None:
+                # G1 = [X W P]^T B [X W P (AP)] first: it does not need A W,
+                # so its half of Rayleigh-Ritz (the Cholesky-QRs and the
+                # pencil's B factor) runs on the host while A W and G2 are
+                # still on the GPU
                 if self.have_p:
                     L = [(self.X, m), (W, kst), (self.P, m)]
                     R = L + [(self.AP, m)]
@@ -859,13 +862,27 @@ class LOBPCGRun:
                     L = [(self.X, m), (W, kst)]
                     G1dev = _timed("gram", lambda: self._gram(n, L, L, self._wmask(2), self.bdiag,
                                                            pair_mode=_MODES_NOP))
+            g1_ready = None
+            if G1dev is not None and G2 is None and self.dev.type == "cuda":
+                cnt = G1dev.numel()
+                self.h_g1[:cnt].copy_(G1dev.reshape(-1), non_blocking=True)
+                g1_ready = torch.cuda.Event()
+                g1_ready.record(torch.cuda.current_stream(self.dev))
+            if G2 is None:
+                self._launch_aw(W, AW, kst, g2)
+            begun = False
+            if g1_ready is not None:
+                g1_ready.synchronize()
+                G1 = self.h_g1[:cnt].numpy().reshape(G1dev.shape)
+                self._ritz.begin(m, kst, self.have_p, G1, J, sel, PIVOT_FLOOR)
+                begun = True
+            elif G1dev is not None:
+                G1 = dv.to_host(G1dev)
             if G2 is None:
                 if self.use_sgram:
                     self._reduce(g2)   # the callback path reduced inside self._gram
                 G2 = self._fetch(g2, self.h_g2, g2_rows * kst).reshape(g2_rows, kst)
-            if G1dev is not None:
-                G1 = dv.to_host(G1dev)
-            self._rayleigh_ritz(G1, G2, J, sel, kst, W, AW)
+            self._rayleigh_ritz(G1, G2, J, sel, kst, W, AW, begun=begun)
         except _Failure as f:
             self.failure = str(f)
             self.done = True
@@ -902,13 +919,17 @@ class LOBPCGRun:
         W[:, :kj] = out.to(torch.float64)
         return W, AW, kj, np.arange(kj)
 
-    def _rayleigh_ritz(self, G1, G2, J, sel, kst, W, AW):
+    def _rayleigh_ritz(self, G1, G2, J, sel, kst, W, AW, begun=False):
         """Rayleigh-Ritz on the projected blocks (lobpcg.py:475-519) in the
-        native host routine b2l_rayleigh_ritz, then the device update."""
+        native host routine b2l_rayleigh_ritz (or its second half when
+        `begun`), then the device update."""
         m, n = self.m, self.n
         try:
-            lam_new, coef, pcols, fb = self._ritz(m, kst, self.have_p, G1, G2, self.lam, J, sel,
-                                                  PIVOT_FLOOR)
+            if begun:
+                lam_new, coef, pcols, fb = self._ritz.finish(m, G2, self.lam)
+            else:
+                lam_new, coef, pcols, fb = self._ritz(m, kst, self.have_p, G1, G2, self.lam, J,
+                                                      sel, PIVOT_FLOOR)
         except RitzFailure as f:
             self.pending += f.fallbacks
             raise _Failure("BasisDegeneracy")

@@ -188,3 +188,40 @@ class NativeRitz:
         ncoef = m * m + kst * m + kp * m
         return (self.lam.copy(), self.coef[:ncoef].copy(), self.pcols[:kp].copy(),
                 self._fb.value)
+
+    def begin(self, m, kst, have_p, g1, jact, sel, pivot_floor):
+        """The G1-only half (b2l_rayleigh_ritz_begin); `finish` completes it."""
+        C, L = self._C, self._lib
+        lib = L.load()
+        self._g1 = np.ascontiguousarray(g1, dtype=np.float64)
+        jact = np.ascontiguousarray(jact, dtype=np.int32)
+        sel = np.ascontiguousarray(sel, dtype=np.int32)
+        self._kst = kst
+        rc = lib.b2l_rayleigh_ritz_begin(
+            m, kst, int(have_p), self._g1.ctypes.data_as(L.c_dp), self._g1.shape[1],
+            jact.ctypes.data_as(L.c_ip), jact.size, sel.ctypes.data_as(L.c_ip),
+            float(pivot_floor), C.byref(self._fb))
+        self._begin_rc = rc
+        if rc != 0 and rc != L.EDEGENERATE:
+            L.check(rc, "b2l_rayleigh_ritz_begin")
+
+    def finish(self, m, g2, lam):
+        """The G2 half: same return value as __call__."""
+        C, L = self._C, self._lib
+        lib = L.load()
+        if self._begin_rc == L.EDEGENERATE:
+            raise RitzFailure(self._fb.value)
+        g2 = np.ascontiguousarray(g2, dtype=np.float64)
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        dp, ip = L.c_dp, L.c_ip
+        rc = lib.b2l_rayleigh_ritz_finish(
+            g2.ctypes.data_as(dp), lam.ctypes.data_as(dp), self.lam.ctypes.data_as(dp),
+            self.coef.ctypes.data_as(dp), self.pcols.ctypes.data_as(ip), C.byref(self._kp),
+            C.byref(self._fb))
+        if rc == L.EDEGENERATE:
+            raise RitzFailure(self._fb.value)
+        L.check(rc, "b2l_rayleigh_ritz_finish")
+        kp = self._kp.value
+        ncoef = m * m + self._kst * m + kp * m
+        return (self.lam.copy(), self.coef[:ncoef].copy(), self.pcols[:kp].copy(),
+                self._fb.value)
