@@ -431,7 +431,24 @@ static int gram_big(int nrows, const HostBlock* L, int nl, const HostBlock* R, i
         A.zblk[A.nzero++] = code;
       }
     }
-  const int gy = (A.nblk + GB_MAXW - 1) / GB_MAXW;
+  // CTA groups: a warp's DMMAs issue on its SM sub-partition, so an SM's
+  // pass over one row chunk takes ceil(wpc / 4) warp-rounds; choose the
+  // split that minimises rounds x chunks per CTA (e.g. 30 tile blocks: 4
+  // groups of 8 warps, not 3 of 10)
+  const int nchunks_est = (nrows + 31) / 32;
+  int gy = (A.nblk + GB_MAXW - 1) / GB_MAXW;
+  {
+    long best = -1;
+    for (int g = gy; g <= A.nblk && g <= sm_count(); ++g) {
+      const int w = (A.nblk + g - 1) / g;
+      const int gxg = sm_count() / g;
+      const long cost = (long)((w + 3) / 4) * ((nchunks_est + gxg - 1) / gxg);
+      if (best < 0 || cost * 50 < best * 49) {   // more groups = more L2 re-reads: need 2%
+        best = cost;
+        gy = g;
+      }
+    }
+  }
   A.wpc = (A.nblk + gy - 1) / gy;
   // stage: padded rows of every distinct block (+ the weights)
   int width = 0;
@@ -439,8 +456,15 @@ static int gram_big(int nrows, const HostBlock* L, int nl, const HostBlock* R, i
     A.ustr[u] = smem_stride(G.uld[u]);
     width += A.ustr[u];
   }
+  // the longest row chunk whose 3-stage ring fits in shared memory (longer
+  // chunks = fewer ring hand-offs per DMMA; B2L_GB_RC overrides for sweeps)
+  constexpr size_t kRing = 222 * 1024;
   A.rc = 64;
-  while (A.rc > 8 && (size_t)A.rc * (width + 1) * 8 * 3 > 200 * 1024) A.rc >>= 1;
+  while (A.rc > 8 && (size_t)A.rc * (width + 16) * 8 * 3 > kRing) A.rc >>= 1;
+  if (const char* e = getenv("B2L_GB_RC")) {
+    const int v = atoi(e);
+    if (v == 8 || v == 16 || v == 32 || v == 64) A.rc = v;
+  }
   int off = 0;
   A.stage_tx = 0;
   for (int u = 0; u < A.nu; ++u) {
@@ -451,7 +475,7 @@ static int gram_big(int nrows, const HostBlock* L, int nl, const HostBlock* R, i
   A.dbase = off;
   off += A.d ? ((A.rc + 15) & ~15) : 0;
   A.stage_doubles = off;
-  A.nst = (size_t)off * 8 * 3 <= 200 * 1024 ? 3 : 2;
+  A.nst = (size_t)off * 8 * 3 <= kRing ? 3 : 2;
   const size_t smem = (size_t)A.nst * off * 8 + 128;
   if (smem > 227 * 1024) return 1;
   GbMaps Mp;

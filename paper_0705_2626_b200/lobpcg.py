@@ -167,12 +167,13 @@ class _Failure(Exception):
 
 # Gram block-pair modes (include/b200lobpcg.h): only what the host reads.
 _UPPER = np.array([[2]], dtype=np.uint8)
-# L = [X, W, P], R = [BX, BW, BP, AP]   (the F1 layout)
-_MODES_P = np.array([[2, 1, 1, 1],
+# L = [X, W, P], R = [BX, BW, BP, AP]   (the F1 layout).  X^T B X is left
+# out: Rayleigh-Ritz takes it as I and the drift check has its own Gram
+_MODES_P = np.array([[0, 1, 1, 1],
                      [0, 2, 1, 1],
                      [0, 0, 2, 1]], dtype=np.uint8)
 # L = [X, W], R = [BX, BW]
-_MODES_NOP = np.array([[2, 1],
+_MODES_NOP = np.array([[0, 1],
                        [0, 2]], dtype=np.uint8)
 
 
