@@ -136,3 +136,40 @@ def test_native_rr_all_w_zero_is_degenerate():
     got, gerr, ref, rerr = _both(m, m, True, z, G2, lam, J, J.copy())
     assert got is None and ref is None
     assert gerr == rerr == m
+
+
+def _split(m, kst, have_p, G1, G2, lam, J, sel):
+    nat = NativeRitz(m)
+    try:
+        nat.begin(m, kst, have_p, G1, J, sel, FLOOR)
+        return nat.finish(m, G2, lam), None
+    except RitzFailure as f:
+        return None, f.fallbacks
+
+
+@pytest.mark.parametrize("m,kst,have_p,bdiag,kw", [
+    (10, 10, True, False, {}), (6, 6, True, True, {}), (4, 4, False, False, {}),
+    (5, 5, True, False, {"dup_w": (1, 3)}), (5, 5, True, False, {"dup_p": (0, 2)}),
+    (24, 24, True, True, {})])   # 72 x 72 pencil: the LAPACK branch
+def test_split_rr_equals_one_call(m, kst, have_p, bdiag, kw):
+    """b2l_rayleigh_ritz_begin + _finish (the overlapped form of the unfused
+    path) give exactly what b2l_rayleigh_ritz gives."""
+    G1, G2, lam = _case(max(300, 4 * m), m, kst, have_p, seed=m + 17, bdiag=bdiag, **kw)
+    J = np.arange(m)
+    one = NativeRitz(m)(m, kst, have_p, G1, G2, lam, J, J.copy(), FLOOR)
+    two, err = _split(m, kst, have_p, G1, G2, lam, J, J.copy())
+    assert err is None
+    assert two[3] == one[3]
+    assert np.array_equal(two[0], one[0])
+    assert np.array_equal(two[1], one[1])
+    assert np.array_equal(two[2], one[2])
+
+
+def test_split_rr_degenerate_raises_at_finish():
+    m = 3
+    G1, G2, lam = _case(100, m, m, True, seed=5)
+    z = np.zeros_like(G1)
+    z[:m, :m] = G1[:m, :m]
+    J = np.arange(m)
+    got, fb = _split(m, m, True, z, G2, lam, J, J.copy())
+    assert got is None and fb == m
