@@ -240,15 +240,17 @@ struct GbArgs {
   int stage_doubles;
   uint32_t stage_tx;
   int wpc, nblk, nzero;
+  int ks, nwc;                       // row (k) slices per chunk; compute warps = wpc * ks
   unsigned short blk[GB_MAXBLK];     // (ti0 << 8) | tj0 of needed 4x4 tile blocks
   unsigned short bmask[GB_MAXBLK];   // needed tiles inside the block, bit i*4+j
   unsigned short zblk[GB_MAXBLK];    // tile blocks nobody computes (zeroed)
-  double* partial;                   // [gridDim.x][a*b]
+  double* partial;                   // [gridDim.x][ks][a*b]
 };
 struct GbMaps {
   CUtensorMap u[GRAM_MAXU];
 };
 
+template <int KS>
 __global__ void __launch_bounds__(32 * (GB_MAXW + 1), 1)
     gram_big_kernel(const __grid_constant__ GbMaps M, const __grid_constant__ GbArgs A) {
   extern __shared__ __align__(128) unsigned char gb_raw[];
@@ -259,16 +261,17 @@ __global__ void __launch_bounds__(32 * (GB_MAXW + 1), 1)
   if (tid == 0) {
     for (int s = 0; s < A.nst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], A.wpc);
+      mbar_init(&empty[s], A.nwc);
     }
     fence_mbar_init();
   }
   __syncthreads();
   const int nchunks = (A.nrows + A.rc - 1) / A.rc;
   const int nloc = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  double* out = A.partial + (size_t)blockIdx.x * A.a * A.b;
+  const int ksl = KS == 1 ? 0 : warp / A.wpc;   // this warp's row slice of every chunk
+  double* out = A.partial + ((size_t)blockIdx.x * KS + (warp < A.nwc ? ksl : 0)) * A.a * A.b;
 
-  if (warp == A.wpc) {
+  if (warp == A.nwc) {
     // ---- producer
     if (lane == 0)
       for (int it = 0; it < nloc; ++it) {
@@ -291,8 +294,8 @@ __global__ void __launch_bounds__(32 * (GB_MAXW + 1), 1)
         for (int u = 0; u < A.nu; ++u) tma_load_2d(st + A.ubase[u], &M.u[u], &full[s], 0, r0);
         if (dbulk) bulk_load(st + A.dbase, A.d + r0, (uint32_t)nvalid * 8u, &full[s]);
       }
-  } else if (warp < A.wpc) {
-    const int bi = blockIdx.y * A.wpc + warp;
+  } else if (warp < A.nwc) {
+    const int bi = blockIdx.y * A.wpc + (KS == 1 ? warp : warp % A.wpc);
     const bool act = bi < A.nblk;
     const int ti0 = act ? (A.blk[bi] >> 8) : 0, tj0 = act ? (A.blk[bi] & 255) : 0;
     const unsigned mask = act ? A.bmask[bi] : 0u;
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(32 * (GB_MAXW + 1), 1)
       if (mask) {
         const double* dw = A.d ? st + A.dbase + q : nullptr;
 #pragma unroll 2
-        for (int r = 0; r < A.rc; r += 4) {
+        for (int r = 4 * ksl; r < A.rc; r += 4 * KS) {
           const int k4 = r >> 2;
           double av[GB_TI], bv[GB_TJ];
 #pragma unroll
@@ -382,12 +385,14 @@ __global__ void __launch_bounds__(32 * (GB_MAXW + 1), 1)
   }
   // tile blocks nobody computes: defined zeros (group 0 of every row range)
   if (blockIdx.y == 0)
-    for (int e = tid; e < A.nzero * 256; e += blockDim.x) {
-      const int zb = e >> 8, t = e & 255;
+    for (int e = tid; e < KS * A.nzero * 256; e += blockDim.x) {
+      const int kz = e / (A.nzero * 256), ez = e % (A.nzero * 256);
+      const int zb = ez >> 8, t = ez & 255;
       const int row = 8 * (A.zblk[zb] >> 8) + (t >> 4);
       const int col = 8 * (A.zblk[zb] & 255) + (t & 15) * 2;
+      double* o = A.partial + ((size_t)blockIdx.x * KS + kz) * A.a * A.b;
       for (int c = col; c < col + 2; ++c)
-        if (row < A.a && c < A.b) out[(size_t)row * A.b + c] = 0.0;
+        if (row < A.a && c < A.b) o[(size_t)row * A.b + c] = 0.0;
     }
 }
 
@@ -450,6 +455,15 @@ static int gram_big(int nrows, const HostBlock* L, int nl, const HostBlock* R, i
     }
   }
   A.wpc = (A.nblk + gy - 1) / gy;
+  // few tile blocks per group (e.g. the drift Gram X^T B X: 3): split each
+  // chunk's rows over ks warps per block so every sub-partition has DMMA
+  // work; the ks partials are summed by the fixed-order second stage
+  A.ks = A.wpc * 4 <= GB_MAXW ? 4 : 1;
+  if (const char* e = getenv("B2L_GB_KS")) {
+    const int v = atoi(e);
+    if ((v == 1 || v == 4) && A.wpc * v <= GB_MAXW) A.ks = v;
+  }
+  A.nwc = A.wpc * A.ks;
   // stage: padded rows of every distinct block (+ the weights)
   int width = 0;
   for (int u = 0; u < A.nu; ++u) {
@@ -481,9 +495,11 @@ static int gram_big(int nrows, const HostBlock* L, int nl, const HostBlock* R, i
   GbMaps Mp;
   for (int u = 0; u < A.nu; ++u)
     if (int rc = encode_tmap_2d(&Mp.u[u], G.up[u], G.uld[u], nrows, A.ustr[u], A.rc)) return rc;
-  const int threads = 32 * (A.wpc + 1);
+  const int threads = 32 * (A.nwc + 1);
   int per_sm = 1;
-  if (int rc = prepare_kernel(reinterpret_cast<const void*>(gram_big_kernel), smem, threads,
+  const void* kfn = A.ks == 4 ? reinterpret_cast<const void*>(gram_big_kernel<4>)
+                               : reinterpret_cast<const void*>(gram_big_kernel<1>);
+  if (int rc = prepare_kernel(kfn, smem, threads,
                               &per_sm))
     return rc;
   const int nchunks = (nrows + A.rc - 1) / A.rc;
@@ -491,13 +507,17 @@ static int gram_big(int nrows, const HostBlock* L, int nl, const HostBlock* R, i
   if (gx > nchunks) gx = nchunks;
   if (gx < 1) gx = 1;
   int werr = 0;
-  double* part = static_cast<double*>(workspace((size_t)gx * A.a * A.b * sizeof(double), &werr));
+  double* part =
+      static_cast<double*>(workspace((size_t)gx * A.ks * A.a * A.b * sizeof(double), &werr));
   if (werr) return werr;
   A.partial = part;
-  gram_big_kernel<<<dim3(gx, gy), threads, smem, st>>>(Mp, A);
+  if (A.ks == 4)
+    gram_big_kernel<4><<<dim3(gx, gy), threads, smem, st>>>(Mp, A);
+  else
+    gram_big_kernel<1><<<dim3(gx, gy), threads, smem, st>>>(Mp, A);
   count_launch();
   B2L_CUDA(cudaGetLastError());
-  return sum_parts(part, gx, A.a * A.b, out, st);
+  return sum_parts(part, gx * A.ks, A.a * A.b, out, st);
 }
 
 // pair_mode[l*nr + r]: 0 = block pair not needed, 1 = full, 2 = upper
