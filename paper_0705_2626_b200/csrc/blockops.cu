@@ -707,19 +707,37 @@ __global__ void __launch_bounds__(256) resid_kernel(ResidArgs A) {
     const double lam = A.lam[j];
     const int p = A.pos ? A.pos[j] : -1;
     const bool padw = (p == A.kw - 1) && (A.ldw > A.kw);
-    for (int r = blockIdx.x * A.rp + rr; r < A.nrows; r += gridDim.x * A.rp) {
-      const double xv = A.x[(size_t)r * A.ldx + j];
-      const double av = A.ax[(size_t)r * A.ldx + j];
-      const double bx = A.d ? __dmul_rn(A.d[r], xv) : xv;
-      const double wf = __dsub_rn(av, __dmul_rn(bx, lam));
-      s_w = fma(wf, wf, s_w);
-      if (A.want_ax) s_a = fma(av, av, s_a);
-      if (p >= 0) {
-        double tv = wf;
-        if (A.tmode == 1) tv = __dmul_rn(A.tinv, wf);
-        else if (A.tmode == 2) tv = __dmul_rn(A.tvec[r], wf);
-        A.w[(size_t)r * A.ldw + p] = tv;
-        if (padw) A.w[(size_t)r * A.ldw + A.kw] = 0.0;
+    // four rows per thread in flight: all loads of a group are issued before
+    // its W stores (which may alias nothing, but the compiler cannot know);
+    // the norm chains still run over the rows in the original order
+    constexpr int U = 4;
+    const int stride = gridDim.x * A.rp;
+    for (int r0 = blockIdx.x * A.rp + rr; r0 < A.nrows; r0 += U * stride) {
+      double xv[U], av[U], dv[U], tvv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int r = r0 + u * stride;
+        const bool ok = r < A.nrows;
+        xv[u] = ok ? A.x[(size_t)r * A.ldx + j] : 0.0;
+        av[u] = ok ? A.ax[(size_t)r * A.ldx + j] : 0.0;
+        dv[u] = (ok && A.d) ? A.d[r] : 1.0;
+        tvv[u] = (ok && A.tmode == 2) ? A.tvec[r] : 1.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int r = r0 + u * stride;
+        if (r >= A.nrows) break;
+        const double bx = A.d ? __dmul_rn(dv[u], xv[u]) : xv[u];
+        const double wf = __dsub_rn(av[u], __dmul_rn(bx, lam));
+        s_w = fma(wf, wf, s_w);
+        if (A.want_ax) s_a = fma(av[u], av[u], s_a);
+        if (p >= 0) {
+          double tv = wf;
+          if (A.tmode == 1) tv = __dmul_rn(A.tinv, wf);
+          else if (A.tmode == 2) tv = __dmul_rn(tvv[u], wf);
+          A.w[(size_t)r * A.ldw + p] = tv;
+          if (padw) A.w[(size_t)r * A.ldw + A.kw] = 0.0;
+        }
       }
     }
   }
