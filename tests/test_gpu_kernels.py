@@ -135,6 +135,27 @@ def test_gram_multiblock(dev, n, cols):
                     assert np.all(np.abs(blk_g[iu] - blk_r[iu]) <= 1e-13 * blk_s[iu] + 1e-300)
 
 
+@pytest.mark.parametrize("n,c,mode", [(200003, 64, 2), (70001, 64, 1), (9, 64, 2), (50021, 40, 1)])
+def test_big_gram_few_blocks(dev, n, c, mode):
+    """X^T B X at m = 64 (the drift Gram of C5): few 4x4 tile blocks, so the
+    big-Gram kernel splits every chunk's rows over 4 warps per block; the 4
+    partials per CTA are summed in a fixed order (deterministic)."""
+    from paper_0705_2626_b200 import device as dv
+
+    r = rng(n + c)
+    X = r.standard_normal((n, c))
+    d = r.uniform(1, 2, n)
+    tX, td = blk(X, dev), torch.from_numpy(d).to(dev)
+    pm = np.array([[mode]], dtype=np.uint8)
+    G = dv.gram(n, [(tX, c)], [(tX, c)], 1, td, pair_mode=pm).cpu().numpy()
+    G2 = dv.gram(n, [(tX, c)], [(tX, c)], 1, td, pair_mode=pm).cpu().numpy()
+    assert np.array_equal(G, G2)
+    ref = X.T @ (d[:, None] * X)
+    scale = np.abs(X).T @ (d[:, None] * np.abs(X))
+    sel = np.triu_indices(c) if mode == 2 else np.nonzero(np.ones((c, c)))
+    assert np.all(np.abs(G[sel] - ref[sel]) <= 1e-13 * scale[sel] + 1e-300)
+
+
 def test_gram_is_deterministic(dev):
     from paper_0705_2626_b200 import device as dv
 
