@@ -19,6 +19,33 @@ from __future__ import annotations
 import numpy as np
 from scipy.linalg import lapack
 
+# Pencils above 64 x 64 (m >= 22) go through scipy's LAPACK / BLAS, whose
+# OpenBLAS is multithreaded: on these sizes the thread hand-offs cost more
+# than they save (C5: 44.8 -> 43.1 ms per iteration on the B200 host) and the
+# rounding depends on the host's core count.  Those calls run with one BLAS
+# thread (scoped: the caller's setting is restored), so the Rayleigh-Ritz
+# step is single-threaded and host-independent, as the reference's solve is.
+_BLAS_LIMIT_M = 22
+_tp_ctl = None
+
+
+def _one_blas_thread():
+    global _tp_ctl
+    if _tp_ctl is None:
+        from threadpoolctl import ThreadpoolController
+
+        _tp_ctl = ThreadpoolController()
+    return _tp_ctl.limit(limits=1, user_api="blas")
+
+
+class _NoLimit:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
 _potrf = lapack.dpotrf
 _trtrs = lapack.dtrtrs
 _trtri = lapack.dtrtri
@@ -167,6 +194,9 @@ class NativeRitz:
         self._kp = C.c_int()
         self._fb = C.c_int()
 
+    def _scope(self):
+        return _one_blas_thread() if self.m >= _BLAS_LIMIT_M else _NoLimit()
+
     def __call__(self, m, kst, have_p, g1, g2, lam, jact, sel, pivot_floor):
         C, L = self._C, self._lib
         lib = L.load()
@@ -176,11 +206,13 @@ class NativeRitz:
         jact = np.ascontiguousarray(jact, dtype=np.int32)
         sel = np.ascontiguousarray(sel, dtype=np.int32)
         dp, ip = L.c_dp, L.c_ip
-        rc = lib.b2l_rayleigh_ritz(
-            m, kst, int(have_p), g1.ctypes.data_as(dp), g1.shape[1], g2.ctypes.data_as(dp),
-            lam.ctypes.data_as(dp), jact.ctypes.data_as(ip), jact.size, sel.ctypes.data_as(ip),
-            float(pivot_floor), self.lam.ctypes.data_as(dp), self.coef.ctypes.data_as(dp),
-            self.pcols.ctypes.data_as(ip), C.byref(self._kp), C.byref(self._fb))
+        with self._scope():
+            rc = lib.b2l_rayleigh_ritz(
+                m, kst, int(have_p), g1.ctypes.data_as(dp), g1.shape[1], g2.ctypes.data_as(dp),
+                lam.ctypes.data_as(dp), jact.ctypes.data_as(ip), jact.size,
+                sel.ctypes.data_as(ip), float(pivot_floor), self.lam.ctypes.data_as(dp),
+                self.coef.ctypes.data_as(dp), self.pcols.ctypes.data_as(ip), C.byref(self._kp),
+                C.byref(self._fb))
         if rc == L.EDEGENERATE:
             raise RitzFailure(self._fb.value)
         L.check(rc, "b2l_rayleigh_ritz")
@@ -197,10 +229,11 @@ class NativeRitz:
         jact = np.ascontiguousarray(jact, dtype=np.int32)
         sel = np.ascontiguousarray(sel, dtype=np.int32)
         self._kst = kst
-        rc = lib.b2l_rayleigh_ritz_begin(
-            m, kst, int(have_p), self._g1.ctypes.data_as(L.c_dp), self._g1.shape[1],
-            jact.ctypes.data_as(L.c_ip), jact.size, sel.ctypes.data_as(L.c_ip),
-            float(pivot_floor), C.byref(self._fb))
+        with self._scope():
+            rc = lib.b2l_rayleigh_ritz_begin(
+                m, kst, int(have_p), self._g1.ctypes.data_as(L.c_dp), self._g1.shape[1],
+                jact.ctypes.data_as(L.c_ip), jact.size, sel.ctypes.data_as(L.c_ip),
+                float(pivot_floor), C.byref(self._fb))
         self._begin_rc = rc
         if rc != 0 and rc != L.EDEGENERATE:
             L.check(rc, "b2l_rayleigh_ritz_begin")
@@ -214,10 +247,11 @@ class NativeRitz:
         g2 = np.ascontiguousarray(g2, dtype=np.float64)
         lam = np.ascontiguousarray(lam, dtype=np.float64)
         dp, ip = L.c_dp, L.c_ip
-        rc = lib.b2l_rayleigh_ritz_finish(
-            g2.ctypes.data_as(dp), lam.ctypes.data_as(dp), self.lam.ctypes.data_as(dp),
-            self.coef.ctypes.data_as(dp), self.pcols.ctypes.data_as(ip), C.byref(self._kp),
-            C.byref(self._fb))
+        with self._scope():
+            rc = lib.b2l_rayleigh_ritz_finish(
+                g2.ctypes.data_as(dp), lam.ctypes.data_as(dp), self.lam.ctypes.data_as(dp),
+                self.coef.ctypes.data_as(dp), self.pcols.ctypes.data_as(ip), C.byref(self._kp),
+                C.byref(self._fb))
         if rc == L.EDEGENERATE:
             raise RitzFailure(self._fb.value)
         L.check(rc, "b2l_rayleigh_ritz_finish")
