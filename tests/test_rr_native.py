@@ -173,3 +173,22 @@ def test_split_rr_degenerate_raises_at_finish():
     J = np.arange(m)
     got, fb = _split(m, m, True, z, G2, lam, J, J.copy())
     assert got is None and fb == m
+
+
+def test_large_pencil_rr_is_host_thread_independent():
+    """m >= 22 (LAPACK/BLAS branch): the result does not depend on the
+    caller's BLAS thread count, and that setting is restored afterwards."""
+    from threadpoolctl import ThreadpoolController
+
+    m = 24
+    G1, G2, lam = _case(400, m, m, True, seed=29)
+    J = np.arange(m)
+    ctl = ThreadpoolController()
+    outs = []
+    for nt in (1, 4):
+        with ctl.limit(limits=nt, user_api="blas"):
+            outs.append(NativeRitz(m)(m, m, True, G1, G2, lam, J, J.copy(), FLOOR))
+            after = {i["num_threads"] for i in ctl.select(user_api="blas").info()}
+            assert after == {nt}
+    for a, b in zip(outs[0][:3], outs[1][:3]):
+        assert np.array_equal(a, b)
