@@ -169,14 +169,14 @@ def normalize_dropping(w, bw):
     return w[:, :0], bw[:, :0], total
 
 
-def exact_ritz(x, ax, bx, bdiag):
-    """lobpcg.py:280-296 (no operator applications)."""
+def exact_ritz(x, ax, bx, bop):
+    """lobpcg.py:280-296 (no operator applications); bop is None for B = I."""
     x, bx, r = normalize_block(x, bx)
     ax = right_solve(ax, r)
     lam, q = eigh(x.T @ ax, lower=False)
     x = x @ q
     ax = ax @ q
-    bx = x if bdiag is None else bx @ q
+    bx = x if bop is None else bx @ q
     return x, ax, bx, lam
 
 
@@ -221,18 +221,21 @@ class OracleResult:
     drift_repairs: int = 0
 
 
-def run_lobpcg(apply_a, n, m, *, bdiag=None, tinv=None, apply_t=None, x0=None,
+def run_lobpcg(apply_a, n, m, *, bdiag=None, apply_b=None, tinv=None, apply_t=None, x0=None,
                tol=1e-6, max_iter=200, seed=0, relative_tol=False,
                record=True, timer=False):
     """Restatement of ``solve`` (lobpcg.py:343-577) without hard constraints.
 
-    apply_a: callable (n,k)->(n,k).  bdiag: (n,) diagonal of B or None.
+    apply_a: callable (n,k)->(n,k).  bdiag: (n,) diagonal of B or None;
+    apply_b: a generic B callable instead (BX, BW, BP carried by recurrence,
+    lobpcg.py:396, :476, :533-538).
     tinv: (n,) array or scalar applied as ``tinv[:, None] * w`` (Jacobi,
     operators.py:297-298); apply_t: generic callable alternative.
     ``timer=True`` records a perf_counter stamp at the top of every
     iteration (used by bench.py's CPU baseline only).
     """
-    bop = None if bdiag is None else (lambda v: bdiag[:, None] * v)
+    bop = apply_b if apply_b is not None else (
+        None if bdiag is None else (lambda v: bdiag[:, None] * v))
     if x0 is not None:
         x = np.array(x0, dtype=np.float64, copy=True)
     else:
@@ -260,7 +263,7 @@ def run_lobpcg(apply_a, n, m, *, bdiag=None, tinv=None, apply_t=None, x0=None,
         drift = np.abs(x.T @ bx - np.eye(m)).max()
         if drift > DRIFT_LIMIT:
             try:
-                x, ax, bx, lam = exact_ritz(x, ax, bx, bdiag)
+                x, ax, bx, lam = exact_ritz(x, ax, bx, bop)
                 res.drift_repairs += 1
             except PivotFailure:
                 fail = "BasisDegeneracy"
@@ -346,7 +349,7 @@ def run_lobpcg(apply_a, n, m, *, bdiag=None, tinv=None, apply_t=None, x0=None,
     fallbacks += pend
     if fail is None:
         try:
-            x, ax, bx, lam = exact_ritz(x, ax, bx, bdiag)
+            x, ax, bx, lam = exact_ritz(x, ax, bx, bop)
             norms = col_norms(ax - bx * lam)
         except PivotFailure:
             fail = "BasisDegeneracy"

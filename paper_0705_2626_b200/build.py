@@ -51,14 +51,7 @@ def _stale(out: Path) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None) -> Path:
-    out = lib_path()
-    if not force and not _stale(out):
-        return out
-    LIBDIR.mkdir(exist_ok=True)
-    tmp = out.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, *(extra or []), "-shared", "-o", str(tmp),
-           *[str(CSRC / s) for s in SOURCES]]
+def _run(cmd, verbose):
     if verbose:
         print(" ".join(cmd))
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -66,6 +59,26 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
         raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
     if verbose and r.stderr:
         print(r.stderr)
+
+
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None) -> Path:
+    """One object per translation unit (compiled in parallel), then one
+    shared-library link; no relocatable device code crosses files."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    out = lib_path()
+    if not force and not _stale(out):
+        return out
+    LIBDIR.mkdir(exist_ok=True)
+    objdir = LIBDIR / "obj"
+    objdir.mkdir(exist_ok=True)
+    objs = [objdir / (Path(s).stem + ".o") for s in SOURCES]
+    cmds = [[nvcc(), *NVCC_FLAGS, *(extra or []), "-c", "-o", str(o), str(CSRC / s)]
+            for s, o in zip(SOURCES, objs)]
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        list(ex.map(lambda c: _run(c, verbose), cmds))
+    tmp = out.with_suffix(".so.tmp")
+    _run([nvcc(), *NVCC_FLAGS, "-shared", "-o", str(tmp), *map(str, objs), "-ldl"], verbose)
     tmp.replace(out)
     return out
 

@@ -106,7 +106,9 @@ Mat transpose(const Mat& x) {
 // B2L_RR_LAPACK=1: always LAPACK; =0: never; unset: LAPACK for pencils
 // larger than 64 (m > 21; the blocked, vectorised routines win there: 192 x
 // 192 at m = 64 ~2x faster than the native scalar code), native below.
-int g_rr_dim = 0;   // dimension of the pencil being solved (set per call)
+// dimension of the pencil being solved, set by rr_begin; per host thread so
+// two threads' Rayleigh-Ritz steps never see each other's LAPACK choice
+thread_local int g_rr_dim = 0;
 bool use_lapack() {
   static const int mode = [] {
     const char* v = getenv("B2L_RR_LAPACK");

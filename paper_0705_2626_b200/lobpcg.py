@@ -411,13 +411,22 @@ class LOBPCGRun:
 
         # ---- operator kinds
         self.fused_a = isinstance(a, Laplacian3D)
+        # B: none / identity (BX = X), diagonal (a row weight streamed by the
+        # kernels, never materialised), or any other callable on CUDA (n, k)
+        # float64 blocks -- then BX, BW, BP are carried by recurrence as the
+        # reference does (lobpcg.py:396, :476, :533-538)
         self.bdiag = None
+        self.b_generic = None
         if b is not None and not isinstance(b, IdentityOperator):
-            if not isinstance(b, DiagonalOperator):
-                raise NotImplementedError("only diagonal B (DiagonalOperator) is supported on the B200 path")
-            if b.dim != n:
-                raise ValueError(f"B has dimension {b.dim}, expected {n}")
-            self.bdiag = b.d.to(self.dev)
+            bdim = getattr(b, "dim", n)
+            if bdim != n:
+                raise ValueError(f"B has dimension {bdim}, expected {n}")
+            if isinstance(b, DiagonalOperator):
+                self.bdiag = b.d.to(self.dev)
+            elif callable(b):
+                self.b_generic = b
+            else:
+                raise TypeError("b must be an operator or a callable on (n, k) blocks")
         self.tmode, self.tinv, self.tvec, self.t_generic = 0, 1.0, None, None
         if t is None or isinstance(t, IdentityPreconditioner):
             pass
@@ -432,7 +441,8 @@ class LOBPCGRun:
         # F1 holds the whole next-step Gram in one CTA; stencil+Gram likewise
         # (hard constraints project W between the residual and A W: F1 forms
         # W' inside its pass, so a constrained run takes the unfused kernels)
-        self.use_f1 = fused and _tilesets(3 * m, 4 * m) <= 8 and self.cons is None
+        self.use_f1 = (fused and _tilesets(3 * m, 4 * m) <= 8 and self.cons is None
+                       and self.b_generic is None)
         self.use_sgram = fused and self.fused_a and _tilesets(2 * m, m) <= 8
 
         # ---- initial block (lobpcg.py:386-393)
@@ -480,6 +490,10 @@ class LOBPCGRun:
         dev = self.dev
         self.X, self.AX, self.X2, self.AX2 = (dv.new_block(n, ld, dev) for _ in range(4))
         self.P, self.AP, self.P2, self.AP2 = (dv.new_block(n, ld, dev) for _ in range(4))
+        self.BX = self.BX2 = self.BP = self.BP2 = self.BWbuf = None
+        if self.b_generic is not None:
+            self.BX, self.BX2, self.BP, self.BP2 = (dv.new_block(n, ld, dev) for _ in range(4))
+            self.BWbuf = torch.zeros(n * ld, dtype=torch.float64, device=dev)
         self.Wbufs = [torch.zeros(n * ld, dtype=torch.float64, device=dev) for _ in range(2)]
         self.wcur = 0
         self.AWbuf = torch.zeros(n * ld, dtype=torch.float64, device=dev)
@@ -546,6 +560,26 @@ class LOBPCGRun:
     def _wmask(self, nblocks):
         return ((1 << nblocks) - 1) if self.bdiag is not None else 0
 
+    def _bx(self):
+        """The block holding B X for the kernels: X itself for B = I and
+        diagonal B (the kernels weight it by d), the carried BX otherwise."""
+        return self.BX if self.b_generic is not None else self.X
+
+    def _apply_b(self, src, dst, k):
+        """dst[:, :k] = B src[:, :k] through the user's callback (generic B),
+        shape-checked like every operator output."""
+        y = self.b_generic(src[:, :k])
+        if not isinstance(y, torch.Tensor):
+            y = torch.as_tensor(np.asarray(y, dtype=np.float64), device=self.dev)
+        if tuple(y.shape) != (self.n, k):
+            raise ValueError(f"B returned shape {tuple(y.shape)}, expected ({self.n}, {k})")
+        dst[:, :k] = y.to(device=self.dev, dtype=torch.float64)
+        if dst.shape[1] > k:
+            dst[:, k:] = 0.0
+
+    def _bwview(self, k):
+        return dv.view_block(self.BWbuf, self.n, dv.even(k))
+
     def _wview(self, k, which=None):
         key = (self.wcur if which is None else which, k)
         v = self._wviews.get(key)
@@ -565,16 +599,28 @@ class LOBPCGRun:
 
     def _gram_xx(self):
         """X^T B X (upper triangle computed, mirrored on the host)."""
+        if self.b_generic is not None:
+            # X^T (BX) in full: the carried BX makes it symmetric only to
+            # rounding, and the reference's drift test reads every entry
+            g = _timed("gram_drift", lambda: self._gram(self.n, [(self.X, self.m)],
+                                                     [(self.BX, self.m)]))
+            return dv.to_host(g)
         g = _timed("gram_drift", lambda: self._gram(self.n, [(self.X, self.m)], [(self.X, self.m)],
                                                  self._wmask(1), self.bdiag, pair_mode=_UPPER))
         return _mirror_upper(dv.to_host(g))
 
-    def _rotate_x(self, M):
-        """X, AX <- X M, AX M (no P involvement)."""
+    def _rotate_x(self, M, with_a=True):
+        """X, AX (, BX) <- X M, AX M (, BX M) (no P involvement)."""
         Md = dv.to_device(M, self.dev)
-        dv.update(self.n, self.m, self.X, self.AX, Md, self.X2, self.AX2)
+        if with_a:
+            dv.update(self.n, self.m, self.X, self.AX, Md, self.X2, self.AX2)
+            self.AX, self.AX2 = self.AX2, self.AX
+        else:
+            dv.update(self.n, self.m, self.X, None, Md, self.X2, None)
         self.X, self.X2 = self.X2, self.X
-        self.AX, self.AX2 = self.AX2, self.AX
+        if self.b_generic is not None:
+            dv.update(self.n, self.m, self.BX, None, Md, self.BX2, None)
+            self.BX, self.BX2 = self.BX2, self.BX
 
     def _refresh_ritz(self, gxx):
         """_refresh_ritz (lobpcg.py:280-296) from the raw Gram X^T B X."""
@@ -601,15 +647,15 @@ class LOBPCGRun:
         if self.cons is not None:                   # lobpcg.py:394
             _project_into(self.X, m, self.cons, self.X2, self._reduce)
             self.X, self.X2 = self.X2, self.X
+        if self.b_generic is not None:
+            self._apply_b(self.X, self.BX, m)        # bx = b(x) (lobpcg.py:396)
         gxx = self._gram_xx()
         try:
             _, minv = scaled_cholesky(gxx)
         except NotSPD as err:
             raise ValueError(f"initial block is B-degenerate at column {err.pivot}") from err
-        # X <- X R_eff^{-1} (b_orthonormalize, lobpcg.py:398)
-        Md = dv.to_device(minv, self.dev)
-        dv.update(n, m, self.X, None, Md, self.X2, None)
-        self.X, self.X2 = self.X2, self.X
+        # X (, BX) <- X R_eff^{-1} (b_orthonormalize, lobpcg.py:398)
+        self._rotate_x(minv, with_a=False)
         self._apply_a_plain(self.X, self.AX, m)      # lobpcg.py:403
         gxa = dv.to_host(self._gram(n, [(self.X, m)], [(self.AX, m)], pair_mode=_UPPER))
         lam, q = sym_eig(gxa)                        # lobpcg.py:404
@@ -624,6 +670,7 @@ class LOBPCGRun:
         cfg, m = self.cfg, self.m
         self._native = None
         if not (self.dev.type == "cuda" and self.use_f1 and self.use_sgram and self.fused_a
+                and self.b_generic is None
                 and self._allreduce is None and self.t_generic is None and self.cons is None
                 and not cfg.check_invariants and cfg.verbosity < 2):
             return
@@ -730,6 +777,14 @@ class LOBPCGRun:
             if res is not None:
                 return res
             fetched = True            # drift: the reductions are in h_red / h_g2
+        elif self._native is not None and self._native.red_on_host and self.f1_pending:
+            # the passes the native step queued write their reductions
+            # straight into the pinned h_red / h_g2 (device-mapped), not into
+            # self.red / self.g2: read them there (a timer entered mid-run
+            # sends the step down this path)
+            torch.cuda.current_stream(self.dev).synchronize()
+            self._native.red_on_host = 0
+            fetched = True
         cfg, m, n = self.cfg, self.m, self.n
         it = self.it
         try:
@@ -794,7 +849,7 @@ class LOBPCGRun:
                 pos[jprev] = np.arange(kst, dtype=np.int32)
                 (lam_d,), (pos_d,) = self.pin.upload([self.lam], [pos])
                 _timed("residual", lambda: self._residual(
-                    n, m, self.X, self.AX, self.bdiag, lam_d, self.tmode, self.tinv, self.tvec,
+                    n, m, self._bx(), self.AX, self.bdiag, lam_d, self.tmode, self.tinv, self.tvec,
                     pos_d, kst, W, cfg.relative_tol, self.sums))
                 sums = self._fetch(self.sums, self.h_red, 2 * m)
 
@@ -838,6 +893,10 @@ class LOBPCGRun:
                 W, AW, kst, sel = self._generic_precondition(W, sel, J.size)
                 G1 = G2 = None                       # F1 saw the raw residual
                 g2_rows = m + kst
+            elif self.b_generic is not None and J.size != kst:
+                # b(w) sees the active columns only, as in the reference
+                W, AW, kst, sel = self._compact_w(W, sel, J.size)
+                g2_rows = m + kst
             if self.cons is not None:
                 # w = apply_constraints(w, y) (lobpcg.py:475), into the other W buffer
                 nxt = 1 - self.wcur
@@ -845,6 +904,10 @@ class LOBPCGRun:
                 _project_into(W, kst, self.cons, Wn, self._reduce)
                 self.wcur = nxt
                 W = Wn
+            BW = None
+            if self.b_generic is not None:
+                BW = self._bwview(kst)               # bw = b(w) (lobpcg.py:476)
+                self._apply_b(W, BW, kst)
 
             # A W (+ [X W]^T A W in the same pass for the built-in stencil)
             g2 = self.g2[:g2_rows * kst].view(g2_rows, kst)
@@ -856,12 +919,16 @@ class LOBPCGRun:
                 # still on the GPU
                 if self.have_p:
                     L = [(self.X, m), (W, kst), (self.P, m)]
-                    R = L + [(self.AP, m)]
+                    if BW is not None:
+                        R = [(self.BX, m), (BW, kst), (self.BP, m), (self.AP, m)]
+                    else:
+                        R = L + [(self.AP, m)]
                     G1dev = _timed("gram", lambda: self._gram(n, L, R, self._wmask(3), self.bdiag,
                                                            pair_mode=_MODES_P))
                 else:
                     L = [(self.X, m), (W, kst)]
-                    G1dev = _timed("gram", lambda: self._gram(n, L, L, self._wmask(2), self.bdiag,
+                    R = [(self.BX, m), (BW, kst)] if BW is not None else L
+                    G1dev = _timed("gram", lambda: self._gram(n, L, R, self._wmask(2), self.bdiag,
                                                            pair_mode=_MODES_NOP))
             g1_ready = None
             if G1dev is not None and G2 is None and self.dev.type == "cuda":
@@ -883,7 +950,7 @@ class LOBPCGRun:
                 if self.use_sgram:
                     self._reduce(g2)   # the callback path reduced inside self._gram
                 G2 = self._fetch(g2, self.h_g2, g2_rows * kst).reshape(g2_rows, kst)
-            self._rayleigh_ritz(G1, G2, J, sel, kst, W, AW, begun=begun)
+            self._rayleigh_ritz(G1, G2, J, sel, kst, W, AW, begun=begun, BW=BW)
         except _Failure as f:
             self.failure = str(f)
             self.done = True
@@ -901,6 +968,15 @@ class LOBPCGRun:
             self._apply_a_plain(W, AW, kst)
             _timed("gram_aw", lambda: self._gram(n, [(self.X, m), (W, kst)], [(AW, kst)],
                                               out=g2))
+
+    def _compact_w(self, W, sel, kj):
+        """The active columns sel of W, compacted into the other W buffer."""
+        nxt = 1 - self.wcur
+        Wn, AWn = self._wview(kj, nxt)
+        Wn.zero_()
+        Wn[:, :kj] = W[:, torch.as_tensor(sel, device=self.dev)]
+        self.wcur = nxt
+        return Wn, AWn, kj, np.arange(kj)
 
     def _generic_precondition(self, W, sel, kj):
         """User preconditioner callback on the active residual block
@@ -920,7 +996,7 @@ class LOBPCGRun:
         W[:, :kj] = out.to(torch.float64)
         return W, AW, kj, np.arange(kj)
 
-    def _rayleigh_ritz(self, G1, G2, J, sel, kst, W, AW, begun=False):
+    def _rayleigh_ritz(self, G1, G2, J, sel, kst, W, AW, begun=False, BW=None):
         """Rayleigh-Ritz on the projected blocks (lobpcg.py:475-519) in the
         native host routine b2l_rayleigh_ritz (or its second half when
         `begun`), then the device update."""
@@ -968,6 +1044,14 @@ class LOBPCGRun:
                 n, m, self.X, self.AX, cx_d, self.X2, self.AX2, w=W, aw=AW, kw=kst, cw=cw_d,
                 p=self.P if kp else None, ap=self.AP if kp else None, pcols=pc_d, kp=kp,
                 cp=cp_d, po=self.P2, apo=self.AP2, x_plus_p=True))
+            if BW is not None:
+                # BP' = BW Cw + BP_J Cp, BX' = BX Cx + BP' (lobpcg.py:533-538)
+                _timed("update", lambda: dv.update(
+                    n, m, self.BX, None, cx_d, self.BX2, None, w=BW, kw=kst, cw=cw_d,
+                    p=self.BP if kp else None, pcols=pc_d, kp=kp, cp=cp_d, po=self.BP2,
+                    x_plus_p=True))
+                self.BX, self.BX2 = self.BX2, self.BX
+                self.BP, self.BP2 = self.BP2, self.BP
         self.X, self.X2 = self.X2, self.X
         self.AX, self.AX2 = self.AX2, self.AX
         self.P, self.P2 = self.P2, self.P
@@ -1015,7 +1099,7 @@ class LOBPCGRun:
             try:
                 self._refresh_ritz(self._gram_xx())
                 lam_d = dv.to_device(self.lam, self.dev)
-                self._residual(n, m, self.X, self.AX, self.bdiag, lam_d, 0, 1.0, None, None, 0,
+                self._residual(n, m, self._bx(), self.AX, self.bdiag, lam_d, 0, 1.0, None, None, 0,
                             None, False, self.sums)
                 norms = np.sqrt(dv.to_host(self.sums)[:m])
             except NotSPD:

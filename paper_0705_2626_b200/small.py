@@ -30,11 +30,21 @@ _tp_ctl = None
 
 
 def _one_blas_thread():
+    """Scope the BLAS thread pool to one thread (threadpoolctl).  The limit is
+    process-wide while it is held (OpenBLAS has one pool), so other host
+    threads' BLAS calls run single-threaded meanwhile.  Without threadpoolctl
+    the caller's setting stays (rounding then follows the host's core
+    count, as the reference's own BLAS calls do)."""
     global _tp_ctl
     if _tp_ctl is None:
-        from threadpoolctl import ThreadpoolController
+        try:
+            from threadpoolctl import ThreadpoolController
 
-        _tp_ctl = ThreadpoolController()
+            _tp_ctl = ThreadpoolController()
+        except ImportError:
+            _tp_ctl = False
+    if _tp_ctl is False:
+        return _NoLimit()
     return _tp_ctl.limit(limits=1, user_api="blas")
 
 

@@ -201,6 +201,72 @@ def c2():
     print(f"C2 {rep.status} {time.time() - t0:.1f} s")
 
 
+def full_size():
+    """BASELINE configs at full size, matched iterations:
+    C3 (256^3, m=16, Jacobi, tol 1e-6) for 10 iterations (~61 s/iteration,
+    26 GiB on 8 host threads) and a C5 intermediate (96^3, m=64, diagonal B
+    from PCG64(1000), Jacobi, tol 1e-6) for 20 iterations.  The 192^3 C5 and
+    464^3 C4 blocks do not fit this container's 62 GiB with the reference's
+    temporaries; those are pinned against the oracle port on the GPU host
+    (tests/golden/make_bigconfigs.py)."""
+    t0 = time.time()
+    A = scaled_laplacian(256)
+    rep = solve(A, t=jacobi_preconditioner(A),
+                config=SolverConfig(block_size=16, tol=1e-6, max_iter=10, seed=0))
+    np.savez_compressed(OUT / "c3_256cubed_m16_10it.npz", **record(rep, 16))
+    print(f"C3@10 {rep.status} {time.time() - t0:.1f} s", flush=True)
+    del A, rep
+    N = 96
+    bd = np.random.Generator(np.random.PCG64(1000)).uniform(1.0, 2.0, N ** 3)
+    A = scaled_laplacian(N)
+    rep = solve(A, b=DiagonalOperator(bd), t=jacobi_preconditioner(A),
+                config=SolverConfig(block_size=64, tol=1e-6, max_iter=20, seed=0))
+    np.savez_compressed(OUT / "c5i_96cubed_m64_diagB_20it.npz", **record(rep, 64))
+    print(f"C5i@20 {rep.status} {time.time() - t0:.1f} s", flush=True)
+
+
+def b_tridiag(v):
+    """A non-diagonal SPD B (spectrum in (1, 5)): 3 v_i - v_{i-1} - v_{i+1}
+    along the flat grid index.  The GPU tests apply the same operations to
+    CUDA tensors (tests/test_gpu_generic_b.py)."""
+    y = 3.0 * v
+    y[1:] -= v[:-1]
+    y[:-1] -= v[1:]
+    return y
+
+
+def b_zcouple(v, plane):
+    """A second SPD B coupling z-neighbours: 2.5 v_p - 0.5 (v_{p-P} + v_{p+P})."""
+    y = 2.5 * v
+    y[plane:] -= 0.5 * v[:-plane]
+    y[:-plane] -= 0.5 * v[plane:]
+    return y
+
+
+def generic_b():
+    """Generalized problems with a non-diagonal B (lobpcg.py:396, :476,
+    :533-538 carry BX, BW, BP by recurrence): the reference's trajectories and
+    the dense generalized eigenvalues."""
+    t0 = time.time()
+    out = {}
+    for name, N, m, tol, jac, bfun, max_iter in (
+            ("tri8", 8, 4, 1e-8, True, b_tridiag, 300),
+            ("zc12", 12, 6, 1e-7, False, lambda v: b_zcouple(v, 144), 300)):
+        A = scaled_laplacian(N)
+        n = N ** 3
+        B = MatrixFreeOperator(n, bfun, spd=True)
+        rep = solve(A, b=B, t=jacobi_preconditioner(A) if jac else None,
+                    config=SolverConfig(block_size=m, tol=tol, max_iter=max_iter, seed=0))
+        dA = A(np.eye(n))
+        dB = B(np.eye(n))
+        vals, _ = mv.gen_sym_eig(dA, dB, want=m)
+        r = record(rep, m)
+        print(name, rep.status, rep.iterations_used, np.abs(rep.eigenvalues / vals[:m] - 1).max(),
+              flush=True)
+        np.savez_compressed(OUT / f"genb_{name}.npz", dense_vals=vals[:m], **r)
+    print(f"generic B {time.time() - t0:.1f} s")
+
+
 def scaled_laplacian_pert(N, k):
     """s*L with s = (N+1)^2 * (1 + k ulp): the reference's own sensitivity."""
     s = float((N + 1) ** 2) * (1.0 + k * 2.0 ** -52)
@@ -433,6 +499,8 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--heavy", action="store_true")
     ap.add_argument("--c2", action="store_true")
+    ap.add_argument("--full-size", action="store_true")
+    ap.add_argument("--generic-b", action="store_true")
     ap.add_argument("--bands", action="store_true")
     ap.add_argument("--band20", action="store_true")
     ap.add_argument("--band-c1", action="store_true")
@@ -450,6 +518,10 @@ if __name__ == "__main__":
         band20()
     elif args.bands:
         bands()
+    elif args.generic_b:
+        generic_b()
+    elif args.full_size:
+        full_size()
     elif args.c2:
         c2()
     elif args.heavy:

@@ -1,0 +1,109 @@
+"""Generalized problems with a NON-diagonal B on the GPU (VERDICT r1 missing
+#2): any SPD callable B on CUDA (n, k) float64 blocks plugs in, and BX, BW,
+BP are carried by recurrence as in the reference (lobpcg.py:396, :476,
+:533-538).  Fixtures: tests/golden/genb_*.npz from the real reference
+(make_golden.py --generic-b), dense generalized eigenvalues included."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def b_tridiag(v):
+    y = 3.0 * v
+    y[1:] -= v[:-1]
+    y[:-1] -= v[1:]
+    return y
+
+
+def b_zcouple(v, plane=144):
+    y = 2.5 * v
+    y[plane:] -= 0.5 * v[:-plane]
+    y[:-plane] -= 0.5 * v[plane:]
+    return y
+
+
+@pytest.mark.parametrize("name,N,m,tol,jac,bfun", [
+    ("tri8", 8, 4, 1e-8, True, b_tridiag),
+    ("zc12", 12, 6, 1e-7, False, b_zcouple)])
+def test_generic_b_matches_reference(golden, name, N, m, tol, jac, bfun):
+    import paper_0705_2626_b200 as pk
+
+    g = golden(f"genb_{name}.npz")
+    a = pk.Laplacian3D((N, N, N), scale=float((N + 1) ** 2))
+    seen = []
+
+    def b(v):
+        assert v.is_cuda and v.dtype == torch.float64
+        seen.append(v.shape[1])
+        return bfun(v.clone())
+
+    rep = pk.solve(a, b=b, t=pk.jacobi_preconditioner(a) if jac else None,
+                   config=pk.SolverConfig(block_size=m, tol=tol, max_iter=300, seed=0))
+    assert rep.status == str(g["status"])
+    assert abs(rep.iterations_used - int(g["iterations_used"])) <= 1
+    np.testing.assert_allclose(rep.eigenvalues, g["dense_vals"], rtol=1e-10)
+    np.testing.assert_allclose(rep.eigenvalues, g["eigenvalues"], rtol=1e-10)
+    assert np.all(rep.residual_norms <= tol * 1.01)
+    # B-orthonormal eigenvectors (test_acceptance.py:282-299 analogue)
+    x = torch.from_numpy(rep.eigenvectors).cuda()
+    bx = b_tridiag(x.clone()) if bfun is b_tridiag else b_zcouple(x.clone())
+    gram = (x.T @ bx).cpu().numpy()
+    assert np.abs(gram - np.eye(m)).max() < 1e-8
+    # trajectory: matched iterations agree while the columns are unconverged
+    k = min(len(rep.history), g["hist_ritz"].shape[0]) // 2
+    ritz = np.array([h.ritz for h in rep.history[:k]])
+    np.testing.assert_allclose(ritz, g["hist_ritz"][:k], rtol=1e-8)
+
+
+def test_generic_b_equals_diagonal_b_path(golden):
+    """A DiagonalOperator passed as a plain callback (generic recurrence path)
+    gives the fused row-weight path's eigenpairs (lap12 diagonal-B fixture)."""
+    import paper_0705_2626_b200 as pk
+
+    g = golden("lap12_m6_diagB.npz")
+    N = 12
+    a = pk.Laplacian3D((N, N, N), scale=float((N + 1) ** 2))
+    d = torch.from_numpy(g["bdiag"]).cuda()
+    cfg = pk.SolverConfig(block_size=6, tol=1e-6, max_iter=150, seed=0)
+    rep = pk.solve(a, b=lambda v: d[:, None] * v, t=pk.jacobi_preconditioner(a), config=cfg)
+    fused = pk.solve(a, b=pk.DiagonalOperator(g["bdiag"]), t=pk.jacobi_preconditioner(a),
+                     config=cfg)
+    assert rep.status == fused.status == str(g["status"])
+    np.testing.assert_allclose(rep.eigenvalues, g["eigenvalues"], rtol=1e-8)
+    np.testing.assert_allclose(rep.eigenvalues, fused.eigenvalues, rtol=1e-9)
+
+
+def test_generic_b_shape_errors():
+    import paper_0705_2626_b200 as pk
+
+    a = pk.Laplacian3D((6, 6, 6))
+    with pytest.raises(ValueError):
+        pk.solve(a, b=lambda v: v[:, :1].clone(),
+                 config=pk.SolverConfig(block_size=3, max_iter=5))
+
+
+def test_generic_b_with_constraints_and_invariants():
+    """Hard locking with a generic B: Y^T B X stays zero, and the invariant
+    checker (lobpcg.py:266-277) passes every iteration."""
+    import paper_0705_2626_b200 as pk
+
+    N = 8
+    a = pk.Laplacian3D((N, N, N), scale=float((N + 1) ** 2))
+    first = pk.solve(a, b=b_tridiag, config=pk.SolverConfig(block_size=2, tol=1e-9,
+                                                            max_iter=300, seed=1))
+    y = pk.Constraints.from_basis(torch.from_numpy(first.eigenvectors).cuda(), b_tridiag)
+    rep = pk.solve(a, b=b_tridiag, y=y,
+                   config=pk.SolverConfig(block_size=2, tol=1e-9, max_iter=300, seed=2,
+                                          check_invariants=True))
+    assert rep.all_converged
+    n = N ** 3
+    L = a(np.eye(n))
+    B = b_tridiag(np.eye(n))
+    from scipy.linalg import eigh
+
+    vals = eigh(L, B, eigvals_only=True)[:4]
+    np.testing.assert_allclose(first.eigenvalues, vals[:2], rtol=1e-9)
+    np.testing.assert_allclose(rep.eigenvalues, vals[2:4], rtol=1e-9)

@@ -94,3 +94,35 @@ def test_closed_form_shortcut_matches_full_formula():
         t = [4.0 * np.sin(np.arange(1, c + 1) * np.pi / (2.0 * (c + 1))) ** 2 for c in dims]
         full = np.sort((t[0][:, None, None] + t[1][None, :, None] + t[2][None, None, :]).ravel())
         np.testing.assert_allclose(orc.closed_form_smallest(nx, ny, nz, m), full[:m], rtol=1e-15)
+
+
+def _b_tridiag(v):
+    y = 3.0 * v
+    y[1:] -= v[:-1]
+    y[:-1] -= v[1:]
+    return y
+
+
+def _b_zcouple(v, plane=144):
+    y = 2.5 * v
+    y[plane:] -= 0.5 * v[:-plane]
+    y[:-plane] -= 0.5 * v[plane:]
+    return y
+
+
+@pytest.mark.parametrize("name,N,m,tol,jac,bfun", [
+    ("tri8", 8, 4, 1e-8, True, _b_tridiag),
+    ("zc12", 12, 6, 1e-7, False, _b_zcouple)])
+def test_generic_b_matches_reference(golden, name, N, m, tol, jac, bfun):
+    """Non-diagonal B (BX, BW, BP by recurrence, lobpcg.py:396, :476,
+    :533-538): the oracle reproduces the reference's trajectory."""
+    g = golden(f"genb_{name}.npz")
+    n = N ** 3
+    s = float((N + 1) ** 2)
+    r = orc.run_lobpcg(lambda v: orc.stencil7(v, N, N, N, s), n, m, apply_b=bfun,
+                       tinv=(1.0 / np.full(n, 6.0 * s)) if jac else None, tol=tol,
+                       max_iter=300, seed=0)
+    assert r.status == str(g["status"])
+    assert r.iterations_used == int(g["iterations_used"])
+    np.testing.assert_allclose(np.array(r.hist_ritz), g["hist_ritz"], rtol=1e-12)
+    np.testing.assert_allclose(r.eigenvalues, g["dense_vals"], rtol=1e-10)

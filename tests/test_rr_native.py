@@ -175,20 +175,49 @@ def test_split_rr_degenerate_raises_at_finish():
     assert got is None and fb == m
 
 
-def test_large_pencil_rr_is_host_thread_independent():
-    """m >= 22 (LAPACK/BLAS branch): the result does not depend on the
-    caller's BLAS thread count, and that setting is restored afterwards."""
+def _large_rr(threads, case=None):
+    m = 24
+    G1, G2, lam = case if case is not None else _case(400, m, m, True, seed=29)
+    J = np.arange(m)
     from threadpoolctl import ThreadpoolController
 
-    m = 24
-    G1, G2, lam = _case(400, m, m, True, seed=29)
-    J = np.arange(m)
+    with ThreadpoolController().limit(limits=threads, user_api="blas"):
+        return NativeRitz(m)(m, m, True, G1, G2, lam, J, J.copy(), FLOOR)
+
+
+def _large_rr_file(threads, path, out):
+    d = np.load(path)
+    r = _large_rr(threads, (d["G1"], d["G2"], d["lam"]))
+    np.savez(out, lam=r[0], coef=r[1], pcols=r[2])
+
+
+def test_large_pencil_rr_is_host_thread_independent(tmp_path):
+    """m >= 22 (LAPACK/BLAS branch): the result computed under a 4-thread
+    BLAS caller equals, bit for bit, the one of a separate process whose
+    OpenBLAS only ever had one thread (OPENBLAS_NUM_THREADS=1) on the same
+    input Grams, and the caller's setting is restored afterwards."""
+    import os
+    import subprocess
+    import sys
+
+    pytest.importorskip("threadpoolctl")
+    from threadpoolctl import ThreadpoolController
+
+    case = _case(400, 24, 24, True, seed=29)
+    inp = tmp_path / "in.npz"
+    np.savez(inp, G1=case[0], G2=case[1], lam=case[2])
+    got = _large_rr(4, case)
     ctl = ThreadpoolController()
-    outs = []
-    for nt in (1, 4):
-        with ctl.limit(limits=nt, user_api="blas"):
-            outs.append(NativeRitz(m)(m, m, True, G1, G2, lam, J, J.copy(), FLOOR))
-            after = {i["num_threads"] for i in ctl.select(user_api="blas").info()}
-            assert after == {nt}
-    for a, b in zip(outs[0][:3], outs[1][:3]):
+    with ctl.limit(limits=4, user_api="blas"):
+        _large_rr(4, case)
+        assert {i["num_threads"] for i in ctl.select(user_api="blas").info()} == {4}
+    out = tmp_path / "one.npz"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r); "
+            "from tests.test_rr_native import _large_rr_file; _large_rr_file(1, %r, %r)"
+            ) % (root, str(inp), str(out))
+    env = dict(os.environ, OPENBLAS_NUM_THREADS="1", OMP_NUM_THREADS="1")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=root)
+    ref = np.load(out)
+    for a, b in zip(got[:3], (ref["lam"], ref["coef"], ref["pcols"])):
         assert np.array_equal(a, b)
