@@ -309,7 +309,17 @@ typedef struct {
   int red_on_host;                    /* in/out: 1 when the queued passes write
                                          h_red / h_g2 directly (mapped pinned
                                          memory); the caller sets 0 whenever it
-                                         queued the passes itself */
+                                         queued the passes itself; 3 when a
+                                         z-slab step left them reduced over
+                                         the ranks in h_red / h_g2 */
+  struct b2l_slab* slab;              /* z-slab context (b2l_slab_create) or
+                                         NULL: one GPU holds the whole grid.
+                                         With a communicator, the halo of W'
+                                         is exchanged under the interior
+                                         stencil planes and F1's reductions
+                                         and the stencil pass's Gram are
+                                         summed over the ranks (NCCL) before
+                                         the host reads them. */
 } b2l_iter_state;
 
 int b2l_fast_iteration(b2l_iter_state* state);
@@ -324,6 +334,47 @@ int b2l_iter_state_size(void);
  * tests, Rayleigh-Ritz, uploads + launches (microseconds, summed over calls).
  */
 int b2l_iter_profile(double* out, int reset);
+
+/*
+ * z-slab decomposition over the GPUs of one node (the survey's
+ * b2l_ctx_create with its NCCL communicator), one process per GPU.  Rank r
+ * owns z-planes [floor(r N/P), floor((r+1) N/P)) -- a contiguous row range of
+ * every block.  Replaces nothing in the reference (single process,
+ * SPEC.md:317); the paper's runs used the same decomposition through MPI
+ * inside hypre.
+ *
+ * NCCL is bound at run time to the libnccl.so.2 already in the process
+ * (PyTorch's), else `path`.  b2l_nccl_unique_id fills a 128-byte id on one
+ * rank; the caller broadcasts it (torch.distributed) and every rank calls
+ * b2l_slab_create with it.  nccl_id NULL (world 1 only): no communicator,
+ * every collective is the identity.
+ *
+ * b2l_slab_stencil7 / _gram: b2l_stencil7 / b2l_stencil7_gram on this rank's
+ * nz_local planes; the two boundary planes of `in` go to the neighbours on
+ * the context's communication stream while the interior planes are
+ * computed, the two edge planes after the halo landed.  gram_out is this
+ * rank's part (sum it with b2l_slab_allreduce).
+ * b2l_slab_allreduce: in-place fp64 sum over the ranks on `stream`.
+ * b2l_stencil7_gram_split: b2l_stencil7_gram in the same interior + edge
+ * launches with a caller-supplied halo and no communication (tests).
+ */
+typedef struct b2l_slab b2l_slab;
+int b2l_nccl_load(const char* path);
+int b2l_nccl_unique_id(unsigned char* out, int len);
+int b2l_slab_create(const unsigned char* nccl_id, int world, int rank, int nx, int ny,
+                    int nz_local, b2l_slab** out);
+int b2l_slab_destroy(b2l_slab* slab);
+int b2l_slab_info(const b2l_slab* slab, int* world, int* rank, int* has_comm);
+int b2l_slab_allreduce(b2l_slab* slab, double* buf, long long count, void* stream);
+int b2l_slab_stencil7(b2l_slab* slab, const double* in, double* out, int ld, double scale,
+                      void* stream);
+int b2l_slab_stencil7_gram(b2l_slab* slab, const double* in, double* out, int ld, double scale,
+                           const double* x, int ldx, int m, int kw, double* gram_out,
+                           void* stream);
+int b2l_stencil7_gram_split(const double* in, double* out, int nx, int ny, int nz, int ld,
+                            const double* halo, int has_lo, int has_hi, double scale,
+                            const double* x, int ldx, int m, int kw, double* gram_out,
+                            void* stream);
 
 /* Number of kernels this library has launched in the process (all entry
  * points, including the ones b2l_fast_iteration queues). */

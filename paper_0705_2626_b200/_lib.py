@@ -48,6 +48,7 @@ class b2l_iter_state(C.Structure):
         ("drift", C.c_double),
         ("fallbacks", C.c_int), ("k_next", C.c_int), ("kp", C.c_int),
         ("red_on_host", C.c_int),
+        ("slab", C.c_void_p),
     ]
 
 
@@ -101,6 +102,22 @@ SIGNATURES = {
                                     C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                                     C.c_void_p, C.c_void_p, C.c_void_p]),
     "b2l_fast_iteration": (C.c_int, [C.POINTER(b2l_iter_state)]),
+    "b2l_nccl_load": (C.c_int, [C.c_char_p]),
+    "b2l_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_int]),
+    "b2l_slab_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                  C.POINTER(C.c_void_p)]),
+    "b2l_slab_destroy": (C.c_int, [C.c_void_p]),
+    "b2l_slab_info": (C.c_int, [C.c_void_p, c_ip, c_ip, c_ip]),
+    "b2l_slab_allreduce": (C.c_int, [C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
+    "b2l_slab_stencil7": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double,
+                                    C.c_void_p]),
+    "b2l_slab_stencil7_gram": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                         C.c_double, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                         C.c_void_p, C.c_void_p]),
+    "b2l_stencil7_gram_split": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                          C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_double,
+                                          C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                          C.c_void_p]),
     "b2l_iter_state_size": (C.c_int, []),
     "b2l_iter_profile": (C.c_int, [C.POINTER(C.c_double), C.c_int]),
     "b2l_launch_count": (C.c_longlong, []),

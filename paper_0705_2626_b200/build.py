@@ -20,7 +20,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "lib"
 LIBNAME = "libb200lobpcg.so"
-SOURCES = ["abi.cu", "stencil.cu", "stencil_gram.cu", "blockops.cu", "fused.cu", "rr.cu", "rng.cu", "pcg.cu", "iterate.cu"]
+SOURCES = ["abi.cu", "stencil.cu", "stencil_gram.cu", "blockops.cu", "fused.cu", "rr.cu", "rng.cu", "pcg.cu", "iterate.cu", "slab.cu"]
 HEADERS = ["common.cuh", "gram_tile.cuh", "stencil.cuh"]
 
 NVCC_FLAGS = [

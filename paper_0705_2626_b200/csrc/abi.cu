@@ -13,7 +13,7 @@ namespace b2l {
 
 int stencil7(const double* in, double* out, int nx, int ny, int nz, int ld,
              const double* halo, int has_lo, int has_hi, double scale,
-             cudaStream_t st);
+             cudaStream_t st, int zmode = 0);
 struct HostBlock {
   const double* p;
   int ld, cols;

@@ -40,6 +40,7 @@ enum : int {
   B2L_EDRIVER = 1002,
   B2L_EDEGENERATE = 1003,   // Rayleigh-Ritz basis repair exhausted
   B2L_ELAPACK = 1004,
+  B2L_ENCCL = 1005,         // NCCL unavailable or a collective failed
 };
 
 // ------------------------------------------------------------- workspace

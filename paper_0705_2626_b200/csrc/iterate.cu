@@ -7,8 +7,10 @@
 //   (b2l_stencil7_gram).
 // Same decisions, same order as the Python driver (paper_0705_2626_b200/
 // lobpcg.py, LOBPCGRun.step); the Python side keeps every other path (first
-// iteration, drift repair, callbacks, constraints, z-slabs) and records the
-// history from the outputs.
+// iteration, drift repair, callbacks, constraints) and records the history
+// from the outputs.  A z-slab rank (s->slab with a communicator) runs the same
+// step with NCCL inside: halo under the interior stencil planes, one
+// all-reduce per fused pass (slab.cu).
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -32,6 +34,15 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx, co
 int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
                   const double* halo, int has_lo, int has_hi, double scale, const double* x,
                   int ldx, int m, int kw, double* gram_out, cudaStream_t st);
+// z-slab context (slab.cu)
+bool slab_multi(const b2l_slab* s);
+cudaStream_t slab_comm_stream(b2l_slab* s);
+cudaEvent_t slab_event(b2l_slab* s, int which);   // 0 f1, 1 red, 2 sg, 3 g2
+int slab_halo_start(b2l_slab* s, const double* in, int ld, cudaStream_t st);
+int slab_sgram_after_halo(b2l_slab* s, const double* in, double* out, int ld, double scale,
+                          const double* x, int ldx, int m, int kw, double* gram_out,
+                          cudaStream_t st);
+int slab_allreduce(b2l_slab* s, double* buf, size_t count, cudaStream_t st);
 }  // namespace b2l
 
 using namespace b2l;
@@ -123,10 +134,18 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
     t0 = t1;
   };
   if (g_prof_on) g_prof[0] += 1.0;
+  b2l_slab* S = s->slab;
+  const bool multi = slab_multi(S);
   // ---- one synchronisation: F1's reductions + the stencil pass's Gram.  The
   // passes this function queued wrote them straight into the pinned h_red /
-  // h_g2 (device-mapped); passes queued elsewhere left them on the device.
+  // h_g2 (device-mapped; a z-slab step: reduced over the ranks and copied on
+  // the communication stream); passes queued elsewhere left them on the
+  // device, unreduced.
   if (!s->red_on_host) {
+    if (multi) {
+      if (int r = slab_allreduce(S, s->red_dev, nred, st)) return r;
+      if (int r = slab_allreduce(S, s->g2_dev, ng2, st)) return r;
+    }
     B2L_CUDA(cudaMemcpyAsync(s->h_red, s->red_dev, nred * sizeof(double), cudaMemcpyDeviceToHost,
                              st));
     B2L_CUDA(cudaMemcpyAsync(s->h_g2, s->g2_dev, ng2 * sizeof(double), cudaMemcpyDeviceToHost,
@@ -138,8 +157,12 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
   // and h_g2, may still run) and do the G1-only half of the Rayleigh-Ritz
   // step meanwhile; the main stream is synchronised before the G2 half.
   SideStream* side0 = side_stream();
-  const bool early = s->red_on_host == 2 && side0 != nullptr && side0->owner == s;
-  if (early) {
+  const bool early_slab = s->red_on_host == 3 && multi;
+  const bool early =
+      early_slab || (s->red_on_host == 2 && side0 != nullptr && side0->owner == s);
+  if (early_slab) {
+    B2L_CUDA(cudaEventSynchronize(slab_event(S, 1)));
+  } else if (early) {
     B2L_CUDA(cudaEventSynchronize(side0->join));
   } else {
     B2L_CUDA(cudaStreamSynchronize(st));
@@ -224,6 +247,42 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
   s->kp = kp;
   s->k_next = kj;
 
+  if (multi) {
+    // ---- z-slab: F1 (row-local), then on the communication stream the halo
+    // of W' (under the interior stencil planes), F1's second reduction stage,
+    // its all-reduce and D2H (the host starts the G1 half on it); the stencil
+    // pass's Gram is all-reduced and copied behind the edge planes.
+    const size_t nred_n = (size_t)2 * m + (size_t)(2 * m + kj) * (3 * m + kj);
+    const size_t ng2_n = (size_t)(m + kj) * kj;
+    cudaStream_t cs = slab_comm_stream(S);
+    const StepHostCoef hc_m{coef, lam_next, pcols, wpos};
+    StepDeferred dfr;
+    int r = lobpcg_step(s->n, m, s->x, s->ax, s->ldx, s->w_cur, s->aw, even(kst), kst,
+                        kp ? s->p : nullptr, kp ? s->ap : nullptr, kp, nullptr, nullptr,
+                        s->x2, s->ax2, s->p2, s->ap2, nullptr, s->bdiag, s->tmode, s->tinv,
+                        s->tvec, nullptr, kj, s->w_next, even(kj), s->relative_tol,
+                        s->red_dev, st, &hc_m, &dfr);
+    if (r) return r;
+    if ((r = slab_halo_start(S, s->w_next, even(kj), st))) return r;   // cs waits for F1
+    if ((r = sum_parts(dfr.part, dfr.nparts, dfr.len, dfr.out, cs))) return r;
+    if ((r = slab_allreduce(S, s->red_dev, nred_n, cs))) return r;
+    B2L_CUDA(cudaMemcpyAsync(s->h_red, s->red_dev, nred_n * sizeof(double),
+                             cudaMemcpyDeviceToHost, cs));
+    B2L_CUDA(cudaEventRecord(slab_event(S, 1), cs));
+    if ((r = slab_sgram_after_halo(S, s->w_next, s->aw, even(kj), s->scale, s->x2, s->ldx, m,
+                                   kj, s->g2_dev, st)))
+      return r;
+    B2L_CUDA(cudaEventRecord(slab_event(S, 2), st));
+    B2L_CUDA(cudaStreamWaitEvent(cs, slab_event(S, 2), 0));
+    if ((r = slab_allreduce(S, s->g2_dev, ng2_n, cs))) return r;
+    B2L_CUDA(cudaMemcpyAsync(s->h_g2, s->g2_dev, ng2_n * sizeof(double),
+                             cudaMemcpyDeviceToHost, cs));
+    B2L_CUDA(cudaEventRecord(slab_event(S, 3), cs));
+    B2L_CUDA(cudaStreamWaitEvent(st, slab_event(S, 3), 0));
+    s->red_on_host = 3;
+    mark(5);
+    return B2L_ITER_OK;
+  }
   // ---- the next fused passes: coefficients by value in the F1 launch (no
   // H2D copies), reductions written into the mapped pinned buffers (no D2H)
   double* red_h = mapped(s->h_red);

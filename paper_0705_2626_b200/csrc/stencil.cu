@@ -40,8 +40,8 @@ __global__ void __launch_bounds__(256)
   const int tid = threadIdx.x;
   const int tx0 = (blockIdx.x % g.tiles_x) * g.TX;
   const int ty0 = (blockIdx.x / g.tiles_x) * g.TY;
-  const int z0 = blockIdx.y * g.zchunk;
-  const int z1 = min(g.nz, z0 + g.zchunk);
+  int z0, z1;
+  stencil_zrange(g, z0, z1);
   if (z0 >= z1) return;
   const int nplanes = (z1 - z0) + 2;  // planes z0-1 .. z1
 
@@ -147,6 +147,27 @@ int choose_zchunk(int tiles, int nz, int slots) {
   return c;
 }
 
+bool apply_zmode(StencilGeom& g, dim3& grid, int tiles, int mode, int slots) {
+  g.zedge = 0;
+  g.zbeg = 0;
+  g.zend = g.nz;
+  if (mode == Z_EDGE) {
+    g.zedge = 1;
+    g.zchunk = 1;
+    grid = dim3(tiles, g.nz > 1 ? 2 : 1, 1);
+    return true;
+  }
+  if (mode == Z_INTERIOR) {
+    g.zbeg = 1;
+    g.zend = g.nz - 1;
+  }
+  const int span = g.zend - g.zbeg;
+  if (span <= 0) return false;
+  g.zchunk = choose_zchunk(tiles, span, slots);
+  grid = dim3(tiles, (span + g.zchunk - 1) / g.zchunk, 1);
+  return true;
+}
+
 int plan_stencil(int nx, int ny, int nz, int ld, StencilPlan* p) {
   StencilGeom& g = p->g;
   g.nx = nx;
@@ -180,9 +201,7 @@ int plan_stencil(int nx, int ny, int nz, int ld, StencilPlan* p) {
   B2L_CHECK(smem <= 227 * 1024, -B2L_EINVAL,
             "stencil tile does not fit in shared memory (ld too large)");
   p->smem = smem;
-  g.zchunk = choose_zchunk(tiles, nz, 2 * sm_count());
-  const int zsplit = (nz + g.zchunk - 1) / g.zchunk;
-  p->grid = dim3(tiles, zsplit, 1);
+  apply_zmode(g, p->grid, tiles, Z_ALL, 2 * sm_count());
   return 0;
 }
 
@@ -201,7 +220,7 @@ static int launch_stencil_t(const StencilPlan& p, const CUtensorMap& tin,
 
 int stencil7(const double* in, double* out, int nx, int ny, int nz, int ld,
              const double* halo, int has_lo, int has_hi, double scale,
-             cudaStream_t st) {
+             cudaStream_t st, int zmode) {
   B2L_CHECK(nx > 0 && ny > 0 && nz > 0, -B2L_EINVAL, "stencil: empty grid");
   B2L_CHECK(ld >= 2 && (ld % 2) == 0, -B2L_EINVAL,
             "stencil: ld must be even (16-B rows for TMA)");
@@ -217,6 +236,10 @@ int stencil7(const double* in, double* out, int nx, int ny, int nz, int ld,
   p.g.has_lo = has_lo;
   p.g.has_hi = has_hi;
   p.g.scale = scale;
+  if (zmode != Z_ALL) {
+    const int tiles = p.grid.x;
+    if (!apply_zmode(p.g, p.grid, tiles, zmode, 2 * sm_count())) return 0;
+  }
   CUtensorMap tin, thalo, tout;
   const uint32_t TX = p.g.TX, TY = p.g.TY;
   rc = encode_tmap_4d(&tin, in, ld, nx, ny, nz, ld, TX + 2, TY + 2, 1);

@@ -19,14 +19,6 @@
 
 namespace b2l {
 
-struct SGramGeom {
-  int m, ldx, kw;   // X columns / leading dim, W columns used
-  int a, b;         // m + kw, kw
-  int npts;         // points per tile (TX*TY)
-  int ngroups;      // ceil(npts / 8)
-  uint32_t x_bytes, x_stride;
-  double* partial;  // [grid][a*b]
-};
 
 // LD = doubles per point of W / AW (template: it fixes the per-lane element
 // count EPT = GPW*LD/4 and the Gram tile counts); GPW = 8-point groups per
@@ -63,8 +55,8 @@ __global__ void __launch_bounds__(256, 2)
   const int warp = tid >> 5, lane = tid & 31;
   const int tx0 = (blockIdx.x % g.tiles_x) * g.TX;
   const int ty0 = (blockIdx.x / g.tiles_x) * g.TY;
-  const int z0 = blockIdx.y * g.zchunk;
-  const int z1 = min(g.nz, z0 + g.zchunk);
+  int z0, z1;
+  stencil_zrange(g, z0, z1);
   const int ystride = (g.TX + 2) * LD;
   auto staged_row = [&](int pt) { return (pt / g.TX + 1) * (g.TX + 2) + (pt % g.TX) + 1; };
 
@@ -284,7 +276,7 @@ __global__ void __launch_bounds__(256, 2)
 }
 
 int stencil7(const double* in, double* out, int nx, int ny, int nz, int ld, const double* halo,
-             int has_lo, int has_hi, double scale, cudaStream_t st);
+             int has_lo, int has_hi, double scale, cudaStream_t st, int zmode = 0);
 struct HostBlock {
   const double* p;
   int ld, cols;
@@ -318,10 +310,9 @@ static int launch_sgram_ld(int gpw, const StencilPlan& p, size_t smem, const CUt
   }
 }
 
-int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
-                  const double* halo, int has_lo, int has_hi, double scale,
-                  const double* x, int ldx, int m, int kw, double* gram_out,
-                  cudaStream_t st) {
+int sgram_plan(const double* in, double* out, int nx, int ny, int nz, int ld, const double* halo,
+               int has_lo, int has_hi, double scale, const double* x, int ldx, int m, int kw,
+               int zmode, SGramPlan* P) {
   B2L_CHECK(nx > 0 && ny > 0 && nz > 0, -B2L_EINVAL, "stencil: empty grid");
   B2L_CHECK(ld >= 2 && (ld % 2) == 0 && (m == 0 || (ldx >= 2 && (ldx % 2) == 0)), -B2L_EINVAL,
             "stencil: ld and ldx must be even (16-B rows for TMA)");
@@ -330,23 +321,33 @@ int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
   B2L_CHECK(in != out, -B2L_EINVAL, "stencil: in-place apply not supported");
   B2L_CHECK(!(has_lo || has_hi) || halo != nullptr, -B2L_EINVAL,
             "stencil: halo flags set without a halo buffer");
-  if (ld > 16 || m > ld) {
-    // outside the fused kernel's templates: the two-pass form (K1, then K5)
-    int rc = stencil7(in, out, nx, ny, nz, ld, halo, has_lo, has_hi, scale, st);
-    if (rc) return rc;
-    const HostBlock L[2] = {{x, ldx, m}, {in, ld, kw}};
-    const HostBlock R[1] = {{out, ld, kw}};
-    if (m == 0) return gram(nx * ny * nz, L + 1, 1, R, 1, 0u, nullptr, nullptr, gram_out, st);
-    return gram(nx * ny * nz, L, 2, R, 1, 0u, nullptr, nullptr, gram_out, st);
-  }
-  SGramGeom G{};
+  *P = SGramPlan{};
+  P->in = in;
+  P->out = out;
+  P->x = x;
+  P->nx = nx;
+  P->ny = ny;
+  P->nz = nz;
+  P->ld = ld;
+  P->ldx = ldx;
+  P->halo = halo;
+  P->has_lo = has_lo;
+  P->has_hi = has_hi;
+  P->scale = scale;
+  P->zmode = zmode;
+  SGramGeom& G = P->G;
   G.m = m;
   G.ldx = ldx;
   G.kw = kw;
   G.a = m + kw;
   G.b = kw;
-
-  StencilPlan p;
+  if (ld > 16 || m > ld) {
+    // outside the fused kernel's templates: the two-pass form (K1, then K5)
+    P->twopass = 1;
+    P->nparts = 0;
+    return 0;
+  }
+  StencilPlan& p = P->p;
   int rc = plan_stencil(nx, ny, nz, ld, &p);
   if (rc) return rc;
   StencilGeom& g = p.g;
@@ -402,52 +403,142 @@ int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
   const size_t red = (size_t)8 * NI * NJ * 64 * 8;
   if (red > smem) smem = red + 128;
   B2L_CHECK(smem <= 227 * 1024, -B2L_EINVAL, "stencil_gram: tile does not fit");
-  g.zchunk = choose_zchunk(tiles, nz, 2 * sm_count());   // two CTAs per SM
-  if (const char* zc = getenv("B2L_SGRAM_ZCHUNK")) {     // tuning override
-    const int v = atoi(zc);
-    if (v >= 1) g.zchunk = v < nz ? v : nz;
+  P->smem = smem;
+  P->gpw = gpw;
+  if (!apply_zmode(g, p.grid, tiles, zmode, 2 * sm_count())) {
+    P->nparts = 0;   // no plane in this mode
+    return 0;
   }
-  const int zsplit = (nz + g.zchunk - 1) / g.zchunk;
-  p.grid = dim3(tiles, zsplit, 1);
+  if (zmode == Z_ALL) {
+    if (const char* zc = getenv("B2L_SGRAM_ZCHUNK")) {     // tuning override
+      const int v = atoi(zc);
+      if (v >= 1) {
+        g.zchunk = v < nz ? v : nz;
+        p.grid.y = (nz + g.zchunk - 1) / g.zchunk;
+      }
+    }
+  }
   g.has_lo = has_lo;
   g.has_hi = has_hi;
   g.scale = scale;
-  const int nparts = tiles * zsplit;
-  int werr = 0;
-  double* part = static_cast<double*>(
-      workspace((size_t)nparts * G.a * G.b * sizeof(double), &werr));
-  if (werr) return werr;
-  G.partial = part;
-  CUtensorMap tin, thalo, tout, txm;
-  rc = encode_tmap_4d(&tin, in, ld, nx, ny, nz, ld, TX + 2, TY + 2, 1);
+  P->nparts = (int)(p.grid.x * p.grid.y);
+  rc = encode_tmap_4d(&P->tin, in, ld, nx, ny, nz, ld, TX + 2, TY + 2, 1);
   if (rc) return rc;
-  rc = encode_tmap_4d(&tout, out, ld, nx, ny, nz, ld, TX, TY, 1);
+  rc = encode_tmap_4d(&P->tout, out, ld, nx, ny, nz, ld, TX, TY, 1);
   if (rc) return rc;
   if (m) {
-    rc = encode_tmap_4d(&txm, x, ldx, nx, ny, nz, ldx, TX, TY, 1);
+    rc = encode_tmap_4d(&P->txm, x, ldx, nx, ny, nz, ldx, TX, TY, 1);
     if (rc) return rc;
   } else {
-    txm = tout;   // never loaded
+    P->txm = P->tout;   // never loaded
   }
   if (halo) {
-    rc = encode_tmap_4d(&thalo, halo, ld, nx, ny, 2, ld, TX + 2, TY + 2, 1);
+    rc = encode_tmap_4d(&P->thalo, halo, ld, nx, ny, 2, ld, TX + 2, TY + 2, 1);
     if (rc) return rc;
   } else {
-    thalo = tin;
+    P->thalo = P->tin;
   }
-  switch (ld) {
-    case 2: rc = launch_sgram_ld<2>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
-    case 4: rc = launch_sgram_ld<4>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
-    case 6: rc = launch_sgram_ld<6>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
-    case 8: rc = launch_sgram_ld<8>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
-    case 10: rc = launch_sgram_ld<10>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
-    case 12: rc = launch_sgram_ld<12>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
-    case 14: rc = launch_sgram_ld<14>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
-    default: rc = launch_sgram_ld<16>(gpw, p, smem, tin, thalo, tout, txm, G, st); break;
+  return 0;
+}
+
+int sgram_launch(SGramPlan& P, double* partial, cudaStream_t st) {
+  if (P.twopass)
+    return stencil7(P.in, P.out, P.nx, P.ny, P.nz, P.ld, P.halo, P.has_lo, P.has_hi, P.scale, st,
+                    P.zmode);
+  if (P.nparts == 0) return 0;
+  P.G.partial = partial;
+  const StencilPlan& p = P.p;
+  const int gpw = P.gpw;
+  const size_t smem = P.smem;
+  const SGramGeom& G = P.G;
+  switch (P.ld) {
+    case 2: return launch_sgram_ld<2>(gpw, p, smem, P.tin, P.thalo, P.tout, P.txm, G, st);
+    case 4: return launch_sgram_ld<4>(gpw, p, smem, P.tin, P.thalo, P.tout, P.txm, G, st);
+    case 6: return launch_sgram_ld<6>(gpw, p, smem, P.tin, P.thalo, P.tout, P.txm, G, st);
+    case 8: return launch_sgram_ld<8>(gpw, p, smem, P.tin, P.thalo, P.tout, P.txm, G, st);
+    case 10: return launch_sgram_ld<10>(gpw, p, smem, P.tin, P.thalo, P.tout, P.txm, G, st);
+    case 12: return launch_sgram_ld<12>(gpw, p, smem, P.tin, P.thalo, P.tout, P.txm, G, st);
+    case 14: return launch_sgram_ld<14>(gpw, p, smem, P.tin, P.thalo, P.tout, P.txm, G, st);
+    default: return launch_sgram_ld<16>(gpw, p, smem, P.tin, P.thalo, P.tout, P.txm, G, st);
   }
+}
+
+// The Gram of a two-pass plan (after its stencil launches), or the sum of
+// the CTA partials of fused launches.
+int sgram_finish(const SGramPlan& P, const double* partial, int nparts, double* gram_out,
+                 cudaStream_t st) {
+  const SGramGeom& G = P.G;
+  if (P.twopass) {
+    const HostBlock L[2] = {{P.x, P.ldx, G.m}, {P.in, P.ld, G.kw}};
+    const HostBlock R[1] = {{P.out, P.ld, G.kw}};
+    const int rows = P.nx * P.ny * P.nz;
+    if (G.m == 0) return gram(rows, L + 1, 1, R, 1, 0u, nullptr, nullptr, gram_out, st);
+    return gram(rows, L, 2, R, 1, 0u, nullptr, nullptr, gram_out, st);
+  }
+  return sum_parts(partial, nparts, G.a * G.b, gram_out, st);
+}
+
+int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
+                  const double* halo, int has_lo, int has_hi, double scale,
+                  const double* x, int ldx, int m, int kw, double* gram_out,
+                  cudaStream_t st) {
+  SGramPlan P;
+  int rc = sgram_plan(in, out, nx, ny, nz, ld, halo, has_lo, has_hi, scale, x, ldx, m, kw, Z_ALL,
+                      &P);
   if (rc) return rc;
-  const int len = G.a * G.b;
-  return sum_parts(part, nparts, len, gram_out, st);
+  double* part = nullptr;
+  if (!P.twopass) {
+    int werr = 0;
+    part = static_cast<double*>(
+        workspace((size_t)P.nparts * P.G.a * P.G.b * sizeof(double), &werr));
+    if (werr) return werr;
+  }
+  rc = sgram_launch(P, part, st);
+  if (rc) return rc;
+  return sgram_finish(P, part, P.nparts, gram_out, st);
+}
+
+// Interior planes (no halo needed), then the two edge planes (halo), one
+// partial buffer, one second-stage sum: the z-slab overlap form
+// (b2l_slab_stencil7_gram runs the halo exchange between the two launches;
+// this single-stream variant serves tests and halo-less callers).
+int stencil7_gram_split(const double* in, double* out, int nx, int ny, int nz, int ld,
+                        const double* halo, int has_lo, int has_hi, double scale,
+                        const double* x, int ldx, int m, int kw, double* gram_out,
+                        cudaStream_t st, double** part_buf, size_t* part_cap,
+                        cudaEvent_t before_edges) {
+  SGramPlan Pi, Pe;
+  int rc = sgram_plan(in, out, nx, ny, nz, ld, halo, has_lo, has_hi, scale, x, ldx, m, kw,
+                      Z_INTERIOR, &Pi);
+  if (rc) return rc;
+  rc = sgram_plan(in, out, nx, ny, nz, ld, halo, has_lo, has_hi, scale, x, ldx, m, kw, Z_EDGE,
+                  &Pe);
+  if (rc) return rc;
+  const size_t len = (size_t)Pi.G.a * Pi.G.b;
+  const size_t need = ((size_t)Pi.nparts + Pe.nparts) * len;
+  double* part = nullptr;
+  if (!Pi.twopass) {
+    if (part_buf) {
+      if (*part_cap < need) {
+        if (*part_buf) B2L_CUDA(cudaFree(*part_buf));
+        *part_buf = nullptr;
+        *part_cap = 0;
+        B2L_CUDA(cudaMalloc(part_buf, need * sizeof(double)));
+        *part_cap = need;
+      }
+      part = *part_buf;
+    } else {
+      int werr = 0;
+      part = static_cast<double*>(workspace(need * sizeof(double), &werr));
+      if (werr) return werr;
+    }
+  }
+  rc = sgram_launch(Pi, part, st);
+  if (rc) return rc;
+  if (before_edges) B2L_CUDA(cudaStreamWaitEvent(st, before_edges, 0));
+  rc = sgram_launch(Pe, part ? part + (size_t)Pi.nparts * len : nullptr, st);
+  if (rc) return rc;
+  return sgram_finish(Pi, part, Pi.nparts + Pe.nparts, gram_out, st);
 }
 
 }  // namespace b2l

@@ -16,16 +16,26 @@ two kinds of exchange:
 Row-local work (update, residual, preconditioner, diagonal B) needs no
 communication.  The reference is single-process; the paper ran
 the same decomposition through MPI inside hypre.
+
+On CUDA both exchanges run inside libb200lobpcg (b2l_slab_*, csrc/slab.cu):
+an NCCL communicator of its own (its id broadcast over torch.distributed),
+the halo posted on a communication stream under the interior stencil planes,
+and the steady-state iteration (b2l_fast_iteration) with both all-reduces
+inside it.  On CPU tensors (the gloo tests) the same exchanges go through
+torch.distributed point-to-point and all_reduce.
 """
 
 from __future__ import annotations
 
+import ctypes
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 import torch.distributed as dist
 
+from . import _lib
 from .operators import Grid3D, Laplacian3D
 
 __all__ = ["SlabPartition", "SlabLaplacian3D", "slab_initial_block"]
@@ -75,7 +85,9 @@ class SlabLaplacian3D(Laplacian3D):
     ``local_rows`` is the slab's row count.  Blocks passed to it hold the
     slab's rows only."""
 
-    def __init__(self, grid, scale=1.0, group=None, device=None):
+    def __init__(self, grid, scale=1.0, group=None, device=None, comm="auto"):
+        """comm: "auto" -- the library's NCCL communicator on CUDA devices,
+        torch.distributed on CPU tensors; "nccl" / "torch" force one."""
         if not isinstance(grid, Grid3D):
             grid = Grid3D(*grid)
         super().__init__(grid, scale=scale, device=device)
@@ -89,6 +101,36 @@ class SlabLaplacian3D(Laplacian3D):
         self.local_rows = self.local_grid.n
         self.plane = grid.nx * grid.ny
         self._halo = {}
+        self._slab = None
+        if comm not in ("auto", "nccl", "torch"):
+            raise ValueError(f"comm must be 'auto', 'nccl' or 'torch', got {comm!r}")
+        if comm == "nccl" or (comm == "auto" and self.device.type == "cuda"):
+            self._slab = self._create_native(world, rank)
+
+    def _create_native(self, world, rank):
+        """b2l_slab_create with an NCCL id made on the group's first rank and
+        broadcast over torch.distributed (any backend)."""
+        lib = _lib.load()
+        _lib.check(lib.b2l_nccl_load(None), "b2l_nccl_load")
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _lib.check(lib.b2l_nccl_unique_id(uid, 128), "b2l_nccl_unique_id")
+        if world > 1:
+            box = [uid.raw if rank == 0 else None]
+            src = dist.get_global_rank(self.group, 0) if self.group is not None else 0
+            dist.broadcast_object_list(box, src=src, group=self.group)
+            uid = ctypes.create_string_buffer(box[0], 128)
+        handle = ctypes.c_void_p()
+        g = self.local_grid
+        _lib.check(lib.b2l_slab_create(uid, world, rank, g.nx, g.ny, g.nz, ctypes.byref(handle)),
+                   "b2l_slab_create")
+        weakref.finalize(self, lib.b2l_slab_destroy, handle.value)
+        return handle.value
+
+    @property
+    def native_slab(self):
+        """The library's z-slab context (b2l_slab*) or None (torch comm)."""
+        return self._slab
 
     # ---------------------------------------------------------- comm hooks
     @property
@@ -96,8 +138,16 @@ class SlabLaplacian3D(Laplacian3D):
         return self.part.world
 
     def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
-        """In-place sum over ranks (no-op on one rank)."""
-        if self.part.world > 1:
+        """In-place sum over ranks (no-op on one rank without a communicator)."""
+        if self._slab is not None:
+            from . import device as dv
+
+            if not t.is_contiguous():
+                raise ValueError("allreduce_ needs a contiguous tensor")
+            _lib.check(_lib.load().b2l_slab_allreduce(self._slab, t.data_ptr(), t.numel(),
+                                                      dv.stream_ptr(t.device)),
+                       "b2l_slab_allreduce")
+        elif self.part.world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t
 
@@ -135,6 +185,14 @@ class SlabLaplacian3D(Laplacian3D):
     def apply_into(self, x: torch.Tensor, out: torch.Tensor) -> None:
         from . import device as dv
 
+        if self._slab is not None:
+            # halo on the communication stream under the interior planes
+            _lib.check(_lib.load().b2l_slab_stencil7(self._slab, x.data_ptr(), out.data_ptr(),
+                                                     x.stride(0), self.scale,
+                                                     dv.stream_ptr(x.device)),
+                       "b2l_slab_stencil7")
+            dv.LAUNCHES[0] += 2
+            return
         g = self.local_grid
         hb, lo, hi = self.halo(x)
         dv.stencil7(x, out, g.nx, g.ny, g.nz, self.scale, hb, lo, hi)
@@ -143,6 +201,14 @@ class SlabLaplacian3D(Laplacian3D):
         """out = A x on the slab and gram_out = [xb ; x]^T out (local part)."""
         from . import device as dv
 
+        if self._slab is not None:
+            _lib.check(_lib.load().b2l_slab_stencil7_gram(
+                self._slab, x.data_ptr(), out.data_ptr(), x.stride(0), self.scale,
+                xb.data_ptr() if xb is not None else None, xb.stride(0) if xb is not None else 0,
+                int(m), int(kw), gram_out.data_ptr(), dv.stream_ptr(x.device)),
+                "b2l_slab_stencil7_gram")
+            dv.LAUNCHES[0] += 3
+            return
         g = self.local_grid
         hb, lo, hi = self.halo(x)
         dv.stencil7_gram(x, out, g.nx, g.ny, g.nz, self.scale, xb, m, kw, gram_out, hb, lo, hi)

@@ -47,7 +47,7 @@ from .operators import (
     IdentityOperator,
     IdentityPreconditioner,
     JacobiPreconditioner,
-    Laplacian3D,
+    as_fused_stencil,
 )
 from .small import (NativeRitz, NotSPD, RitzFailure, chol_solve, cholesky, gen_sym_eig,
                     scaled_cholesky, sym_eig)
@@ -410,7 +410,12 @@ class LOBPCGRun:
         _lib.ensure_device(self.dev.index if self.dev.index is not None else 0)
 
         # ---- operator kinds
-        self.fused_a = isinstance(a, Laplacian3D)
+        # the built-in stencil, or the reference harness MatrixFreeOperator(n,
+        # lambda v: s * L(v)) recognised as one (operators.as_fused_stencil)
+        lap = as_fused_stencil(a)
+        if lap is not None and lap is not a:
+            self.a = a = lap
+        self.fused_a = lap is not None
         # B: none / identity (BX = X), diagonal (a row weight streamed by the
         # kernels, never materialised), or any other callable on CUDA (n, k)
         # float64 blocks -- then BX, BW, BP are carried by recurrence as the
@@ -669,14 +674,19 @@ class LOBPCGRun:
         Jacobi/identity T, no constraints, one GPU)."""
         cfg, m = self.cfg, self.m
         self._native = None
+        slab = getattr(self.a, "native_slab", None)
         if not (self.dev.type == "cuda" and self.use_f1 and self.use_sgram and self.fused_a
                 and self.b_generic is None
-                and self._allreduce is None and self.t_generic is None and self.cons is None
+                and (self._allreduce is None or slab is not None)
+                and self.t_generic is None and self.cons is None
                 and not cfg.check_invariants and cfg.verbosity < 2):
             return
         dev = self.dev
         st = _lib.b2l_iter_state()
-        g = self.a.grid
+        # a z-slab rank steps its own planes; the library exchanges the halo
+        # and sums the reductions over the ranks inside the step
+        g = getattr(self.a, "local_grid", self.a.grid)
+        st.slab = slab
         st.n, st.m, st.ldx = self.n, m, self.ld
         st.nx, st.ny, st.nz, st.scale = g.nx, g.ny, g.nz, self.a.scale
         st.tmode, st.tinv = self.tmode, self.tinv

@@ -253,7 +253,11 @@ def test_stencil7_gram(dev, dims, m, kw):
 
 @pytest.mark.parametrize("n,m,kw,kp,kwn,useb,tmode", [
     (100000, 10, 10, 10, 10, False, 1), (65537, 10, 9, 9, 7, True, 2), (5000, 4, 4, 0, 4, False, 0),
-    (300001, 16, 16, 16, 16, False, 1), (1003, 7, 3, 5, 2, True, 1), (10, 1, 1, 1, 1, False, 0)])
+    (300001, 16, 16, 16, 16, False, 1), (1003, 7, 3, 5, 2, True, 1), (10, 1, 1, 1, 1, False, 0),
+    # full-block specialisations of the local (m <= 8: C4's m = 8) and pair
+    # (m = 9..10) variants, and their partial-block twins
+    (200003, 8, 8, 8, 8, False, 1), (150001, 8, 8, 8, 8, True, 1), (120007, 8, 6, 5, 5, False, 2),
+    (180001, 9, 9, 9, 9, False, 1), (100003, 9, 9, 9, 9, True, 2), (90001, 9, 8, 7, 6, False, 1)])
 def test_lobpcg_step_kernel(dev, n, m, kw, kp, kwn, useb, tmode):
     from paper_0705_2626_b200 import device as dv
 

@@ -268,3 +268,32 @@ def test_interleaved_runs_match_solo_runs(pk):
     for r, ref in zip((r1, r2), solo):
         got = np.array([h.ritz for h in r.history])
         assert got.shape == ref.shape and np.array_equal(got, ref)
+
+
+def test_timer_entered_mid_run_matches_solo(pk):
+    """A step that leaves the native loop (a timer entered mid-run sends it
+    down the Python path) must read the reductions the native step's passes
+    wrote into the mapped host buffers, not stale device copies."""
+    N, m = 48, 10
+    a = pk.Laplacian3D((N, N, N), scale=float((N + 1) ** 2))
+    t = pk.jacobi_preconditioner(a)
+    cfg = pk.SolverConfig(block_size=m, tol=1e-8, max_iter=30, seed=0)
+    solo = pk.solve(a, t=t, config=cfg)
+    run = pk.LOBPCGRun(a, t=t, config=cfg)
+    for _ in range(6):
+        assert run.step()
+    assert run._native is not None
+
+    def timer(name, fn):
+        return fn()
+
+    with pk.device_options(timer=timer):
+        for _ in range(4):
+            run.step()
+    while run.step():
+        pass
+    rep = run.report()
+    assert rep.status == solo.status and rep.iterations_used == solo.iterations_used
+    a_ = np.array([h.ritz for h in rep.history])
+    b_ = np.array([h.ritz for h in solo.history])
+    np.testing.assert_allclose(a_, b_, rtol=1e-12)
