@@ -269,8 +269,9 @@ int b2l_rayleigh_ritz_finish(const double* g2, const double* lam, double* lam_ou
  * device-mapped pinned buffers (red_on_host = 1), else into red_dev / g2_dev
  * and copied at the next call.  coef_dev / lam_dev / pcols_dev are unused.
  * Returns B2L_ITER_OK (next passes queued; lam_next, k_next, kp, fallbacks
- * set), B2L_ITER_DRIFT (nothing changed but drift and the fetched h_red /
- * h_g2: the caller repairs), B2L_ITER_DONE (lock test applied, loop over),
+ * set), B2L_ITER_DRIFT (the block lost B-orthonormality beyond repair by
+ * the native path -- X^T B X not SPD, or B2L_NATIVE_REPAIR=0 -- nothing changed
+ * but drift and the fetched h_red / h_g2: the caller repairs), B2L_ITER_DONE (lock test applied, loop over),
  * -1003 (B2L_EDEGENERATE, lock test applied) or another negative error.
  */
 #define B2L_ITER_OK 0
@@ -312,6 +313,12 @@ typedef struct {
                                          queued the passes itself; 3 when a
                                          z-slab step left them reduced over
                                          the ranks in h_red / h_g2 */
+  int repaired;                       /* out: 1 when the drift test fired and
+                                         the step repaired the block natively
+                                         (the repaired Ritz values are in lam;
+                                         the step's outputs then sit in x, ax,
+                                         p, ap, w_cur -- DONE / EDEGENERATE:
+                                         in x2, ax2, p2, ap2, w_next) */
   struct b2l_slab* slab;              /* z-slab context (b2l_slab_create) or
                                          NULL: one GPU holds the whole grid.
                                          With a communicator, the halo of W'

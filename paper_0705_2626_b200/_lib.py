@@ -48,6 +48,7 @@ class b2l_iter_state(C.Structure):
         ("drift", C.c_double),
         ("fallbacks", C.c_int), ("k_next", C.c_int), ("kp", C.c_int),
         ("red_on_host", C.c_int),
+        ("repaired", C.c_int),
         ("slab", C.c_void_p),
     ]
 

@@ -43,7 +43,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
                 const double* d, int tmode, double tinv, const double* tvec,
                 const int* wpos, int kwn, double* wo, int ldwn, int want_ax,
                 double* red_out, cudaStream_t st, const StepHostCoef* hc,
-                StepDeferred* defer);
+                StepDeferred* defer, int x_plus_p = 1);
 
 static thread_local std::string g_err;
 

@@ -85,6 +85,7 @@ struct StepArgs {
   int tmode;
   double tinv;
   int want_ax;
+  int xpp;              // 1: X' = X Cx + P' (the update); 0: X' = X Cx (drift repair)
   int rc, nst;
   uint32_t stage_tx;    // TMA bytes per stage (full boxes)
   // shared-memory layout, in doubles
@@ -331,8 +332,8 @@ __global__ void __launch_bounds__(STEP_THREADS, 1)
             const double apn = (bw && bp) ? __dadd_rn(acc[nt][1][e], acc[nt][3][e])
                                           : (bw ? acc[nt][1][e] : acc[nt][3][e]);
             if (co + e < A.ldx) {
-              O0[r * sx + co + e] = __dadd_rn(acc[nt][4][e], pn);
-              O1[r * sx + co + e] = __dadd_rn(acc[nt][5][e], apn);
+              O0[r * sx + co + e] = A.xpp ? __dadd_rn(acc[nt][4][e], pn) : acc[nt][4][e];
+              O1[r * sx + co + e] = A.xpp ? __dadd_rn(acc[nt][5][e], apn) : acc[nt][5][e];
               O2[r * sx + co + e] = pn;
               O3[r * sx + co + e] = apn;
             }
@@ -892,8 +893,8 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
                                          : (bw ? acc[nt][0][e] : acc[nt][2][e]);
             const double apn = (bw && bp) ? __dadd_rn(acc[nt][1][e], acc[nt][3][e])
                                           : (bw ? acc[nt][1][e] : acc[nt][3][e]);
-            const double xn = __dadd_rn(acc[nt][4][e], pn);
-            const double axn = __dadd_rn(acc[nt][5][e], apn);
+            const double xn = A.xpp ? __dadd_rn(acc[nt][4][e], pn) : acc[nt][4][e];
+            const double axn = A.xpp ? __dadd_rn(acc[nt][5][e], apn) : acc[nt][5][e];
             if (co + e < A.ldx) {
               O0[r * sx + co + e] = xn;
               O1[r * sx + co + e] = axn;
@@ -1227,7 +1228,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
             sx_ = fma(x2.y, cx[(k + 1) * MFIX], sx_);
           }
           const double pv = __dadd_rn(sw_, sp_);
-          const double xv = __dadd_rn(sx_, pv);
+          const double xv = A.xpp ? __dadd_rn(sx_, pv) : sx_;
           pn_[0] = pv;
           xn_[0] = xv;
           pn_[1] = __shfl_down_sync(0xffffffffu, pv, 1);
@@ -1261,8 +1262,8 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         for (int e = 0; e < 2; ++e) {
           pn_[e] = (bw && bp) ? __dadd_rn(acc[0][e], acc[2][e]) : (bw ? acc[0][e] : acc[2][e]);
           apn_[e] = (bw && bp) ? __dadd_rn(acc[1][e], acc[3][e]) : (bw ? acc[1][e] : acc[3][e]);
-          xn_[e] = __dadd_rn(acc[4][e], pn_[e]);
-          axn_[e] = __dadd_rn(acc[5][e], apn_[e]);
+          xn_[e] = A.xpp ? __dadd_rn(acc[4][e], pn_[e]) : acc[4][e];
+          axn_[e] = A.xpp ? __dadd_rn(acc[5][e], apn_[e]) : acc[5][e];
         }
         }
         double* O0 = sm + A.out_off[0] + ob;
@@ -1473,7 +1474,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
                 const double* d, int tmode, double tinv, const double* tvec,
                 const int* wpos, int kwn, double* wo, int ldwn, int want_ax,
                 double* red_out, cudaStream_t st, const StepHostCoef* hc,
-                StepDeferred* defer) {
+                StepDeferred* defer, int x_plus_p) {
   B2L_CHECK(m >= 1 && m <= 16, -B2L_EINVAL, "step: 1 <= m <= 16 (larger blocks: b2l_update)");
   B2L_CHECK(nrows >= 1, -B2L_EINVAL, "step: empty block");
   B2L_CHECK(ldx >= m && (ldx & 1) == 0, -B2L_EINVAL, "step: ldx must be even and >= m");
@@ -1518,6 +1519,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.tmode = tmode;
   A.tinv = tinv;
   A.want_ax = want_ax;
+  A.xpp = x_plus_p;
   // Gram of the next step: L = [X' W' P'], R = [X' W' P' AP']
   A.lcum[0] = 0;
   A.lcum[1] = m;

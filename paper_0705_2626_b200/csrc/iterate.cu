@@ -30,7 +30,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx, co
                 double* apo, const double* lam, const double* d, int tmode, double tinv,
                 const double* tvec, const int* wpos, int kwn, double* wo, int ldwn, int want_ax,
                 double* red_out, cudaStream_t st, const StepHostCoef* hc,
-                StepDeferred* defer);
+                StepDeferred* defer, int x_plus_p = 1);
 int stencil7_gram(const double* in, double* out, int nx, int ny, int nz, int ld,
                   const double* halo, int has_lo, int has_hi, double scale, const double* x,
                   int ldx, int m, int kw, double* gram_out, cudaStream_t st);
@@ -43,6 +43,13 @@ int slab_sgram_after_halo(b2l_slab* s, const double* in, double* out, int ld, do
                           const double* x, int ldx, int m, int kw, double* gram_out,
                           cudaStream_t st);
 int slab_allreduce(b2l_slab* s, double* buf, size_t count, cudaStream_t st);
+int repair_coef(int m, const double* gxx, const double* gxa, double* lam_out, double* m_out);
+struct HostBlock {
+  const double* p;
+  int ld, cols;
+};
+int gram(int nrows, const HostBlock* L, int nl, const HostBlock* R, int nr, unsigned rw_mask,
+         const double* d, const unsigned char* pair_mode, double* out, cudaStream_t st);
 }  // namespace b2l
 
 using namespace b2l;
@@ -117,6 +124,84 @@ extern "C" int b2l_iter_profile(double* out, int reset) {
   return g_prof_on ? 1 : 0;
 }
 
+// Drift repair on the device state (_refresh_ritz, lobpcg.py:280-296, at the
+// top of the iteration, lobpcg.py:419-428), without leaving the native loop:
+// X^T A X by one Gram pass (X^T B X is F1's), the folded rotation
+// M = R_eff^-1 Q on the host (repair_coef), then ONE F1 pass in its
+// no-update form -- X'' = X M, AX'' = AX M (x_plus_p = 0), P and AP carried
+// through (Cp = I), the residual W'' with the repaired Ritz values, its
+// norms and the Grams -- and the stencil pass on W''.  On return h_red /
+// h_g2 hold the repaired iteration's reductions (the main stream is
+// synchronised), s->lam the repaired Ritz values, and the state's block
+// pointers are swapped to the repaired blocks.  B2L_ITER_DRIFT: X^T B X is
+// not SPD, the caller's path reports the failure.
+static int native_repair(b2l_iter_state* s, b2l_slab* S, bool multi, cudaStream_t st) {
+  const int m = s->m, kst = s->kst;
+  const int b = 3 * m + kst;
+  if (!s->have_p) return B2L_ITER_DRIFT;
+  std::vector<double> gxx((size_t)m * m), gxa((size_t)m * m), M((size_t)m * m), lam(m);
+  const double* G1 = s->h_red + 2 * m;
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) gxx[(size_t)i * m + j] = G1[(size_t)i * b + j];
+  // X^T A X (upper), into the reduction scratch, summed over the slab ranks
+  const HostBlock L[1] = {{s->x, s->ldx, m}};
+  const HostBlock R[1] = {{s->ax, s->ldx, m}};
+  const unsigned char upper = 2;
+  if (int r = gram(s->n, L, 1, R, 1, 0u, nullptr, &upper, s->red_dev, st)) return r;
+  if (multi)
+    if (int r = slab_allreduce(S, s->red_dev, (size_t)m * m, st)) return r;
+  B2L_CUDA(cudaMemcpyAsync(gxa.data(), s->red_dev, (size_t)m * m * sizeof(double),
+                           cudaMemcpyDeviceToHost, st));
+  B2L_CUDA(cudaStreamSynchronize(st));
+  const int rc = repair_coef(m, gxx.data(), gxa.data(), lam.data(), M.data());
+  if (rc == 1) return B2L_ITER_DRIFT;
+  if (rc) return rc;
+  for (int j = 0; j < m; ++j) s->lam[j] = lam[j];
+  // coefficients by value: [Cx = M | Cp = I], the stored W columns stay put
+  std::vector<double> coef((size_t)2 * m * m, 0.0);
+  for (size_t i = 0; i < (size_t)m * m; ++i) coef[i] = M[i];
+  for (int i = 0; i < m; ++i) coef[(size_t)m * m + (size_t)i * m + i] = 1.0;
+  std::vector<int> pcols(m), wpos(m, -1);
+  for (int j = 0; j < m; ++j) pcols[j] = j;
+  for (int j = 0, q = 0; j < m; ++j)
+    if (s->active[j]) wpos[j] = q++;
+  const StepHostCoef hc{coef.data(), lam.data(), pcols.data(), wpos.data()};
+  const size_t nred = (size_t)2 * m + (size_t)(2 * m + kst) * b;
+  const size_t ng2 = (size_t)(m + kst) * kst;
+  double* red_h = multi ? nullptr : mapped(s->h_red);
+  double* g2_h = multi ? nullptr : mapped(s->h_g2);
+  int r = lobpcg_step(s->n, m, s->x, s->ax, s->ldx, nullptr, nullptr, 0, 0, s->p, s->ap, m,
+                      nullptr, nullptr, s->x2, s->ax2, s->p2, s->ap2, nullptr, s->bdiag, s->tmode,
+                      s->tinv, s->tvec, nullptr, kst, s->w_next, even(kst), s->relative_tol,
+                      red_h ? red_h : s->red_dev, st, &hc, nullptr, /*x_plus_p=*/0);
+  if (r) return r;
+  if (multi) {
+    if ((r = slab_halo_start(S, s->w_next, even(kst), st))) return r;
+    if ((r = slab_sgram_after_halo(S, s->w_next, s->aw, even(kst), s->scale, s->x2, s->ldx, m,
+                                   kst, s->g2_dev, st)))
+      return r;
+    if ((r = slab_allreduce(S, s->red_dev, nred, st))) return r;
+    if ((r = slab_allreduce(S, s->g2_dev, ng2, st))) return r;
+  } else {
+    r = stencil7_gram(s->w_next, s->aw, s->nx, s->ny, s->nz, even(kst), nullptr, 0, 0, s->scale,
+                      s->x2, s->ldx, m, kst, g2_h ? g2_h : s->g2_dev, st);
+    if (r) return r;
+  }
+  if (!red_h)
+    B2L_CUDA(cudaMemcpyAsync(s->h_red, s->red_dev, nred * sizeof(double),
+                             cudaMemcpyDeviceToHost, st));
+  if (!g2_h)
+    B2L_CUDA(cudaMemcpyAsync(s->h_g2, s->g2_dev, ng2 * sizeof(double), cudaMemcpyDeviceToHost,
+                             st));
+  B2L_CUDA(cudaStreamSynchronize(st));
+  std::swap(s->x, s->x2);
+  std::swap(s->ax, s->ax2);
+  std::swap(s->p, s->p2);
+  std::swap(s->ap, s->ap2);
+  std::swap(s->w_cur, s->w_next);
+  return 0;
+}
+
 extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
   if (!s || s->m < 1 || s->kst < 1 || s->kst > s->m)
     return fail(-B2L_EINVAL, "fast_iteration: bad state");
@@ -188,9 +273,17 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
       if (!(v <= drift)) drift = v;   // NaN-propagating max
     }
   s->drift = drift;
+  s->repaired = 0;
   if (!(drift <= s->drift_limit)) {
     if (int r = sync_main()) return r;   // the caller reads h_g2 too
-    return B2L_ITER_DRIFT;
+    static const bool python_repair = [] {
+      const char* v = getenv("B2L_NATIVE_REPAIR");
+      return v && v[0] == '0';
+    }();
+    if (python_repair) return B2L_ITER_DRIFT;
+    const int r = native_repair(s, S, multi, st);
+    if (r) return r;   // B2L_ITER_DRIFT: the caller's repair path
+    s->repaired = 1;   // h_red / h_g2 and the block pointers are the repaired ones
   }
 
   // ---- lock test (lobpcg.py:429-437)

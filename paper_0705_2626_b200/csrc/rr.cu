@@ -774,6 +774,62 @@ int rr_finish_tls(const double* g2, const double* lam, double* lam_out, double* 
   return rr_finish(*p, g2, lam, lam_out, coef_out, pcols_out, kp_out, fallbacks_out);
 }
 
+// Drift repair, folded (_refresh_ritz lobpcg.py:280-296): from the Grams
+// gxx = X^T B X and gxa = X^T A X of the drifted block (m x m row-major,
+// upper triangles read), the rotation M = R_eff^-1 Q that the reference
+// applies in two steps -- X <- X R_eff^-1 (b_orthonormalize) then X <- X Q
+// with (lam, Q) = eigh of the re-projected X^T A X -- computed on the small
+// matrices: Q diagonalises R_eff^-T gxa R_eff^-1.  The LAPACK routines the
+// Python path uses (small.scaled_cholesky / sym_eig: dpotrf, dtrtri, dsyevr)
+// when registered.  m_out row-major m x m; lam_out ascending.  Returns 0,
+// or 1 when gxx is not SPD (the caller's path reports BasisDegeneracy).
+int repair_coef(int m, const double* gxx, const double* gxa, double* lam_out, double* m_out) {
+  const int saved = g_rr_dim;
+  g_rr_dim = 1 << 20;   // use_lapack(): the routines small.py calls
+  struct Restore {
+    int v;
+    ~Restore() { g_rr_dim = v; }
+  } restore{saved};
+  try {
+    Mat G(m, m), A(m, m);
+    for (int i = 0; i < m; ++i)
+      for (int j = i; j < m; ++j) {
+        G(i, j) = G(j, i) = gxx[(size_t)i * m + j];
+        A(i, j) = A(j, i) = gxa[(size_t)i * m + j];
+      }
+    const Mat minv = scaled_cholesky_inv(G, 0.0);
+    const Mat T = matmul(transpose(minv), matmul(A, minv));
+    Mat S(m, m);   // upper triangle of T read, as eigh(lower=False)
+    for (int j = 0; j < m; ++j)
+      for (int i = 0; i <= j; ++i) S(i, j) = S(j, i) = T(i, j);
+    Mat V(m, m);
+    if (g_syevr) {
+      char jobz = 'V', range = 'A', uplo = 'U';
+      int n = m, lda = m, il = 1, iu = m, mfound = 0, ldz = m, info = 0;
+      double vl = 0.0, vu = 0.0, abstol = 0.0;
+      std::vector<double> z((size_t)m * m), work((size_t)26 * m + 64);
+      std::vector<int> isuppz(2 * m + 2), iwork((size_t)10 * m + 16);
+      int lwork = (int)work.size(), liwork = (int)iwork.size();
+      g_syevr(&jobz, &range, &uplo, &n, S.p(), &lda, &vl, &vu, &il, &iu, &abstol, &mfound,
+              lam_out, z.data(), &ldz, isuppz.data(), work.data(), &lwork, iwork.data(), &liwork,
+              &info);
+      if (info != 0) throw LapackError{"dsyevr", info};
+      V.a = z;
+    } else if (symeig_ql(m, S.p(), m, lam_out, V.p()) != 0) {
+      throw LapackError{"tql2 (no convergence)", 1};
+    }
+    const Mat M = matmul(minv, V);
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) m_out[(size_t)i * m + j] = M(i, j);
+    return 0;
+  } catch (const NotSPD&) {
+    return 1;
+  } catch (const LapackError& e) {
+    return fail(-B2L_ELAPACK, std::string("drift repair: ") + e.what + " info " +
+                                   std::to_string(e.info));
+  }
+}
+
 }  // namespace b2l
 
 extern "C" int b2l_rayleigh_ritz_begin(int m, int kst, int have_p, const double* g1, int ldg1,

@@ -742,6 +742,14 @@ class LOBPCGRun:
         newly = self._n_newly
         self.norms = norms
         self.f1_pending = self.sg_pending = False
+        if st.repaired:
+            # the drift test fired and the step repaired the block on the
+            # device (lam now holds the repaired Ritz values): the repaired
+            # blocks sit in the "next" buffers
+            self.drift_repairs += 1
+            self._swap_blocks()
+            if cfg.verbosity >= 2:
+                print(f"  it {it:4d}  Ritz block re-orthonormalized (drift {st.drift:.1e})")
         self.history.append(HistoryEntry(
             iteration=it,
             ritz=lam.copy() if cfg.lock_history else None,
@@ -763,16 +771,19 @@ class LOBPCGRun:
             return False
         # ITER_OK: the next F1 and stencil pass are queued
         self.pending += st.fallbacks
-        self.X, self.X2 = self.X2, self.X
-        self.AX, self.AX2 = self.AX2, self.AX
-        self.P, self.P2 = self.P2, self.P
-        self.AP, self.AP2 = self.AP2, self.AP
+        self._swap_blocks()
         self.have_p = True
-        self.wcur = 1 - self.wcur
         self.lam = self._n_lamnext.copy()
         self.f1_pending = self.sg_pending = True
         self.it += 1
         return True
+
+    def _swap_blocks(self):
+        self.X, self.X2 = self.X2, self.X
+        self.AX, self.AX2 = self.AX2, self.AX
+        self.P, self.P2 = self.P2, self.P
+        self.AP, self.AP2 = self.AP2, self.AP
+        self.wcur = 1 - self.wcur
 
     # ---------------------------------------------------------- iteration
     def step(self):

@@ -263,7 +263,21 @@ def generic_b():
         r = record(rep, m)
         print(name, rep.status, rep.iterations_used, np.abs(rep.eigenvalues / vals[:m] - 1).max(),
               flush=True)
-        np.savez_compressed(OUT / f"genb_{name}.npz", dense_vals=vals[:m], **r)
+        # the reference's own iteration band: A scaled by (1 + k ulp)
+        band = []
+        for k in (1, -1, 2, -2, 3, -3, 4, -4):
+            s1 = 1.0 + k * 2.0 ** -52
+
+            def ap(v, A=A, s1=s1):
+                return s1 * A(v)
+
+            Ap = MatrixFreeOperator(n, ap, spd=True, diag=np.full(n, 6.0 * s1 * (N + 1) ** 2))
+            rp = solve(Ap, b=B, t=jacobi_preconditioner(Ap) if jac else None,
+                       config=SolverConfig(block_size=m, tol=tol, max_iter=max_iter, seed=0))
+            band.append(rp.iterations_used)
+        print(name, "band", band, flush=True)
+        np.savez_compressed(OUT / f"genb_{name}.npz", dense_vals=vals[:m],
+                            band_iterations=np.array(band), **r)
     print(f"generic B {time.time() - t0:.1f} s")
 
 

@@ -297,3 +297,48 @@ def test_timer_entered_mid_run_matches_solo(pk):
     a_ = np.array([h.ritz for h in rep.history])
     b_ = np.array([h.ritz for h in solo.history])
     np.testing.assert_allclose(a_, b_, rtol=1e-12)
+
+
+_REPAIR_CASE = """
+import json, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import paper_0705_2626_b200 as pk
+N, m = 64, 10
+a = pk.Laplacian3D((N, N, N), scale=float((N + 1) ** 2))
+run = pk.LOBPCGRun(a, t=pk.jacobi_preconditioner(a),
+                   config=pk.SolverConfig(block_size=m, tol=1e-8, max_iter=150, seed=0))
+while run.step():
+    pass
+rep = run.report()
+print(json.dumps(dict(repairs=run.drift_repairs, status=rep.status, it=rep.iterations_used,
+                      ritz=[list(map(float, h.ritz)) for h in rep.history],
+                      eig=list(map(float, rep.eigenvalues)))))
+"""
+
+
+def test_native_drift_repair_matches_python_repair():
+    """The drift repair inside the native loop (one X^T A X Gram, the folded
+    rotation, one no-update F1 pass) against the Python repair path
+    (B2L_NATIVE_REPAIR=0: rotations + Grams + residual as separate kernels)
+    on the same problem: same repair count, status and iterations, Ritz
+    trajectory equal to rounding."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parents[1])
+    out = {}
+    for mode in ("1", "0"):
+        env = dict(os.environ, B2L_NATIVE_REPAIR=mode)
+        r = subprocess.run([sys.executable, "-c", _REPAIR_CASE.format(root=root)], env=env,
+                           capture_output=True, text=True, timeout=600, cwd=root)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[mode] = json.loads(r.stdout.strip().splitlines()[-1])
+    nat, py = out["1"], out["0"]
+    assert nat["repairs"] >= 1 and nat["repairs"] == py["repairs"]
+    assert nat["status"] == py["status"] and nat["it"] == py["it"]
+    np.testing.assert_allclose(np.array(nat["ritz"]), np.array(py["ritz"]), rtol=1e-9)
+    np.testing.assert_allclose(nat["eig"], py["eig"], rtol=1e-10)
