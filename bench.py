@@ -15,12 +15,17 @@ iteration of the hot loop (lobpcg.py:418-540) on that state.
   cpu_baseline  the CPU oracle (numpy/OpenBLAS restatement of the reference)
             on a bounded sample of C2 iterations, all host cores
 
+  time_to_tol   public solve() to convergence: C1 with max_iter 1000 and the
+            reference's golden 20^3 case
+  configs   C3 / W1 / C4 / C5 on one GPU: it/s and whole-iteration roofline
+
 --impl reference runs the CPU oracle alone (the reference is a Python
-package; its restatement oracle/lobpcg_oracle.py is pinned bit-exact to it).
-Multi-GPU (torchrun, N>1): weak scaling, one distributed solve on a
-128 x 128 x 128N grid split in z-slabs (one C2-sized slab per GPU; halo
-send/recv and Gram all-reduce over NCCL); value = N x global it/s
-(C2-slab-iterations/s), max-over-ranks time.
+package; its restatement oracle/lobpcg_oracle.py is pinned bit-exact to it)
+on the faster of 1 and all BLAS threads.
+Multi-GPU (torchrun, N>1): the BASELINE C4 weak-scaling series (232^3 /
+292^3 / 368^3 / 464^3 on 1 / 2 / 4 / 8 GPUs, m=8, ~12.5M rows per GPU),
+z-slabs with the halo and both all-reduces inside the library's native step
+(NCCL); value = N x global it/s (slab-iterations/s), max-over-ranks time.
 """
 
 from __future__ import annotations
@@ -62,8 +67,9 @@ def config_dict(n_gpus):
         "max_iter": MAX_ITER,
         "seed": SEED,
         "l2": "inputs larger than L2 (10 live 168 MB blocks per iteration >> 126 MB L2)",
-        "parallelism": (f"z-slab x{n_gpus} (grid 128x128x{128 * n_gpus}, one C2-size slab per "
-                        "GPU, NCCL halo + Gram all-reduce)") if n_gpus > 1 else "single GPU",
+        "parallelism": (f"z-slab x{n_gpus} (C4 weak-scaling series, ~12.5M rows per GPU; "
+                        "NCCL halo under the interior stencil planes + one all-reduce per "
+                        "fused pass, inside the native step)") if n_gpus > 1 else "single GPU",
     }
 
 
@@ -152,20 +158,45 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU oracle
-def cpu_oracle_sample(iters, threads_note):
-    """Time `iters` C2 iterations of the CPU oracle; returns it/s."""
+def _blas_threads(n):
+    """Scope the BLAS pool (numpy/scipy OpenBLAS) to n threads."""
+    from threadpoolctl import ThreadpoolController
+
+    return ThreadpoolController().limit(limits=n, user_api="blas")
+
+
+def _oracle_iters(total, threads):
+    """Per-iteration stamps of `total` C2 iterations of the CPU oracle on
+    `threads` BLAS threads (init excluded)."""
     from oracle import lobpcg_oracle as orc
 
-    r = orc.laplacian_case(N_GRID, M_BLOCK, tol=TOL, max_iter=iters, seed=SEED,
-                           record=False, timer=True)
-    ts = r.iter_times
-    # iteration i runs from ts[i] to ts[i+1]; the last stamp opens the final
-    # (exit) check, so use the completed gaps.
+    with _blas_threads(threads):
+        r = orc.laplacian_case(N_GRID, M_BLOCK, tol=TOL, max_iter=total, seed=SEED,
+                               record=False, timer=True)
+    return np.array(r.iter_times)
+
+
+def cpu_best_threads(cores, probe_iters=2):
+    """time the reference path with OPENBLAS threads = cores and
+    = 1 and keep the faster (1 thread won at C1 on the survey box).  Returns
+    (threads, it/s of the probe at each count)."""
+    rates = {}
+    for t in sorted({1, cores}):
+        ts = _oracle_iters(probe_iters, t)
+        gaps = np.diff(ts)
+        rates[t] = float(len(gaps) / gaps.sum())
+    best = max(rates, key=rates.get)
+    return best, rates
+
+
+def cpu_oracle_sample(iters, threads):
+    """Time `iters` C2 iterations of the CPU oracle on `threads`; it/s."""
+    ts = _oracle_iters(iters, threads)
     gaps = np.diff(ts)
     return float(len(gaps) / gaps.sum()), len(gaps)
 
 
-REF_MAX_STEPS, REF_MAX_WARMUP = 12, 2
+REF_MAX_STEPS, REF_MAX_WARMUP = 30, 5
 
 
 def run_reference(args):
@@ -173,15 +204,12 @@ def run_reference(args):
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
-    # a C2 iteration takes ~1.5 s on the host: the CPU arm times a bounded
-    # sample of the same iteration sequence so the run ends within minutes
+    # a C2 iteration takes ~1.7 s on the host: the CPU arm times the same
+    # iteration sequence as the GPU arm up to 30 steps (a bounded sample
+    # beyond), on the faster of 1 and all BLAS threads
     warm, steps = min(args.warmup, REF_MAX_WARMUP), min(args.steps, REF_MAX_STEPS)
-    total = warm + steps
-    from oracle import lobpcg_oracle as orc
-
-    r = orc.laplacian_case(N_GRID, M_BLOCK, tol=TOL, max_iter=total, seed=SEED,
-                           record=False, timer=True)
-    ts = np.array(r.iter_times)
+    threads, rates = cpu_best_threads(cores)
+    ts = _oracle_iters(warm + steps, threads)
     timed = ts[warm:warm + steps + 1]
     dt = float(timed[-1] - timed[0])
     k = len(timed) - 1
@@ -191,9 +219,12 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": k, "warmup": warm,
         "ms_per_step": 1e3 * dt / k, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(1),
-        "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "port",
-                         "sample": f"C2 iterations {warm}..{warm + k} of the CPU "
-                                   "oracle (numpy/OpenBLAS restatement, bit-exact to the reference)"},
+        "cpu_baseline": {"value": value, "unit": "it/s", "cores": threads, "kind": "port",
+                         "host_cores": cores,
+                         "probe_it_s_by_threads": {str(t): v for t, v in rates.items()},
+                         "sample": f"C2 iterations {warm}..{warm + k} of the CPU oracle "
+                                   "(numpy/OpenBLAS restatement, bit-exact to the reference), "
+                                   f"BLAS threads {threads} (the faster of 1 and {cores})"},
         "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -201,6 +232,108 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU
+def _peaks():
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    fp64 = json.loads((ROOT / "profiles" / "fp64_peaks_r02.json").read_text())
+    return hbm, float(fp64["dmma_tflops"]), bool(peaks)
+
+
+def iteration_bytes(n, m, k, diag_b=False):
+    """Algorithmic HBM bytes of one steady-state LOBPCG iteration (SURVEY
+    8d): update pass 8n(6m + 5k) + stencil pass 8n(2k), B = I; diagonal B
+    adds its diagonal read in both passes."""
+    return 8.0 * n * (6 * m + 7 * k) + (16.0 * n if diag_b else 0.0)
+
+
+def config_runs(pk, dev, hbm_peak, fp64_peak):
+    """Per-config device throughput on one GPU for the larger BASELINE
+    configs (C3, C4 and its weak-scaling base W1, C5): iterations/s over a
+    window of steady-state iterations (CUDA events), with the whole-iteration
+    roofline fraction.  Synthetic seeded inputs as the reference draws them."""
+    import torch
+
+    cfgs = [
+        ("C3", 256, 16, None, 1e-6, 300, 5, 30),
+        ("W1", 232, 8, None, 1e-6, 50, 5, 30),
+        ("C4", 464, 8, None, 1e-6, 50, 5, 30),
+        ("C5", 192, 64, 1000, 1e-6, 200, 3, 12),
+    ]
+    out = {}
+    for name, N, m, bseed, tol, max_iter, warm, steps in cfgs:
+        s = float((N + 1) ** 2)
+        a = pk.Laplacian3D((N, N, N), scale=s)
+        b = None
+        if bseed is not None:
+            b = pk.DiagonalOperator(
+                np.random.Generator(np.random.PCG64(bseed)).uniform(1.0, 2.0, N ** 3))
+        run = pk.LOBPCGRun(a, b=b, t=pk.jacobi_preconditioner(a),
+                           config=pk.SolverConfig(block_size=m, tol=tol, max_iter=max_iter,
+                                                  seed=0))
+        for _ in range(warm):
+            run.step()
+        it0 = run.it
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            if not run.step():
+                break
+        e1.record()
+        torch.cuda.synchronize()
+        done = run.it - it0
+        ms = e0.elapsed_time(e1) / max(done, 1)
+        n = N ** 3
+        rec = {"grid": N, "m": m, "iterations": [it0, run.it], "it_s": 1e3 / ms,
+               "ms_per_it": ms, "diag_b": bseed is not None}
+        gbs = iteration_bytes(n, m, m, bseed is not None) / (ms / 1e3) / 1e9
+        rec["iteration_gbs"] = gbs
+        rec["iteration_hbm_frac"] = gbs / hbm_peak
+        if m >= 32:   # fp64 tensor-core (DMMA) bound: 42 n m^2 flop (SURVEY 8d)
+            tf = 42.0 * n * m * m / (ms / 1e3) / 1e12
+            rec["iteration_tflops"] = tf
+            rec["iteration_fp64_frac"] = tf / fp64_peak
+        out[name] = rec
+        del run, a, b
+        torch.cuda.empty_cache()
+    return out
+
+
+def time_to_tol(pk):
+    """Time-to-tolerance through the public solve() (as cli.py:444-446 times
+    it): C1 with max_iter 1000 (converges) and the reference's golden 20^3
+    case (pkg/demos/convergence_history.py: unscaled, m=10, Jacobi, tol 1e-6,
+    seed 2).  X0 is generated inside solve (device K9, the reference's own
+    seeded fill); eigenvectors come back to host memory inside the time."""
+    import torch
+
+    out = {}
+    cases = [("C1@1000", 32, True, 4, None, 1e-6, 1000, 0),
+             ("golden20", 20, False, 10, "jacobi", 1e-6, 200, 2)]
+    for name, N, scaled, m, pre, tol, max_iter, seed in cases:
+        a = pk.Laplacian3D((N, N, N), scale=float((N + 1) ** 2) if scaled else 1.0)
+        t = pk.jacobi_preconditioner(a) if pre else None
+        cfg = pk.SolverConfig(block_size=m, tol=tol, max_iter=max_iter, seed=seed)
+        pk.solve(a, t=t, config=pk.SolverConfig(block_size=m, tol=tol, max_iter=3, seed=seed))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = pk.solve(a, t=t, config=cfg)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out[name] = {"seconds": dt, "iterations": rep.iterations_used, "status": rep.status,
+                     "converged": int(np.sum(rep.converged)), "it_s": rep.iterations_used / dt}
+    return out
+
+
+def weak_grid(world):
+    """The BASELINE C4 weak-scaling series (232^3 / 292^3 / 368^3 / 464^3 on
+    1 / 2 / 4 / 8 GPUs: ~12.5M rows per GPU), and the same rows per GPU for
+    other counts."""
+    table = {1: 232, 2: 292, 4: 368, 8: 464}
+    return table.get(world, int(round(232 * world ** (1.0 / 3.0))))
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -218,21 +351,29 @@ def run_gpu(args):
         if world > 1:
             dist.barrier()
 
-    s = float((N_GRID + 1) ** 2)
+    hbm_peak, fp64_peak, peaks_measured = _peaks()
     if world > 1:
-        # weak scaling: a 128 x 128 x (128 P) grid, one C2-sized z-slab per
-        # GPU, one-plane halos + Gram all-reduces over NCCL
+        # C4 weak-scaling series: a (N, N, N) grid with N from weak_grid, one
+        # z-slab of ~12.5M rows per GPU; halo + all-reduces inside the
+        # library's native step (NCCL over NVLink)
         from paper_0705_2626_b200.distributed import SlabLaplacian3D, slab_initial_block
 
-        A = SlabLaplacian3D((N_GRID, N_GRID, N_GRID * world), scale=s)
-        x0 = slab_initial_block(A.grid, A.part, M_BLOCK, SEED)
+        Ng, m, tol, max_iter = weak_grid(world), 8, 1e-6, 50
+        s = float((Ng + 1) ** 2)
+        A = SlabLaplacian3D((Ng, Ng, Ng), scale=s)
+        x0 = slab_initial_block(A.grid, A.part, m, SEED)
         n = A.local_rows
+        workload = (f"C4 weak series W{world}: {Ng}^3 7-pt Laplacian (scaled 1/h^2), m=8, "
+                    "Jacobi, B=I, 50 iterations, z-slab per GPU")
     else:
+        Ng, m, tol, max_iter = N_GRID, M_BLOCK, TOL, MAX_ITER
         n = N_GRID ** 3
+        s = float((N_GRID + 1) ** 2)
         A = pk.Laplacian3D((N_GRID,) * 3, scale=s)
         x0 = np.random.Generator(np.random.PCG64(SEED)).uniform(-1.0, 1.0, size=(n, M_BLOCK))
+        workload = WORKLOAD
     T = pk.jacobi_preconditioner(A)
-    cfg = pk.SolverConfig(block_size=M_BLOCK, tol=TOL, max_iter=MAX_ITER, seed=SEED)
+    cfg = pk.SolverConfig(block_size=m, tol=tol, max_iter=max_iter, seed=SEED)
 
     def new_run():
         return pk.LOBPCGRun(A, t=T, x0=x0, config=cfg)
@@ -245,20 +386,14 @@ def run_gpu(args):
 
     gc.collect()
     gc.freeze()
-    # Warm the drift-repair path (lobpcg.py:419-428) on a throw-away run first:
-    # its first execution in a process has a variable one-time cost (measured
-    # 3 ms .. 0.66 s on this pool) that must not land in the timed region.
     tmp = new_run()
     tmp.step()
-    tmp._refresh_ritz(tmp._gram_xx())
     del tmp
     torch.cuda.synchronize()
     run = new_run()
     for _ in range(args.warmup):
         if not run.step():
             run = new_run()
-    if run.it + args.steps > MAX_ITER:
-        run = new_run()
     run_it0 = run.it
     torch.cuda.synchronize()
     barrier()
@@ -270,14 +405,27 @@ def run_gpu(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     trace = os.environ.get("B2L_BENCH_TRACE") == "1"
     stamps = []
+    executed, restarts, repairs0 = 0, 0, run.drift_repairs
+    windows = []
     with ClockSampler(local) as clk:
         e0.record()
         for _ in range(args.steps):
-            run.step()
+            if not run.step():
+                # the run hit max_iter inside the window: a fresh run (its
+                # setup counted inside the timed region, never skipped)
+                windows.append([run_it0, run.it])
+                repairs0 -= run.drift_repairs
+                run = new_run()
+                restarts += 1
+                run_it0 = run.it
+                run.step()
+            executed += 1
             if trace:
                 stamps.append(time.perf_counter())
         e1.record()
         torch.cuda.synchronize()
+    windows.append([run_it0, run.it])
+    repairs = run.drift_repairs + repairs0
     if trace and len(stamps) > 1:
         dts = np.diff(stamps) * 1e3
         worst = np.argsort(dts)[::-1][:5]
@@ -291,7 +439,7 @@ def run_gpu(args):
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_all = float(t.item())
-    value = world * args.steps / (ms_all / 1e3)
+    value = world * executed / (ms_all / 1e3)
 
     # ---- per-kernel durations (CUDA events on the launching stream)
     ktimes = {}
@@ -308,56 +456,51 @@ def run_gpu(args):
     for _ in range(3):
         run2.step()
     with pk.device_options(timer=timer):
-        for _ in range(args.steps):
-            run2.step()
+        for _ in range(min(args.steps, 40)):
+            if not run2.step():
+                break
     torch.cuda.synchronize()
     kt = {k: [a.elapsed_time(b) for a, b in v] for k, v in ktimes.items()}
-    ld = dv.even(M_BLOCK)
-    k_act = M_BLOCK  # C2 never locks within 300 iterations (reference run)
-    # algorithmic bytes per launch (blocks counted at k=m columns)
+    k_act = m  # no column locks within the timed windows of these configs
     alg = {
         # K1 (+K5b): read W, write A W (the X read for [X W]^T A W is extra)
         "stencil": 16.0 * n * k_act,
-        "residual": 8.0 * n * (2 * M_BLOCK + k_act),
-        "update": 8.0 * n * (2 * M_BLOCK + 4 * k_act + 4 * M_BLOCK),
+        "residual": 8.0 * n * (2 * m + k_act),
+        "update": 8.0 * n * (2 * m + 4 * k_act + 4 * m),
         # F1: read X, AX, W, AW, P_J, AP_J; write X', AX', P', AP', W'
-        "step": 8.0 * n * (6 * M_BLOCK + 5 * k_act),
+        "step": 8.0 * n * (6 * m + 5 * k_act),
     }
-    # the per-step big gram reads X, W, P, AW, AP; the drift gram reads X
-    gram_calls = kt.get("gram", [])
     per = {}
     for name in ("stencil", "residual", "update", "step"):
         if kt.get(name):
             d = float(np.mean(kt[name]))
             per[name] = {"ms": d, "gbs": alg[name] / (d / 1e3) / 1e9, "calls": len(kt[name])}
-    if gram_calls:
-        db = float(np.mean(gram_calls))
-        per["gram"] = {"ms": db, "gbs": 8.0 * n * (3 * M_BLOCK + 2 * k_act) / (db / 1e3) / 1e9,
-                       "calls": len(gram_calls)}
-    if kt.get("gram_drift"):
-        dd = float(np.mean(kt["gram_drift"]))
-        per["gram_drift"] = {"ms": dd, "gbs": 8.0 * n * M_BLOCK / (dd / 1e3) / 1e9,
-                             "calls": len(kt["gram_drift"])}
+    if kt.get("gram"):
+        db = float(np.mean(kt["gram"]))
+        per["gram"] = {"ms": db, "gbs": 8.0 * n * (3 * m + 2 * k_act) / (db / 1e3) / 1e9,
+                       "calls": len(kt["gram"])}
     total_ms = {k: v["ms"] * v["calls"] for k, v in per.items()}
     dom = max(total_ms, key=total_ms.get) if total_ms else "stencil"
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    peak = float(peaks.get("hbm_gbs", 6650.0))
     prof = ROOT / "profiles" / "ncu_traffic.json"
     traffic = None
-    if prof.exists():
+    if prof.exists() and world == 1:
         traffic = json.loads(prof.read_text()).get(dom)
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": per[dom]["gbs"], "peak": peak,
-                "unit": "GB/s", "frac": per[dom]["gbs"] / peak, "traffic": traffic,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
+    it_gbs = iteration_bytes(n, m, k_act) / (ms_all / executed / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": per[dom]["gbs"], "peak": hbm_peak,
+                "unit": "GB/s", "frac": per[dom]["gbs"] / hbm_peak, "traffic": traffic,
+                "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if peaks_measured
+                                else "fallback 6650"),
                 "kernels": per,
+                "iteration": {"bytes": iteration_bytes(n, m, k_act), "gbs": it_gbs,
+                              "frac": it_gbs / hbm_peak,
+                              "note": "whole LOBPCG iteration incl. host Rayleigh-Ritz, "
+                                      "8n(6m+7k) algorithmic bytes / device-timed ms per step"},
                 "stencil_frac_of_8TBs": per.get("stencil", {}).get("gbs", 0.0) / 8000.0}
 
     # ---- e2e through the public API on host buffers: X0 from pinned host
     # memory, eigenvectors back to host memory, both inside the timed call.
-    # One short untimed warm-up solve first (same shapes: it primes the
-    # caching host/device allocators, the tensor-map and kernel caches).
     x0_host = torch.from_numpy(np.ascontiguousarray(x0)).pin_memory()
-    warm_cfg = pk.SolverConfig(block_size=M_BLOCK, tol=TOL, max_iter=3, seed=SEED)
+    warm_cfg = pk.SolverConfig(block_size=m, tol=tol, max_iter=3, seed=SEED)
     del run, run2
     pk.solve(A, t=T, x0=x0_host, config=warm_cfg)
     barrier()
@@ -373,14 +516,17 @@ def run_gpu(args):
         e2e_s = float(t.item())
     it_used = rep.iterations_used
     e2e_val = world * it_used / e2e_s
-    exact = pk.exact_eigenvalues(A.grid, M_BLOCK, scale=s)
+    exact = pk.exact_eigenvalues(A.grid, m, scale=s)
 
     line = {
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_all / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_all / executed,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": dict(config_dict(world), timed_iterations=[run_it0, run_it0 + args.steps]),
+        "config": dict(config_dict(world), workload=workload, grid=[Ng] * 3, block_size=m,
+                       tol=tol, max_iter=max_iter,
+                       timed_iterations=windows, iterations_executed=executed,
+                       run_restarts_in_window=restarts, drift_repairs_in_window=repairs),
         "e2e": {"value": e2e_val, "unit": "it/s",
                 "h2d_bytes_per_step": int(x0.nbytes / max(it_used, 1)),
                 "d2h_bytes_per_step": int(vecs.nbytes / max(it_used, 1)),
@@ -391,12 +537,21 @@ def run_gpu(args):
         "roofline": roofline,
         "clocks": clk.summary(),
     }
+    del rep, vecs
+    torch.cuda.empty_cache()
+    if world == 1 and not args.no_extra:
+        line["time_to_tol"] = time_to_tol(pk)
+        line["configs"] = config_runs(pk, dev, hbm_peak, fp64_peak)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        v, k = cpu_oracle_sample(args.cpu_iters, cores)
-        line["cpu_baseline"] = {"value": v, "unit": "it/s", "cores": cores, "kind": "port",
+        threads, rates = cpu_best_threads(cores)
+        v, k = cpu_oracle_sample(args.cpu_iters, threads)
+        line["cpu_baseline"] = {"value": v, "unit": "it/s", "cores": threads, "kind": "port",
+                                "host_cores": cores,
+                                "probe_it_s_by_threads": {str(t): r for t, r in rates.items()},
                                 "sample": f"{k} C2 iterations (after init) of the CPU oracle, "
-                                          "numpy/OpenBLAS on all host cores"}
+                                          f"numpy/OpenBLAS on {threads} BLAS threads (the "
+                                          f"faster of 1 and {cores})"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -414,6 +569,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-iters", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the time-to-tol and per-config (C3/C4/C5/W1) runs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

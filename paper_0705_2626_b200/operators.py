@@ -273,8 +273,15 @@ class Laplacian3D(LinearOperator):
         g = self.grid
         dv.stencil7_gram(x, out, g.nx, g.ny, g.nz, self.scale, xb, m, kw, gram_out)
 
+    # widest column group one stencil launch takes (its plane tiles must fit
+    # shared memory); wider blocks -- e.g. L(eye(n)) -- go in groups
+    MAX_COLS = 32
+
     def _apply(self, x):
         n, k = x.shape
+        if k > self.MAX_COLS:
+            return torch.cat([self._apply(x[:, c:c + self.MAX_COLS])
+                              for c in range(0, k, self.MAX_COLS)], dim=1)
         ld = dv.even(k)
         if x.stride(1) == 1 and x.stride(0) == ld and x.data_ptr() % 16 == 0 and k == ld:
             xin = x
