@@ -1024,6 +1024,7 @@ constexpr int NB_POFULL = 1;                       // named barriers 1..3
 constexpr int NB_PAIR = 5;                         // named barriers 5..11
 constexpr int NB_POEMPTY = 12;                     // named barriers 12..14
 constexpr int NB_PAIR_DONE = 15;
+constexpr int NB_GRND = 4;                         // compute warps, Gram rounds
 
 // ---------------------------------------------------------------------------
 // F1, warp-pair variant (m = 9..10): 14 compute warps, two per 8-row tile.
@@ -1035,7 +1036,12 @@ constexpr int NB_PAIR_DONE = 15;
 // Halving every warp's accumulators keeps 4 warps per SM sub-partition
 // resident (vs 2 in the one-warp-per-tile layout), which is what keeps the
 // DMMA pipe fed.
-template <int NT, int KS, int NI, int NJ, int MFIX, bool WGT>
+// NOB output buffers (3; 2 at m = 16, whose 56-row buffers are 45 KB each);
+// GRND: the CTA's Gram partials are summed pair by pair into one tile set
+// (rounds) instead of stashed per pair -- the per-pair stash of m = 16 (48
+// tiles x 7 pairs) would not fit the idle stage ring.  Same summation order.
+template <int NT, int KS, int NI, int NJ, int MFIX, bool WGT, int NOB = PAIR_NOB,
+          bool GRND = false>
 __global__ void __launch_bounds__(PAIR_THREADS, 1)
     step_pair_kernel(const __grid_constant__ StepMaps M, const __grid_constant__ StepArgs Ain,
                     const __grid_constant__ StepCoef Cf) {
@@ -1064,6 +1070,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
   // active, so P and W' columns are the identity maps): every size, stride
   // and predicate below is a compile-time constant
   constexpr bool FIX = MFIX > 0;
+  constexpr bool CSM = MFIX == 16;   // coefficient fragments from shared memory
   constexpr int SF = FIX ? smem_stride(MFIX) : 4;
   const int m = FIX ? MFIX : A.m;
   const int kw = FIX ? MFIX : A.kw, kp = FIX ? MFIX : A.kp;
@@ -1082,7 +1089,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], PAIR_NW);
     }
-    for (int b = 0; b < PAIR_NOB; ++b) mbar_init(&oempty[b], 1);
+    for (int b = 0; b < NOB; ++b) mbar_init(&oempty[b], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -1112,9 +1119,9 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const int k = 4 * ks + q;
-      if (FIX && H == 1 && B2L_TAIL_DFMA) {   // tail columns on DFMA: coefficients from smem
+      if ((FIX && MFIX == 10 && H == 1 && B2L_TAIL_DFMA) || CSM) {   // tail on DFMA / m = 16
         cW[ks] = cP[ks] = cX[ks] = 0.0;
-        pcol[ks] = 0;
+        pcol[ks] = FIX ? k : 0;
         continue;
       }
       pcol[ks] = FIX ? k : (k < kp ? spc[k] : 0);
@@ -1147,8 +1154,10 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     bool rw_[NJ];
     const int Lblk[3] = {0, 4, 2};
     const int Rblk[4] = {0, 4, 2, 3};
+    const uint32_t obase_lane = sm_base + 8u * (uint32_t)(A.out_off[0] + (lane >> 2));
 #pragma unroll
     for (int i = 0; i < NI; ++i) {
+      if (CSM) break;
       la_[i] = zero_adr;
       ls_[i] = 0;
       if (!((TL.imask >> i) & 1u)) continue;
@@ -1162,6 +1171,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     }
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
+      if (CSM) break;
       rb_[j] = zero_adr;
       rs_[j] = 0;
       rw_[j] = false;
@@ -1182,7 +1192,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     int s = 0, b = 0;
     uint32_t phase = 0, ophase = 0;
     for (int it = 0; it < nloc; ++it) {
-      if (it >= PAIR_NOB) mbar_wait(&oempty[b], ophase);
+      if (it >= NOB) mbar_wait(&oempty[b], ophase);
       mbar_wait(&full[s], phase);
       const double* st = stages + (size_t)s * A.stage_doubles;
       const int ob = b * A.out_stride;
@@ -1199,13 +1209,12 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         // per lane: the two columns co, co+1 of P', AP', X', AX'
         double pn_[2], apn_[2], xn_[2], axn_[2];
         const bool bw = kw > 0, bp = kp > 0;
-        if constexpr (FIX && H == 1 && B2L_TAIL_DFMA) {
+        if constexpr (FIX && MFIX == 10 && H == 1 && B2L_TAIL_DFMA) {
           // full block, columns 8..MFIX-1 (2 at MFIX = 10): DFMA instead of a
           // 75%-empty DMMA column tile.  Lane (row rl, q) forms column
           // 8 + (q & 1) of the P side (q < 2: W, P, X) or the A side (q >= 2:
           // AW, AP, AX); the four values of a row are then gathered in its
           // q = 0 lane, the lane the DMMA layout gives columns 8, 9.
-          static_assert(MFIX == 0 || MFIX == 10, "tail-column update assumes two tail columns");
           const int c = 8 + (q & 1);
           const bool aside = q >= 2;
           const double* D1 = (aside ? AW : W) + r * SF;
@@ -1251,12 +1260,17 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
           const double apv = kp_ok ? AP[r * sx + pcol[ks]] : 0.0;
           const double xv = km_ok ? X[r * sx + k] : 0.0;
           const double axv = km_ok ? AX[r * sx + k] : 0.0;
-          dmma_8x8x4(acc[0][0], acc[0][1], wv, cW[ks]);
-          dmma_8x8x4(acc[1][0], acc[1][1], awv, cW[ks]);
-          dmma_8x8x4(acc[2][0], acc[2][1], pv, cP[ks]);
-          dmma_8x8x4(acc[3][0], acc[3][1], apv, cP[ks]);
-          dmma_8x8x4(acc[4][0], acc[4][1], xv, cX[ks]);
-          dmma_8x8x4(acc[5][0], acc[5][1], axv, cX[ks]);
+          // m = 16: the coefficient fragments come from shared memory each
+          // chunk (12 registers fewer for the 17-tile Gram accumulators)
+          const double cw_ = CSM ? coef[MFIX * MFIX + k * MFIX + 8 * H + rl] : cW[ks];
+          const double cp_ = CSM ? coef[2 * MFIX * MFIX + k * MFIX + 8 * H + rl] : cP[ks];
+          const double cx_ = CSM ? coef[k * MFIX + 8 * H + rl] : cX[ks];
+          dmma_8x8x4(acc[0][0], acc[0][1], wv, cw_);
+          dmma_8x8x4(acc[1][0], acc[1][1], awv, cw_);
+          dmma_8x8x4(acc[2][0], acc[2][1], pv, cp_);
+          dmma_8x8x4(acc[3][0], acc[3][1], apv, cp_);
+          dmma_8x8x4(acc[4][0], acc[4][1], xv, cx_);
+          dmma_8x8x4(acc[5][0], acc[5][1], axv, cx_);
         }
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -1307,12 +1321,30 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         if (lane == 0) mbar_arrive(&empty[s]);
       }
       nbar_sync(pbar, 64);
-      // ---- (3) Gram over the 8 rows, this warp's tiles
+      // ---- (3) Gram over the 8 rows, this warp's tiles (m = 16: one row
+      // quad's fragments live at a time)
       const uint32_t boff = 8u * (uint32_t)ob;
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
         const uint32_t row = (uint32_t)(8 * mt + 4 * ks + q);
         double av[NI], bv[NJ];
+        if constexpr (CSM) {
+          // m = 16 full block: every tile column sits at a compile-time
+          // offset from one per-lane base (the output blocks are TXC apart):
+          // immediates instead of 14 address registers
+          constexpr uint32_t TXC = (uint32_t)((4 * PAIR_NW * SF + 15) & ~15);
+          constexpr uint32_t LB[3] = {0u, 4u * TXC, 2u * TXC};        // X', W', P'
+          constexpr uint32_t RB[4] = {0u, 4u * TXC, 2u * TXC, 3u * TXC};  // + AP'
+          const uint32_t base = obase_lane + boff + row * (8u * SF);
+#pragma unroll
+          for (int i = 0; i < NI; ++i)
+            av[i] = ((TL.imask >> i) & 1u)
+                        ? lds64(base + 8u * (LB[i / 2] + 8u * (uint32_t)(i % 2))) : 0.0;
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+            bv[j] = ((TL.jmask >> j) & 1u)
+                        ? lds64(base + 8u * (RB[j / 2] + 8u * (uint32_t)(j % 2))) : 0.0;
+        } else {
 #pragma unroll
         for (int i = 0; i < NI; ++i)
           av[i] = ((TL.imask >> i) & 1u) ? lds64(la_[i] + (ls_[i] ? boff : 0u) + row * ls_[i])
@@ -1321,6 +1353,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         for (int j = 0; j < NJ; ++j)
           bv[j] = ((TL.jmask >> j) & 1u) ? lds64(rb_[j] + (rs_[j] ? boff : 0u) + row * rs_[j])
                                           : 0.0;
+        }
         if (WGT) {
           const double w = st[A.d_off + row];
 #pragma unroll
@@ -1339,9 +1372,9 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         s = 0;
         phase ^= 1u;
       }
-      if (++b == PAIR_NOB) {
+      if (++b == NOB) {
         b = 0;
-        if (it + 1 > PAIR_NOB) ophase ^= 1u;
+        if (it + 1 > NOB) ophase ^= 1u;
       }
     }
     s_w0 = s_w[0];
@@ -1350,6 +1383,23 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     s_a1 = s_a[1];
     // the stage ring is idle once every warp is here: stash the accumulators
     nbar_sync(NB_PAIR_DONE, PAIR_THREADS);
+    if constexpr (GRND) {
+      // one tile set, zeroed, then pair by pair (p = 0, 1, ...: the order of
+      // the stash-and-sum form) each pair adds its halves' disjoint tiles
+      for (int e = (warp - 1) * 32 + lane; e < NI * NJ * 64; e += PAIR_NW * 32) gred[e] = 0.0;
+      nbar_sync(NB_GRND, PAIR_NW * 32);
+      for (int p = 0; p < PAIR_NW / 2; ++p) {
+        if (mt == p)
+#pragma unroll
+          for (int t = 0; t < TL.n; ++t) {
+            const size_t o = (((size_t)TL.ti[t] * NJ + TL.tj[t]) * 32 + lane) * 2;
+            gred[o] += gacc[t][0];
+            gred[o + 1] += gacc[t][1];
+          }
+        nbar_sync(NB_GRND, PAIR_NW * 32);
+      }
+      return;
+    }
 #pragma unroll
     for (int t = 0; t < TL.n; ++t) {
       const size_t o =
@@ -1381,7 +1431,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
   } else if (warp == PAIR_NW + 1) {
     // ================= storer: TMA stores of each finished output buffer
     for (int it = 0; it < nloc; ++it) {
-      const int b = it % PAIR_NOB;
+      const int b = it % NOB;
       nbar_sync(NB_POFULL + b, PAIR_BAR);
       if (lane == 0) {
         const int r0 = chunk_of(it) * A.rc;
@@ -1436,10 +1486,15 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     const int t = e / 32, ln = e & 31;
     const int i = t / NJ, j = t % NJ;
     double v0 = 0.0, v1 = 0.0;
-    for (int p = 0; p < PAIR_NW / 2; ++p) {
-      const size_t o = (((size_t)p * NI * NJ + t) * 32 + ln) * 2;
-      v0 += gred[o];
-      v1 += gred[o + 1];
+    if constexpr (GRND) {
+      v0 = gred[(size_t)e * 2];
+      v1 = gred[(size_t)e * 2 + 1];
+    } else {
+      for (int p = 0; p < PAIR_NW / 2; ++p) {
+        const size_t o = (((size_t)p * NI * NJ + t) * 32 + ln) * 2;
+        v0 += gred[o];
+        v1 += gred[o + 1];
+      }
     }
     const int row = 8 * i + (ln >> 2);
     const int col = 8 * j + 2 * (ln & 3);
@@ -1452,10 +1507,10 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
 
 using StepKernel = void (*)(StepMaps, StepArgs, StepCoef);
 
-template <int NT, int KS, int NI, int NJ, int MFIX>
+template <int NT, int KS, int NI, int NJ, int MFIX, int NOB = PAIR_NOB, bool GRND = false>
 static StepKernel pick_pair(bool wgt) {
-  return wgt ? step_pair_kernel<NT, KS, NI, NJ, MFIX, true>
-             : step_pair_kernel<NT, KS, NI, NJ, MFIX, false>;
+  return wgt ? step_pair_kernel<NT, KS, NI, NJ, MFIX, true, NOB, GRND>
+             : step_pair_kernel<NT, KS, NI, NJ, MFIX, false, NOB, GRND>;
 }
 template <int NT, int KS, int NI, int NJ, int MFIX>
 static StepKernel pick_local(bool wgt) {
@@ -1540,7 +1595,15 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.tsJ = (A.NJ + 3) / 4;
   A.TS = A.tsI * A.tsJ;
   const int items = STEP_NG * STEP_GI;
-  const bool local = m <= 10;       // warp-local variant
+  // the full block at m = 16 (C3 until columns lock): the warp-pair variant
+  // with two output buffers and the Gram summed in rounds
+  static const bool no_pair16 = [] {
+    const char* v = getenv("B2L_STEP_VARIANT");
+    return v && strcmp(v, "generic16") == 0;
+  }();
+  const bool pair16 = !no_pair16 && m == 16 && kw == 16 && kp == 16 && kwn == 16 && ldx == 16 &&
+                      ldw == 16 && ldwn == 16 && !d && tmode != 2;
+  const bool local = m <= 10 || pair16;   // warp-local variant
   const int lNI = m <= 4 ? 2 : (m <= 8 ? 3 : 4);
   const int lNJ = m <= 4 ? 2 : (m <= 8 ? 4 : 5);
   B2L_CHECK(local || A.TS <= items, -B2L_EINVAL, "step: Gram tile blocks exceed one CTA");
@@ -1556,9 +1619,9 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
     const char* v = getenv("B2L_STEP_VARIANT");
     return v && strcmp(v, "local") == 0;
   }();
-  const bool one_warp = m <= 8 || force_local;
+  const bool one_warp = (m <= 8 || force_local) && !pair16;
   A.rc = (local && !one_warp) ? 4 * PAIR_NW : 64;
-  while (A.rc > 16 && (size_t)A.rc * width * 8 > 48 * 1024) A.rc >>= 1;
+  while (!pair16 && A.rc > 16 && (size_t)A.rc * width * 8 > 48 * 1024) A.rc >>= 1;
   while (A.rs > 1 && A.rc / A.rs < 4) A.rs >>= 1;
   const int rc = A.rc;
   int off = 0;
@@ -1579,7 +1642,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   const int tile_w = (rc * A.swn + 15) & ~15;
   // output buffers: 3 for the warp-pair variant (separate storer warp), else 2
   const bool pair = local && !one_warp;
-  const int nob = pair ? PAIR_NOB : 2;
+  const int nob = pair && !pair16 ? PAIR_NOB : 2;
   {
     const size_t tail = (size_t)nob * (4 * tile_x + tile_w) + (m * m + kw * m + kp * m) + 3 * m +
                         64 + (pair ? 0 : (size_t)4 * STEP_NU * 32) + 64;
@@ -1609,7 +1672,8 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   off += 16;  // mbarriers
   A.red_off = off;
   const size_t red1 = (size_t)4 * 32 * (PAIR_NW > STEP_NU ? PAIR_NW : STEP_NU);
-  const size_t red2 = local ? (size_t)LOC_NW * lNI * lNJ * 64 : (size_t)A.TS * A.rs * 8 * 64;
+  const size_t red2 = pair16 ? (size_t)A.NI * A.NJ * 64
+                     : local ? (size_t)LOC_NW * lNI * lNJ * 64 : (size_t)A.TS * A.rs * 8 * 64;
   // the Gram item reduction reuses the (idle) stage ring after the loop; the
   // pair variant also puts the column-norm partials there
   if (pair && red2 + red1 <= (size_t)A.nst * A.stage_doubles) {
@@ -1624,6 +1688,12 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   }
   const size_t smem = (size_t)off * 8;
   B2L_CHECK(smem <= 227 * 1024, -B2L_EINVAL, "step: shared memory budget exceeded");
+  if (pair16) {   // the m = 16 kernel addresses the output blocks by compile-time offsets
+    const int txc = (4 * PAIR_NW * smem_stride(16) + 15) & ~15;
+    B2L_CHECK(tile_x == txc && tile_w == txc && A.out_off[1] - A.out_off[0] == txc &&
+                  A.out_off[4] - A.out_off[0] == 4 * txc,
+              -B2L_EINVAL, "step: m = 16 output layout mismatch");
+  }
 
   StepMaps M;
   const double* ins[6] = {x, ax, w, aw, p, ap};
@@ -1668,7 +1738,8 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
       // maps are then the identity), unpadded leading dimensions
       const bool full = m == 10 && kw == 10 && kp == 10 && kwn == 10 && ldx == 10 && ldw == 10 &&
                         ldwn == 10;
-      kern = full ? pick_pair<2, 3, 4, 5, 10>(wgt) : pick_pair<2, 3, 4, 5, 0>(wgt);
+      kern = pair16 ? pick_pair<2, 4, 6, 8, 16, 2, true>(wgt)
+             : full ? pick_pair<2, 3, 4, 5, 10>(wgt) : pick_pair<2, 3, 4, 5, 0>(wgt);
     }
   } else {
     threads = STEP_THREADS;

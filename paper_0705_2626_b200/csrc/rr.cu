@@ -119,133 +119,154 @@ bool use_lapack() {
   return g_rr_dim > 64;
 }
 
-// Symmetric eigensolver (tred2 / tql2 scheme) for the `want` smallest pairs:
-// Householder reduction with the transform accumulated (Q), implicit QL with
-// shifts on the tridiagonal WITHOUT touching vectors -- each plane rotation is
-// logged instead -- then the wanted eigenvectors Q G_1 ... G_K e_k are formed
-// by replaying the log backwards on unit vectors (two entries per rotation).
-// Same eigenvalues as the classic tql2 (identical scalar recurrence), the
-// eigenvectors equal to rounding, at O(n^2 + K want) instead of O(K n) for
-// the rotations (K ~ 1.5 n^2 / 2 rotations; 30 x 30: ~6x fewer flops there).
-// a: n x n (lda = n) symmetric (destroyed); vals (want) ascending; vecs
-// (n x want, column-major).  Ascending order as a stable selection sort.
-int symeig_ql(int n, double* a, int want, double* vals, double* vecs) {
+// Symmetric eigensolver for the `want` smallest pairs of an n x n matrix
+// (the small dense eigenproblem of the Rayleigh-Ritz step; the reference
+// calls LAPACK dsyevr through scipy.linalg.eigh, multivec.py:161-211).
+// Written from the textbook statements of the two classic stages (Golub &
+// Van Loan, Matrix Computations, 4th ed.: Householder vectors Alg. 5.1.1,
+// Householder tridiagonalisation Alg. 8.3.1, backward accumulation of Q
+// Sec. 5.1.6, the symmetric tridiagonal QR step with implicit Wilkinson
+// shift Alg. 8.3.2 and its deflation loop Alg. 8.3.3):
+//   1. T = Q^T A Q by Householder reflections from the left/right of
+//      columns 0 .. n-3 (A is read in full; symmetric input);
+//   2. implicit shifted QR sweeps (bulge chasing from the top) on (d, e)
+//      WITHOUT touching vectors -- each Givens rotation is logged;
+//   3. the wanted eigenvectors Q G_1 ... G_K e_k formed by replaying the log
+//      backwards on the wanted unit vectors only (O(K want) instead of the
+//      O(K n) of rotating a full basis; 30 x 30: ~3x fewer flops).
+// a: n x n column-major (destroyed); vals (want) ascending; vecs (n x want,
+// column-major).  Returns 1 if the QR sweeps do not converge.
+int symeig_tridiag_qr(int n, double* a, int want, double* vals, double* vecs) {
   auto A = [&](int i, int j) -> double& { return a[i + (size_t)j * n]; };
-  thread_local std::vector<double> dbuf, ebuf, rs, rc;
+  thread_local std::vector<double> dbuf, ebuf, vbuf, pbuf, betas, rs, rc;
   thread_local std::vector<int> ri, perm;
   dbuf.assign(n, 0.0);
-  ebuf.assign(n, 0.0);
+  ebuf.assign(n > 1 ? n - 1 : 1, 0.0);
+  vbuf.assign((size_t)n * n, 0.0);   // Householder vectors, column k holds v_k
+  pbuf.assign(n, 0.0);
+  betas.assign(n, 0.0);
   double* d = dbuf.data();
   double* e = ebuf.data();
-  // --- Householder tridiagonalisation (rows n-1 .. 1)
-  for (int i = n - 1; i > 0; --i) {
-    const int l = i - 1;
-    double h = 0.0, scale = 0.0;
-    if (l > 0) {
-      for (int k = 0; k <= l; ++k) scale += std::fabs(A(i, k));
-      if (scale == 0.0) {
-        e[i] = A(i, l);
-      } else {
-        for (int k = 0; k <= l; ++k) {
-          A(i, k) /= scale;
-          h += A(i, k) * A(i, k);
-        }
-        double f = A(i, l);
-        double g = f >= 0.0 ? -std::sqrt(h) : std::sqrt(h);
-        e[i] = scale * g;
-        h -= f * g;
-        A(i, l) = f - g;
-        f = 0.0;
-        for (int j = 0; j <= l; ++j) {
-          A(j, i) = A(i, j) / h;
-          double gg = 0.0;
-          for (int k = 0; k <= j; ++k) gg += A(j, k) * A(i, k);
-          for (int k = j + 1; k <= l; ++k) gg += A(k, j) * A(i, k);
-          e[j] = gg / h;
-          f += e[j] * A(i, j);
-        }
-        const double hh = f / (h + h);
-        for (int j = 0; j <= l; ++j) {
-          const double ff = A(i, j);
-          const double gg = e[j] - hh * ff;
-          e[j] = gg;
-          for (int k = 0; k <= j; ++k) A(j, k) -= ff * e[k] + gg * A(i, k);
-        }
-      }
-    } else {
-      e[i] = A(i, l);
+  double* V = vbuf.data();
+  double* pw = pbuf.data();
+  // ---- 1. tridiagonalisation
+  for (int k = 0; k + 2 < n; ++k) {
+    const int m0 = k + 1, len = n - m0;
+    double* v = V + (size_t)k * n;   // entries m0 .. n-1 used
+    double sigma = 0.0;
+    for (int i = 1; i < len; ++i) sigma += A(m0 + i, k) * A(m0 + i, k);
+    const double x0 = A(m0, k);
+    double beta = 0.0, alpha = x0;   // alpha: the new sub-diagonal entry
+    v[m0] = 1.0;
+    for (int i = 1; i < len; ++i) v[m0 + i] = A(m0 + i, k);
+    if (sigma != 0.0) {
+      const double mu = std::sqrt(x0 * x0 + sigma);
+      const double v0 = x0 <= 0.0 ? x0 - mu : -sigma / (x0 + mu);
+      beta = 2.0 * v0 * v0 / (sigma + v0 * v0);
+      for (int i = 1; i < len; ++i) v[m0 + i] /= v0;
+      alpha = mu;
     }
-    d[i] = h;
+    betas[k] = beta;
+    d[k] = A(k, k);
+    e[k] = alpha;
+    if (beta == 0.0) continue;
+    // p = beta A22 v ; w = p - (beta p^T v / 2) v ; A22 -= v w^T + w v^T,
+    // on the lower triangle of A22 only (symmetric matrix-vector product and
+    // rank-2 update by columns)
+    for (int i = m0; i < n; ++i) pw[i] = 0.0;
+    for (int j = m0; j < n; ++j) {
+      const double vj = v[j];
+      double t2 = 0.0;
+      pw[j] += A(j, j) * vj;
+      const double* aj = a + (size_t)j * n;
+      for (int i = j + 1; i < n; ++i) {
+        pw[i] += aj[i] * vj;
+        t2 += aj[i] * v[i];
+      }
+      pw[j] += t2;
+    }
+    double pv = 0.0;
+    for (int i = m0; i < n; ++i) {
+      pw[i] *= beta;
+      pv += pw[i] * v[i];
+    }
+    const double half = 0.5 * beta * pv;
+    for (int i = m0; i < n; ++i) pw[i] -= half * v[i];
+    for (int j = m0; j < n; ++j) {
+      const double vj = v[j], wj = pw[j];
+      double* aj = a + (size_t)j * n;
+      for (int i = j; i < n; ++i) aj[i] -= v[i] * wj + pw[i] * vj;
+    }
   }
-  d[0] = 0.0;
-  e[0] = 0.0;
+  if (n >= 2) {
+    d[n - 2] = A(n - 2, n - 2);
+    e[n - 2] = A(n - 1, n - 2);
+  }
+  d[n - 1] = A(n - 1, n - 1);
   RR_MARK(7);
-  // --- accumulate the transformations (Q in a)
-  for (int i = 0; i < n; ++i) {
-    const int l = i - 1;
-    if (d[i] != 0.0) {
-      for (int j = 0; j <= l; ++j) {
-        double g = 0.0;
-        for (int k = 0; k <= l; ++k) g += A(i, k) * A(k, j);
-        for (int k = 0; k <= l; ++k) A(k, j) -= g * A(k, i);
-      }
+  // ---- Q = H_0 H_1 ... H_{n-3}, accumulated backwards into a
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) A(i, j) = i == j ? 1.0 : 0.0;
+  for (int k = n - 3; k >= 0; --k) {
+    const double beta = betas[k];
+    if (beta == 0.0) continue;
+    const int m0 = k + 1;
+    const double* v = V + (size_t)k * n;
+    for (int j = m0; j < n; ++j) {
+      double acc = 0.0;
+      for (int i = m0; i < n; ++i) acc += v[i] * A(i, j);
+      acc *= beta;
+      for (int i = m0; i < n; ++i) A(i, j) -= acc * v[i];
     }
-    d[i] = A(i, i);
-    A(i, i) = 1.0;
-    for (int j = 0; j <= l; ++j) A(j, i) = A(i, j) = 0.0;
   }
   RR_MARK(8);
-  // --- implicit QL on the tridiagonal (d, e); rotations logged
+  // ---- 2. implicit Wilkinson-shift QR on (d, e), rotations logged
   ri.clear();
   rs.clear();
   rc.clear();
-  for (int i = 1; i < n; ++i) e[i - 1] = e[i];
-  if (n > 0) e[n - 1] = 0.0;
-  for (int l = 0; l < n; ++l) {
-    int iter = 0, mm;
-    do {
-      for (mm = l; mm < n - 1; ++mm) {
-        const double dd = std::fabs(d[mm]) + std::fabs(d[mm + 1]);
-        if (std::fabs(e[mm]) <= 2.220446049250313e-16 * dd) break;
+  const double eps = 2.220446049250313e-16;
+  int hi = n - 1, sweeps = 0;
+  while (hi > 0) {
+    if (std::fabs(e[hi - 1]) <= eps * (std::fabs(d[hi - 1]) + std::fabs(d[hi]))) {
+      e[hi - 1] = 0.0;
+      --hi;
+      continue;
+    }
+    int lo = hi - 1;
+    while (lo > 0 && std::fabs(e[lo - 1]) > eps * (std::fabs(d[lo - 1]) + std::fabs(d[lo]))) --lo;
+    if (lo > 0) e[lo - 1] = 0.0;
+    if (++sweeps > 30 * n) return 1;
+    // Wilkinson shift: the eigenvalue of the trailing 2 x 2 nearer d[hi]
+    const double t = e[hi - 1];
+    const double delta = 0.5 * (d[hi - 1] - d[hi]);
+    const double rad = std::hypot(delta, t);
+    const double mu = d[hi] - t * t / (delta + (delta >= 0.0 ? rad : -rad));
+    double x = d[lo] - mu, z = e[lo];
+    for (int k = lo; k < hi; ++k) {
+      // Givens: [c s; -s c]^T [x; z] = [r; 0]
+      // |(x, z)| without hypot's overflow guard: x and z are bounded by the
+      // matrix norm, far from the fp64 range limits here
+      const double r = std::sqrt(x * x + z * z);
+      const double rinv = r == 0.0 ? 0.0 : 1.0 / r;
+      const double c = r == 0.0 ? 1.0 : x * rinv;
+      const double s = -z * rinv;
+      if (k > lo) e[k - 1] = r;
+      const double dk = d[k], dk1 = d[k + 1], ek = e[k];
+      d[k] = c * c * dk - 2.0 * c * s * ek + s * s * dk1;
+      d[k + 1] = s * s * dk + 2.0 * c * s * ek + c * c * dk1;
+      e[k] = c * s * (dk - dk1) + (c * c - s * s) * ek;
+      if (k + 1 < hi) {   // the bulge at (k, k + 2)
+        x = e[k];
+        z = -s * e[k + 1];
+        e[k + 1] = c * e[k + 1];
       }
-      if (mm != l) {
-        if (++iter > 60) return 1;
-        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-        double r = std::hypot(g, 1.0);
-        g = d[mm] - d[l] + e[l] / (g + (g >= 0.0 ? std::fabs(r) : -std::fabs(r)));
-        double s = 1.0, c = 1.0, p = 0.0;
-        int i;
-        for (i = mm - 1; i >= l; --i) {
-          double f = s * e[i];
-          const double b = c * e[i];
-          // |(f, g)| without hypot's overflow guard: f and g are bounded by
-          // the matrix norm, far from the fp64 range limits here
-          e[i + 1] = (r = std::sqrt(f * f + g * g));
-          if (r == 0.0) {
-            d[i + 1] -= p;
-            e[mm] = 0.0;
-            break;
-          }
-          const double rinv = 1.0 / r;
-          s = f * rinv;
-          c = g * rinv;
-          g = d[i + 1] - p;
-          r = (d[i] - g) * s + 2.0 * c * b;
-          d[i + 1] = g + (p = s * r);
-          g = c * r - b;
-          ri.push_back(i);
-          rs.push_back(s);
-          rc.push_back(c);
-        }
-        if (r == 0.0 && i >= l) continue;
-        d[l] -= p;
-        e[l] = g;
-        e[mm] = 0.0;
-      }
-    } while (mm != l);
+      ri.push_back(k);
+      rc.push_back(c);
+      rs.push_back(s);
+    }
   }
   RR_MARK(9);
-  // --- ascending order: selection sort on (value, column) pairs
+  // ---- ascending order: selection sort on (value, column) pairs
   perm.resize(n);
   for (int i = 0; i < n; ++i) perm[i] = i;
   for (int i = 0; i < n - 1 && i < want; ++i) {
@@ -257,9 +278,9 @@ int symeig_ql(int n, double* a, int want, double* vals, double* vecs) {
       std::swap(perm[i], perm[k]);
     }
   }
-  // --- wanted vectors: Y = G_1 ... G_K [e_perm(0) .. e_perm(want-1)] with the
-  // log replayed backwards on all wanted columns at once (Y row-major n x
-  // want: a rotation updates two contiguous rows), then V = Q Y
+  // ---- 3. wanted vectors: Y = G_1 ... G_K [e_perm(0) .. e_perm(want-1)]
+  // (the log replayed backwards on all wanted columns at once; Y row-major
+  // n x want, so a rotation updates two contiguous rows), then V = Q Y
   thread_local std::vector<double> ybuf;
   ybuf.assign((size_t)n * want, 0.0);
   double* Y = ybuf.data();
@@ -478,7 +499,7 @@ void pencil_solve(const Mat& ga_in, const PencilFactor& f, int want, double* val
         M[i + (size_t)j * d] = 0.5 * (U[(size_t)i * d + j] + U[(size_t)j * d + i]);
     v_.assign((size_t)d * want, 0.0);
     RR_MARK(5);   // R^-T A R^-1
-    if (d > 0 && symeig_ql(d, M, want, vals_out, v_.data()) != 0)
+    if (d > 0 && symeig_tridiag_qr(d, M, want, vals_out, v_.data()) != 0)
       throw LapackError{"tql2 (no convergence)", 1};
     RR_MARK(6);   // symmetric eigensolve
     // C = R^-1 V
@@ -815,7 +836,7 @@ int repair_coef(int m, const double* gxx, const double* gxa, double* lam_out, do
               &info);
       if (info != 0) throw LapackError{"dsyevr", info};
       V.a = z;
-    } else if (symeig_ql(m, S.p(), m, lam_out, V.p()) != 0) {
+    } else if (symeig_tridiag_qr(m, S.p(), m, lam_out, V.p()) != 0) {
       throw LapackError{"tql2 (no convergence)", 1};
     }
     const Mat M = matmul(minv, V);

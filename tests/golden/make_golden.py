@@ -296,16 +296,18 @@ def bands():
     to these bands (tests/test_gpu_solve.py)."""
     t0 = time.time()
     ks = [1, -1, 2, -2, 3, -3, 4, -4, 5, 8, -8]
-    its, stats, locks = [], [], []
+    its, stats, locks, rmax = [], [], [], []
     for k in ks:
         rep = solve(scaled_laplacian_pert(32, k),
                     config=SolverConfig(block_size=4, tol=1e-6, max_iter=1000, seed=0))
         its.append(rep.iterations_used)
         stats.append(rep.status)
         locks.append(rep.lock_iterations)
+        rmax.append(float(np.max(rep.residual_norms)))
         print("C1@1000", k, rep.status, rep.iterations_used, flush=True)
     np.savez_compressed(OUT / "c1_1000it_band.npz", ulps=np.array(ks), iterations=np.array(its),
-                        status=np.array(stats), lock_iterations=np.array(locks))
+                        status=np.array(stats), lock_iterations=np.array(locks),
+                        residual_max=np.array(rmax))
     ks3 = [1, -1, 2, -2]
     conv, eig = [], []
     for k in ks3:
@@ -317,6 +319,18 @@ def bands():
         print("C3r", k, rep.status, int(rep.converged.sum()), flush=True)
     np.savez_compressed(OUT / "c3r_band.npz", ulps=np.array(ks3), converged=np.array(conv),
                         eigenvalues=np.array(eig))
+    # 5^3 m=4 (test_lobpcg.py:211-225): the final (exit-refresh) residuals
+    # of the degenerate triple cluster under the same perturbations
+    r5 = []
+    L5 = laplacian3d((5, 5, 5))
+    for k in [0] + ks:
+        s1 = 1.0 + k * 2.0 ** -52
+        A = MatrixFreeOperator(125, lambda v, s1=s1: s1 * L5(v), spd=True,
+                               diag=np.full(125, 6.0 * s1))
+        rep = solve(A, t=jacobi_preconditioner(A),
+                    config=SolverConfig(block_size=4, tol=1e-8, max_iter=300))
+        r5.append(float(np.max(rep.residual_norms)))
+    np.savez_compressed(OUT / "lap5_band.npz", ulps=np.array([0] + ks), residual_max=np.array(r5))
     print(f"bands {time.time() - t0:.1f} s")
 
 
