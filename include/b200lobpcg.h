@@ -337,8 +337,9 @@ int b2l_iter_state_size(void);
 /*
  * Diagnostics: host-side phase times of b2l_fast_iteration, accumulated when
  * the environment has B2L_ITER_PROFILE=1 (returns 1 then, else 0).
- * out[6] = calls, fetch enqueue, wait in the synchronisation, drift + lock
- * tests, Rayleigh-Ritz, uploads + launches (microseconds, summed over calls).
+ * out[8] = calls, fetch enqueue, wait in the synchronisation, drift + lock
+ * tests, Rayleigh-Ritz second half, uploads + launches, Rayleigh-Ritz first
+ * half, wait for the stencil pass's Gram (microseconds, summed over calls).
  */
 int b2l_iter_profile(double* out, int reset);
 

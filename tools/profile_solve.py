@@ -75,7 +75,7 @@ import ctypes  # noqa: E402
 from paper_0705_2626_b200 import _lib  # noqa: E402
 
 lib = _lib.load()
-buf = (ctypes.c_double * 6)()
+buf = (ctypes.c_double * 8)()
 lib.b2l_iter_profile(buf, 1)
 run = lb.LOBPCGRun(A, t=T, x0=x0, config=cfg)
 t0 = tick()
@@ -86,4 +86,5 @@ on = lib.b2l_iter_profile(buf, 0)
 c = max(buf[0], 1)
 print(f"profile on={on}: {int(buf[0])} native steps, {1e3*(t1-t0)/run.it:.3f} ms/step; per step us: "
       f"fetch-enqueue {buf[1]/c:.1f}, sync-wait {buf[2]/c:.1f}, drift+lock {buf[3]/c:.1f}, "
-      f"rayleigh-ritz {buf[4]/c:.1f}, uploads+launches {buf[5]/c:.1f}")
+      f"RR first half {buf[6]/c:.1f}, wait G2 {buf[7]/c:.1f}, RR second half {buf[4]/c:.1f}, "
+      f"uploads+launches {buf[5]/c:.1f}")
