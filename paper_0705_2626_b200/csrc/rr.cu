@@ -471,8 +471,24 @@ void pencil_solve(const Mat& ga_in, const PencilFactor& f, int want, double* val
     // chain of dependent dot products, latency-bound at these sizes)
     const double* Ri = f.Ri.data();
     thread_local std::vector<double> t_, m_, u_, v_;
+    m_.assign((size_t)d * d, 0.0);    // column-major (the eigensolver's layout)
+    double* M = m_.data();
+    if (g_dgemm) {
+      // two BLAS products (one thread at these sizes): T = ga R^-1, then
+      // U = R^-T T; Ri is R^-1 row-major, i.e. R^-T as a column-major array
+      t_.assign((size_t)d * d, 0.0);
+      u_.assign((size_t)d * d, 0.0);
+      char nn = 'N', tt = 'T';
+      int n_ = d;
+      double one = 1.0, zero = 0.0;
+      g_dgemm(&nn, &tt, &n_, &n_, &n_, &one, ga.a.data(), &n_, Ri, &n_, &zero, t_.data(), &n_);
+      g_dgemm(&nn, &nn, &n_, &n_, &n_, &one, Ri, &n_, t_.data(), &n_, &zero, u_.data(), &n_);
+      const double* U = u_.data();   // column-major
+      for (int j = 0; j < d; ++j)
+        for (int i = 0; i < d; ++i)
+          M[i + (size_t)j * d] = 0.5 * (U[i + (size_t)j * d] + U[j + (size_t)i * d]);
+    } else {
     t_.assign((size_t)d * d, 0.0);    // ga R^-1, row-major
-    m_.assign((size_t)d * d, 0.0);    // column-major (symeig_ql layout)
     double* T = t_.data();
     for (int i = 0; i < d; ++i) {
       double* ti = T + (size_t)i * d;
@@ -493,10 +509,10 @@ void pencil_solve(const Mat& ga_in, const PencilFactor& f, int want, double* val
         for (int j = 0; j < d; ++j) ui[j] += rki * tk[j];
       }
     }
-    double* M = m_.data();
     for (int j = 0; j < d; ++j)
       for (int i = 0; i < d; ++i)
         M[i + (size_t)j * d] = 0.5 * (U[(size_t)i * d + j] + U[(size_t)j * d + i]);
+    }
     v_.assign((size_t)d * want, 0.0);
     RR_MARK(5);   // R^-T A R^-1
     if (d > 0 && symeig_tridiag_qr(d, M, want, vals_out, v_.data()) != 0)
@@ -574,6 +590,7 @@ struct RRPlan {
   Mat mw, mp;
   std::vector<int> wcols, jact;
   Mat gXAP, gWAP, gPAP;   // A-side blocks that come from G1
+  Mat axp, awp, app;      // ... folded with the W / P factors (first half)
   PencilFactor fac;       // of the final gb (after the repair ladder)
 };
 
@@ -695,6 +712,15 @@ int rr_begin(RRPlan& P, int m, int kst, int have_p, const double* g1, int ldg1, 
         }
       }
     }
+    // the pencil's A side that G1 already determines (the P blocks), so the
+    // second half -- on the critical path once A W lands -- only adds the
+    // blocks of [X ; W]^T A W
+    if (P.use_p) {
+      const Mat mwT = transpose(P.mw), mpT = transpose(P.mp);
+      P.axp = matmul(P.gXAP, P.mp);
+      P.awp = matmul(matmul(mwT, P.gWAP), P.mp);
+      P.app = matmul(matmul(mpT, P.gPAP), P.mp);
+    }
     *fallbacks_out = P.pending;
     return 0;
   } catch (const LapackError& e) {
@@ -731,10 +757,9 @@ int rr_finish(RRPlan& P, const double* g2, const double* lam, double* lam_out, d
       for (int i = 0; i < m; ++i) ga(i, m + j) = axw(i, j);
     }
     if (kp) {
-      const Mat mpT = transpose(P.mp);
-      const Mat axp = matmul(P.gXAP, P.mp);
-      const Mat awp = matmul(matmul(mwT, P.gWAP), P.mp);
-      const Mat app = matmul(matmul(mpT, P.gPAP), P.mp);
+      const Mat& axp = P.axp;
+      const Mat& awp = P.awp;
+      const Mat& app = P.app;
       const int o = m + kw;
       for (int j = 0; j < kp; ++j) {
         for (int i = 0; i < m; ++i) ga(i, o + j) = axp(i, j);

@@ -4,6 +4,7 @@
 //   -Xcompiler -O2 -std=c++17 --expt-relaxed-constexpr -DB2L_RR_PROF
 //   -o rr_harness tools/rr_harness.cu
 #include <chrono>
+#include <dlfcn.h>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -22,6 +23,20 @@ namespace b2l {
 int fail(int c, const std::string&) { return c; }
 }
 int main(int argc, char** argv) {
+  // optional: B2L_HARNESS_BLAS=<libscipy_openblas.so> registers its LAPACK /
+  // BLAS as the library does from scipy (cython_lapack / cython_blas)
+  if (const char* lib = getenv("B2L_HARNESS_BLAS")) {
+    void* h = dlopen(lib, RTLD_NOW);
+    auto sym = [&](const char* a, const char* b) {
+      void* f = h ? dlsym(h, a) : nullptr;
+      return f ? f : (h ? dlsym(h, b) : nullptr);
+    };
+    if (h) {
+      b2l_set_lapack(sym("scipy_dpotrf_", "dpotrf_"), sym("scipy_dtrtrs_", "dtrtrs_"),
+                     sym("scipy_dtrtri_", "dtrtri_"), sym("scipy_dsyevr_", "dsyevr_"));
+      b2l_set_blas(sym("scipy_dgemm_", "dgemm_"));
+    }
+  }
   for (int a = 1; a < argc; ++a) {
     FILE* f = fopen(argv[a], "rb");
     long long hd[5];
