@@ -124,16 +124,17 @@ bool use_lapack() {
 // calls LAPACK dsyevr through scipy.linalg.eigh, multivec.py:161-211).
 // Written from the textbook statements of the two classic stages (Golub &
 // Van Loan, Matrix Computations, 4th ed.: Householder vectors Alg. 5.1.1,
-// Householder tridiagonalisation Alg. 8.3.1, backward accumulation of Q
-// Sec. 5.1.6, the symmetric tridiagonal QR step with implicit Wilkinson
-// shift Alg. 8.3.2 and its deflation loop Alg. 8.3.3):
+// Householder tridiagonalisation Alg. 8.3.1, the symmetric tridiagonal QR
+// step with implicit Wilkinson shift Alg. 8.3.2 and its deflation loop
+// Alg. 8.3.3):
 //   1. T = Q^T A Q by Householder reflections from the left/right of
 //      columns 0 .. n-3 (A is read in full; symmetric input);
 //   2. implicit shifted QR sweeps (bulge chasing from the top) on (d, e)
 //      WITHOUT touching vectors -- each Givens rotation is logged;
 //   3. the wanted eigenvectors Q G_1 ... G_K e_k formed by replaying the log
 //      backwards on the wanted unit vectors only (O(K want) instead of the
-//      O(K n) of rotating a full basis; 30 x 30: ~3x fewer flops).
+//      O(K n) of rotating a full basis; 30 x 30: ~3x fewer flops), then the
+//      reflectors applied to those `want` columns (Q is never formed).
 // a: n x n column-major (destroyed); vals (want) ascending; vecs (n x want,
 // column-major).  Returns 1 if the QR sweeps do not converge.
 int symeig_tridiag_qr(int n, double* a, int want, double* vals, double* vecs) {
@@ -204,21 +205,6 @@ int symeig_tridiag_qr(int n, double* a, int want, double* vals, double* vecs) {
   }
   d[n - 1] = A(n - 1, n - 1);
   RR_MARK(7);
-  // ---- Q = H_0 H_1 ... H_{n-3}, accumulated backwards into a
-  for (int j = 0; j < n; ++j)
-    for (int i = 0; i < n; ++i) A(i, j) = i == j ? 1.0 : 0.0;
-  for (int k = n - 3; k >= 0; --k) {
-    const double beta = betas[k];
-    if (beta == 0.0) continue;
-    const int m0 = k + 1;
-    const double* v = V + (size_t)k * n;
-    for (int j = m0; j < n; ++j) {
-      double acc = 0.0;
-      for (int i = m0; i < n; ++i) acc += v[i] * A(i, j);
-      acc *= beta;
-      for (int i = m0; i < n; ++i) A(i, j) -= acc * v[i];
-    }
-  }
   RR_MARK(8);
   // ---- 2. implicit Wilkinson-shift QR on (d, e), rotations logged
   ri.clear();
@@ -280,7 +266,9 @@ int symeig_tridiag_qr(int n, double* a, int want, double* vals, double* vecs) {
   }
   // ---- 3. wanted vectors: Y = G_1 ... G_K [e_perm(0) .. e_perm(want-1)]
   // (the log replayed backwards on all wanted columns at once; Y row-major
-  // n x want, so a rotation updates two contiguous rows), then V = Q Y
+  // n x want, so a rotation updates two contiguous rows), then the
+  // reflectors applied to Y itself, V = H_0 ... H_{n-3} Y (O(n^2 want); Q is
+  // never formed)
   thread_local std::vector<double> ybuf;
   ybuf.assign((size_t)n * want, 0.0);
   double* Y = ybuf.data();
@@ -298,15 +286,27 @@ int symeig_tridiag_qr(int n, double* a, int want, double* vals, double* vecs) {
       y1[w] = c * yj - s * yi;
     }
   }
-  for (int w = 0; w < want; ++w) {
-    double* v = vecs + (size_t)w * n;
-    for (int r = 0; r < n; ++r) v[r] = 0.0;
-    for (int k = 0; k < n; ++k) {
-      const double yk = Y[(size_t)k * want + w];
-      if (yk == 0.0) continue;
-      const double* q = a + (size_t)k * n;
-      for (int r = 0; r < n; ++r) v[r] += q[r] * yk;
+  for (int k = n - 3; k >= 0; --k) {
+    const double beta = betas[k];
+    if (beta == 0.0) continue;
+    const double* v = V + (size_t)k * n;
+    double* wv = pw;   // beta v^T Y (want values)
+    for (int w = 0; w < want; ++w) wv[w] = 0.0;
+    for (int i = k + 1; i < n; ++i) {
+      const double vi = v[i];
+      const double* yi = Y + (size_t)i * want;
+      for (int w = 0; w < want; ++w) wv[w] += vi * yi[w];
     }
+    for (int w = 0; w < want; ++w) wv[w] *= beta;
+    for (int i = k + 1; i < n; ++i) {
+      const double vi = v[i];
+      double* yi = Y + (size_t)i * want;
+      for (int w = 0; w < want; ++w) yi[w] -= vi * wv[w];
+    }
+  }
+  for (int w = 0; w < want; ++w) {
+    double* vcol = vecs + (size_t)w * n;
+    for (int r = 0; r < n; ++r) vcol[r] = Y[(size_t)r * want + w];
   }
   return 0;
 }
