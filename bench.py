@@ -339,7 +339,6 @@ def run_gpu(args):
     import torch.distributed as dist
 
     import paper_0705_2626_b200 as pk
-    from paper_0705_2626_b200 import device as dv
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)

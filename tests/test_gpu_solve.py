@@ -360,3 +360,38 @@ def test_native_drift_repair_matches_python_repair():
     assert nat["status"] == py["status"] and nat["it"] == py["it"]
     np.testing.assert_allclose(np.array(nat["ritz"]), np.array(py["ritz"]), rtol=1e-7)
     np.testing.assert_allclose(nat["eig"], py["eig"], rtol=1e-9)
+
+
+@pytest.mark.parametrize("diag_b,rel_tol,m", [(False, False, 10), (True, True, 6), (False, True, 16)])
+def test_native_repair_under_forced_drift(pk, monkeypatch, diag_b, rel_tol, m):
+    """The native drift repair in the configurations the steady state runs
+    (identity / diagonal B, absolute / relative tol, m = 6 / 10 / 16, with
+    columns locking on the way): with the drift limit lowered to 1e-15 the
+    repair fires every few iterations; the native loop (the repair inside
+    b2l_fast_iteration) and the Python repair path must land on the same
+    eigenpairs."""
+    from paper_0705_2626_b200 import lobpcg as lb
+
+    N = 24
+    s = float((N + 1) ** 2)
+    a = pk.Laplacian3D((N, N, N), scale=s)
+    b = None
+    if diag_b:
+        b = pk.DiagonalOperator(np.random.Generator(np.random.PCG64(4)).uniform(1.0, 2.0, N ** 3))
+    cfg = pk.SolverConfig(block_size=m, tol=1e-7 if rel_tol else 1e-6, max_iter=60, seed=1,
+                          relative_tol=rel_tol)
+    monkeypatch.setattr(lb, "DRIFT_LIMIT", 1e-15)
+    out = []
+    for fused in (True, False):
+        with pk.device_options(fused=fused):
+            run = pk.LOBPCGRun(a, b=b, t=pk.jacobi_preconditioner(a), config=cfg)
+            assert (run._native is not None) == fused
+            while run.step():
+                pass
+            out.append((run.report(), run.drift_repairs))
+    (nat, nrep), (py, prep) = out
+    assert nrep >= 5 and prep >= 5, (nrep, prep)
+    assert nat.status == py.status
+    assert abs(nat.iterations_used - py.iterations_used) <= 1
+    np.testing.assert_allclose(nat.eigenvalues, py.eigenvalues, rtol=1e-9)
+    assert np.any(~nat.history[-1].active) or nat.iterations_used == 60
