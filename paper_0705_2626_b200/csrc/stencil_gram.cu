@@ -25,7 +25,12 @@ namespace b2l {
 // warp.  Every per-lane offset is precomputed once, so the plane loop is
 // branch free: the stencil chains of a lane's EPT elements interleave and the
 // Gram loads of all its rows issue ahead of the DMMAs.
-template <int LD, int GPW, int NST, int NOB>
+// FULLB: the full block of the steady state (m = kw = ldx = LD) on a tile
+// whose points fill every 8-point group and every lane's stencil elements
+// (TX TY = 64 GPW, TX TY LD = 256 EPT): the Gram's shape, its lane-to-column
+// maps and the X row stride are compile-time constants and no element or row
+// predicate is needed (fewer address / predicate instructions per plane).
+template <int LD, int GPW, int NST, int NOB, bool FULLB = false>
 __global__ void __launch_bounds__(256, 2)
     stencil7_gram_kernel(const __grid_constant__ CUtensorMap tin,
                          const __grid_constant__ CUtensorMap thalo,
@@ -79,6 +84,8 @@ __global__ void __launch_bounds__(256, 2)
   }
   // Gram rows: lane (q4 = lane & 3) holds point 8 grp + 4 ks + q4
   const int q4 = lane & 3;
+  const int Gm = FULLB ? LD : G.m, Gkw = FULLB ? LD : G.kw, Gldx = FULLB ? LD : G.ldx;
+  const int Ga = Gm + Gkw, Gb = Gkw;
   int xo[GPW][2], po[GPW][2], oo[GPW][2];
   unsigned rmask = 0;
 #pragma unroll
@@ -88,7 +95,7 @@ __global__ void __launch_bounds__(256, 2)
       const int pt0 = 8 * (warp + 8 * gi) + 4 * ks + q4;
       const bool ok = pt0 < G.npts;
       const int pt = ok ? pt0 : 0;
-      xo[gi][ks] = pt * G.ldx;
+      xo[gi][ks] = pt * Gldx;
       po[gi][ks] = staged_row(pt) * LD;
       oo[gi][ks] = pt * LD;
       rmask |= (ok ? 1u : 0u) << (2 * gi + ks);
@@ -99,19 +106,26 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
   for (int i = 0; i < NI; ++i) {
     const int ci = 8 * i + (lane >> 2);
-    aok[i] = ci < G.a;
-    aisx[i] = ci < G.m;
-    acol[i] = !aok[i] ? 0 : (aisx[i] ? ci : ci - G.m);
+    aok[i] = ci < Ga;
+    aisx[i] = ci < Gm;
+    acol[i] = !aok[i] ? 0 : (aisx[i] ? ci : ci - Gm);
   }
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     const int cj = 8 * j + (lane >> 2);
-    bok[j] = cj < G.b;
+    bok[j] = cj < Gb;
     bcol[j] = bok[j] ? cj : 0;
   }
-  const int ni = (G.a + 7) / 8, nj = (G.b + 7) / 8;
+  const int ni = (Ga + 7) / 8, nj = (Gb + 7) / 8;
 
   double gacc[NA][NI][NJ][2];
+  // m = 10 full block: the Gram columns 8, 9 (AW's last two) on DFMA instead
+  // of three 75%-empty DMMA column tiles; lane (row rl, point q4) keeps
+  // sum over its points of L[row 8i + rl] * AW[8 + c] (reduced over q4 at the end)
+  constexpr bool TAIL2 = FULLB && LD == 10 && NJ == 2;
+  double tail[NI][2];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) tail[i][0] = tail[i][1] = 0.0;
 #pragma unroll
   for (int sa = 0; sa < NA; ++sa)
 #pragma unroll
@@ -145,7 +159,7 @@ __global__ void __launch_bounds__(256, 2)
       mbar_expect_tx(&xbar[sl], G.x_bytes);
       tma_load_4d(xbuf(sl), &tx_map, &xbar[sl], 0, tx0, ty0, z);
     };
-    const bool have_x = G.m > 0;   // m = 0: W^T AW only (PCG curvatures)
+    const bool have_x = Gm > 0;   // m = 0: W^T AW only (PCG curvatures)
     if (tid == 0) {
       for (int q = 0; q < NST && q < nplanes; ++q) issue(q);
       if (have_x) {
@@ -184,7 +198,7 @@ __global__ void __launch_bounds__(256, 2)
         r = __dsub_rn(r, P[o + ystride]);
         r = __dsub_rn(r, prev[i]);
         r = __dsub_rn(r, nx_);
-        if (vmask & (1u << i)) O[oel[i]] = __dmul_rn(sc, r);
+        if (FULLB || (vmask & (1u << i))) O[oel[i]] = __dmul_rn(sc, r);
         prev[i] = cur[i];
         cur[i] = nx_;
       }
@@ -198,19 +212,31 @@ __global__ void __launch_bounds__(256, 2)
       for (int gi = 0; gi < GPW; ++gi)
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
-          const bool rok = rmask & (1u << (2 * gi + ks));
+          // Lanes past the Gram's rows (ci >= a) or columns (cj >= b) load a
+          // finite in-tile value (column 0): it only reaches output entries
+          // that are never written back, so no select is needed.  Points past
+          // the tile (rok false, partial last groups) must contribute zero:
+          // zeroing one operand (B) suffices.
+          const bool rok = FULLB || (rmask & (1u << (2 * gi + ks)));
           double av[NI], bv[NJ];
 #pragma unroll
-          for (int i = 0; i < NI; ++i) {
-            const double v = aisx[i] ? Xb[xo[gi][ks] + acol[i]] : P[po[gi][ks] + acol[i]];
-            av[i] = (aok[i] && rok) ? v : 0.0;
-          }
+          for (int i = 0; i < NI; ++i)
+            av[i] = aisx[i] ? Xb[xo[gi][ks] + acol[i]] : P[po[gi][ks] + acol[i]];
 #pragma unroll
           for (int j = 0; j < NJ; ++j) {
             const double v = O[oo[gi][ks] + bcol[j]];
-            bv[j] = (bok[j] && rok) ? v : 0.0;
+            bv[j] = rok ? v : 0.0;
           }
           const int sa = (2 * gi + ks) % NA;
+          if constexpr (TAIL2) {
+            const double aw8 = O[oo[gi][ks] + 8], aw9 = O[oo[gi][ks] + 9];
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+              dmma_8x8x4(gacc[0][i][0][0], gacc[0][i][0][1], av[i], bv[0]);
+              tail[i][0] = fma(av[i], aw8, tail[i][0]);
+              tail[i][1] = fma(av[i], aw9, tail[i][1]);
+            }
+          } else {
 #pragma unroll
           for (int i = 0; i < NI; ++i)
 #pragma unroll
@@ -220,6 +246,7 @@ __global__ void __launch_bounds__(256, 2)
                 for (int t = 0; t < NA; ++t)
                   if (t == sa) dmma_8x8x4(gacc[t][i][j][0], gacc[t][i][j][1], av[i], bv[j]);
               }
+          }
         }
       // The next plane writes output slot (z + 1) % NOB, last stored for
       // plane z + 1 - NOB: its TMA store must have read the slot before the
@@ -238,6 +265,18 @@ __global__ void __launch_bounds__(256, 2)
     if (tid == 0) bulk_wait<0>();
   }
 
+  if constexpr (TAIL2) {
+    // columns 8, 9: the sum over the lane's 4 point slots (q4), fixed order,
+    // lands where the DMMA fragment layout keeps C[row][8 + e] (lane q4 = 0)
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double v01 = tail[i][e] + __shfl_xor_sync(0xffffffffu, tail[i][e], 1);
+        const double v = v01 + __shfl_xor_sync(0xffffffffu, v01, 2);
+        gacc[0][i][1][e] = q4 == 0 ? v : 0.0;
+      }
+  }
   // ---- CTA partial: fixed-order sum over the 8 warps (reuse stage memory)
   __syncthreads();
   double* red = reinterpret_cast<double*>(base);
@@ -289,8 +328,16 @@ static int launch_sgram_t(const StencilPlan& p, size_t smem, const CUtensorMap& 
                           const CUtensorMap& thalo, const CUtensorMap& tout,
                           const CUtensorMap& txm, const SGramGeom& G, cudaStream_t st) {
   // a 4-deep plane ring with double-buffered outputs when it fits two CTAs
-  // per SM (more loads in flight), else 3 + 3
-  auto kern = p.nst == 4 ? stencil7_gram_kernel<LD, GPW, 4, 2> : stencil7_gram_kernel<LD, GPW, 3, 3>;
+  // per SM (more loads in flight), else 3 + 3; the compile-time full block
+  // for the block sizes of the BASELINE configs (m = 8, 10, 16)
+  constexpr bool FB_OK = LD == 8 || LD == 10 || LD == 16;
+  constexpr int EPT = (GPW * LD + 3) / 4;
+  const bool full = FB_OK && G.m == LD && G.kw == LD && G.ldx == LD && G.npts == 64 * GPW &&
+                    p.g.nelem == 256 * EPT;
+  auto kern = p.nst == 4 ? (full ? stencil7_gram_kernel<LD, GPW, 4, 2, FB_OK>
+                                 : stencil7_gram_kernel<LD, GPW, 4, 2, false>)
+                         : (full ? stencil7_gram_kernel<LD, GPW, 3, 3, FB_OK>
+                                 : stencil7_gram_kernel<LD, GPW, 3, 3, false>);
   if (int rc = prepare_kernel(reinterpret_cast<const void*>(kern), smem, 256, nullptr)) return rc;
   kern<<<p.grid, 256, smem, st>>>(tin, thalo, tout, txm, p.g, G);
   count_launch();
