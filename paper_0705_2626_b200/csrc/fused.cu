@@ -697,6 +697,10 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
   const int warp = tid >> 5, lane = tid & 31;
   const int m = A.m;
   const int sx = A.sx, sw = A.sw, swn = A.swn;
+  // MFIX > 0: the full block (kw = kp = kw_next = m = MFIX, ld = MFIX): every
+  // output block has the row stride SF
+  constexpr bool FIX = MFIX > 0;
+  constexpr int SF = FIX ? smem_stride(MFIX) : 4;
   const int ncoef = m * m + A.kw * m + A.kp * m;
   const bool inl = A.coef == nullptr;
   for (int i = tid; i < ncoef; i += blockDim.x) coef[i] = inl ? Cf.c[i] : A.coef[i];
@@ -797,6 +801,28 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
     bool rw_[NJ];
     const int Lblk[3] = {0, 4, 2};
     const int Rblk[4] = {0, 4, 2, 3};
+    if constexpr (FIX) {
+      // full block: a = 3m rows, b = 4m columns, every block at row stride
+      // SF -- compile-time strides; lanes past the last row / column read a
+      // valid in-tile address (their entries are never written back)
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const int ci0 = 8 * i + (lane >> 2);
+        const int ci = ci0 < 3 * MFIX ? ci0 : 0;
+        const int l = ci / MFIX;
+        la_[i] = sm_base + 8u * (uint32_t)(A.out_off[Lblk[l]] + (ci - l * MFIX));
+        ls_[i] = 8u * SF;
+      }
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int cj0 = 8 * j + (lane >> 2);
+        const int cj = cj0 < 4 * MFIX ? cj0 : 0;
+        const int r = cj / MFIX;
+        rb_[j] = sm_base + 8u * (uint32_t)(A.out_off[Rblk[r]] + (cj - r * MFIX));
+        rs_[j] = 8u * SF;
+        rw_[j] = r < 3 && cj0 < 4 * MFIX;
+      }
+    } else {
 #pragma unroll
     for (int i = 0; i < NI; ++i) {
       const int ci = 8 * i + (lane >> 2);
@@ -822,6 +848,7 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
         rs_[j] = 8u * (r == 1 ? swn : sx);
         rw_[j] = r < 3;
       }
+    }
     }
     unsigned tm[NI];
 #pragma unroll
@@ -1155,6 +1182,28 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     const int Lblk[3] = {0, 4, 2};
     const int Rblk[4] = {0, 4, 2, 3};
     const uint32_t obase_lane = sm_base + 8u * (uint32_t)(A.out_off[0] + (lane >> 2));
+    if constexpr (FIX && !CSM) {
+      // full block: a = 3m rows, b = 4m columns, every block at row stride
+      // SF -- compile-time strides; lanes past the last row / column read a
+      // valid in-tile address (their entries are never written back)
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const int ci0 = 8 * i + (lane >> 2);
+        const int ci = ci0 < 3 * MFIX ? ci0 : 0;
+        const int l = ci / MFIX;
+        la_[i] = sm_base + 8u * (uint32_t)(A.out_off[Lblk[l]] + (ci - l * MFIX));
+        ls_[i] = 8u * SF;
+      }
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int cj0 = 8 * j + (lane >> 2);
+        const int cj = cj0 < 4 * MFIX ? cj0 : 0;
+        const int r = cj / MFIX;
+        rb_[j] = sm_base + 8u * (uint32_t)(A.out_off[Rblk[r]] + (cj - r * MFIX));
+        rs_[j] = 8u * SF;
+        rw_[j] = r < 3 && cj0 < 4 * MFIX;
+      }
+    } else {
 #pragma unroll
     for (int i = 0; i < NI; ++i) {
       if (CSM) break;
@@ -1184,6 +1233,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         rs_[j] = 8u * (r == 1 ? swn : sx);
         rw_[j] = r < 3;
       }
+    }
     }
     double gacc[TL.n > 0 ? TL.n : 1][2];
 #pragma unroll
