@@ -139,8 +139,19 @@ __global__ void __launch_bounds__(256)
 // chunks of 64 planes 138 us, 26 planes 148 us, 8 planes 161 us,
 // tools/sweep_sgram.py), so: the longest chunks that still give every
 // resident slot at most one CTA (one wave), chunks of >= 4 planes.
+// More tiles than slots: enough z-chunks for about four waves (the last,
+// partial wave then costs little), chunks of >= 64 planes (measured: C3
+// 1024 tiles, 2 chunks of 128 planes 1.40 ms vs 1.54 ms unsplit; W1 464
+// tiles, 3 chunks 0.44 ms vs 0.50 ms; C4 1740 tiles unsplit, flat).
 int choose_zchunk(int tiles, int nz, int slots) {
-  int zs = tiles >= slots ? 1 : slots / tiles;
+  int zs;
+  if (tiles >= slots) {
+    zs = (4 * slots + tiles - 1) / tiles;
+    const int cap = nz / 64 < 1 ? 1 : nz / 64;
+    if (zs > cap) zs = cap;
+  } else {
+    zs = slots / tiles;
+  }
   if (zs < 1) zs = 1;
   int c = (nz + zs - 1) / zs;
   if (c < 4) c = nz < 4 ? nz : 4;
