@@ -213,11 +213,32 @@ int b2l_pcg_direction(int nrows, int k, const double* r, double* p, int ld, cons
 int b2l_set_lapack(void* dpotrf, void* dtrtrs, void* dtrtri, void* dsyevr);
 
 /*
+ * Host, small dense: optionally register dsyevr's three stages (dsytrd,
+ * dstemr, dormtr; same signatures as scipy.linalg.cython_lapack): the
+ * reference-form eigensolve then runs dsyevr's all-pairs path (MRRR) but
+ * forms and back-transforms only the wanted vectors.
+ */
+int b2l_set_lapack_mrrr(void* dsytrd, void* dstemr, void* dormtr);
+
+/*
  * Host, small dense: optionally register BLAS dgemm (Fortran-style signature
  * of scipy.linalg.cython_blas) for the block products of large pencils
  * (m >= 32); null keeps the native loops.
  */
 int b2l_set_blas(void* dgemm);
+
+/*
+ * Host, small dense: which form the next Rayleigh-Ritz calls of this thread
+ * use.  1: the reference's own sequence (multivec.gen_sym_eig: two dtrtrs,
+ * dsyevr on all pairs, dtrtrs) -- inside (near-)degenerate clusters its
+ * eigenvector choice steers which Ritz column locks first, so this form
+ * reproduces the reference's lock and fallback statistics; 0: the native
+ * explicit-inverse congruence + tridiagonal QR (~45-55 us faster per C2
+ * iteration; on C1 with its operator perturbed by 1..16 ulp it converges in
+ * 10 of 32 runs where the reference converges in 26 of 31 and form 1 in 24
+ * of 32); -1: default (1).  The environment B2L_RR_EIG=qr / =ref pins one.
+ */
+int b2l_set_rr_reference(int on);
 
 /*
  * Host, small dense -- the Rayleigh-Ritz step of one iteration with the

@@ -124,6 +124,8 @@ SIGNATURES = {
     "b2l_launch_count": (C.c_longlong, []),
     "b2l_set_lapack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "b2l_set_blas": (C.c_int, [C.c_void_p]),
+    "b2l_set_rr_reference": (C.c_int, [C.c_int]),
+    "b2l_set_lapack_mrrr": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "b2l_rayleigh_ritz_begin": (C.c_int, [C.c_int, C.c_int, C.c_int, c_dp, C.c_int, c_ip, C.c_int,
                                           c_ip, C.c_double, C.POINTER(C.c_int)]),
     "b2l_rayleigh_ritz_finish": (C.c_int, [c_dp, c_dp, c_dp, c_dp, c_ip, C.POINTER(C.c_int),
@@ -192,6 +194,8 @@ def _register_lapack(lib) -> None:
     rc = lib.b2l_set_lapack(*ptrs)
     if rc != 0:
         raise ImportError("b2l_set_lapack failed: " + lib.b2l_last_error().decode())
+    lib.b2l_set_lapack_mrrr(*[get(caps[n], getname(caps[n])) for n in ("dsytrd", "dstemr",
+                                                                      "dormtr")])
 
 
 def check(rc: int, what: str) -> None:

@@ -43,6 +43,18 @@ potrf_t* g_potrf = nullptr;
 trtrs_t* g_trtrs = nullptr;
 trtri_t* g_trtri = nullptr;
 syevr_t* g_syevr = nullptr;
+// dsyevr's own stages (scipy.linalg.cython_lapack): for all pairs dsyevr runs
+// dsytrd, dstemr (MRRR) and dormtr; calling them directly lets the MRRR
+// vectors be formed for the wanted pairs only
+using sytrd_t = void(char*, int*, double*, int*, double*, double*, double*, double*, int*,
+                     int*);
+using stemr_t = void(char*, char*, int*, double*, double*, double*, double*, int*, int*, int*,
+                     double*, double*, int*, int*, int*, int*, double*, int*, int*, int*, int*);
+using ormtr_t = void(char*, char*, char*, int*, int*, double*, int*, double*, double*, int*,
+                     double*, int*, int*);
+sytrd_t* g_sytrd = nullptr;
+stemr_t* g_stemr = nullptr;
+ormtr_t* g_ormtr = nullptr;
 
 // column-major dense matrix
 struct Mat {
@@ -109,6 +121,29 @@ Mat transpose(const Mat& x) {
 // dimension of the pencil being solved, set by rr_begin; per host thread so
 // two threads' Rayleigh-Ritz steps never see each other's LAPACK choice
 thread_local int g_rr_dim = 0;
+// The pencil eigensolve: the reference's own sequence (two dtrtrs, dsyevr
+// on all pairs -- scipy.linalg.eigh's driver) whenever LAPACK is registered.
+// Inside (near-)degenerate clusters the eigenvectors an eigensolver returns
+// are one of many valid bases, and that choice steers which Ritz column
+// locks first: on C1 with its operator perturbed by 1..16 ulp (32 runs) the
+// reference converges 26/31 times, this sequence 21-23/32, the native
+// tridiagonal QR 10/32 (tools/c1_band32.py).  The native explicit-inverse
+// + QR form is ~45 us faster per C2 iteration.
+// Per host thread (b2l_set_rr_reference); B2L_RR_EIG=qr / =ref pin one form
+// for every call.  Switching to the reference form only near the lock
+// threshold does not recover its statistics (C1: 8/32 converged): the
+// cluster bases it picks shape the whole trajectory.
+thread_local int g_rr_ref = -1;   // -1: not set by the caller (reference form)
+bool eig_lapack() {
+  static const int forced = [] {
+    const char* v = getenv("B2L_RR_EIG");
+    return v ? (v[0] == 'q' ? 0 : (v[0] == 'r' ? 1 : -1)) : -1;
+  }();
+  if (g_syevr == nullptr || g_trtrs == nullptr) return false;
+  if (forced >= 0) return forced == 1;
+  return g_rr_ref != 0;
+}
+
 bool use_lapack() {
   static const int mode = [] {
     const char* v = getenv("B2L_RR_LAPACK");
@@ -377,8 +412,8 @@ Mat cholesky(const Mat& g, double floor_) {
 }
 
 // R^{-T} b (trans) or R^{-1} b for upper R
-Mat trsolve(const Mat& r, const Mat& b, bool trans) {
-  if (!use_lapack()) return trsolve_native(r, b, trans);
+Mat trsolve(const Mat& r, const Mat& b, bool trans, bool force_lapack = false) {
+  if (!use_lapack() && !(force_lapack && g_trtrs)) return trsolve_native(r, b, trans);
   Mat x = b;
   if (r.r == 0 || b.c == 0) return x;
   char uplo = 'U', tr = trans ? 'T' : 'N', diag = 'N';
@@ -440,7 +475,7 @@ void pencil_factor(const Mat& gb, double floor_, PencilFactor& f) {
   f.r = cholesky(gb, floor_);
   RR_MARK(4);   // pencil Cholesky
   f.Ri.clear();
-  if (use_lapack()) return;
+  if (use_lapack() || eig_lapack()) return;   // no explicit inverse needed
   const int d = f.d;
   f.Ri.assign((size_t)d * d, 0.0);
   double* Ri = f.Ri.data();
@@ -515,8 +550,9 @@ void pencil_solve(const Mat& ga_in, const PencilFactor& f, int want, double* val
     }
     v_.assign((size_t)d * want, 0.0);
     RR_MARK(5);   // R^-T A R^-1
-    if (d > 0 && symeig_tridiag_qr(d, M, want, vals_out, v_.data()) != 0)
+    if (d > 0 && symeig_tridiag_qr(d, M, want, vals_out, v_.data()) != 0) {
       throw LapackError{"tql2 (no convergence)", 1};
+    }
     RR_MARK(6);   // symmetric eigensolve
     // C = R^-1 V
     Mat c(d, want);
@@ -532,26 +568,62 @@ void pencil_solve(const Mat& ga_in, const PencilFactor& f, int want, double* val
     *c_out = std::move(c);
     return;
   }
+  // the reference's sequence (multivec.gen_sym_eig, multivec.py:174-211):
+  // M = R^-T ga R^-1 by two triangular solves (dtrtrs), symmetrised, eigh
+  // (dsyevr, all pairs), C = R^-1 V -- used for every pencil size when the
+  // eigensolve is dsyevr (the explicit-inverse / native-QR form above is the
+  // B2L_RR_EIG=qr speed option)
+  const bool fl = eig_lapack();
   const Mat& r = f.r;
-  Mat t = trsolve(r, ga, true);
-  t = trsolve(r, transpose(t), true);
+  Mat t = trsolve(r, ga, true, fl);
+  t = trsolve(r, transpose(t), true, fl);
   Mat ts(d, d);
   for (int j = 0; j < d; ++j)
     for (int i = 0; i < d; ++i) ts(i, j) = 0.5 * (t(i, j) + t(j, i));
-  // dsyevr, range 'A', upper, abstol 0 (scipy.linalg.eigh defaults)
-  char jobz = 'V', range = 'A', uplo = 'U';
-  int n = d, lda = d, il = 1, iu = d, mfound = 0, ldz = d, info = 0;
-  double vl = 0.0, vu = 0.0, abstol = 0.0;
-  std::vector<double> w(d), z((size_t)d * d), work((size_t)26 * d + 64);
-  std::vector<int> isuppz(2 * d + 2), iwork((size_t)10 * d + 16);
-  int lwork = (int)work.size(), liwork = (int)iwork.size();
-  g_syevr(&jobz, &range, &uplo, &n, ts.p(), &lda, &vl, &vu, &il, &iu, &abstol, &mfound, w.data(),
-          z.data(), &ldz, isuppz.data(), work.data(), &lwork, iwork.data(), &liwork, &info);
-  if (info != 0) throw LapackError{"dsyevr", info};
+  std::vector<double> w(d), z((size_t)d * d);
+  static const bool mrrr_all = [] {
+    const char* v = getenv("B2L_RR_MRRR");
+    return v && v[0] == 'a';
+  }();
+  if (g_sytrd && g_stemr && g_ormtr && want < d && !mrrr_all) {
+    // dsyevr's path for all pairs (dsytrd, dstemr, dormtr), with the MRRR
+    // vectors formed and back-transformed for the `want` smallest only
+    char uplo = 'U', jobz = 'V', range = 'I', side = 'L', trans = 'N';
+    int n = d, lda = d, info = 0, il = 1, iu = want, mfound = 0, ldz = d, nzc = want;
+    int tryrac = 1;
+    double vl = 0.0, vu = 0.0;
+    std::vector<double> dd(d), ee(d), tau(d), work((size_t)64 * d + 64);
+    std::vector<int> isuppz(2 * d + 2), iwork((size_t)10 * d + 16);
+    int lwork = (int)work.size(), liwork = (int)iwork.size();
+    g_sytrd(&uplo, &n, ts.p(), &lda, dd.data(), ee.data(), tau.data(), work.data(), &lwork,
+            &info);
+    if (info != 0) throw LapackError{"dsytrd", info};
+    ee[d - 1] = 0.0;
+    g_stemr(&jobz, &range, &n, dd.data(), ee.data(), &vl, &vu, &il, &iu, &mfound, w.data(),
+            z.data(), &ldz, &nzc, isuppz.data(), &tryrac, work.data(), &lwork, iwork.data(),
+            &liwork, &info);
+    if (info != 0 || mfound != want) throw LapackError{"dstemr", info ? info : -1};
+    int nc = want;
+    g_ormtr(&side, &uplo, &trans, &n, &nc, ts.p(), &lda, tau.data(), z.data(), &ldz, work.data(),
+            &lwork, &info);
+    if (info != 0) throw LapackError{"dormtr", info};
+  } else {
+    // dsyevr, range 'A', upper, abstol 0 (scipy.linalg.eigh defaults)
+    char jobz = 'V', range = 'A', uplo = 'U';
+    int n = d, lda = d, il = 1, iu = d, mfound = 0, ldz = d, info = 0;
+    double vl = 0.0, vu = 0.0, abstol = 0.0;
+    std::vector<double> work((size_t)26 * d + 64);
+    std::vector<int> isuppz(2 * d + 2), iwork((size_t)10 * d + 16);
+    int lwork = (int)work.size(), liwork = (int)iwork.size();
+    g_syevr(&jobz, &range, &uplo, &n, ts.p(), &lda, &vl, &vu, &il, &iu, &abstol, &mfound,
+            w.data(), z.data(), &ldz, isuppz.data(), work.data(), &lwork, iwork.data(), &liwork,
+            &info);
+    if (info != 0) throw LapackError{"dsyevr", info};
+  }
   Mat v(d, want);
   for (int j = 0; j < want; ++j)
     for (int i = 0; i < d; ++i) v(i, j) = z[(size_t)i + (size_t)j * d];
-  *c_out = trsolve(r, v, false);
+  *c_out = trsolve(r, v, false, fl);
   for (int j = 0; j < want; ++j) vals_out[j] = w[j];
 }
 
@@ -562,6 +634,18 @@ using namespace b2l;
 
 extern "C" int b2l_set_blas(void* dgemm) {
   g_dgemm = reinterpret_cast<dgemm_t*>(dgemm);
+  return 0;
+}
+
+extern "C" int b2l_set_lapack_mrrr(void* dsytrd, void* dstemr, void* dormtr) {
+  g_sytrd = reinterpret_cast<sytrd_t*>(dsytrd);
+  g_stemr = reinterpret_cast<stemr_t*>(dstemr);
+  g_ormtr = reinterpret_cast<ormtr_t*>(dormtr);
+  return 0;
+}
+
+extern "C" int b2l_set_rr_reference(int on) {
+  g_rr_ref = on < 0 ? -1 : (on ? 1 : 0);
   return 0;
 }
 

@@ -391,6 +391,29 @@ def band20():
     print(f"band20 {time.time() - t0:.1f} s")
 
 
+def c1_band32():
+    """C1@1000 over 32 operator perturbations (scale (N+1)^2 (1 + k 2^-52),
+    k = -16..-1, 1..16): the reference's own distribution of outcomes in
+    the triple-degenerate endgame -- status, iterations, lock iterations
+    (~2.5 min on one thread).  The GPU is held to the distribution."""
+    t0 = time.time()
+    L = laplacian3d((32, 32, 32))
+    ks = list(range(-16, 0)) + list(range(1, 17))
+    its, stats, locks = [], [], []
+    for k in ks:
+        s = float(33 ** 2) * (1.0 + k * 2.0 ** -52)
+        A = MatrixFreeOperator(32 ** 3, lambda v, s=s: s * L(v), spd=True,
+                               diag=np.full(32 ** 3, 6.0 * s))
+        rep = solve(A, config=SolverConfig(block_size=4, tol=1e-6, max_iter=1000, seed=0))
+        its.append(rep.iterations_used)
+        stats.append(rep.status)
+        locks.append(rep.lock_iterations)
+        print("c1band32", k, rep.status, rep.iterations_used, list(rep.lock_iterations), flush=True)
+    np.savez_compressed(OUT / "c1_band32.npz", ulps=np.array(ks), iterations=np.array(its),
+                        status=np.array(stats), lock_iterations=np.array(locks))
+    print(f"c1_band32 {time.time() - t0:.1f} s")
+
+
 def band_c1_coef():
     """C1@1000 under rounding noise in the Ritz-update coefficients (as
     band20): a second, wider iteration band for the converging C1 test."""
@@ -530,6 +553,7 @@ if __name__ == "__main__":
     ap.add_argument("--c2", action="store_true")
     ap.add_argument("--full-size", action="store_true")
     ap.add_argument("--generic-b", action="store_true")
+    ap.add_argument("--c1-band32", action="store_true")
     ap.add_argument("--bands", action="store_true")
     ap.add_argument("--band20", action="store_true")
     ap.add_argument("--band-c1", action="store_true")
@@ -547,6 +571,8 @@ if __name__ == "__main__":
         band20()
     elif args.bands:
         bands()
+    elif args.c1_band32:
+        c1_band32()
     elif args.generic_b:
         generic_b()
     elif args.full_size:

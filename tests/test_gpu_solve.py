@@ -395,3 +395,36 @@ def test_native_repair_under_forced_drift(pk, monkeypatch, diag_b, rel_tol, m):
     assert abs(nat.iterations_used - py.iterations_used) <= 1
     np.testing.assert_allclose(nat.eigenvalues, py.eigenvalues, rtol=1e-9)
     assert np.any(~nat.history[-1].active) or nat.iterations_used == 60
+
+
+def test_c1_outcome_distribution_matches_reference(pk, golden):
+    """A single converging C1 run lands anywhere in the reference's chaotic
+    band, which cannot catch a change of behaviour.  Here the GPU runs the
+    SAME 32 perturbed problems as the reference's own distribution
+    (c1_band32.npz: operator scale (N+1)^2 (1 + k 2^-52), k = +-1..16; the
+    kernel's scale epilogue rounds the same single product s * L(v)), and
+    the outcome distributions must agree: how many runs converge (the rest
+    end in BasisFallback), how many lock their second column by iteration
+    215, and the median iteration count.  (The native tridiagonal-QR
+    Rayleigh-Ritz form, B2L_RR_EIG=qr, fails this: 10 of 32 converge against
+    the reference's 26 of 31 -- DESIGN.md.)"""
+    band = golden("c1_band32.npz")
+    N = 32
+    base = float((N + 1) ** 2)
+    its, conv, early = [], 0, 0
+    for k in band["ulps"]:
+        a = pk.Laplacian3D((N, N, N), scale=base * (1.0 + int(k) * 2.0 ** -52))
+        rep = pk.solve(a, config=pk.SolverConfig(block_size=4, tol=1e-6, max_iter=1000, seed=0))
+        assert rep.status == "Converged" or rep.status.startswith("BasisFallback"), rep.status
+        its.append(rep.iterations_used)
+        conv += rep.status == "Converged"
+        early += sorted(rep.lock_iterations)[1] <= 215
+    ref_conv = int(sum(str(x) == "Converged" for x in band["status"]))
+    ref_early = int(sum(sorted(l)[1] <= 215 for l in band["lock_iterations"]))
+    n = len(its)
+    # two independent binomials over 32 runs at p ~ 0.8 / 0.7: the sd of their
+    # difference is ~3.2 / ~3.7 runs; hold both to 3 sd (the QR form's 10 vs
+    # 27 converged is 5 sd away)
+    assert abs(conv - ref_conv) <= 10, (conv, ref_conv, n)
+    assert abs(early - ref_early) <= 11, (early, ref_early, n)
+    assert abs(np.median(its) - np.median(band["iterations"])) <= 0.1 * np.median(band["iterations"])
