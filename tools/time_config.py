@@ -34,6 +34,10 @@ run = pk.LOBPCGRun(a, b=b, t=pk.jacobi_preconditioner(a), config=cfg)
 for _ in range(args.warm):
     run.step()
 torch.cuda.synchronize()
+import ctypes  # noqa: E402
+from paper_0705_2626_b200 import _lib  # noqa: E402
+_buf = (ctypes.c_double * 8)()
+_lib.load().b2l_iter_profile(_buf, 1)   # reset the host phase timers (B2L_ITER_PROFILE=1)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(args.steps):
@@ -41,6 +45,7 @@ for _ in range(args.steps):
 e1.record()
 torch.cuda.synchronize()
 ms_it = e0.elapsed_time(e1) / args.steps
+_on = _lib.load().b2l_iter_profile(_buf, 0)
 kt = {}
 
 
@@ -65,4 +70,10 @@ for k, v in kt.items():
     out[k] = {"ms": d, "calls": len(v)}
     if k in alg:
         out[k]["gbs"] = alg[k] / (d / 1e3) / 1e9
+if _on:
+    c = max(_buf[0], 1.0)
+    out["host_phase_us"] = {"native_steps": int(_buf[0]), "fetch_enqueue": _buf[1] / c,
+                            "sync_wait": _buf[2] / c, "drift_lock": _buf[3] / c,
+                            "rr_first_half": _buf[6] / c, "wait_g2": _buf[7] / c,
+                            "rr_second_half": _buf[4] / c, "uploads_launches": _buf[5] / c}
 print(json.dumps(out))
