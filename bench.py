@@ -477,7 +477,10 @@ def run_gpu(args):
             d = float(np.median(kt[name]))
             per[name] = {"ms": d, "gbs": alg[name] / (d / 1e3) / 1e9, "calls": len(kt[name])}
     if kt.get("gram"):
-        db = float(np.median(kt["gram"]))
+        # the standalone Gram runs only on a repair / refresh step of the
+        # timer pass: a handful of calls, the first carrying one-time host
+        # work (imports, workspace growth), so the fastest call is reported
+        db = float(np.min(kt["gram"]))
         per["gram"] = {"ms": db, "gbs": 8.0 * n * (3 * m + 2 * k_act) / (db / 1e3) / 1e9,
                        "calls": len(kt["gram"])}
     # the dominant kernel of the steady-state step (F1 or the stencil pass;

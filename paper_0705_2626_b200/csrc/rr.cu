@@ -580,6 +580,7 @@ void pencil_solve(const Mat& ga_in, const PencilFactor& f, int want, double* val
   Mat ts(d, d);
   for (int j = 0; j < d; ++j)
     for (int i = 0; i < d; ++i) ts(i, j) = 0.5 * (t(i, j) + t(j, i));
+  RR_MARK(5);   // R^-T A R^-1
   std::vector<double> w(d), z((size_t)d * d);
   // B2L_RR_MRRR=i: dsyevr's own stages with the MRRR vectors formed for the
   // `want` smallest only (cheaper; 20 / 32 converged on the C1 band against
@@ -621,6 +622,7 @@ void pencil_solve(const Mat& ga_in, const PencilFactor& f, int want, double* val
             &info);
     if (info != 0) throw LapackError{"dsyevr", info};
   }
+  RR_MARK(6);   // symmetric eigensolve
   Mat v(d, want);
   for (int j = 0; j < want; ++j)
     for (int i = 0; i < d; ++i) v(i, j) = z[(size_t)i + (size_t)j * d];

@@ -35,6 +35,8 @@ int main(int argc, char** argv) {
       b2l_set_lapack(sym("scipy_dpotrf_", "dpotrf_"), sym("scipy_dtrtrs_", "dtrtrs_"),
                      sym("scipy_dtrtri_", "dtrtri_"), sym("scipy_dsyevr_", "dsyevr_"));
       b2l_set_blas(sym("scipy_dgemm_", "dgemm_"));
+      b2l_set_lapack_mrrr(sym("scipy_dsytrd_", "dsytrd_"), sym("scipy_dstemr_", "dstemr_"),
+                          sym("scipy_dormtr_", "dormtr_"));
     }
   }
   for (int a = 1; a < argc; ++a) {
