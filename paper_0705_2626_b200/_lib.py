@@ -10,8 +10,11 @@ import ctypes as C
 import threading
 from pathlib import Path
 
+import os
+
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "lib" / "libb200lobpcg.so"
+# B2L_LIB_PATH: an A/B build of the same sources (tools/build_variant.py); diagnostic only
+LIB_PATH = Path(os.environ.get("B2L_LIB_PATH") or _HERE / "lib" / "libb200lobpcg.so")
 
 _lock = threading.Lock()
 _lib = None

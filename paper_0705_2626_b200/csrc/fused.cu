@@ -95,6 +95,7 @@ struct StepArgs {
   int out_off[5];       // buffer 0
   int out_stride;       // doubles between the two output buffers
   int coef_off, lam_off, int_off, zero_off;
+  int tail_off;         // m = 10 full block: tail-column coefficient table (72 doubles)
   int bar_off, red_off, gred_off;
   // Gram of the next step
   int a, b;
@@ -1040,8 +1041,15 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
   }
 }
 
-#ifndef B2L_TAIL_DFMA   // full-block tail columns on DFMA (0: DMMA, for A/B timing)
-#define B2L_TAIL_DFMA 1
+// full-block tail columns (8, 9 at m = 10) on DFMA.  0: DMMA (a 75%-empty
+// column tile); 1: lane = (row, side, column), every lane sums k = 0..9 (each
+// 16-byte load serves two lanes: 8 shared-memory wavefronts per load, 150 per
+// warp-chunk with the coefficient loads); 2: lane = (row, side, k-half), 32
+// distinct conflict-free 16-byte loads per instruction and three shuffles
+// (72 wavefronts per warp-chunk).  The pass is bound by the shared-memory
+// data pipe (ncu: l1tex__data_pipe_lsu_wavefronts at 81% of peak with form 1).
+#ifndef B2L_TAIL_DFMA
+#define B2L_TAIL_DFMA 2
 #endif
 constexpr int PAIR_NW = 14;                        // compute warps (7 pairs, 56-row chunks)
 constexpr int PAIR_THREADS = 32 * (2 + PAIR_NW);   // 512: loader + 14 compute + storer warps
@@ -1052,6 +1060,24 @@ constexpr int NB_PAIR = 5;                         // named barriers 5..11
 constexpr int NB_POEMPTY = 12;                     // named barriers 12..14
 constexpr int NB_PAIR_DONE = 15;
 constexpr int NB_GRND = 4;                         // compute warps, Gram rounds
+
+// Which half of its pair compute warp cw is.  A warp issues on SM
+// sub-partition (warp index) % 4, and at m = 10 half 0 carries ~1.8x the fp64
+// pipe time of half 1 (18 + 14 DMMA against the DFMA tail + 14 DMMA per
+// chunk): with H = cw & 1 every half-0 warp lands on sub-partitions 1 and 3.
+// Flipping every other pair of pairs gives each sub-partition both kinds.
+// timing ablations of the pair kernel (wrong results; tools/time_f1.py only):
+// 1 no Gram phase, 2 no update math, 4 no TMA stores, 8 no pair barrier,
+// 16 no output stores to shared memory
+#ifndef B2L_ABLATE
+#define B2L_ABLATE 0
+#endif
+#ifndef B2L_PAIR_BALANCE
+#define B2L_PAIR_BALANCE 1
+#endif
+__device__ __forceinline__ int pair_half(int cw) {
+  return B2L_PAIR_BALANCE ? ((cw & 1) ^ ((cw >> 2) & 1)) : (cw & 1);
+}
 
 // ---------------------------------------------------------------------------
 // F1, warp-pair variant (m = 9..10): 14 compute warps, two per 8-row tile.
@@ -1120,6 +1146,20 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     fence_mbar_init();
   }
   __syncthreads();
+  if constexpr (FIX && MFIX == 10 && B2L_TAIL_DFMA == 2) {
+    // tail table: entry ((kh*3 + j)*2 + e)*3 + blk = rows k of (Cw, Cp, Cx),
+    // columns 8 and 9, k = 4j + 2kh + e (j < 2), k = 8 + e (j = 2, kh = 0);
+    // (j = 2, kh = 1) re-reads k = 8, 9 against zeros
+    if (tid < 36) {
+      const int blk = tid % 3, e = (tid / 3) & 1, j = (tid / 6) % 3, kh = tid / 18;
+      const int k = j == 2 ? 8 + e : 4 * j + 2 * kh + e;
+      const bool z = j == 2 && kh == 1;
+      const double* cb = coef + (blk == 0 ? MFIX * MFIX : blk == 1 ? 2 * MFIX * MFIX : 0) + k * MFIX;
+      sm[A.tail_off + 2 * tid] = z ? 0.0 : cb[8];
+      sm[A.tail_off + 2 * tid + 1] = z ? 0.0 : cb[9];
+    }
+    __syncthreads();
+  }
 
   const int nchunks = (A.nrows + A.rc - 1) / A.rc;
   const int nloc = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -1247,7 +1287,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
       const double* st = stages + (size_t)s * A.stage_doubles;
       const int ob = b * A.out_stride;
       const int r = 8 * mt + rl;
-      {
+      if constexpr (!(B2L_ABLATE & 2)) {
         // ---- (1) update of this warp's column tile, all six products, and
         // (2) the next residual straight from the accumulators
         const double* W = st + A.in_off[2];
@@ -1259,6 +1299,64 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         // per lane: the two columns co, co+1 of P', AP', X', AX'
         double pn_[2], apn_[2], xn_[2], axn_[2];
         const bool bw = kw > 0, bp = kp > 0;
+        if constexpr (FIX && MFIX == 10 && H == 1 && B2L_TAIL_DFMA == 2) {
+          // full block, columns 8, 9 on DFMA, k split over lane pairs: lane =
+          // (kh = lane & 1, row = 4 (lane >> 4) + ((lane >> 1) & 3), side =
+          // (lane >> 3) & 1).  An 8-lane phase of a 16-byte load covers 4 rows
+          // x 2 k-halves of one block: rows 96 B apart, halves 16 B apart --
+          // eight distinct 16-byte bank groups.
+          const int kh = lane & 1;
+          const int tr_ = 8 * mt + 4 * (lane >> 4) + ((lane >> 1) & 3);
+          const bool aside = (lane >> 3) & 1;
+          const double* D1 = (aside ? AW : W) + tr_ * SF;
+          const double* D2 = (aside ? AP : P) + tr_ * SF;
+          const double* D3 = (aside ? AX : X) + tr_ * SF;
+          const double2* T2 = reinterpret_cast<const double2*>(sm + A.tail_off) + 18 * kh;
+          double sw0 = 0.0, sw1 = 0.0, sp0 = 0.0, sp1 = 0.0, sx0 = 0.0, sx1 = 0.0;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            const int kk = j == 2 ? 8 : 4 * j + 2 * kh;
+            const double2 w2 = *reinterpret_cast<const double2*>(D1 + kk);
+            const double2 p2 = *reinterpret_cast<const double2*>(D2 + kk);
+            const double2 x2 = *reinterpret_cast<const double2*>(D3 + kk);
+            const double2 cwa = T2[(2 * j) * 3], cpa = T2[(2 * j) * 3 + 1], cxa = T2[(2 * j) * 3 + 2];
+            const double2 cwb = T2[(2 * j + 1) * 3], cpb = T2[(2 * j + 1) * 3 + 1],
+                          cxb = T2[(2 * j + 1) * 3 + 2];
+            sw0 = fma(w2.x, cwa.x, sw0);
+            sw1 = fma(w2.x, cwa.y, sw1);
+            sp0 = fma(p2.x, cpa.x, sp0);
+            sp1 = fma(p2.x, cpa.y, sp1);
+            sx0 = fma(x2.x, cxa.x, sx0);
+            sx1 = fma(x2.x, cxa.y, sx1);
+            sw0 = fma(w2.y, cwb.x, sw0);
+            sw1 = fma(w2.y, cwb.y, sw1);
+            sp0 = fma(p2.y, cpb.x, sp0);
+            sp1 = fma(p2.y, cpb.y, sp1);
+            sx0 = fma(x2.y, cxb.x, sx0);
+            sx1 = fma(x2.y, cxb.y, sx1);
+          }
+          // lane kh keeps column 8 + kh: it sends its partial of the other
+          // column and adds the partner's partial of its own
+          const double t0 = __dadd_rn(sw0, sp0), t1 = __dadd_rn(sw1, sp1);
+          const double pv = __dadd_rn(kh ? t1 : t0, __shfl_xor_sync(0xffffffffu, kh ? t0 : t1, 1));
+          const double sxv =
+              __dadd_rn(kh ? sx1 : sx0, __shfl_xor_sync(0xffffffffu, kh ? sx0 : sx1, 1));
+          const double xv = A.xpp ? __dadd_rn(sxv, pv) : sxv;   // X' / AX' entry
+          const double ov = __shfl_xor_sync(0xffffffffu, xv, 8);   // the other side's
+          const int oc = tr_ * SF + 8 + kh;
+          (sm + A.out_off[aside ? 1 : 0] + ob)[oc] = xv;
+          (sm + A.out_off[aside ? 3 : 2] + ob)[oc] = pv;
+          if (!aside) {
+            const double dr = weighted ? st[A.d_off + tr_] : 1.0;
+            const double bx = weighted ? __dmul_rn(dr, xv) : xv;
+            const double wf = __dsub_rn(ov, __dmul_rn(bx, slam[8 + kh]));
+            s_w[0] = fma(wf, wf, s_w[0]);
+            const double trw = tmode == 2 ? st[A.t_off + tr_] : tinv;
+            (sm + A.out_off[4] + ob)[oc] = tmode == 0 ? wf : __dmul_rn(trw, wf);
+          } else if (want_ax) {
+            s_a[0] = fma(xv, xv, s_a[0]);
+          }
+        } else {
         if constexpr (FIX && MFIX == 10 && H == 1 && B2L_TAIL_DFMA) {
           // full block, columns 8..MFIX-1 (2 at MFIX = 10): DFMA instead of a
           // 75%-empty DMMA column tile.  Lane (row rl, q) forms column
@@ -1363,6 +1461,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
             const int rr = e / npad;
             O4[(8 * mt + rr) * swn + (FIX ? MFIX : A.kwn) + (e - rr * npad)] = 0.0;
           }
+        }
       }
       // the stage is free once the update has read it (the B-weighted Gram
       // still reads d from it): the loader refills it while the Gram runs
@@ -1370,12 +1469,12 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
       }
-      nbar_sync(pbar, 64);
+      if constexpr (!(B2L_ABLATE & 8)) nbar_sync(pbar, 64);
       // ---- (3) Gram over the 8 rows, this warp's tiles (m = 16: one row
       // quad's fragments live at a time)
       const uint32_t boff = 8u * (uint32_t)ob;
 #pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
+      for (int ks = 0; ks < ((B2L_ABLATE & 1) ? 0 : 2); ++ks) {
         const uint32_t row = (uint32_t)(8 * mt + 4 * ks + q);
         double av[NI], bv[NJ];
         if constexpr (CSM) {
@@ -1426,6 +1525,22 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         b = 0;
         if (it + 1 > NOB) ophase ^= 1u;
       }
+    }
+    if constexpr (FIX && MFIX == 10 && H == 1 && B2L_TAIL_DFMA == 2) {
+      // the k-split tail keeps column 8 + c of row g in lane (c | (g & 3) << 1
+      // | (g >> 2) << 4) (P side: |W'|^2) and that lane | 8 (A side: |AX'|^2);
+      // the CTA reduction reads lane 4g, entry c
+      const int g = lane >> 2;
+      const int src = ((g & 3) << 1) | ((g >> 2) << 4);
+      const double w0 = __shfl_sync(0xffffffffu, s_w[0], src);
+      const double w1 = __shfl_sync(0xffffffffu, s_w[0], src | 1);
+      const double a0 = __shfl_sync(0xffffffffu, s_a[0], src | 8);
+      const double a1 = __shfl_sync(0xffffffffu, s_a[0], src | 9);
+      const bool own = (lane & 3) == 0;
+      s_w[0] = own ? w0 : 0.0;
+      s_w[1] = own ? w1 : 0.0;
+      s_a[0] = own ? a0 : 0.0;
+      s_a[1] = own ? a1 : 0.0;
     }
     s_w0 = s_w[0];
     s_w1 = s_w[1];
@@ -1486,7 +1601,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
       if (lane == 0) {
         const int r0 = chunk_of(it) * A.rc;
         const int ob = b * A.out_stride;
-        for (int k = 0; k < 5; ++k) {
+        for (int k = 0; k < ((B2L_ABLATE & 4) ? 0 : 5); ++k) {
           if (k == 4 && A.kwn == 0) continue;
           tma_store_2d(&M.out[k], sm + A.out_off[k] + ob, 0, r0);
         }
@@ -1499,7 +1614,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     if (lane == 0) bulk_wait<0>();
     __syncwarp();
     nbar_sync(NB_PAIR_DONE, PAIR_THREADS);
-  } else if (((warp - 1) & 1) == 0) {
+  } else if (pair_half(warp - 1) == 0) {
     run_half(std::integral_constant<int, 0>{});
   } else {
     run_half(std::integral_constant<int, 1>{});
@@ -1510,7 +1625,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
   double* red = sm + A.red_off;
   const int NL = PAIR_NW * 64;      // [warp][lane][e]
   if (warp >= 1 && warp <= PAIR_NW) {
-    const int o = ((warp - 1) * 32 + lane) * 2;
+    const int o = ((((warp - 1) & ~1) + pair_half(warp - 1)) * 32 + lane) * 2;   // [2 pair + H]
     red[o] = s_w0;
     red[o + 1] = s_w1;
     red[NL + o] = s_a0;
@@ -1695,7 +1810,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   const int nob = pair && !pair16 ? PAIR_NOB : 2;
   {
     const size_t tail = (size_t)nob * (4 * tile_x + tile_w) + (m * m + kw * m + kp * m) + 3 * m +
-                        64 + (pair ? 0 : (size_t)4 * STEP_NU * 32) + 64;
+                        64 + 80 + (pair ? 0 : (size_t)4 * STEP_NU * 32) + 64;
     const size_t budget = pair ? 224 * 1024 : 200 * 1024;
     A.nst = 4;
     while (A.nst > 2 && ((size_t)A.nst * A.stage_doubles + tail) * 8 > budget) --A.nst;
@@ -1718,6 +1833,8 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   off = (off + 15) & ~15;
   A.zero_off = off;
   off += 16;
+  A.tail_off = off;
+  off += 80;   // 72 used (pair kernel, m = 10 full block)
   A.bar_off = off;
   off += 16;  // mbarriers
   A.red_off = off;
