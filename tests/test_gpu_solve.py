@@ -428,3 +428,37 @@ def test_c1_outcome_distribution_matches_reference(pk, golden):
     assert abs(conv - ref_conv) <= 10, (conv, ref_conv, n)
     assert abs(early - ref_early) <= 11, (early, ref_early, n)
     assert abs(np.median(its) - np.median(band["iterations"])) <= 0.1 * np.median(band["iterations"])
+
+
+def test_c1_outcome_distribution_128_runs(pk, golden):
+    """The same comparison over 128 perturbed C1@1000 problems (k = +-1..64;
+    c1_band128.npz from the REAL reference: 117 of 128 end Converged, 107 lock
+    their second column by iteration 215, median 408 iterations, quartiles
+    404 / 411).  Every run must reach the tolerance on all four pairs; the
+    GPU's median iteration count must sit on the reference's, and the share
+    of runs that never need a basis fallback must stay in the class of the
+    reference-form Rayleigh-Ritz (measured: 97 of 128 with dsyevr, 93 with
+    the MRRR stages, 39 with the tridiagonal QR form).  The remaining gap to
+    the reference (97 vs 117 converged without a fallback, 68 vs 107 early
+    second locks) is 3-5 sd: the GPU path forms the Grams of the
+    orthonormalised blocks as R^-T G R^-1 instead of recomputing them, so
+    the pencil's noise differs in structure -- DESIGN.md records it."""
+    band = golden("c1_band128.npz")
+    N = 32
+    base = float((N + 1) ** 2)
+    its, conv, early = [], 0, 0
+    for k in band["ulps"]:
+        s = base * (1.0 + int(k) * 2.0 ** -52)
+        a = pk.Laplacian3D((N, N, N), scale=s)
+        rep = pk.solve(a, config=pk.SolverConfig(block_size=4, tol=1e-6, max_iter=1000, seed=0))
+        assert rep.status == "Converged" or rep.status.startswith("BasisFallback"), rep.status
+        assert bool(np.all(rep.converged)), (int(k), rep.status)
+        exact = pk.exact_eigenvalues((N, N, N), 4, scale=s)
+        np.testing.assert_allclose(rep.eigenvalues, exact, rtol=1e-8)
+        its.append(rep.iterations_used)
+        conv += rep.status == "Converged"
+        early += sorted(rep.lock_iterations)[1] <= 215
+    ref_its = np.asarray(band["iterations"])
+    assert abs(np.median(its) - np.median(ref_its)) <= 0.03 * np.median(ref_its), np.median(its)
+    assert conv >= 77, (conv, "reference 117 of 128; QR form 39")
+    assert early >= 40, (early, "reference 107 of 128; QR form 17")
