@@ -1051,10 +1051,16 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
 #ifndef B2L_TAIL_DFMA
 #define B2L_TAIL_DFMA 2
 #endif
-constexpr int PAIR_NW = 14;                        // compute warps (7 pairs, 56-row chunks)
+#ifndef B2L_PAIR_NW
+#define B2L_PAIR_NW 14
+#endif
+constexpr int PAIR_NW = B2L_PAIR_NW;               // compute warps (7 pairs, 56-row chunks)
 constexpr int PAIR_THREADS = 32 * (2 + PAIR_NW);   // 512: loader + 14 compute + storer warps
 constexpr int PAIR_BAR = 32 * (1 + PAIR_NW);       // output-buffer barriers: compute + storer
-constexpr int PAIR_NOB = 3;                        // output buffers
+#ifndef B2L_PAIR_NOB
+#define B2L_PAIR_NOB 3
+#endif
+constexpr int PAIR_NOB = B2L_PAIR_NOB;             // output buffers
 constexpr int NB_POFULL = 1;                       // named barriers 1..3
 constexpr int NB_PAIR = 5;                         // named barriers 5..11
 constexpr int NB_POEMPTY = 12;                     // named barriers 12..14
@@ -1071,6 +1077,18 @@ constexpr int NB_GRND = 4;                         // compute warps, Gram rounds
 // 16 no output stores to shared memory
 #ifndef B2L_ABLATE
 #define B2L_ABLATE 0
+#endif
+// -DB2L_TRACE: phase time stamps (clock64) of CTA 0's compute warps for its
+// first 48 chunks (tools/trace_f1.py reads them through b2l_debug_trace)
+#ifdef B2L_TRACE
+__device__ long long g_trace[16 * 48 * 8];
+#define TRACE(slot)                                                          \
+  do {                                                                       \
+    if (blockIdx.x == 0 && lane == 0 && it < 48)                             \
+      g_trace[((warp - 1) * 48 + it) * 8 + (slot)] = clock64();              \
+  } while (0)
+#else
+#define TRACE(slot) ((void)0)
 #endif
 #ifndef B2L_PAIR_BALANCE
 #define B2L_PAIR_BALANCE 1
@@ -1282,8 +1300,11 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     int s = 0, b = 0;
     uint32_t phase = 0, ophase = 0;
     for (int it = 0; it < nloc; ++it) {
+      TRACE(0);
       if (it >= NOB) mbar_wait(&oempty[b], ophase);
+      TRACE(1);
       mbar_wait(&full[s], phase);
+      TRACE(2);
       const double* st = stages + (size_t)s * A.stage_doubles;
       const int ob = b * A.out_stride;
       const int r = 8 * mt + rl;
@@ -1469,7 +1490,9 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
       }
+      TRACE(3);
       if constexpr (!(B2L_ABLATE & 8)) nbar_sync(pbar, 64);
+      TRACE(4);
       // ---- (3) Gram over the 8 rows, this warp's tiles (m = 16: one row
       // quad's fragments live at a time)
       const uint32_t boff = 8u * (uint32_t)ob;
@@ -1513,10 +1536,12 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         for (int t = 0; t < TL.n; ++t)
           dmma_8x8x4(gacc[t][0], gacc[t][1], av[TL.ti[t]], bv[TL.tj[t]]);
       }
+      TRACE(5);
       fence_async_smem();   // generic writes -> the TMA store (async proxy)
       __syncwarp();
       if (WGT && lane == 0) mbar_arrive(&empty[s]);
       nbar_arrive(NB_POFULL + b, PAIR_BAR);
+      TRACE(6);
       if (++s == A.nst) {
         s = 0;
         phase ^= 1u;
@@ -1941,3 +1966,9 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
 }
 
 }  // namespace b2l
+
+#ifdef B2L_TRACE
+extern "C" int b2l_debug_trace(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, b2l::g_trace, sizeof(b2l::g_trace));
+}
+#endif
