@@ -1055,6 +1055,17 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
 #define B2L_PAIR_NW 14
 #endif
 constexpr int PAIR_NW = B2L_PAIR_NW;               // compute warps (7 pairs, 56-row chunks)
+// m = 16 full block: 6 pairs, 48-row chunks -- three compute warps on every SM
+// sub-partition (14 = 4 + 4 + 3 + 3 leaves the pace to the fuller ones); the
+// DMMA-bound pass gains 3-6% (C3 F1 5.37 -> 5.18 ms), the m = 10 pass nothing
+#ifndef B2L_PAIR16_NW
+#define B2L_PAIR16_NW 12
+#endif
+constexpr int PAIR16_NW = B2L_PAIR16_NW;
+#ifndef B2L_PAIR16_NOB
+#define B2L_PAIR16_NOB 2
+#endif
+constexpr int PAIR16_NOB = B2L_PAIR16_NOB;         // its output buffers
 constexpr int PAIR_THREADS = 32 * (2 + PAIR_NW);   // 512: loader + 14 compute + storer warps
 constexpr int PAIR_BAR = 32 * (1 + PAIR_NW);       // output-buffer barriers: compute + storer
 #ifndef B2L_PAIR_NOB
@@ -1112,8 +1123,8 @@ __device__ __forceinline__ int pair_half(int cw) {
 // (rounds) instead of stashed per pair -- the per-pair stash of m = 16 (48
 // tiles x 7 pairs) would not fit the idle stage ring.  Same summation order.
 template <int NT, int KS, int NI, int NJ, int MFIX, bool WGT, int NOB = PAIR_NOB,
-          bool GRND = false>
-__global__ void __launch_bounds__(PAIR_THREADS, 1)
+          bool GRND = false, int NW = PAIR_NW>
+__global__ void __launch_bounds__(32 * (2 + NW), 1)
     step_pair_kernel(const __grid_constant__ StepMaps M, const __grid_constant__ StepArgs Ain,
                     const __grid_constant__ StepCoef Cf) {
   extern __shared__ __align__(128) unsigned char sm_raw[];
@@ -1158,7 +1169,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
   if (tid == 0) {
     for (int s = 0; s < A.nst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], PAIR_NW);
+      mbar_init(&empty[s], NW);
     }
     for (int b = 0; b < NOB; ++b) mbar_init(&oempty[b], 1);
     fence_mbar_init();
@@ -1504,7 +1515,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
           // m = 16 full block: every tile column sits at a compile-time
           // offset from one per-lane base (the output blocks are TXC apart):
           // immediates instead of 14 address registers
-          constexpr uint32_t TXC = (uint32_t)((4 * PAIR_NW * SF + 15) & ~15);
+          constexpr uint32_t TXC = (uint32_t)((4 * NW * SF + 15) & ~15);
           constexpr uint32_t LB[3] = {0u, 4u * TXC, 2u * TXC};        // X', W', P'
           constexpr uint32_t RB[4] = {0u, 4u * TXC, 2u * TXC, 3u * TXC};  // + AP'
           const uint32_t base = obase_lane + boff + row * (8u * SF);
@@ -1540,7 +1551,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
       fence_async_smem();   // generic writes -> the TMA store (async proxy)
       __syncwarp();
       if (WGT && lane == 0) mbar_arrive(&empty[s]);
-      nbar_arrive(NB_POFULL + b, PAIR_BAR);
+      nbar_arrive(NB_POFULL + b, (32 * (1 + NW)));
       TRACE(6);
       if (++s == A.nst) {
         s = 0;
@@ -1572,13 +1583,13 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     s_a0 = s_a[0];
     s_a1 = s_a[1];
     // the stage ring is idle once every warp is here: stash the accumulators
-    nbar_sync(NB_PAIR_DONE, PAIR_THREADS);
+    nbar_sync(NB_PAIR_DONE, (32 * (2 + NW)));
     if constexpr (GRND) {
       // one tile set, zeroed, then pair by pair (p = 0, 1, ...: the order of
       // the stash-and-sum form) each pair adds its halves' disjoint tiles
-      for (int e = (warp - 1) * 32 + lane; e < NI * NJ * 64; e += PAIR_NW * 32) gred[e] = 0.0;
-      nbar_sync(NB_GRND, PAIR_NW * 32);
-      for (int p = 0; p < PAIR_NW / 2; ++p) {
+      for (int e = (warp - 1) * 32 + lane; e < NI * NJ * 64; e += NW * 32) gred[e] = 0.0;
+      nbar_sync(NB_GRND, NW * 32);
+      for (int p = 0; p < NW / 2; ++p) {
         if (mt == p)
 #pragma unroll
           for (int t = 0; t < TL.n; ++t) {
@@ -1586,7 +1597,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
             gred[o] += gacc[t][0];
             gred[o + 1] += gacc[t][1];
           }
-        nbar_sync(NB_GRND, PAIR_NW * 32);
+        nbar_sync(NB_GRND, NW * 32);
       }
       return;
     }
@@ -1617,12 +1628,12 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         step_issue(M, A, stages + (size_t)s * A.stage_doubles, &full[s], chunk_of(j));
       }
     __syncwarp();
-    nbar_sync(NB_PAIR_DONE, PAIR_THREADS);
-  } else if (warp == PAIR_NW + 1) {
+    nbar_sync(NB_PAIR_DONE, (32 * (2 + NW)));
+  } else if (warp == NW + 1) {
     // ================= storer: TMA stores of each finished output buffer
     for (int it = 0; it < nloc; ++it) {
       const int b = it % NOB;
-      nbar_sync(NB_POFULL + b, PAIR_BAR);
+      nbar_sync(NB_POFULL + b, (32 * (1 + NW)));
       if (lane == 0) {
         const int r0 = chunk_of(it) * A.rc;
         const int ob = b * A.out_stride;
@@ -1638,7 +1649,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     }
     if (lane == 0) bulk_wait<0>();
     __syncwarp();
-    nbar_sync(NB_PAIR_DONE, PAIR_THREADS);
+    nbar_sync(NB_PAIR_DONE, (32 * (2 + NW)));
   } else if (pair_half(warp - 1) == 0) {
     run_half(std::integral_constant<int, 0>{});
   } else {
@@ -1648,8 +1659,8 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
 
   // ---- CTA reductions (fixed order over pairs / rows)
   double* red = sm + A.red_off;
-  const int NL = PAIR_NW * 64;      // [warp][lane][e]
-  if (warp >= 1 && warp <= PAIR_NW) {
+  const int NL = NW * 64;      // [warp][lane][e]
+  if (warp >= 1 && warp <= NW) {
     const int o = ((((warp - 1) & ~1) + pair_half(warp - 1)) * 32 + lane) * 2;   // [2 pair + H]
     red[o] = s_w0;
     red[o + 1] = s_w1;
@@ -1662,7 +1673,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
     // column j lives in warp half H = j / 8, lanes with (lane & 3) = (j % 8) / 2, e = j % 2
     const int H = tid >> 3, qq = (tid & 7) >> 1, e = tid & 1;
     double a = 0.0, bb = 0.0;
-    for (int p = 0; p < PAIR_NW / 2; ++p)
+    for (int p = 0; p < NW / 2; ++p)
       for (int g = 0; g < 8; ++g) {
         const int o = (((2 * p + H) * 32) + 4 * g + qq) * 2 + e;
         a += red[o];
@@ -1680,7 +1691,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
       v0 = gred[(size_t)e * 2];
       v1 = gred[(size_t)e * 2 + 1];
     } else {
-      for (int p = 0; p < PAIR_NW / 2; ++p) {
+      for (int p = 0; p < NW / 2; ++p) {
         const size_t o = (((size_t)p * NI * NJ + t) * 32 + ln) * 2;
         v0 += gred[o];
         v1 += gred[o + 1];
@@ -1697,10 +1708,11 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
 
 using StepKernel = void (*)(StepMaps, StepArgs, StepCoef);
 
-template <int NT, int KS, int NI, int NJ, int MFIX, int NOB = PAIR_NOB, bool GRND = false>
+template <int NT, int KS, int NI, int NJ, int MFIX, int NOB = PAIR_NOB, bool GRND = false,
+          int NW = PAIR_NW>
 static StepKernel pick_pair(bool wgt) {
-  return wgt ? step_pair_kernel<NT, KS, NI, NJ, MFIX, true, NOB, GRND>
-             : step_pair_kernel<NT, KS, NI, NJ, MFIX, false, NOB, GRND>;
+  return wgt ? step_pair_kernel<NT, KS, NI, NJ, MFIX, true, NOB, GRND, NW>
+             : step_pair_kernel<NT, KS, NI, NJ, MFIX, false, NOB, GRND, NW>;
 }
 template <int NT, int KS, int NI, int NJ, int MFIX>
 static StepKernel pick_local(bool wgt) {
@@ -1810,7 +1822,8 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
     return v && strcmp(v, "local") == 0;
   }();
   const bool one_warp = (m <= 8 || force_local) && !pair16;
-  A.rc = (local && !one_warp) ? 4 * PAIR_NW : 64;
+  const int pair_nw = pair16 ? PAIR16_NW : PAIR_NW;
+  A.rc = (local && !one_warp) ? 4 * pair_nw : 64;
   while (!pair16 && A.rc > 16 && (size_t)A.rc * width * 8 > 48 * 1024) A.rc >>= 1;
   while (A.rs > 1 && A.rc / A.rs < 4) A.rs >>= 1;
   const int rc = A.rc;
@@ -1832,7 +1845,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   const int tile_w = (rc * A.swn + 15) & ~15;
   // output buffers: 3 for the warp-pair variant (separate storer warp), else 2
   const bool pair = local && !one_warp;
-  const int nob = pair && !pair16 ? PAIR_NOB : 2;
+  const int nob = pair16 ? PAIR16_NOB : (pair ? PAIR_NOB : 2);
   {
     const size_t tail = (size_t)nob * (4 * tile_x + tile_w) + (m * m + kw * m + kp * m) + 3 * m +
                         64 + 80 + (pair ? 0 : (size_t)4 * STEP_NU * 32) + 64;
@@ -1863,7 +1876,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.bar_off = off;
   off += 16;  // mbarriers
   A.red_off = off;
-  const size_t red1 = (size_t)4 * 32 * (PAIR_NW > STEP_NU ? PAIR_NW : STEP_NU);
+  const size_t red1 = (size_t)4 * 32 * (PAIR_NW > STEP_NU ? PAIR_NW : STEP_NU);   // PAIR16_NW <= PAIR_NW
   const size_t red2 = pair16 ? (size_t)A.NI * A.NJ * 64
                      : local ? (size_t)LOC_NW * lNI * lNJ * 64 : (size_t)A.TS * A.rs * 8 * 64;
   // the Gram item reduction reuses the (idle) stage ring after the loop; the
@@ -1881,7 +1894,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   const size_t smem = (size_t)off * 8;
   B2L_CHECK(smem <= 227 * 1024, -B2L_EINVAL, "step: shared memory budget exceeded");
   if (pair16) {   // the m = 16 kernel addresses the output blocks by compile-time offsets
-    const int txc = (4 * PAIR_NW * smem_stride(16) + 15) & ~15;
+    const int txc = (4 * PAIR16_NW * smem_stride(16) + 15) & ~15;
     B2L_CHECK(tile_x == txc && tile_w == txc && A.out_off[1] - A.out_off[0] == txc &&
                   A.out_off[4] - A.out_off[0] == 4 * txc,
               -B2L_EINVAL, "step: m = 16 output layout mismatch");
@@ -1914,7 +1927,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   StepKernel kern;
   int threads;
   if (local) {
-    B2L_CHECK(rc == (one_warp ? 8 * LOC_NW : 4 * PAIR_NW), -B2L_EINVAL,
+    B2L_CHECK(rc == (one_warp ? 8 * LOC_NW : 4 * pair_nw), -B2L_EINVAL,
               "step: warp-local variants need 64- / 56-row chunks");
     if (one_warp) {
       const bool full = kwn == m;   // the compile-time needed-tile lists assume kw_next = m
@@ -1925,12 +1938,12 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
       else if (m <= 8) kern = pick_local<1, 2, 3, 4, 0>(wgt);
       else kern = pick_local<2, 3, 4, 5, 0>(wgt);
     } else {
-      threads = PAIR_THREADS;
+      threads = 32 * (2 + pair_nw);
       // the full-block specialisation: every column active (P and W' column
       // maps are then the identity), unpadded leading dimensions
       const bool full = m == 10 && kw == 10 && kp == 10 && kwn == 10 && ldx == 10 && ldw == 10 &&
                         ldwn == 10;
-      kern = pair16 ? pick_pair<2, 4, 6, 8, 16, 2, true>(wgt)
+      kern = pair16 ? pick_pair<2, 4, 6, 8, 16, PAIR16_NOB, true, PAIR16_NW>(wgt)
              : full ? pick_pair<2, 3, 4, 5, 10>(wgt) : pick_pair<2, 3, 4, 5, 0>(wgt);
     }
   } else {
