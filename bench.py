@@ -84,13 +84,14 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index=0, period=0.05):
+    def __init__(self, index=0, period=float(os.environ.get("B2L_BENCH_CLOCK_PERIOD", "0.005"))):
         self.index = index
         self.period = period
         self.rows = []
         self._stop = threading.Event()
         self._t = None
         self._nvml = None
+        self._mx = None
         try:
             import pynvml
 
@@ -110,7 +111,9 @@ class ClockSampler:
     def _sample_nvml(self):
         nv, h = self._nvml
         sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        if self._mx is None:   # constant: asked once, so a sample is two NVML calls
+            self._mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = self._mx
         r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
         flags = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
                  nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
