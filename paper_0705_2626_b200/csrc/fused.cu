@@ -1051,6 +1051,9 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
 #ifndef B2L_TAIL_DFMA
 #define B2L_TAIL_DFMA 2
 #endif
+#ifndef B2L_STORE_SWZ   // conflict-free output stores of the full-block pair kernels
+#define B2L_STORE_SWZ 1
+#endif
 #ifndef B2L_PAIR_NW
 #define B2L_PAIR_NW 14
 #endif
@@ -1159,7 +1162,13 @@ __global__ void __launch_bounds__(32 * (2 + NW), 1)
   const int sx = FIX ? SF : A.sx, sw = FIX ? SF : A.sw, swn = FIX ? SF : A.swn;
   const int ncoef = m * m + kw * m + kp * m;
   const bool inl = A.coef == nullptr;
-  for (int i = tid; i < ncoef; i += blockDim.x) coef[i] = inl ? Cf.c[i] : A.coef[i];
+  // m = 16 full block: the coefficient rows at the padded stride of the tiles
+  // (20 doubles) -- a fragment load takes rows k = 4 ks + q of one column
+  // octet, and at a 128-byte pitch its four q lanes meet on one bank
+  // (8 wavefronts instead of 2: 29% of the pass's shared-memory wavefronts)
+  constexpr int CPITCH = CSM ? SF : 0;
+  for (int i = tid; i < ncoef; i += blockDim.x)
+    coef[CSM ? (i / MFIX) * CPITCH + (i % MFIX) : i] = inl ? Cf.c[i] : A.coef[i];
   for (int i = tid; i < m; i += blockDim.x) {
     slam[i] = inl ? Cf.lam[i] : A.lam[i];
     swp[i] = inl ? Cf.wpos[i] : A.wpos[i];
@@ -1238,7 +1247,8 @@ __global__ void __launch_bounds__(32 * (2 + NW), 1)
       lamc[e] = colok[e] ? slam[c] : 0.0;
       wposc[e] = colok[e] ? (FIX ? c : swp[c]) : -1;
     }
-    const bool weighted = A.d != nullptr, want_ax = A.want_ax != 0;
+    constexpr bool weighted = WGT;   // the launcher picks WGT = (d != nullptr)
+    const bool want_ax = A.want_ax != 0;
     const int tmode = A.tmode;
     const double tinv = A.tinv;
     const int npad = FIX ? 0 : A.ldwn - A.kwn;
@@ -1442,9 +1452,9 @@ __global__ void __launch_bounds__(32 * (2 + NW), 1)
           const double axv = km_ok ? AX[r * sx + k] : 0.0;
           // m = 16: the coefficient fragments come from shared memory each
           // chunk (12 registers fewer for the 17-tile Gram accumulators)
-          const double cw_ = CSM ? coef[MFIX * MFIX + k * MFIX + 8 * H + rl] : cW[ks];
-          const double cp_ = CSM ? coef[2 * MFIX * MFIX + k * MFIX + 8 * H + rl] : cP[ks];
-          const double cx_ = CSM ? coef[k * MFIX + 8 * H + rl] : cX[ks];
+          const double cw_ = CSM ? coef[(MFIX + k) * CPITCH + 8 * H + rl] : cW[ks];
+          const double cp_ = CSM ? coef[(2 * MFIX + k) * CPITCH + 8 * H + rl] : cP[ks];
+          const double cx_ = CSM ? coef[k * CPITCH + 8 * H + rl] : cX[ks];
           dmma_8x8x4(acc[0][0], acc[0][1], wv, cw_);
           dmma_8x8x4(acc[1][0], acc[1][1], awv, cw_);
           dmma_8x8x4(acc[2][0], acc[2][1], pv, cp_);
@@ -1468,6 +1478,38 @@ __global__ void __launch_bounds__(32 * (2 + NW), 1)
         const double dr = weighted ? st[A.d_off + r] : 1.0;
         const double tr = tmode == 2 ? st[A.t_off + r] : tinv;
         const int co = 8 * H + 2 * q;
+        // m = 10 full block, columns 0..7: odd rows store their second column
+        // first.  A lane's two 8-byte columns sit in one 16-byte slot, and at
+        // the 96-byte row pitch two rows of a half-warp share every slot
+        // (2-way conflicts, 4 wavefronts per store); with the odd rows'
+        // halves swapped the 16 lanes cover 16 distinct bank pairs (C2 F1
+        // 0.388 -> 0.374 ms).  The register-bound m = 16 kernel spills on the
+        // selects and loses (5.04 -> 5.49 ms), so it keeps the plain order.
+        constexpr bool SWZ = FIX && MFIX == 10 && H == 0 && B2L_STORE_SWZ;
+        if constexpr (SWZ) {
+          double wv_[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            // W'_j = T (AX'_j - BX'_j lam_j) (lobpcg.py:429-430, :466-467)
+            const double bx = weighted ? __dmul_rn(dr, xn_[e]) : xn_[e];
+            const double wf = __dsub_rn(axn_[e], __dmul_rn(bx, lamc[e]));
+            s_w[e] = fma(wf, wf, s_w[e]);
+            if (want_ax) s_a[e] = fma(axn_[e], axn_[e], s_a[e]);
+            wv_[e] = tmode == 0 ? wf : __dmul_rn(tr, wf);
+          }
+          const bool odd = rl & 1;
+          const int a0 = r * SF + co + (odd ? 1 : 0), a1 = r * SF + co + (odd ? 0 : 1);
+          O0[a0] = odd ? xn_[1] : xn_[0];
+          O1[a0] = odd ? axn_[1] : axn_[0];
+          O2[a0] = odd ? pn_[1] : pn_[0];
+          O3[a0] = odd ? apn_[1] : apn_[0];
+          O4[a0] = odd ? wv_[1] : wv_[0];
+          O0[a1] = odd ? xn_[0] : xn_[1];
+          O1[a1] = odd ? axn_[0] : axn_[1];
+          O2[a1] = odd ? pn_[0] : pn_[1];
+          O3[a1] = odd ? apn_[0] : apn_[1];
+          O4[a1] = odd ? wv_[0] : wv_[1];
+        } else {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const double pn = pn_[e], apn = apn_[e], xn = xn_[e], axn = axn_[e];
@@ -1486,6 +1528,7 @@ __global__ void __launch_bounds__(32 * (2 + NW), 1)
             const double wv = tmode == 0 ? wf : __dmul_rn(tr, wf);
             if (wposc[e] >= 0) O4[r * swn + wposc[e]] = wv;
           }
+        }
         }
         // W' padding columns (kw_next .. ldw_next-1) of this warp's rows
         if (H == 1)
@@ -1848,7 +1891,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   const int nob = pair16 ? PAIR16_NOB : (pair ? PAIR_NOB : 2);
   {
     const size_t tail = (size_t)nob * (4 * tile_x + tile_w) + (m * m + kw * m + kp * m) + 3 * m +
-                        64 + 80 + (pair ? 0 : (size_t)4 * STEP_NU * 32) + 64;
+                        64 + 80 + (pair16 ? 192 : 0) + (pair ? 0 : (size_t)4 * STEP_NU * 32) + 64;
     const size_t budget = pair ? 224 * 1024 : 200 * 1024;
     A.nst = 4;
     while (A.nst > 2 && ((size_t)A.nst * A.stage_doubles + tail) * 8 > budget) --A.nst;
@@ -1863,7 +1906,7 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   A.out_stride = off - A.out_off[0];
   off += (nob - 1) * A.out_stride;  // the other output buffers
   A.coef_off = off;
-  off += (m * m + kw * m + kp * m + 1) & ~1;
+  off += pair16 ? 3 * 16 * smem_stride(16) : ((m * m + kw * m + kp * m + 1) & ~1);
   A.lam_off = off;
   off += (m + 1) & ~1;
   A.int_off = off;
