@@ -17,8 +17,11 @@
 #include "gram_tile.cuh"
 #include "stencil.cuh"
 
-namespace b2l {
+#ifndef B2L_SGRAM_KSTRIDE
+#define B2L_SGRAM_KSTRIDE 1
+#endif
 
+namespace b2l {
 
 // LD = doubles per point of W / AW (template: it fixes the per-lane element
 // count EPT = GPW*LD/4 and the Gram tile counts); GPW = 8-point groups per
@@ -82,7 +85,15 @@ __global__ void __launch_bounds__(256, 2)
     oel[i] = v ? e : 0;
     vmask |= (v ? 1u : 0u) << i;
   }
-  // Gram rows: lane (q4 = lane & 3) holds point 8 grp + 4 ks + q4
+  // Gram rows: lane (q4 = lane & 3) holds point 8 grp + 4 ks + q4, or, where
+  // that helps, 8 grp + 2 q4 + ks (the four points of a k-step two apart; any
+  // fixed split of a group's 8 points over its two k-steps is a valid Gram).
+  // At the 80-byte pitch of 10-column rows consecutive points put lanes of
+  // one half-warp on the same banks (3-4 wavefronts per fragment load instead
+  // of 2) and every other point does not (C2 pass 0.110 -> 0.107 ms); at 64-
+  // or 128-byte pitches (m = 8, 16) the stride only makes it worse (W1 pass
+  // 0.47 -> 0.58 ms), so it is taken only when 16 LD = 32 or 96 (mod 128).
+  constexpr bool KS2 = B2L_SGRAM_KSTRIDE && ((16 * LD) % 128 == 32 || (16 * LD) % 128 == 96);
   const int q4 = lane & 3;
   const int Gm = FULLB ? LD : G.m, Gkw = FULLB ? LD : G.kw, Gldx = FULLB ? LD : G.ldx;
   const int Ga = Gm + Gkw, Gb = Gkw;
@@ -92,7 +103,7 @@ __global__ void __launch_bounds__(256, 2)
   for (int gi = 0; gi < GPW; ++gi)
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
-      const int pt0 = 8 * (warp + 8 * gi) + 4 * ks + q4;
+      const int pt0 = 8 * (warp + 8 * gi) + (KS2 ? 2 * q4 + ks : 4 * ks + q4);
       const bool ok = pt0 < G.npts;
       const int pt = ok ? pt0 : 0;
       xo[gi][ks] = pt * Gldx;
