@@ -25,6 +25,7 @@ struct StencilGeom {
 struct StencilPlan {
   StencilGeom g;
   int ept, nst;
+  int nob = 3;      // output tiles of the stencil + Gram ring (with nst)
   size_t smem;
   dim3 grid;
 };
@@ -53,6 +54,7 @@ int choose_zchunk(int tiles, int nz, int slots);
 // K1+K5b geometry (stencil_gram.cu)
 struct SGramGeom {
   int m, ldx, kw;   // X columns / leading dim, W columns used
+  int ldxp;         // pitch of the X tile in shared memory (sgram_pitch(ldx))
   int a, b;         // m + kw, kw
   int npts;         // points per tile (TX*TY)
   int ngroups;      // ceil(npts / 8)

@@ -17,6 +17,19 @@
 #include "gram_tile.cuh"
 #include "stencil.cuh"
 
+// Shared-memory pitch (doubles per point) of the staged W planes, the A W
+// tile and the X tile.  Rows of 16 doubles are 128 bytes: every point of a
+// tile then starts on bank 0 and the four points of a Gram k-step meet on the
+// same banks (8 wavefronts per fragment load instead of 2 -- two thirds of
+// the C3 pass's shared-memory wavefronts, its data pipe at 83%).  The TMA
+// boxes are therefore 20 wide there (columns 16..19 out of bounds: zero-
+// filled on load, clipped on store), 160-byte rows.
+#ifndef B2L_SGRAM_PAD16
+#define B2L_SGRAM_PAD16 1
+#endif
+__host__ __device__ constexpr int sgram_pitch(int ld) {
+  return (ld == 16 && B2L_SGRAM_PAD16) ? 20 : ld;
+}
 #ifndef B2L_SGRAM_KSTRIDE
 #define B2L_SGRAM_KSTRIDE 1
 #endif
@@ -43,6 +56,7 @@ __global__ void __launch_bounds__(256, 2)
   constexpr int EPT = (GPW * LD + 3) / 4;
   constexpr int NI = (2 * LD + 7) / 8, NJ = (LD + 7) / 8;
   constexpr int NA = (NI * NJ >= 4) ? 1 : (NI * NJ >= 2 ? 2 : 4);
+  constexpr int LDP = sgram_pitch(LD);   // pitch of the staged / output rows
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* base = smem_raw;
   auto stage = [&](int s) -> double* {
@@ -65,7 +79,7 @@ __global__ void __launch_bounds__(256, 2)
   const int ty0 = (blockIdx.x / g.tiles_x) * g.TY;
   int z0, z1;
   stencil_zrange(g, z0, z1);
-  const int ystride = (g.TX + 2) * LD;
+  const int ystride = (g.TX + 2) * LDP;
   auto staged_row = [&](int pt) { return (pt / g.TX + 1) * (g.TX + 2) + (pt % g.TX) + 1; };
 
   // stencil elements: the warp's groups (grp = warp + 8 gi) enumerated flat,
@@ -81,8 +95,8 @@ __global__ void __launch_bounds__(256, 2)
     const bool v = gi < GPW && grp < G.ngroups && e < g.nelem;
     const int p = v ? e / LD : 0;
     const int c = v ? e - p * LD : 0;
-    off[i] = staged_row(p) * LD + c;
-    oel[i] = v ? e : 0;
+    off[i] = staged_row(p) * LDP + c;
+    oel[i] = v ? p * LDP + c : 0;
     vmask |= (v ? 1u : 0u) << i;
   }
   // Gram rows: lane (q4 = lane & 3) holds point 8 grp + 4 ks + q4, or, where
@@ -95,7 +109,8 @@ __global__ void __launch_bounds__(256, 2)
   // 0.47 -> 0.58 ms), so it is taken only when 16 LD = 32 or 96 (mod 128).
   constexpr bool KS2 = B2L_SGRAM_KSTRIDE && ((16 * LD) % 128 == 32 || (16 * LD) % 128 == 96);
   const int q4 = lane & 3;
-  const int Gm = FULLB ? LD : G.m, Gkw = FULLB ? LD : G.kw, Gldx = FULLB ? LD : G.ldx;
+  const int Gm = FULLB ? LD : G.m, Gkw = FULLB ? LD : G.kw;
+  const int Gldx = FULLB ? LDP : G.ldxp;   // pitch of the X tile
   const int Ga = Gm + Gkw, Gb = Gkw;
   int xo[GPW][2], po[GPW][2], oo[GPW][2];
   unsigned rmask = 0;
@@ -107,8 +122,8 @@ __global__ void __launch_bounds__(256, 2)
       const bool ok = pt0 < G.npts;
       const int pt = ok ? pt0 : 0;
       xo[gi][ks] = pt * Gldx;
-      po[gi][ks] = staged_row(pt) * LD;
-      oo[gi][ks] = pt * LD;
+      po[gi][ks] = staged_row(pt) * LDP;
+      oo[gi][ks] = pt * LDP;
       rmask |= (ok ? 1u : 0u) << (2 * gi + ks);
     }
   // lane columns: L = [X (m) ; W (kw)], R = AW (kw)
@@ -203,8 +218,8 @@ __global__ void __launch_bounds__(256, 2)
         const int o = off[i];
         const double nx_ = N[o];
         double r = __dmul_rn(six, cur[i]);
-        r = __dsub_rn(r, P[o - LD]);
-        r = __dsub_rn(r, P[o + LD]);
+        r = __dsub_rn(r, P[o - LDP]);
+        r = __dsub_rn(r, P[o + LDP]);
         r = __dsub_rn(r, P[o - ystride]);
         r = __dsub_rn(r, P[o + ystride]);
         r = __dsub_rn(r, prev[i]);
@@ -347,8 +362,10 @@ static int launch_sgram_t(const StencilPlan& p, size_t smem, const CUtensorMap& 
                     p.g.nelem == 256 * EPT;
   auto kern = p.nst == 4 ? (full ? stencil7_gram_kernel<LD, GPW, 4, 2, FB_OK>
                                  : stencil7_gram_kernel<LD, GPW, 4, 2, false>)
-                         : (full ? stencil7_gram_kernel<LD, GPW, 3, 3, FB_OK>
-                                 : stencil7_gram_kernel<LD, GPW, 3, 3, false>);
+              : p.nob == 3 ? (full ? stencil7_gram_kernel<LD, GPW, 3, 3, FB_OK>
+                                   : stencil7_gram_kernel<LD, GPW, 3, 3, false>)
+                           : (full ? stencil7_gram_kernel<LD, GPW, 3, 2, FB_OK>
+                                   : stencil7_gram_kernel<LD, GPW, 3, 2, false>);
   if (int rc = prepare_kernel(reinterpret_cast<const void*>(kern), smem, 256, nullptr)) return rc;
   kern<<<p.grid, 256, smem, st>>>(tin, thalo, tout, txm, p.g, G);
   count_launch();
@@ -410,17 +427,26 @@ int sgram_plan(const double* in, double* out, int nx, int ny, int nz, int ld, co
   if (rc) return rc;
   StencilGeom& g = p.g;
   const int TX = g.TX;
+  // shared-memory pitches (sgram_pitch): the boxes of the tensor maps below
+  const int ldp = sgram_pitch(ld), ldxp = m ? sgram_pitch(ldx) : ldx;
+  G.ldxp = ldxp;
   auto need = [&](int ty) {
-    const size_t stg = (((size_t)(TX + 2) * (ty + 2) * ld * 8) + 127) & ~(size_t)127;
-    const size_t ob = (((size_t)TX * ty * ld * 8) + 127) & ~(size_t)127;
-    const size_t xb = m ? ((((size_t)TX * ty * ldx * 8) + 127) & ~(size_t)127) : 0;
+    const size_t stg = (((size_t)(TX + 2) * (ty + 2) * ldp * 8) + 127) & ~(size_t)127;
+    const size_t ob = (((size_t)TX * ty * ldp * 8) + 127) & ~(size_t)127;
+    const size_t xb = m ? ((((size_t)TX * ty * ldxp * 8) + 127) & ~(size_t)127) : 0;
     return 3 * stg + 3 * ob + 2 * xb + 128;
   };
   auto need4 = [&](int ty) {
-    const size_t stg = (((size_t)(TX + 2) * (ty + 2) * ld * 8) + 127) & ~(size_t)127;
-    const size_t ob = (((size_t)TX * ty * ld * 8) + 127) & ~(size_t)127;
-    const size_t xb = m ? ((((size_t)TX * ty * ldx * 8) + 127) & ~(size_t)127) : 0;
+    const size_t stg = (((size_t)(TX + 2) * (ty + 2) * ldp * 8) + 127) & ~(size_t)127;
+    const size_t ob = (((size_t)TX * ty * ldp * 8) + 127) & ~(size_t)127;
+    const size_t xb = m ? ((((size_t)TX * ty * ldxp * 8) + 127) & ~(size_t)127) : 0;
     return 4 * stg + 2 * ob + 2 * xb + 128;
+  };
+  auto need32 = [&](int ty) {   // the smallest ring: 3 planes, 2 output tiles
+    const size_t stg = (((size_t)(TX + 2) * (ty + 2) * ldp * 8) + 127) & ~(size_t)127;
+    const size_t ob = (((size_t)TX * ty * ldp * 8) + 127) & ~(size_t)127;
+    const size_t xb = m ? ((((size_t)TX * ty * ldxp * 8) + 127) & ~(size_t)127) : 0;
+    return 3 * stg + 2 * ob + 2 * xb + 128;
   };
   // 8 warps x GPW groups of 8 points per tile; the largest tile that keeps
   // two CTAs resident per SM (<= ~110 KB shared memory) wins
@@ -432,7 +458,7 @@ int sgram_plan(const double* in, double* out, int nx, int ny, int nz, int ld, co
     if (ty > ny) ty = ny;
     if (ty > 254) ty = 254;
     if (TX * ty > 64 * cand) continue;
-    if (need(ty) > 110 * 1024) continue;
+    if (need32(ty) > 110 * 1024) continue;
     gpw = cand;
     TY = ty;
     break;
@@ -446,16 +472,20 @@ int sgram_plan(const double* in, double* out, int nx, int ny, int nz, int ld, co
   G.ngroups = (G.npts + 7) / 8;
   const int tiles_y = (ny + TY - 1) / TY;
   const int tiles = g.tiles_x * tiles_y;
-  g.stage_bytes = (uint32_t)((TX + 2) * (TY + 2) * ld * 8);
+  g.stage_bytes = (uint32_t)((TX + 2) * (TY + 2) * ldp * 8);
   g.stage_stride = (g.stage_bytes + 127u) & ~127u;
-  g.out_stride = ((uint32_t)(TX * TY * ld * 8) + 127u) & ~127u;
-  G.x_bytes = m ? (uint32_t)(TX * TY * ldx * 8) : 0u;
+  g.out_stride = ((uint32_t)(TX * TY * ldp * 8) + 127u) & ~127u;
+  G.x_bytes = m ? (uint32_t)(TX * TY * ldxp * 8) : 0u;
   G.x_stride = (G.x_bytes + 127u) & ~127u;
-  size_t smem = need(TY);
+  size_t smem = need32(TY);
   p.nst = 3;
+  p.nob = 2;
   if (need4(TY) <= 110 * 1024) {
     p.nst = 4;
     smem = need4(TY);
+  } else if (need(TY) <= 110 * 1024) {
+    p.nob = 3;
+    smem = need(TY);
   }
   const int NI = (2 * ld + 7) / 8, NJ = (ld + 7) / 8;
   const size_t red = (size_t)8 * NI * NJ * 64 * 8;
@@ -480,18 +510,18 @@ int sgram_plan(const double* in, double* out, int nx, int ny, int nz, int ld, co
   g.has_hi = has_hi;
   g.scale = scale;
   P->nparts = (int)(p.grid.x * p.grid.y);
-  rc = encode_tmap_4d(&P->tin, in, ld, nx, ny, nz, ld, TX + 2, TY + 2, 1);
+  rc = encode_tmap_4d(&P->tin, in, ld, nx, ny, nz, ldp, TX + 2, TY + 2, 1);
   if (rc) return rc;
-  rc = encode_tmap_4d(&P->tout, out, ld, nx, ny, nz, ld, TX, TY, 1);
+  rc = encode_tmap_4d(&P->tout, out, ld, nx, ny, nz, ldp, TX, TY, 1);
   if (rc) return rc;
   if (m) {
-    rc = encode_tmap_4d(&P->txm, x, ldx, nx, ny, nz, ldx, TX, TY, 1);
+    rc = encode_tmap_4d(&P->txm, x, ldx, nx, ny, nz, ldxp, TX, TY, 1);
     if (rc) return rc;
   } else {
     P->txm = P->tout;   // never loaded
   }
   if (halo) {
-    rc = encode_tmap_4d(&P->thalo, halo, ld, nx, ny, 2, ld, TX + 2, TY + 2, 1);
+    rc = encode_tmap_4d(&P->thalo, halo, ld, nx, ny, 2, ldp, TX + 2, TY + 2, 1);
     if (rc) return rc;
   } else {
     P->thalo = P->tin;
