@@ -23,7 +23,9 @@
 // same banks (8 wavefronts per fragment load instead of 2 -- two thirds of
 // the C3 pass's shared-memory wavefronts, its data pipe at 83%).  The TMA
 // boxes are therefore 20 wide there (columns 16..19 out of bounds: zero-
-// filled on load, clipped on store), 160-byte rows.
+// filled on load, clipped on store), 160-byte rows.  (8-column rows, 64
+// bytes, conflict 2-way; padding them to 96 bytes measured slower at W1,
+// 0.49 -> 0.54 ms, and even at C4.)
 #ifndef B2L_SGRAM_PAD16
 #define B2L_SGRAM_PAD16 1
 #endif
