@@ -32,8 +32,11 @@
 __host__ __device__ constexpr int sgram_pitch(int ld) {
   return (ld == 16 && B2L_SGRAM_PAD16) ? 20 : ld;
 }
+// Off by default: the other point order changes the Gram's rounding, and the
+// golden 20^3 run (a chaotic degenerate-cluster endgame the tests hold to the
+// reference's own 180..197 iteration band) then ends at 199.
 #ifndef B2L_SGRAM_KSTRIDE
-#define B2L_SGRAM_KSTRIDE 1
+#define B2L_SGRAM_KSTRIDE 0
 #endif
 
 namespace b2l {
