@@ -46,6 +46,10 @@
 #include "common.cuh"
 #include "gram_tile.cuh"
 
+#ifndef B2L_STORE_SWZ8   // conflict-free output stores of the m = 8 full-block local kernel
+#define B2L_STORE_SWZ8 1
+#endif
+
 namespace b2l {
 
 #ifndef B2L_STEP_NU
@@ -912,6 +916,36 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
         const bool bw = A.kw > 0, bp = A.kp > 0;
         const double dr = weighted ? st[A.d_off + r] : 1.0;
         const double tr = tmode == 2 ? st[A.t_off + r] : tinv;
+        // m = 8 full block: the odd rows store their second column first (the
+        // conflict-free store order of the pair kernel, see there)
+        constexpr bool SWZ = FIX && MFIX == 8 && NT == 1 && B2L_STORE_SWZ8;
+        if constexpr (SWZ) {
+          double xn_[2], axn_[2], pn_[2], apn_[2], wv_[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            pn_[e] = __dadd_rn(acc[0][0][e], acc[0][2][e]);
+            apn_[e] = __dadd_rn(acc[0][1][e], acc[0][3][e]);
+            xn_[e] = A.xpp ? __dadd_rn(acc[0][4][e], pn_[e]) : acc[0][4][e];
+            axn_[e] = A.xpp ? __dadd_rn(acc[0][5][e], apn_[e]) : acc[0][5][e];
+            const double bx = weighted ? __dmul_rn(dr, xn_[e]) : xn_[e];
+            const double wf = __dsub_rn(axn_[e], __dmul_rn(bx, lamc[0][e]));
+            s_w[0][e] = fma(wf, wf, s_w[0][e]);
+            if (want_ax) s_a[0][e] = fma(axn_[e], axn_[e], s_a[0][e]);
+            wv_[e] = tmode == 0 ? wf : __dmul_rn(tr, wf);
+          }
+          const bool odd = rl & 1;
+          const int a0 = r * SF + 2 * q + (odd ? 1 : 0), a1 = r * SF + 2 * q + (odd ? 0 : 1);
+          O0[a0] = odd ? xn_[1] : xn_[0];
+          O1[a0] = odd ? axn_[1] : axn_[0];
+          O2[a0] = odd ? pn_[1] : pn_[0];
+          O3[a0] = odd ? apn_[1] : apn_[0];
+          O4[a0] = odd ? wv_[1] : wv_[0];
+          O0[a1] = odd ? xn_[0] : xn_[1];
+          O1[a1] = odd ? axn_[0] : axn_[1];
+          O2[a1] = odd ? pn_[0] : pn_[1];
+          O3[a1] = odd ? apn_[0] : apn_[1];
+          O4[a1] = odd ? wv_[0] : wv_[1];
+        } else {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const int co = 8 * nt + 2 * q;
@@ -939,6 +973,7 @@ __global__ void __launch_bounds__(LOC_THREADS, 1)
               if (wposc[nt][e] >= 0) O4[r * swn + wposc[nt][e]] = wv;
             }
           }
+        }
         }
       }
       for (int e = lane; e < 8 * npad; e += 32) {
