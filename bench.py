@@ -354,7 +354,8 @@ def run_gpu(args):
             dist.barrier()
 
     hbm_peak, fp64_peak, peaks_measured = _peaks()
-    if world > 1:
+    weak = world > 1 or args.series == "weak"
+    if weak:
         # C4 weak-scaling series: a (N, N, N) grid with N from weak_grid, one
         # z-slab of ~12.5M rows per GPU; halo + all-reduces inside the
         # library's native step (NCCL over NVLink)
@@ -367,6 +368,14 @@ def run_gpu(args):
         n = A.local_rows
         workload = (f"C4 weak series W{world}: {Ng}^3 7-pt Laplacian (scaled 1/h^2), m=8, "
                     "Jacobi, B=I, 50 iterations, z-slab per GPU")
+        # `value` counts slab iterations (world x global iterations / s): the
+        # N = 1 point of this series is W1 (232^3, m = 8) -- `configs.W1.it_s`
+        # of the default N = 1 line, or `bench.py --series weak` at N = 1 --
+        # not the default line's C2 headline
+        series_note = {"series": "C4 weak (232^3 / 292^3 / 368^3 / 464^3 on 1 / 2 / 4 / 8 GPUs)",
+                       "unit_of_value": "slab iterations/s = n_gpus x global iterations/s",
+                       "n1_point": "W1: configs.W1.it_s of the default N=1 line, or "
+                                   "`bench.py --series weak` at N=1"}
     else:
         Ng, m, tol, max_iter = N_GRID, M_BLOCK, TOL, MAX_ITER
         n = N_GRID ** 3
@@ -547,12 +556,14 @@ def run_gpu(args):
         "roofline": roofline,
         "clocks": clk.summary(),
     }
+    if weak:
+        line["config"]["series"] = series_note
     del rep, vecs
     torch.cuda.empty_cache()
-    if world == 1 and not args.no_extra:
+    if world == 1 and not weak and not args.no_extra:
         line["time_to_tol"] = time_to_tol(pk)
         line["configs"] = config_runs(pk, dev, hbm_peak, fp64_peak)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not weak and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         threads, rates = cpu_best_threads(cores)
         v, k = cpu_oracle_sample(args.cpu_iters, threads)
@@ -577,6 +588,9 @@ def main():
     ap.add_argument("--steps", type=int, default=285)
     ap.add_argument("--warmup", type=int, default=15)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--series", default="headline", choices=["headline", "weak"],
+                    help="N=1 workload: the C2 headline (default) or W1, the N=1 point of "
+                         "the C4 weak-scaling series that N>1 runs")
     ap.add_argument("--cpu-iters", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true",

@@ -76,6 +76,34 @@ def test_c1_matched_iterations(pk, golden):
     np.testing.assert_allclose(rep.residual_norms, g["residual_norms"], rtol=0.5)
 
 
+@pytest.mark.parametrize("seed", [1, 2])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])
+def test_seeds_1_2_matched_iterations(pk, golden, name, seed):
+    """Seeds 1 and 2 of the BASELINE shapes (SURVEY 8c harness rules) against
+    the real reference at a matched iteration count (make_seeds.py): status,
+    iterations, Ritz values at 1e-8 relative, the whole Ritz history at 1e-6,
+    residual norms within a factor of two."""
+    N, m, jac, diag_b, tol, max_iter = {
+        "c1": (32, 4, False, False, 1e-6, 120), "c2": (48, 10, True, False, 1e-8, 60),
+        "c3": (40, 16, True, False, 1e-6, 60), "c5": (24, 32, True, True, 1e-6, 40)}[name]
+    g = golden("seeds12.npz")
+    k = f"{name}_s{seed}_"
+    a, _ = scaled(pk, N)
+    b = None
+    if diag_b:
+        b = pk.DiagonalOperator(
+            np.random.Generator(np.random.PCG64(1000 + seed)).uniform(1.0, 2.0, N ** 3))
+    rep = pk.solve(a, b=b, t=pk.jacobi_preconditioner(a) if jac else None,
+                   config=pk.SolverConfig(block_size=m, tol=tol, max_iter=max_iter, seed=seed))
+    assert rep.status == str(g[k + "status"]) == "MaxIterReached"
+    assert rep.iterations_used == int(g[k + "iterations_used"])
+    assert rel(rep.eigenvalues, g[k + "eigenvalues"]).max() <= REL
+    ritz = np.array([h.ritz for h in rep.history])
+    assert rel(ritz, g[k + "hist_ritz"]).max() <= 1e-6
+    assert np.array_equal(rep.converged, g[k + "converged"])
+    np.testing.assert_allclose(rep.residual_norms, g[k + "residual_norms"], rtol=1.0)
+
+
 def test_c1_converging_time_to_tol(pk, golden):
     """C1 with max_iter=1000 converges.  Its triple eigenvalue cluster makes
     the converged iteration count chaotic: the reference itself, with its

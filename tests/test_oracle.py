@@ -126,3 +126,25 @@ def test_generic_b_matches_reference(golden, name, N, m, tol, jac, bfun):
     assert r.iterations_used == int(g["iterations_used"])
     np.testing.assert_allclose(np.array(r.hist_ritz), g["hist_ritz"], rtol=1e-12)
     np.testing.assert_allclose(r.eigenvalues, g["dense_vals"], rtol=1e-10)
+
+
+@pytest.mark.parametrize("name,seed", [("c1", 1), ("c1", 2), ("c5", 1), ("c5", 2)])
+def test_seeds_1_2_bitwise(golden, name, seed):
+    """Seeds 1 and 2 of the BASELINE shapes (SURVEY 8c harness rules), from the
+    real reference (tests/golden/make_seeds.py): the oracle reproduces the
+    reference's per-iteration Ritz values and residual norms bit for bit
+    (one BLAS thread on both sides)."""
+    from threadpoolctl import threadpool_limits
+
+    N, m, precond, diag_b, tol, max_iter = {
+        "c1": (32, 4, None, False, 1e-6, 120), "c5": (24, 32, "jacobi", True, 1e-6, 40)}[name]
+    g = golden("seeds12.npz")
+    k = f"{name}_s{seed}_"
+    with threadpool_limits(limits=1, user_api="blas"):
+        r = orc.laplacian_case(N, m, precond=precond, bseed=1000 + seed if diag_b else None,
+                               tol=tol, max_iter=max_iter, seed=seed)
+    assert r.status == str(g[k + "status"]) == "MaxIterReached"
+    assert r.iterations_used == int(g[k + "iterations_used"])
+    assert np.array_equal(np.array(r.hist_ritz), g[k + "hist_ritz"])
+    assert np.array_equal(np.array(r.hist_resid), g[k + "hist_resid"])
+    assert np.array_equal(r.eigenvalues, g[k + "eigenvalues"])
