@@ -60,6 +60,7 @@ __all__ = [
     "solve_staged",
     "device_options",
     "LOBPCGRun",
+    "project_pencil",
 ]
 
 PIVOT_FLOOR = 1e-8   # lobpcg.py:57
@@ -350,6 +351,48 @@ def b_orthonormalize(x, bx, pivot_floor=0.0):
         xo = dv.to_host(xo).copy()
         bxo = xo if shared else dv.to_host(bxo).copy()
     return xo, bxo, reff
+
+
+def project_pencil(lam, x, ax, w, aw, bw, pj, apj, bpj, bx, exact_diagonal=False):
+    """The projected pencil (gramA, gramB) on the basis [x, w, p]
+    (`_project_pencil`, lobpcg.py:299-340), upper-triangular blocks only, from
+    tall blocks on the GPU (K5 Grams; CUDA (n, k) tensors or host arrays).
+
+    The diagonal blocks are Lambda and identities by construction;
+    ``exact_diagonal=True`` computes them instead (lobpcg.py:317-321,
+    :334-336): the reference's cross-check of the B-orthonormality the solver
+    assumes.  The solver itself folds the orthonormalisation into its
+    coefficients and never calls this; it is the diagnostic twin of the
+    reference's private helper."""
+    from . import multivec as mv
+
+    lam = np.asarray(lam, dtype=np.float64)
+    m = int(x.shape[1])
+    nw = int(w.shape[1])
+    npj = 0 if pj is None else int(pj.shape[1])
+    dim = m + nw + npj
+    ga = np.zeros((dim, dim))
+    gb = np.zeros((dim, dim))
+    sx, sw, sp = slice(0, m), slice(m, m + nw), slice(m + nw, dim)
+    if exact_diagonal:
+        ga[sx, sx] = mv.gram(x, ax)
+        gb[sx, sx] = mv.gram(x, bx)
+        gb[sw, sw] = mv.gram(w, bw)
+    else:
+        ga[sx, sx] = np.diag(lam)
+        gb[sx, sx] = np.eye(m)
+        gb[sw, sw] = np.eye(nw)
+    ga[sw, sw] = mv.gram(w, aw)
+    ga[sx, sw] = mv.gram(x, aw)
+    gb[sx, sw] = mv.gram(x, bw)
+    if npj:
+        ga[sx, sp] = mv.gram(x, apj)
+        ga[sw, sp] = mv.gram(w, apj)
+        gb[sx, sp] = mv.gram(x, bpj)
+        gb[sw, sp] = mv.gram(w, bpj)
+        ga[sp, sp] = mv.gram(pj, apj)
+        gb[sp, sp] = mv.gram(pj, bpj) if exact_diagonal else np.eye(npj)
+    return ga, gb
 
 
 def apply_constraints(x, constraints, b=None):

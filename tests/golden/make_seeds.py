@@ -75,6 +75,30 @@ def main():
             print(name, seed, rep.status, rep.iterations_used, int(rep.converged.sum()),
                   f"{time.time() - t0:.1f}s", flush=True)
     np.savez_compressed(OUT / "seeds12.npz", **out)
+    pencil_fixture()
+
+
+def pencil_fixture():
+    """The reference's private `_project_pencil` (lobpcg.py:299-340) on seeded
+    random blocks, with and without exact_diagonal -> project_pencil.npz."""
+    from blockeig.lobpcg import _project_pencil
+
+    r = np.random.Generator(np.random.PCG64(77))
+    n, m, nw, npj = 501, 4, 3, 2
+    blocks = {k: r.standard_normal((n, c)) for k, c in
+              [("x", m), ("ax", m), ("bx", m), ("w", nw), ("aw", nw), ("bw", nw),
+               ("pj", npj), ("apj", npj), ("bpj", npj)]}
+    lam = r.uniform(1.0, 5.0, m)
+    out = dict(blocks, lam=lam)
+    for exact in (False, True):
+        ga, gb = _project_pencil(lam, blocks["x"], blocks["ax"], blocks["w"], blocks["aw"],
+                                 blocks["bw"], blocks["pj"], blocks["apj"], blocks["bpj"],
+                                 blocks["bx"], exact_diagonal=exact)
+        out[f"ga_{int(exact)}"], out[f"gb_{int(exact)}"] = ga, gb
+    ga, gb = _project_pencil(lam, blocks["x"], blocks["ax"], blocks["w"], blocks["aw"],
+                             blocks["bw"], None, None, None, blocks["bx"])
+    out["ga_nop"], out["gb_nop"] = ga, gb
+    np.savez_compressed(OUT / "project_pencil.npz", **out)
 
 
 if __name__ == "__main__":

@@ -129,3 +129,25 @@ def test_dense_oracle_spectrum(pk):
     np.testing.assert_allclose(vals, pk.exact_eigenvalues((4, 5, 3), 60), rtol=1e-12)
     with pytest.raises(ValueError):
         pk.dense_oracle_spectrum(pk.laplacian3d((10, 10, 10)))
+
+
+def test_project_pencil_matches_reference(pk, golden):
+    """project_pencil against the reference's private _project_pencil
+    (lobpcg.py:299-340) on the same blocks, with and without exact_diagonal
+    (SURVEY 8 f-4), host arrays and CUDA tensors."""
+    g = golden("project_pencil.npz")
+    names = ("x", "ax", "w", "aw", "bw", "pj", "apj", "bpj", "bx")
+    host = {k: g[k] for k in names}
+    dev = {k: torch.from_numpy(g[k]).cuda() for k in names}
+    for blocks in (host, dev):
+        args = [blocks[k] for k in names]
+        for exact in (False, True):
+            ga, gb = pk.project_pencil(g["lam"], *args, exact_diagonal=exact)
+            np.testing.assert_allclose(ga, g[f"ga_{int(exact)}"], rtol=1e-12, atol=1e-11)
+            np.testing.assert_allclose(gb, g[f"gb_{int(exact)}"], rtol=1e-12, atol=1e-11)
+        a2 = args[:5] + [None, None, None, args[8]]
+        ga, gb = pk.project_pencil(g["lam"], *a2)
+        np.testing.assert_allclose(ga, g["ga_nop"], rtol=1e-12, atol=1e-11)
+        np.testing.assert_allclose(gb, g["gb_nop"], rtol=1e-12, atol=1e-11)
+        # the lower-triangular blocks stay empty, as in the reference
+        assert np.all(ga[4:, :4] == 0.0) and np.all(gb[4:, :4] == 0.0)
