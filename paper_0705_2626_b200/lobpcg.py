@@ -61,6 +61,9 @@ __all__ = [
     "device_options",
     "LOBPCGRun",
     "project_pencil",
+    "Constraints",
+    "apply_constraints",
+    "b_orthonormalize",
 ]
 
 PIVOT_FLOOR = 1e-8   # lobpcg.py:57

@@ -38,7 +38,24 @@ __all__ = [
     "IdentityPreconditioner",
     "JacobiPreconditioner",
     "jacobi_preconditioner",
+    "probe_diagonal",
+    # the reference keeps its inner PCG in operators.py (:336-427); here it
+    # lives in pcg.py and is re-exported lazily (pcg imports this module)
+    "PCGBreakdown",
+    "pcg_solve",
+    "InnerPCGPreconditioner",
+    "inner_pcg_preconditioner",
 ]
+
+_PCG_NAMES = ("PCGBreakdown", "pcg_solve", "InnerPCGPreconditioner", "inner_pcg_preconditioner")
+
+
+def __getattr__(name):
+    if name in _PCG_NAMES:
+        from . import pcg
+
+        return getattr(pcg, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")
 
 
 def _default_device():
