@@ -441,7 +441,7 @@ def run_gpu(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     trace = os.environ.get("B2L_BENCH_TRACE") == "1"
     stamps = []
-    executed, restarts, repairs0 = 0, 0, run.drift_repairs
+    executed, restarts, repairs0, repairs_done = 0, 0, run.drift_repairs, 0
     windows = []
     with ClockSampler(local) as clk:
         e0.record()
@@ -450,7 +450,8 @@ def run_gpu(args):
                 # the run hit max_iter inside the window: a fresh run (its
                 # setup counted inside the timed region, never skipped)
                 windows.append([run_it0, run.it])
-                repairs0 -= run.drift_repairs
+                repairs_done += run.drift_repairs - repairs0
+                repairs0 = 0
                 run = new_run()
                 restarts += 1
                 run_it0 = run.it
@@ -461,7 +462,7 @@ def run_gpu(args):
         e1.record()
         torch.cuda.synchronize()
     windows.append([run_it0, run.it])
-    repairs = run.drift_repairs + repairs0
+    repairs = repairs_done + run.drift_repairs - repairs0
     if trace and len(stamps) > 1:
         dts = np.diff(stamps) * 1e3
         worst = np.argsort(dts)[::-1][:5]
