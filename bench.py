@@ -26,6 +26,9 @@ Multi-GPU (torchrun, N>1): the BASELINE C4 weak-scaling series (232^3 /
 292^3 / 368^3 / 464^3 on 1 / 2 / 4 / 8 GPUs, m=8, ~12.5M rows per GPU),
 z-slabs with the halo and both all-reduces inside the library's native step
 (NCCL); value = N x global it/s (slab-iterations/s), max-over-ranks time.
+--series weak runs that series at any N (W1 at N=1, its N=1 point);
+--series strong runs C3 (256^3, m=16; BASELINE's strong-scaling config) on N
+z-slabs, value = global it/s, "scaling": "strong".
 """
 
 from __future__ import annotations
@@ -67,9 +70,9 @@ def config_dict(n_gpus):
         "max_iter": MAX_ITER,
         "seed": SEED,
         "l2": "inputs larger than L2 (10 live 168 MB blocks per iteration >> 126 MB L2)",
-        "parallelism": (f"z-slab x{n_gpus} (C4 weak-scaling series, ~12.5M rows per GPU; "
-                        "NCCL halo under the interior stencil planes + one all-reduce per "
-                        "fused pass, inside the native step)") if n_gpus > 1 else "single GPU",
+        "parallelism": (f"z-slab x{n_gpus} (NCCL halo under the interior stencil planes + one "
+                        "all-reduce per fused pass, inside the native step)")
+        if n_gpus > 1 else "single GPU",
     }
 
 
@@ -379,8 +382,26 @@ def run_gpu(args):
             dist.barrier()
 
     hbm_peak, fp64_peak, peaks_measured = _peaks()
-    weak = world > 1 or args.series == "weak"
-    if weak:
+    strong = args.series == "strong"
+    weak = (world > 1 or args.series == "weak") and not strong
+    mult = 1 if strong else world   # strong: `value` counts global iterations
+    if strong:
+        # BASELINE configs[2], the strong-scaling config: C3 (256^3, m = 16,
+        # Jacobi, tol 1e-6, 300 iterations) on z-slabs of 256 / N planes
+        from paper_0705_2626_b200.distributed import SlabLaplacian3D, slab_initial_block
+
+        Ng, m, tol, max_iter = 256, 16, 1e-6, 300
+        s = float((Ng + 1) ** 2)
+        A = SlabLaplacian3D((Ng, Ng, Ng), scale=s)
+        x0 = slab_initial_block(A.grid, A.part, m, SEED)
+        n = A.local_rows
+        workload = (f"C3 strong scaling on {world} GPU(s): 256^3 7-pt Laplacian (scaled 1/h^2), "
+                    "m=16, Jacobi, B=I, tol 1e-6, max_iter 300, z-slab per GPU")
+        series_note = {"series": "C3 strong (256^3, m = 16 on 1 / 2 / 4 / 8 GPUs)",
+                       "unit_of_value": "global iterations/s",
+                       "n1_point": "`bench.py --series strong` at N=1 (configs.C3 of the "
+                                   "default N=1 line is the same workload)"}
+    elif weak:
         # C4 weak-scaling series: a (N, N, N) grid with N from weak_grid, one
         # z-slab of ~12.5M rows per GPU; halo + all-reduces inside the
         # library's native step (NCCL over NVLink)
@@ -476,7 +497,7 @@ def run_gpu(args):
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_all = float(t.item())
-    value = world * executed / (ms_all / 1e3)
+    value = mult * executed / (ms_all / 1e3)
 
     # ---- per-kernel durations (CUDA events on the launching stream)
     ktimes = {}
@@ -567,13 +588,14 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     it_used = rep.iterations_used
-    e2e_val = world * it_used / e2e_s
+    e2e_val = mult * it_used / e2e_s
     exact = pk.exact_eigenvalues(A.grid, m, scale=s)
 
     line = {
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_all / executed,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": dict(config_dict(world), workload=workload, grid=[Ng] * 3, block_size=m,
                        tol=tol, max_iter=max_iter,
@@ -589,10 +611,11 @@ def run_gpu(args):
         "roofline": roofline,
         "clocks": clk.summary(),
     }
-    if weak:
+    if weak or strong:
         line["config"]["series"] = series_note
     del rep, vecs
     torch.cuda.empty_cache()
+    weak = weak or strong   # neither series line carries the N=1 extras
     if world == 1 and not weak and not args.no_extra:
         line["time_to_tol"] = time_to_tol(pk)
         line["configs"] = config_runs(pk, dev, hbm_peak, fp64_peak)
@@ -621,9 +644,10 @@ def main():
     ap.add_argument("--steps", type=int, default=285)
     ap.add_argument("--warmup", type=int, default=15)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--series", default="headline", choices=["headline", "weak"],
-                    help="N=1 workload: the C2 headline (default) or W1, the N=1 point of "
-                         "the C4 weak-scaling series that N>1 runs")
+    ap.add_argument("--series", default="headline", choices=["headline", "weak", "strong"],
+                    help="headline: C2 at N=1, the C4 weak-scaling series at N>1 (default); "
+                         "weak: that series at any N (W1 at N=1); strong: C3 (256^3, m=16) on "
+                         "N z-slabs, the BASELINE strong-scaling config")
     ap.add_argument("--cpu-iters", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true",
