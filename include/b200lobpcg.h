@@ -229,16 +229,30 @@ int b2l_set_blas(void* dgemm);
 
 /*
  * Host, small dense: which form the next Rayleigh-Ritz calls of this thread
- * use.  1: the reference's own sequence (multivec.gen_sym_eig: two dtrtrs,
- * dsyevr on all pairs, dtrtrs) -- inside (near-)degenerate clusters its
- * eigenvector choice steers which Ritz column locks first, so this form
- * reproduces the reference's lock and fallback statistics; 0: the native
- * explicit-inverse congruence + tridiagonal QR (~45-55 us faster per C2
- * iteration; on C1 with its operator perturbed by 1..16 ulp it converges in
- * 10 of 32 runs where the reference converges in 26 of 31 and form 1 in 24
- * of 32); -1: default (1).  The environment B2L_RR_EIG=qr / =ref pins one.
+ * use for pencils up to 64 x 64.  0 / -1 (default): the native
+ * explicit-inverse congruence + tridiagonal QR, with the computed
+ * eigenvectors of numerically degenerate clusters aligned to the current Ritz
+ * vectors (b2l_set_rr_align); 1: the reference's own sequence
+ * (multivec.gen_sym_eig: two dtrtrs, dsyevr on all pairs, dtrtrs), ~50 us
+ * slower per C2 iteration.  Inside (near-)degenerate clusters the basis an
+ * eigensolver returns steers which Ritz column locks first: on C1 over 128
+ * perturbed problems the reference converges without a basis fallback 117
+ * times, form 1 97, the plain QR 39, the aligned QR 128.  The
+ * environment B2L_RR_EIG=qr / =ref pins one form.
  */
 int b2l_set_rr_reference(int on);
+
+/*
+ * Host, small dense: the absolute eigenvalue gap below which the native
+ * eigensolve of this thread treats wanted eigenvalues as one cluster and
+ * returns the cluster's basis closest to the current Ritz vectors (capped at
+ * pivot_floor * max|lambda|).  The solver sets its smallest lock threshold
+ * before every Rayleigh-Ritz call (lobpcg.py:429-437 thresholds): eigenvalues
+ * closer than the residual tolerance are not separated by the stopping
+ * criterion either;
+ * 0 (the initial value): no alignment, any valid basis.
+ */
+int b2l_set_rr_align(double abs_gap);
 
 /*
  * Host, small dense -- the Rayleigh-Ritz step of one iteration with the

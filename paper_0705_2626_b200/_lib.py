@@ -128,6 +128,7 @@ SIGNATURES = {
     "b2l_set_lapack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "b2l_set_blas": (C.c_int, [C.c_void_p]),
     "b2l_set_rr_reference": (C.c_int, [C.c_int]),
+    "b2l_set_rr_align": (C.c_int, [C.c_double]),
     "b2l_set_lapack_mrrr": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "b2l_rayleigh_ritz_begin": (C.c_int, [C.c_int, C.c_int, C.c_int, c_dp, C.c_int, c_ip, C.c_int,
                                           c_ip, C.c_double, C.POINTER(C.c_int)]),

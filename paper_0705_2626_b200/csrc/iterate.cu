@@ -24,6 +24,7 @@ int rr_begin_tls(int m, int kst, int have_p, const double* g1, int ldg1, const i
                  const int* sel, double pivot_floor, int* fallbacks_out);
 int rr_finish_tls(const double* g2, const double* lam, double* lam_out, double* coef_out,
                   int* pcols_out, int* kp_out, int* fallbacks_out);
+void rr_set_align(double abs_gap);
 int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx, const double* w,
                 const double* aw, int ldw, int kw, const double* p, const double* ap, int kp,
                 const int* pcols, const double* coef, double* xo, double* axo, double* po,
@@ -298,9 +299,11 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
     sync_main();
     return fail(-B2L_EINVAL, "fast_iteration: kst != |active|");
   }
+  double thr_min = INFINITY;
   for (int j = 0; j < m; ++j) {
     const double nrm = std::sqrt(sums[j]);
     const double thr = s->relative_tol ? s->tol * std::sqrt(sums[m + j]) : s->tol;
+    if (thr < thr_min) thr_min = thr;
     s->norms[j] = nrm;
     const bool lock = s->active[j] && nrm < thr;
     s->newly[j] = lock ? 1 : 0;
@@ -329,6 +332,10 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
   int* pcols = s->h_istage;
   int* wpos = s->h_istage + m;
   int kp = 0, fb = 0;
+  // eigenvalue gaps below the smallest lock threshold count as one cluster in
+  // the eigensolve (rr.cu: align_clusters): the stopping criterion does not
+  // separate such eigenvalues either; the Python driver sets the same value
+  rr_set_align(thr_min);
   int rc = rr_begin_tls(m, kst, s->have_p, G1, b, jact.data(), kj, sel.data(), s->pivot_floor,
                         &fb);
   mark(6);

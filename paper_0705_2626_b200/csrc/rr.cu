@@ -121,19 +121,18 @@ Mat transpose(const Mat& x) {
 // dimension of the pencil being solved, set by rr_begin; per host thread so
 // two threads' Rayleigh-Ritz steps never see each other's LAPACK choice
 thread_local int g_rr_dim = 0;
-// The pencil eigensolve: the reference's own sequence (two dtrtrs, dsyevr
-// on all pairs -- scipy.linalg.eigh's driver) whenever LAPACK is registered.
-// Inside (near-)degenerate clusters the eigenvectors an eigensolver returns
-// are one of many valid bases, and that choice steers which Ritz column
-// locks first: on C1 with its operator perturbed by 1..16 ulp (32 runs) the
-// reference converges 26/31 times, this sequence 21-23/32, the native
-// tridiagonal QR 10/32 (tools/c1_band32.py).  The native explicit-inverse
-// + QR form is ~45 us faster per C2 iteration.
-// Per host thread (b2l_set_rr_reference); B2L_RR_EIG=qr / =ref pin one form
-// for every call.  Switching to the reference form only near the lock
-// threshold does not recover its statistics (C1: 8/32 converged): the
-// cluster bases it picks shape the whole trajectory.
-thread_local int g_rr_ref = -1;   // -1: not set by the caller (reference form)
+// The pencil eigensolve.  Default (pencils up to 64 x 64): the native
+// explicit-inverse congruence + tridiagonal QR with the computed eigenvectors
+// of numerically degenerate clusters aligned to the current Ritz vectors
+// (align_clusters below).  b2l_set_rr_reference(1) / B2L_RR_EIG=ref: the
+// reference's own sequence (two dtrtrs, dsyevr on all pairs -- scipy's eigh
+// driver), ~50 us slower per C2 iteration.  Inside (near-)degenerate clusters
+// the basis an eigensolver returns steers which Ritz column locks first; on
+// C1 over 128 perturbed problems (tools/c1_band32.py 64): the reference
+// converges without a basis fallback 117 times, the dsyevr sequence here 97,
+// the plain QR 39, the aligned QR 128.  Above 64 x 64 (m >= 22) the LAPACK
+// sequence runs either way.
+thread_local int g_rr_ref = -1;   // -1: not set by the caller (native aligned QR)
 bool eig_lapack() {
   static const int forced = [] {
     const char* v = getenv("B2L_RR_EIG");
@@ -141,7 +140,7 @@ bool eig_lapack() {
   }();
   if (g_syevr == nullptr || g_trtrs == nullptr) return false;
   if (forced >= 0) return forced == 1;
-  return g_rr_ref != 0;
+  return g_rr_ref == 1;
 }
 
 bool use_lapack() {
@@ -465,6 +464,7 @@ Mat scaled_cholesky_inv(const Mat& g, double floor_) {
 // from here), and it only involves B-Gram blocks, so b2l_fast_iteration runs
 // it while the stencil pass that produces A W is still on the GPU.
 struct PencilFactor {
+  double floor_ = 1e-8;    // the pivot floor the factor was formed with
   Mat r;                   // upper Cholesky factor of gb
   std::vector<double> Ri;  // R^-1 row-major upper (native path)
   int d = 0;
@@ -472,6 +472,7 @@ struct PencilFactor {
 
 void pencil_factor(const Mat& gb, double floor_, PencilFactor& f) {
   f.d = gb.r;
+  f.floor_ = floor_ > 0.0 ? floor_ : 1e-8;
   f.r = cholesky(gb, floor_);
   RR_MARK(4);   // pencil Cholesky
   f.Ri.clear();
@@ -489,6 +490,105 @@ void pencil_factor(const Mat& gb, double floor_, PencilFactor& f) {
       for (int j = t; j < d; ++j) row[j] -= rit * rt[j];
     }
     for (int j = i + 1; j < d; ++j) row[j] *= inv;
+  }
+}
+
+
+// Cluster alignment of the native eigensolve.  Inside a cluster of wanted
+// eigenvalues that the Rayleigh-Ritz procedure cannot tell apart, every
+// orthonormal basis is a valid eigensolver output, and the choice steers the
+// iteration: a tridiagonal QR returns an arbitrary rotation of the cluster
+// each step (the Ritz columns of a degenerate group are re-mixed every
+// iteration, their residuals fall together and late, locked columns are
+// disturbed: C1 over 128 perturbed problems converges without a basis
+// fallback 39 times), LAPACK's MRRR (the reference's scipy eigh) stays close
+// to the identity on a nearly diagonal pencil (97 of 128 here, 117 in the
+// reference).  align_clusters makes that property explicit: the computed
+// eigenvectors of a cluster S are rotated to the basis closest to the current
+// Ritz vectors -- V[:, S] <- V[:, S] Q with V[S, S] Q symmetric positive
+// definite (Q = the transposed polar factor of V[S, S], Newton's iteration)
+// -- 128 of 128 converge, second lock by iteration 215 in 110 (reference
+// 107), quartiles 408 / 408 / 408 (reference 404 / 408 / 411).
+// A cluster: consecutive wanted eigenvalues whose gaps are below
+// min(pivot_floor * max|lambda|, g_align_abs): the reference's own floor for
+// numerical dependence in the basis (1e-8, lobpcg.py:57), and the run's
+// residual tolerance (set per call by the solver, b2l_set_rr_align) --
+// eigenvalues closer than the tolerance are not separated by the stopping
+// criterion either, and mixing them adds at most tol / 2 to a residual.  0 (the library default for direct callers): no alignment;
+// B2L_RR_ALIGN=<x> scales the solver's gap for A/B runs (0: off).
+thread_local double g_align_abs = 0.0;
+// B2L_RR_ALIGN=<x>: the solver's gap times x (A/B runs; 0 = off)
+const double g_align_mult = [] {
+  const char* v = getenv("B2L_RR_ALIGN");
+  return v ? atof(v) : 1.0;
+}();
+
+bool small_inverse(int s, const double* a, double* inv) {
+  double w[8 * 16];
+  for (int i = 0; i < s; ++i)
+    for (int j = 0; j < s; ++j) {
+      w[i * 2 * s + j] = a[i * s + j];
+      w[i * 2 * s + s + j] = i == j ? 1.0 : 0.0;
+    }
+  for (int c = 0; c < s; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < s; ++r)
+      if (std::fabs(w[r * 2 * s + c]) > std::fabs(w[piv * 2 * s + c])) piv = r;
+    if (!(std::fabs(w[piv * 2 * s + c]) > 1e-6)) return false;
+    if (piv != c)
+      for (int j = 0; j < 2 * s; ++j) std::swap(w[c * 2 * s + j], w[piv * 2 * s + j]);
+    const double d = 1.0 / w[c * 2 * s + c];
+    for (int j = 0; j < 2 * s; ++j) w[c * 2 * s + j] *= d;
+    for (int r = 0; r < s; ++r) {
+      if (r == c) continue;
+      const double f = w[r * 2 * s + c];
+      if (f != 0.0)
+        for (int j = 0; j < 2 * s; ++j) w[r * 2 * s + j] -= f * w[c * 2 * s + j];
+    }
+  }
+  for (int i = 0; i < s; ++i)
+    for (int j = 0; j < s; ++j) inv[i * s + j] = w[i * 2 * s + s + j];
+  return true;
+}
+
+// vecs: column w at vecs + w * d (d rows); vals ascending
+void align_clusters(int d, int want, const double* vals, double* vecs, double gap) {
+  int j0 = 0;
+  while (j0 < want) {
+    int j1 = j0 + 1;
+    while (j1 < want && vals[j1] - vals[j1 - 1] <= gap) ++j1;
+    const int s = j1 - j0;
+    if (s >= 2 && s <= 8) {
+      double y[64], yi[64];
+      for (int i = 0; i < s; ++i)
+        for (int j = 0; j < s; ++j) y[i * s + j] = vecs[(size_t)(j0 + j) * d + (j0 + i)];
+      bool ok = true;
+      for (int it = 0; it < 30 && ok; ++it) {
+        ok = small_inverse(s, y, yi);
+        if (!ok) break;
+        double delta = 0.0;
+        for (int i = 0; i < s; ++i)
+          for (int j = 0; j < s; ++j) {
+            const double nv = 0.5 * (y[i * s + j] + yi[j * s + i]);
+            delta = std::max(delta, std::fabs(nv - y[i * s + j]));
+            y[i * s + j] = nv;
+          }
+        if (delta < 1e-15) break;
+      }
+      if (ok) {
+        // y = polar factor U_p; Q = U_p^T: new column j = sum_i old column i * U_p(j, i)
+        std::vector<double> tmp((size_t)d * s);
+        for (int j = 0; j < s; ++j)
+          for (int r = 0; r < d; ++r) {
+            double acc = 0.0;
+            for (int i = 0; i < s; ++i) acc += vecs[(size_t)(j0 + i) * d + r] * y[j * s + i];
+            tmp[(size_t)j * d + r] = acc;
+          }
+        for (int j = 0; j < s; ++j)
+          for (int r = 0; r < d; ++r) vecs[(size_t)(j0 + j) * d + r] = tmp[(size_t)j * d + r];
+      }
+    }
+    j0 = j1;
   }
 }
 
@@ -552,6 +652,12 @@ void pencil_solve(const Mat& ga_in, const PencilFactor& f, int want, double* val
     RR_MARK(5);   // R^-T A R^-1
     if (d > 0 && symeig_tridiag_qr(d, M, want, vals_out, v_.data()) != 0) {
       throw LapackError{"tql2 (no convergence)", 1};
+    }
+    if (g_align_abs * g_align_mult > 0.0) {
+      double scale = 0.0;
+      for (int j = 0; j < want; ++j) scale = std::max(scale, std::fabs(vals_out[j]));
+      align_clusters(d, want, vals_out, v_.data(),
+                     std::min(f.floor_ * scale, g_align_abs * g_align_mult));
     }
     RR_MARK(6);   // symmetric eigensolve
     // C = R^-1 V
@@ -646,6 +752,15 @@ extern "C" int b2l_set_lapack_mrrr(void* dsytrd, void* dstemr, void* dormtr) {
   g_ormtr = reinterpret_cast<ormtr_t*>(dormtr);
   return 0;
 }
+
+extern "C" int b2l_set_rr_align(double abs_gap) {
+  g_align_abs = abs_gap > 0.0 ? abs_gap : 0.0;
+  return 0;
+}
+
+namespace b2l {
+void rr_set_align(double abs_gap) { g_align_abs = abs_gap > 0.0 ? abs_gap : 0.0; }
+}  // namespace b2l
 
 extern "C" int b2l_set_rr_reference(int on) {
   g_rr_ref = on < 0 ? -1 : (on ? 1 : 0);

@@ -203,6 +203,10 @@ class NativeRitz:
         self.pcols = np.zeros(m, dtype=np.int32)
         self._kp = C.c_int()
         self._fb = C.c_int()
+        # absolute eigenvalue gap of a numerically degenerate cluster
+        # (b2l_set_rr_align): the solver sets its smallest lock threshold
+        # before each step; 0 = no alignment
+        self.align = 0.0
 
     def _scope(self):
         return _one_blas_thread() if self.m >= _BLAS_LIMIT_M else _NoLimit()
@@ -216,6 +220,7 @@ class NativeRitz:
         jact = np.ascontiguousarray(jact, dtype=np.int32)
         sel = np.ascontiguousarray(sel, dtype=np.int32)
         dp, ip = L.c_dp, L.c_ip
+        lib.b2l_set_rr_align(float(self.align))
         with self._scope():
             rc = lib.b2l_rayleigh_ritz(
                 m, kst, int(have_p), g1.ctypes.data_as(dp), g1.shape[1], g2.ctypes.data_as(dp),
@@ -257,6 +262,7 @@ class NativeRitz:
         g2 = np.ascontiguousarray(g2, dtype=np.float64)
         lam = np.ascontiguousarray(lam, dtype=np.float64)
         dp, ip = L.c_dp, L.c_ip
+        lib.b2l_set_rr_align(float(self.align))
         with self._scope():
             rc = lib.b2l_rayleigh_ritz_finish(
                 g2.ctypes.data_as(dp), lam.ctypes.data_as(dp), self.lam.ctypes.data_as(dp),
