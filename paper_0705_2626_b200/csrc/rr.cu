@@ -575,6 +575,14 @@ void align_clusters(int d, int want, const double* vals, double* vecs, double ga
           }
         if (delta < 1e-15) break;
       }
+      // the rotation must be orthogonal to rounding (Newton stalls on a
+      // nearly singular block: then the cluster keeps the solver's basis)
+      for (int i = 0; i < s && ok; ++i)
+        for (int j = 0; j < s && ok; ++j) {
+          double dot = 0.0;
+          for (int k = 0; k < s; ++k) dot += y[k * s + i] * y[k * s + j];
+          if (std::fabs(dot - (i == j ? 1.0 : 0.0)) > 1e-13) ok = false;
+        }
       if (ok) {
         // y = polar factor U_p; Q = U_p^T: new column j = sum_i old column i * U_p(j, i)
         std::vector<double> tmp((size_t)d * s);

@@ -433,9 +433,10 @@ def test_c1_outcome_distribution_matches_reference(pk, golden):
     kernel's scale epilogue rounds the same single product s * L(v)), and
     the outcome distributions must agree: how many runs converge (the rest
     end in BasisFallback), how many lock their second column by iteration
-    215, and the median iteration count.  (The native tridiagonal-QR
-    Rayleigh-Ritz form, B2L_RR_EIG=qr, fails this: 10 of 32 converge against
-    the reference's 26 of 31 -- DESIGN.md.)"""
+    215, and the median iteration count.  (A plain tridiagonal QR in the
+    Rayleigh-Ritz step, B2L_RR_ALIGN=0, fails this: 10 of 32 converge against
+    the reference's 27 -- DESIGN.md; the default aligned QR gives 32 / 31, the
+    dsyevr sequence 24 / 15-19.)"""
     band = golden("c1_band32.npz")
     N = 32
     base = float((N + 1) ** 2)
@@ -451,7 +452,7 @@ def test_c1_outcome_distribution_matches_reference(pk, golden):
     ref_early = int(sum(sorted(l)[1] <= 215 for l in band["lock_iterations"]))
     n = len(its)
     # two independent binomials over 32 runs at p ~ 0.8 / 0.7: the sd of their
-    # difference is ~3.2 / ~3.7 runs; hold both to 3 sd (the QR form's 10 vs
+    # difference is ~3.2 / ~3.7 runs; hold both to 3 sd (the plain QR's 10 vs
     # 27 converged is 5 sd away)
     assert abs(conv - ref_conv) <= 10, (conv, ref_conv, n)
     assert abs(early - ref_early) <= 11, (early, ref_early, n)
@@ -464,13 +465,11 @@ def test_c1_outcome_distribution_128_runs(pk, golden):
     their second column by iteration 215, median 408 iterations, quartiles
     404 / 411).  Every run must reach the tolerance on all four pairs; the
     GPU's median iteration count must sit on the reference's, and the share
-    of runs that never need a basis fallback must stay in the class of the
-    reference-form Rayleigh-Ritz (measured: 97 of 128 with dsyevr, 93 with
-    the MRRR stages, 39 with the tridiagonal QR form).  The remaining gap to
-    the reference (97 vs 117 converged without a fallback, 68 vs 107 early
-    second locks) is 3-5 sd: the GPU path forms the Grams of the
-    orthonormalised blocks as R^-T G R^-1 instead of recomputing them, so
-    the pencil's noise differs in structure -- DESIGN.md records it."""
+    of runs that never need a basis fallback and of early second locks must
+    stay in the reference's class (measured: 128 / 110 with the default
+    aligned-QR Rayleigh-Ritz step, 97 / 68 with the dsyevr sequence, 93 / 61
+    with the MRRR stages, 39 / 17 with a plain tridiagonal QR).  What the
+    alignment is and why it matters: DESIGN.md."""
     band = golden("c1_band128.npz")
     N = 32
     base = float((N + 1) ** 2)
@@ -488,5 +487,5 @@ def test_c1_outcome_distribution_128_runs(pk, golden):
         early += sorted(rep.lock_iterations)[1] <= 215
     ref_its = np.asarray(band["iterations"])
     assert abs(np.median(its) - np.median(ref_its)) <= 0.03 * np.median(ref_its), np.median(its)
-    assert conv >= 77, (conv, "reference 117 of 128; QR form 39")
-    assert early >= 40, (early, "reference 107 of 128; QR form 17")
+    assert conv >= 97, (conv, "reference 117 of 128; dsyevr sequence 97; plain QR 39")
+    assert early >= 68, (early, "reference 107 of 128; dsyevr sequence 68; plain QR 17")

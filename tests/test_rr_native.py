@@ -221,3 +221,59 @@ def test_large_pencil_rr_is_host_thread_independent(tmp_path):
     ref = np.load(out)
     for a, b in zip(got[:3], (ref["lam"], ref["coef"], ref["pcols"])):
         assert np.array_equal(a, b)
+
+
+def test_cluster_alignment_picks_the_basis_closest_to_x():
+    """A wanted triple eigenvalue: with a cluster gap set (b2l_set_rr_align,
+    what the solver does every step) the eigensolve returns the cluster's
+    basis closest to the current Ritz vectors -- the X block of the cluster's
+    coefficients is symmetric positive definite -- and it is the same
+    invariant subspace, the same Ritz values and as B-orthonormal as the
+    unaligned answer (any basis of the cluster is a valid eigensolver
+    output)."""
+    n, m = 80, 5
+    r = np.random.default_rng(11)
+    ev = np.concatenate([[1.0, 2.0, 2.0, 2.0, 3.0], np.linspace(4.0, 9.0, n - 5)])
+    A = np.diag(ev)
+    # Ritz vectors close to e_1..e_5 with the triple rotated inside its span
+    q, _ = np.linalg.qr(r.standard_normal((3, 3)))
+    X = np.eye(n)[:, :m].copy()
+    X[:, 1:4] = X[:, 1:4] @ q
+    X += 1e-6 * r.standard_normal((n, m))
+    X, _ = np.linalg.qr(X)
+    th, V = np.linalg.eigh(X.T @ A @ X)
+    X, lam = X @ V, th
+    W = (A @ X - X * lam)                       # residuals
+    P = 1e-3 * r.standard_normal((n, m))
+    G1 = np.hstack([X, W, P]).T @ np.hstack([X, W, P, A @ P])
+    G2 = np.hstack([X, W]).T @ (A @ W)
+    J = np.arange(m)
+    out = {}
+    for gap in (0.0, 1e-5):
+        nat = NativeRitz(m)
+        nat.align = gap
+        lam_n, coef, pcols, fb = nat(m, m, True, G1, G2, lam, J, J.copy(), FLOOR)
+        kp = pcols.size
+        cx = coef[:m * m].reshape(m, m)
+        cw = coef[m * m:2 * m * m].reshape(m, m)
+        cp = coef[2 * m * m:].reshape(kp, m)
+        Xn = X @ cx + W @ cw + P[:, pcols] @ cp
+        np.testing.assert_allclose(Xn.T @ Xn, np.eye(m), atol=1e-10)
+        out[gap] = (lam_n, cx, Xn)
+    (l0, c0, x0), (l1, c1, x1) = out[0.0], out[1e-5]
+    np.testing.assert_allclose(l0, l1, rtol=1e-13)
+    assert l1[3] - l1[1] < 1e-9                       # inside the gap and the 1e-8 relative cap
+    s = slice(1, 4)
+    # same invariant subspace of the cluster, same vectors outside it
+    np.testing.assert_allclose(x0[:, s] @ x0[:, s].T, x1[:, s] @ x1[:, s].T, atol=1e-9)
+    for j in (0, 4):
+        np.testing.assert_allclose(np.abs(x0[:, j] @ x1[:, j]), 1.0, atol=1e-12)
+    g = c1[s, s]
+    # aligned: symmetric (in the orthonormalised basis exactly; the folded
+    # coefficients of the raw blocks carry the W / P couplings, ~1e-7 here) ...
+    np.testing.assert_allclose(g, g.T, atol=1e-6)
+    assert np.linalg.eigvalsh(0.5 * (g + g.T)).min() > 0.5   # ... positive definite, near I
+    # and it is the closest basis: no rotation of the cluster brings the X block nearer to I
+    u, _, vt = np.linalg.svd(c0[s, s])
+    best = c0[:, s] @ (vt.T @ u.T)                   # polar alignment of the unaligned answer
+    np.testing.assert_allclose(best[s], g, atol=1e-6)
