@@ -10,8 +10,13 @@ pivot (the first numerically dependent column), which drives the basis-repair
 ladder of lobpcg.py:182-200 and :501-519.  dpotrf computes the same factor;
 the first pivot that is non-positive, non-finite or below the relative floor
 is recovered from its diagonal (pivot_j = R_jj^2 vs floor * G_jj), so the
-NotSPD(pivot) contract is unchanged.  The symmetric eigensolver is dsyevr,
-the driver scipy.linalg.eigh (the reference's call) uses.
+NotSPD(pivot) contract is unchanged.  The symmetric eigensolver of these
+helpers (multivec API, drift repair, exit refresh) is dsyevr, the driver
+scipy.linalg.eigh (the reference's call) uses.  The per-iteration
+Rayleigh-Ritz step itself runs in the library (NativeRitz ->
+b2l_rayleigh_ritz, csrc/rr.cu): native congruence + tridiagonal QR with the
+eigenvectors of numerically degenerate clusters aligned to the current Ritz
+vectors, LAPACK above a 64 x 64 pencil.
 """
 
 from __future__ import annotations
