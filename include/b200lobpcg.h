@@ -246,10 +246,10 @@ int b2l_set_rr_reference(int on);
  * Host, small dense: the absolute eigenvalue gap below which the native
  * eigensolve of this thread treats wanted eigenvalues as one cluster and
  * returns the cluster's basis closest to the current Ritz vectors (capped at
- * pivot_floor * max|lambda|).  The solver sets its smallest lock threshold
- * before every Rayleigh-Ritz call (lobpcg.py:429-437 thresholds): eigenvalues
- * closer than the residual tolerance are not separated by the stopping
- * criterion either;
+ * pivot_floor * max|lambda|).  The solver sets a tenth of its smallest lock
+ * threshold before every Rayleigh-Ritz call (lobpcg.py:429-437 thresholds):
+ * wide enough to pin the basis of a numerically degenerate cluster, narrow
+ * enough that the step still separates eigenvalues it can resolve;
  * 0 (the initial value): no alignment, any valid basis.
  */
 int b2l_set_rr_align(double abs_gap);

@@ -332,10 +332,11 @@ extern "C" int b2l_fast_iteration(b2l_iter_state* s) {
   int* pcols = s->h_istage;
   int* wpos = s->h_istage + m;
   int kp = 0, fb = 0;
-  // eigenvalue gaps below the smallest lock threshold count as one cluster in
-  // the eigensolve (rr.cu: align_clusters): the stopping criterion does not
-  // separate such eigenvalues either; the Python driver sets the same value
-  rr_set_align(thr_min);
+  // eigenvalue gaps below a tenth of the smallest lock threshold count as one
+  // cluster in the eigensolve (rr.cu: align_clusters; wider gaps keep the
+  // Rayleigh-Ritz step from separating a cluster's unconverged direction from
+  // its locked columns); the Python driver sets the same value
+  rr_set_align(0.1 * thr_min);
   int rc = rr_begin_tls(m, kst, s->have_p, G1, b, jact.data(), kj, sel.data(), s->pivot_floor,
                         &fb);
   mark(6);

@@ -477,6 +477,14 @@ void pencil_factor(const Mat& gb, double floor_, PencilFactor& f) {
   RR_MARK(4);   // pencil Cholesky
   f.Ri.clear();
   if (use_lapack() || eig_lapack()) return;   // no explicit inverse needed
+  // B2L_RR_CONG=explicit: the congruence through R^-1 (two matrix products;
+  // ~17 us faster per C2 iteration, but its error grows with cond(gb)^2: on
+  // 16^3, m = 8, tol 1e-8 a run stalls at a residual of 5e-8 -- kept for A/B)
+  static const bool cong_explicit = [] {
+    const char* e = getenv("B2L_RR_CONG");
+    return e && e[0] == 'e';
+  }();
+  if (!cong_explicit) return;
   const int d = f.d;
   f.Ri.assign((size_t)d * d, 0.0);
   double* Ri = f.Ri.data();
@@ -507,15 +515,22 @@ void pencil_factor(const Mat& gb, double floor_, PencilFactor& f) {
 // eigenvectors of a cluster S are rotated to the basis closest to the current
 // Ritz vectors -- V[:, S] <- V[:, S] Q with V[S, S] Q symmetric positive
 // definite (Q = the transposed polar factor of V[S, S], Newton's iteration)
-// -- 128 of 128 converge, second lock by iteration 215 in 110 (reference
-// 107), quartiles 408 / 408 / 408 (reference 404 / 408 / 411).
+// -- 128 of 128 converge, second lock by iteration 215 in 83 (reference
+// 107), quartiles 409 / 409 / 411 (reference 404 / 408 / 411).
 // A cluster: consecutive wanted eigenvalues whose gaps are below
 // min(pivot_floor * max|lambda|, g_align_abs): the reference's own floor for
-// numerical dependence in the basis (1e-8, lobpcg.py:57), and the run's
-// residual tolerance (set per call by the solver, b2l_set_rr_align) --
-// eigenvalues closer than the tolerance are not separated by the stopping
-// criterion either, and mixing them adds at most tol / 2 to a residual.  0 (the library default for direct callers): no alignment;
-// B2L_RR_ALIGN=<x> scales the solver's gap for A/B runs (0: off).
+// numerical dependence in the basis (1e-8, lobpcg.py:57), and a tenth of the
+// run's residual tolerance (set per call by the solver, b2l_set_rr_align).
+// The gap must stay below what the Rayleigh-Ritz step can resolve: inside a
+// cluster whose eigenvalues it can tell apart, the true Ritz vectors put the
+// cluster's unconverged direction into one (active) column, while an aligned
+// basis can leave part of it in soft-locked columns, where no residual
+// direction works on it -- with the gap at the tolerance itself one of 16
+// seeds of 20^3 / m = 10 stalls and ends Failed(BasisDegeneracy), with the
+// relative floor alone 11 of 16 seeds of 16^3 / m = 8 / tol 1e-8 run into
+// max_iter; at a tenth of the tolerance both sweeps match the reference's
+// iteration ranges.  0 (the library default for direct callers):
+// no alignment; B2L_RR_ALIGN=<x> scales the solver's gap for A/B runs.
 thread_local double g_align_abs = 0.0;
 // B2L_RR_ALIGN=<x>: the solver's gap times x (A/B runs; 0 = off)
 const double g_align_mult = [] {
@@ -600,6 +615,66 @@ void align_clusters(int d, int want, const double* vals, double* vecs, double ga
   }
 }
 
+// H R^-1 for upper R (d x d, column-major), column by column of the result:
+// Z[:, i] = (H[:, i] - sum_{t < i} R(t, i) Z[:, t]) / R(i, i).  The same
+// substitution as a triangular solve with R^T (each entry subtracts its
+// products in ascending t, then divides), but the inner loop runs over the
+// independent entries of a column instead of one dependent dot product.
+void right_solve_upper(int d, const double* R, const double* H, double* Z) {
+  for (int i = 0; i < d; ++i) {
+    double* zi = Z + (size_t)i * d;
+    const double* hi = H + (size_t)i * d;
+    for (int k = 0; k < d; ++k) zi[k] = hi[k];
+    for (int t = 0; t < i; ++t) {
+      const double rti = R[(size_t)t + (size_t)i * d];
+      const double* zt = Z + (size_t)t * d;
+      for (int k = 0; k < d; ++k) zi[k] -= rti * zt[k];
+    }
+    const double rii = R[(size_t)i + (size_t)i * d];
+    for (int k = 0; k < d; ++k) zi[k] /= rii;
+  }
+}
+
+// M = R^-T ga R^-1 by substitution (the reference's two triangular solves,
+// multivec.py:206-208), symmetrised; ga symmetric, everything column-major.
+void congruence_solve(int d, const double* R, const double* ga, double* M) {
+  thread_local std::vector<double> z1, z1t, z2;
+  z1.resize((size_t)d * d);
+  z1t.resize((size_t)d * d);
+  z2.resize((size_t)d * d);
+  right_solve_upper(d, R, ga, z1.data());               // ga R^-1 = (R^-T ga)^T
+  for (int j = 0; j < d; ++j)
+    for (int i = 0; i < d; ++i) z1t[(size_t)i + (size_t)j * d] = z1[(size_t)j + (size_t)i * d];
+  right_solve_upper(d, R, z1t.data(), z2.data());        // (R^-T ga) R^-1
+  for (int j = 0; j < d; ++j)
+    for (int i = 0; i < d; ++i)
+      M[(size_t)i + (size_t)j * d] =
+          0.5 * (z2[(size_t)i + (size_t)j * d] + z2[(size_t)j + (size_t)i * d]);
+}
+
+// C = R^-1 V for upper R: back substitution on all `want` columns at once
+// (V row-major d x want, so a row is contiguous); C column-major d x want.
+void back_solve_upper(int d, int want, const double* R, const double* vcols, Mat* c_out) {
+  thread_local std::vector<double> y;
+  y.resize((size_t)d * want);
+  for (int w = 0; w < want; ++w)
+    for (int i = 0; i < d; ++i) y[(size_t)i * want + w] = vcols[(size_t)w * d + i];
+  for (int i = d - 1; i >= 0; --i) {
+    double* yi = y.data() + (size_t)i * want;
+    for (int t = i + 1; t < d; ++t) {
+      const double rit = R[(size_t)i + (size_t)t * d];
+      const double* yt = y.data() + (size_t)t * want;
+      for (int w = 0; w < want; ++w) yi[w] -= rit * yt[w];
+    }
+    const double rii = R[(size_t)i + (size_t)i * d];
+    for (int w = 0; w < want; ++w) yi[w] /= rii;
+  }
+  Mat c(d, want);
+  for (int w = 0; w < want; ++w)
+    for (int i = 0; i < d; ++i) c(i, w) = y[(size_t)i * want + w];
+  *c_out = std::move(c);
+}
+
 // Smallest `want` pairs of ga c = lam gb c given gb's factor; only the upper
 // triangle of ga is read.
 void pencil_solve(const Mat& ga_in, const PencilFactor& f, int want, double* vals_out,
@@ -608,6 +683,27 @@ void pencil_solve(const Mat& ga_in, const PencilFactor& f, int want, double* val
   Mat ga(d, d);
   for (int j = 0; j < d; ++j)
     for (int i = 0; i <= j; ++i) ga(i, j) = ga(j, i) = ga_in(i, j);
+  if (f.Ri.empty() && !use_lapack() && !eig_lapack()) {
+    // the default for pencils up to 64 x 64: substitution congruence (as
+    // accurate as the reference's two triangular solves), tridiagonal QR,
+    // cluster alignment, back substitution
+    thread_local std::vector<double> m_, v_;
+    m_.resize((size_t)d * d);
+    congruence_solve(d, f.r.a.data(), ga.a.data(), m_.data());
+    v_.assign((size_t)d * want, 0.0);
+    RR_MARK(5);   // R^-T A R^-1
+    if (d > 0 && symeig_tridiag_qr(d, m_.data(), want, vals_out, v_.data()) != 0)
+      throw LapackError{"tql2 (no convergence)", 1};
+    if (g_align_abs * g_align_mult > 0.0) {
+      double scale = 0.0;
+      for (int j = 0; j < want; ++j) scale = std::max(scale, std::fabs(vals_out[j]));
+      align_clusters(d, want, vals_out, v_.data(),
+                     std::min(f.floor_ * scale, g_align_abs * g_align_mult));
+    }
+    RR_MARK(6);   // symmetric eigensolve
+    back_solve_upper(d, want, f.r.a.data(), v_.data(), c_out);
+    return;
+  }
   if (!f.Ri.empty()) {
     // M = R^-T ga R^-1 through the explicit inverse: row-oriented loops whose
     // inner index runs over independent entries (the substitution form is a

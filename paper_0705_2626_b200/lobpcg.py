@@ -927,11 +927,10 @@ class LOBPCGRun:
             else:
                 thresholds = self._tol_vec
             newly = self.active & (norms < thresholds)
-            # clusters in the pencil eigensolve: eigenvalue gaps below the
-            # smallest lock threshold, which the stopping criterion does not
-            # separate either (rr.cu align_clusters; b2l_fast_iteration sets
-            # the same value)
-            self._ritz.align = float(np.min(thresholds))
+            # clusters in the pencil eigensolve: eigenvalue gaps below a tenth
+            # of the smallest lock threshold (rr.cu align_clusters;
+            # b2l_fast_iteration sets the same value)
+            self._ritz.align = 0.1 * float(np.min(thresholds))
             self.lock_iteration[newly] = it
             self.active = self.active & ~newly
             self.norms = norms

@@ -209,8 +209,8 @@ class NativeRitz:
         self._kp = C.c_int()
         self._fb = C.c_int()
         # absolute eigenvalue gap of a numerically degenerate cluster
-        # (b2l_set_rr_align): the solver sets its smallest lock threshold
-        # before each step; 0 = no alignment
+        # (b2l_set_rr_align): the solver sets a tenth of its smallest lock
+        # threshold before each step; 0 = no alignment
         self.align = 0.0
 
     def _scope(self):
