@@ -435,7 +435,7 @@ def test_c1_outcome_distribution_matches_reference(pk, golden):
     end in BasisFallback), how many lock their second column by iteration
     215, and the median iteration count.  (A plain tridiagonal QR in the
     Rayleigh-Ritz step, B2L_RR_ALIGN=0, fails this: 10 of 32 converge against
-    the reference's 27 -- DESIGN.md; the default aligned QR gives 32 / 31, the
+    the reference's 27 -- DESIGN.md; the default aligned QR gives 32 / 22, the
     dsyevr sequence 24 / 15-19.)"""
     band = golden("c1_band32.npz")
     N = 32
@@ -466,7 +466,7 @@ def test_c1_outcome_distribution_128_runs(pk, golden):
     404 / 411).  Every run must reach the tolerance on all four pairs; the
     GPU's median iteration count must sit on the reference's, and the share
     of runs that never need a basis fallback and of early second locks must
-    stay in the reference's class (measured: 128 / 110 with the default
+    stay in the reference's class (measured: 128 / 83 with the default
     aligned-QR Rayleigh-Ritz step, 97 / 68 with the dsyevr sequence, 93 / 61
     with the MRRR stages, 39 / 17 with a plain tridiagonal QR).  What the
     alignment is and why it matters: DESIGN.md."""
