@@ -230,7 +230,7 @@ int b2l_set_blas(void* dgemm);
 /*
  * Host, small dense: which form the next Rayleigh-Ritz calls of this thread
  * use for pencils up to 64 x 64.  0 / -1 (default): the native
- * explicit-inverse congruence + tridiagonal QR, with the computed
+ * substitution congruence + tridiagonal QR, with the computed
  * eigenvectors of numerically degenerate clusters aligned to the current Ritz
  * vectors (b2l_set_rr_align); 1: the reference's own sequence
  * (multivec.gen_sym_eig: two dtrtrs, dsyevr on all pairs, dtrtrs), ~50 us

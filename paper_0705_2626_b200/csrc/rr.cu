@@ -122,7 +122,7 @@ Mat transpose(const Mat& x) {
 // two threads' Rayleigh-Ritz steps never see each other's LAPACK choice
 thread_local int g_rr_dim = 0;
 // The pencil eigensolve.  Default (pencils up to 64 x 64): the native
-// explicit-inverse congruence + tridiagonal QR with the computed eigenvectors
+// substitution congruence + tridiagonal QR with the computed eigenvectors
 // of numerically degenerate clusters aligned to the current Ritz vectors
 // (align_clusters below).  b2l_set_rr_reference(1) / B2L_RR_EIG=ref: the
 // reference's own sequence (two dtrtrs, dsyevr on all pairs -- scipy's eigh
@@ -781,8 +781,8 @@ void pencil_solve(const Mat& ga_in, const PencilFactor& f, int want, double* val
   // the reference's sequence (multivec.gen_sym_eig, multivec.py:174-211):
   // M = R^-T ga R^-1 by two triangular solves (dtrtrs), symmetrised, eigh
   // (dsyevr, all pairs), C = R^-1 V -- used for every pencil size when the
-  // eigensolve is dsyevr (the explicit-inverse / native-QR form above is the
-  // B2L_RR_EIG=qr speed option)
+  // eigensolve is dsyevr (B2L_RR_EIG=ref, or a pencil above 64 x 64; the
+  // native forms above are the default below that size)
   const bool fl = eig_lapack();
   const Mat& r = f.r;
   Mat t = trsolve(r, ga, true, fl);
