@@ -443,8 +443,14 @@ def run_gpu(args):
 
     gc.collect()
     gc.freeze()
+    # a throw-away run through its first drift repairs (iterations 12 and 13
+    # at C2): the one-time host costs of that path (kernel attributes, tensor
+    # maps and workspace of the drift Gram, LAPACK's first call) are paid
+    # before the timed region, like every other first call
     tmp = new_run()
-    tmp.step()
+    for _ in range(16):
+        if not tmp.step():
+            break
     del tmp
     torch.cuda.synchronize()
     run = new_run()
