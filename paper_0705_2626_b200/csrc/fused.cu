@@ -1966,6 +1966,13 @@ int lobpcg_step(int nrows, int m, const double* x, const double* ax, int ldx,
   } else if (red2 <= (size_t)A.nst * A.stage_doubles) {
     A.gred_off = 0;
     off += (int)red1;
+  } else if (pair) {
+    // narrow stages (few active columns and no P: the ring is smaller than
+    // the Gram scratch): the pair kernel's column-norm partials and Gram
+    // partials are live together, so they get disjoint regions
+    const int r1 = (int)((red1 + 15) & ~(size_t)15);
+    A.gred_off = A.red_off + r1;
+    off += r1 + (int)red2;
   } else {
     A.gred_off = A.red_off;
     off += (int)(red1 > red2 ? red1 : red2);
