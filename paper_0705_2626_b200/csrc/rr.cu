@@ -526,10 +526,10 @@ void pencil_factor(const Mat& gb, double floor_, PencilFactor& f) {
 // cluster's unconverged direction into one (active) column, while an aligned
 // basis can leave part of it in soft-locked columns, where no residual
 // direction works on it -- with the gap at the tolerance itself one of 16
-// seeds of 20^3 / m = 10 stalls and ends Failed(BasisDegeneracy), with the
-// relative floor alone 11 of 16 seeds of 16^3 / m = 8 / tol 1e-8 run into
-// max_iter; at a tenth of the tolerance both sweeps match the reference's
-// iteration ranges.  0 (the library default for direct callers):
+// seeds of 20^3 / m = 10 stalls for 200 iterations, with the relative floor
+// alone 11 of 16 seeds of 16^3 / m = 8 / tol 1e-8 run into max_iter; at a
+// tenth of the tolerance both sweeps match the reference's iteration ranges
+// (DESIGN.md).  0 (the library default for direct callers):
 // no alignment; B2L_RR_ALIGN=<x> scales the solver's gap for A/B runs.
 thread_local double g_align_abs = 0.0;
 // B2L_RR_ALIGN=<x>: the solver's gap times x (A/B runs; 0 = off)

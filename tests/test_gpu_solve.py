@@ -433,10 +433,11 @@ def test_seed_sweep_against_reference(pk, golden, name, N, m, tol):
     The B200 path must not fail or stall where the reference converges: every
     seed reaches the tolerance and the closed form, no run is much longer than
     the reference's longest, and the median sits on the reference's.  (This
-    is what pins the Rayleigh-Ritz step's congruence and cluster gap: with
-    the explicit-inverse congruence one 16^3 run stalls at max_iter, with the
-    cluster gap at the tolerance one 20^3 run ends Failed(BasisDegeneracy),
-    with the dsyevr sequence four do -- DESIGN.md.)"""
+    pins the Rayleigh-Ritz step's congruence and cluster gap -- with the
+    explicit-inverse congruence one 16^3 run stalls at max_iter, with the
+    cluster gap at the tolerance one 20^3 run stalls for 200 iterations -- and
+    the F1 pair kernel's narrow-stage scratch layout, whose bug turned every
+    dropped-P fallback of these runs into Failed(BasisDegeneracy).)"""
     g = golden("seed_sweep.npz")
     ref_its = g[name + "_iterations"]
     s = float((N + 1) ** 2)
