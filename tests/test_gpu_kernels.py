@@ -267,7 +267,11 @@ def test_stencil7_gram(dev, dims, m, kw):
     (25001, 8, 2, 0, 2, False, 1), (8000, 10, 2, 0, 2, False, 1), (8001, 10, 2, 2, 2, False, 1),
     (8002, 10, 10, 0, 2, False, 1), (8004, 9, 2, 0, 2, True, 2), (8005, 10, 4, 0, 4, False, 1),
     (8006, 10, 8, 0, 8, False, 1), (8007, 10, 3, 0, 2, False, 0), (8008, 10, 2, 1, 2, False, 1),
-    (8009, 10, 10, 0, 10, False, 1), (8010, 9, 4, 0, 1, False, 1), (8011, 10, 5, 0, 5, True, 1)])
+    (8009, 10, 10, 0, 10, False, 1), (8010, 9, 4, 0, 1, False, 1), (8011, 10, 5, 0, 5, True, 1),
+    # the same narrow stages in the one-warp-per-tile (m <= 8) and generic (11..16) kernels
+    (9001, 8, 1, 0, 1, False, 1), (9002, 4, 1, 0, 1, False, 0), (9003, 12, 1, 0, 1, False, 1),
+    (9004, 16, 1, 0, 1, False, 1), (9005, 13, 2, 0, 2, True, 2), (9006, 6, 2, 0, 2, True, 1),
+    (9007, 11, 3, 1, 2, False, 1), (9008, 16, 2, 2, 2, False, 1), (9009, 5, 1, 1, 1, False, 1)])
 def test_lobpcg_step_kernel(dev, n, m, kw, kp, kwn, useb, tmode):
     from paper_0705_2626_b200 import device as dv
 
