@@ -1324,8 +1324,13 @@ int update(int nrows, int m, const double* x, const double* ax, int ldx,
   A.apo = apo;
   A.ldpo = ldpo;
   A.x_plus_p = x_plus_p;
-  const int mt_r = m <= 4 ? 4 : (m <= 8 ? 8 : (m <= 10 ? 10 : 16));
-  if (m <= 16 && !scalar_only && ldo <= mt_r && (!po || ldpo <= mt_r)) {
+  // the row kernel keeps its coefficient blocks as MT x MT tiles: MT must
+  // cover the W block's width too (a constraint projection passes kw = the
+  // number of constraints, which can exceed m: with m = 2 and six constraints
+  // the Cw rows used to run past the 4 x 4 tile and the shared-memory block)
+  const int mk = m > kw ? m : kw;
+  const int mt_r = mk <= 4 ? 4 : (mk <= 8 ? 8 : (mk <= 10 ? 10 : 16));
+  if (mk <= 16 && !scalar_only && ldo <= mt_r && (!po || ldpo <= mt_r)) {
     // one thread per row (memory-bound form); MT = the next of 4 / 8 / 10 / 16
     const int blocks_r = (int)(((size_t)nrows + 255) / 256);
     int grid_r = blocks_r < 8 * sm_count() ? blocks_r : 8 * sm_count();
@@ -1335,9 +1340,9 @@ int update(int nrows, int m, const double* x, const double* ax, int ldx,
       update_row_kernel<MT><<<grid_r, 256, 3 * MT * MT * sizeof(double), st>>>(A);
       count_launch();
     };
-    if (m <= 4) launch(std::integral_constant<int, 4>{});
-    else if (m <= 8) launch(std::integral_constant<int, 8>{});
-    else if (m <= 10) launch(std::integral_constant<int, 10>{});
+    if (mt_r == 4) launch(std::integral_constant<int, 4>{});
+    else if (mt_r == 8) launch(std::integral_constant<int, 8>{});
+    else if (mt_r == 10) launch(std::integral_constant<int, 10>{});
     else launch(std::integral_constant<int, 16>{});
     B2L_CUDA(cudaGetLastError());
     return 0;

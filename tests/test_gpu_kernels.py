@@ -202,7 +202,11 @@ def test_residual_kernel(dev, m, tmode, useb):
 
 @pytest.mark.parametrize("m,kw,kp", [(10, 10, 10), (10, 7, 7), (4, 3, 0), (16, 16, 9), (64, 40, 40),
                                     (64, 64, 64), (64, 63, 0), (24, 24, 24), (33, 20, 11),
-                                    (17, 5, 17), (1, 1, 1), (3, 3, 2), (13, 11, 6), (15, 15, 0)])
+                                    (17, 5, 17), (1, 1, 1), (3, 3, 2), (13, 11, 6), (15, 15, 0),
+                                    # a W block wider than m: the constraint projection
+                                    # X - Y c of a staged solve (kw = number of constraints)
+                                    (2, 10, 0), (4, 9, 0), (3, 16, 0), (2, 20, 0), (8, 12, 3),
+                                    (1, 7, 0), (10, 14, 0)])
 def test_update_kernel(dev, m, kw, kp):
     from paper_0705_2626_b200 import device as dv
 
