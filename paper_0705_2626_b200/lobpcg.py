@@ -588,6 +588,11 @@ class LOBPCGRun:
         self.it = 0
         self.done = False
         self.drift_repairs = 0
+        # stall watch for the implicit-AX refresh (see _refresh_ax_if_stalled)
+        self.ax_refreshes = 0
+        self._force_repair = False
+        self._stall_best = np.full(m, np.inf)
+        self._stall_it = 0
         self.f1_pending = False    # self.red holds F1 results for this step
         self.sg_pending = False    # self.g2 / AW hold the stencil pass for this step
 
@@ -776,6 +781,8 @@ class LOBPCGRun:
         st.active = active.ctypes.data
         st.lock_iteration = self.lock_iteration.ctypes.data
         st.it, st.have_p, st.kst = self.it, int(self.have_p), kst
+        st.drift_limit = -1.0 if self._force_repair else DRIFT_LIMIT
+        self._force_repair = False
         st.stream = torch.cuda.current_stream(self.dev).cuda_stream
         lib = _lib.load()
         rc = lib.b2l_fast_iteration(ctypes.byref(st))
@@ -832,11 +839,55 @@ class LOBPCGRun:
         self.wcur = 1 - self.wcur
 
     # ---------------------------------------------------------- iteration
+    STALL_WINDOW = 100   # iterations without any active residual halving
+
+    def _refresh_ax_if_stalled(self):
+        """AX and AP are carried by recurrence (the reference never recomputes
+        them, lobpcg.py:520-540).  The fused path folds the orthonormalisation
+        of W and P into the update coefficients, so `A P_orth` is formed as
+        `(A P_raw) M_p`: when two active columns of one cluster make P nearly
+        dependent, that product and `P_raw M_p` lose `eps cond(P)` to
+        cancellation independently and the recurrence drifts by
+        `eps cond(P) |A|` per step.  Once the drift exceeds the tolerance the
+        computed residuals cannot fall below it (Ritz values freeze, slightly
+        BELOW the exact eigenvalues) and the run stalls.  Watch for exactly
+        that -- no active column has halved its best residual for
+        STALL_WINDOW iterations -- and then recompute AX = A X and AP = A P
+        (two applies): more accurate than the recurrence, never less."""
+        if self.it == 0 or self.norms is None:
+            return
+        act = self.active
+        if not act.any():
+            return
+        better = act & (self.norms < 0.5 * self._stall_best)
+        if better.any() or not np.isfinite(self._stall_best[act]).all():
+            self._stall_best = np.where(act, np.minimum(self._stall_best, self.norms),
+                                        self._stall_best)
+            self._stall_it = self.it
+            return
+        if self.it - self._stall_it < self.STALL_WINDOW or not self.have_p:
+            return
+        if self.b_generic is not None or self._allreduce is not None:
+            return   # B-side recurrences / slab runs: not covered here
+        self._apply_a_plain(self.X, self.AX, self.m)
+        self._apply_a_plain(self.P, self.AP, self.m)
+        # ... and have this step run the reference's own repair
+        # (_refresh_ritz, lobpcg.py:280-296) on them: the pencil's X block is
+        # the carried diag(Lambda) (lobpcg.py:323), which is only as good as
+        # the recurrences; the repair re-diagonalises the fresh X^T A X
+        self._force_repair = True
+        self.ax_refreshes += 1
+        self._stall_it = self.it
+        self._stall_best = np.where(act, self.norms, self._stall_best)
+        if self.cfg.verbosity >= 2:
+            print(f"  it {self.it:4d}  A X and A P recomputed (stalled residuals)")
+
     def step(self):
         """One pass of the hot loop body (lobpcg.py:418-540).  Returns False
         once the loop has exited (converged, max_iter or failure)."""
         if self.done:
             return False
+        self._refresh_ax_if_stalled()
         fetched = False
         if self._native is not None and self.f1_pending and self.sg_pending \
                 and _OPTS["timer"] is None:
@@ -897,9 +948,10 @@ class LOBPCGRun:
             # upper triangle (the Gram is symmetric)
             gu = G1[:m, :m] if gxx is None else gxx
             drift = float(np.abs(gu[self._triu] - self._eye_triu).max())
-            if gxx is None and (drift > DRIFT_LIMIT or cfg.check_invariants):
+            forced, self._force_repair = self._force_repair, False
+            if gxx is None and (drift > DRIFT_LIMIT or forced or cfg.check_invariants):
                 gxx = _mirror_upper(gu)
-            if drift > DRIFT_LIMIT:
+            if drift > DRIFT_LIMIT or forced:
                 try:
                     self._refresh_ritz(gxx)
                 except NotSPD:

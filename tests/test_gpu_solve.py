@@ -458,6 +458,33 @@ def test_seed_sweep_against_reference(pk, golden, name, N, m, tol):
         (np.median(its), np.median(ref_its))
 
 
+def test_stalled_run_is_refreshed(pk):
+    """24^3, m = 9 (the block cuts a triple eigenvalue), absolute tol 1e-8 at
+    |A| = 7,500, seed 1757: the reference converges at iteration 752 (oracle,
+    bit-exact).  On the fused path the carried diag(Lambda) / AX drift above
+    the tolerance around iteration 420 and two columns would stall at
+    residuals of 1e-7 until max_iter; the stall watch recomputes A X, A P and
+    runs the reference's own repair on them, after which the run converges."""
+    N, m = 24, 9
+    s = float((N + 1) ** 2)
+    a = pk.Laplacian3D((N, N, N), scale=s)
+    run = pk.LOBPCGRun(a, t=pk.jacobi_preconditioner(a),
+                       config=pk.SolverConfig(block_size=m, tol=1e-8, max_iter=3000, seed=1757))
+    while run.step():
+        pass
+    rep = run.report()
+    assert rep.all_converged, rep.status
+    assert rep.iterations_used <= 1.25 * 752, rep.iterations_used
+    assert run.ax_refreshes <= 3
+    assert rel(rep.eigenvalues, pk.exact_eigenvalues((N, N, N), m, scale=s)).max() <= REL
+    # a healthy run never triggers the watch
+    run2 = pk.LOBPCGRun(a, t=pk.jacobi_preconditioner(a),
+                        config=pk.SolverConfig(block_size=m, tol=1e-8, max_iter=3000, seed=1759))
+    while run2.step():
+        pass
+    assert run2.ax_refreshes == 0 and run2.report().all_converged
+
+
 def test_c1_outcome_distribution_matches_reference(pk, golden):
     """A single converging C1 run lands anywhere in the reference's chaotic
     band, which cannot catch a change of behaviour.  Here the GPU runs the

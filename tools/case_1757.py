@@ -8,7 +8,11 @@ s = float((N + 1) ** 2)
 a = pk.Laplacian3D((N, N, N), scale=s)
 exact = pk.exact_eigenvalues((N, N, N), m, scale=s)
 for seed in (1757, 1758, 1759, 1760):
-    rep = pk.solve(a, t=pk.jacobi_preconditioner(a), config=pk.SolverConfig(block_size=m, tol=1e-8, max_iter=3000, seed=seed))
+    run = pk.LOBPCGRun(a, t=pk.jacobi_preconditioner(a), config=pk.SolverConfig(block_size=m, tol=1e-8, max_iter=3000, seed=seed))
+    while run.step():
+        pass
+    rep = run.report()
+    print("   refreshes", run.ax_refreshes, "repairs", run.drift_repairs)
     h = rep.history[-1]
     act = np.flatnonzero(h.active)
     print(seed, rep.status, rep.iterations_used, int(rep.converged.sum()), sorted(int(x) for x in rep.lock_iterations),
