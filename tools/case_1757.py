@@ -1,3 +1,5 @@
+"""The fuzz case that stalled before the stall watch (24^3, m = 9, tol 1e-8,
+seeds 1757..1760): status, iterations, refreshes.  Diagnostic."""
 import sys
 from pathlib import Path
 import numpy as np

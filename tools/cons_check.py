@@ -1,3 +1,6 @@
+"""Constrained solves with random dense constraints: `python tools/cons_check.py ours`
+on the GPU, `... ref` in the build container (imports the reference from
+/root/reference): both end BasisFallback / MaxIterReached.  Diagnostic."""
 import sys, numpy as np
 which = sys.argv[1]
 if which == "ref":
